@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Vietoris-Rips filtration build (BASELINE.json metric:
+ranked simplices/s (edges + triangles + tetrahedra) and HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5B] [--impl ours|reference]
+
+One step = one full vrb_build (S1-S8: distances, edge ranking, neighbourhood
+lists, triangle count + fill with D_2 rows, tie-group sort) over the
+workload's synthetic points, already resident in HBM.  Outputs (55 GB for
+C5B) are far larger than L2 and L2 is additionally flushed between steps.
+For N > 1 (torchrun) every rank runs vrb_build_dist; time = max over ranks.
+
+--impl reference times the CPU oracle (oracle/, single thread) on a bounded
+sample of the same workload (the base contract's reference arm; this tier has
+no reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "ranked simplices/sec (edges+tri+tet)"
+UNIT = "simplices/s"
+# bytes each triangle's outputs take (vertices 12 + filt 4 + D_2 rows 12):
+# the fill kernel's algorithmic bytes per unit
+TRI_OUT_BYTES = 28
+# SURVEY 8(d) B_alg per unit for the whole path (sort-based accounting)
+SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44}
+ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 600, "C4": 1500, "C5A": 3000, "C5B": 3000}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _ncu_traffic(workload: str):
+    """dram read+write bytes per fill launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "fill_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def oracle_sample(workload: workloads.Workload, m: int):
+    """Time the oracle (as it stands) on the first m points of the workload:
+    steps 1-7 (edges, ranks, simplices, order, boundary).  Returns
+    (simplices, seconds)."""
+    import oracle
+
+    X = workload.points()[:m]
+    t0 = time.perf_counter()
+    o = oracle.Oracle(X, workload.radius)
+    units = o.E
+    if workload.maxdim >= 1:
+        units += o.simplices(2)[0].shape[0]
+    if workload.maxdim >= 2:
+        units += o.simplices(3)[0].shape[0]
+    dt = time.perf_counter() - t0
+    del o
+    return units, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w = workloads.WORKLOADS[args.workload]
+    m = min(ORACLE_SAMPLE.get(args.workload, 2000), w.points().shape[0])
+    for _ in range(args.warmup):
+        oracle_sample(w, m)
+    tot_units, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        u, s = oracle_sample(w, m)
+        tot_units += u
+        tot_s += s
+    value = tot_units / tot_s
+    sample = f"first {m} of {w.points().shape[0]} points of {args.workload}, full oracle steps 1-7"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32",
+        "data": "synthetic", "config": {"workload": args.workload, "desc": w.config, "maxdim": w.maxdim,
+                                        "radius": w.radius if math.isfinite(w.radius) else "inf",
+                                        "sample_points": m},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C5B", choices=sorted(workloads.WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_04424_b200 as vrb
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workloads.WORKLOADS[args.workload]
+    X = w.points()
+    Xd = torch.from_numpy(X).cuda()
+    vrb.use_torch_allocator(True)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # 512 MB > 126 MB L2
+
+    def one_build(points):
+        if world > 1:
+            return vrb.build_dist(points, maxdim=w.maxdim, radius=w.radius)
+        return vrb.build(points, maxdim=w.maxdim, radius=w.radius)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        r = one_build(Xd)
+        del r
+    torch.cuda.synchronize()
+
+    vrb.set_profiling(True)
+    step_ms, fill_ms, stage_acc = [], [], {}
+    counts = None
+    launches = 0
+    s = torch.cuda.current_stream()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = vrb.launch_count()
+            e0.record(s)
+            r = one_build(Xd)
+            e1.record(s)
+            torch.cuda.synchronize()
+            launches += vrb.launch_count() - l0
+            step_ms.append(e0.elapsed_time(e1))
+            st = vrb.last_stage_ms()
+            fill_ms.append(st["fill"])
+            for k, v in st.items():
+                stage_acc[k] = stage_acc.get(k, 0.0) + v
+            if counts is None:
+                counts = [r.count(k) for k in range(w.maxdim + 2)]
+            del r
+    vrb.set_profiling(False)
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    units_global = sum(c[0] for c in counts[1:])            # E + T (+ Q), global
+    value = units_global * args.steps / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # roofline of the dominant kernel: the triangle fill (k_triangles<true>)
+    peak, peak_kind = _peaks()
+    T_local = counts[2][2] if len(counts) > 2 else 0
+    fill_avg = float(np.mean(fill_ms)) if fill_ms else 0.0
+    roofline = None
+    if T_local and fill_avg > 0:
+        bytes_per_launch = TRI_OUT_BYTES * T_local
+        achieved = bytes_per_launch / (fill_avg / 1e3) / 1e9
+        traffic = _ncu_traffic(args.workload)
+        roofline = {"bound": "hbm", "kernel": "k_triangles<fill>", "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "fill_ms": fill_avg, "share_of_step": fill_avg / (ms_per_step or 1.0)}
+    # whole-path fraction against SURVEY 8(d) B_alg
+    E = counts[1][0]
+    T = counts[2][0] if len(counts) > 2 else 0
+    balg = E * (SURVEY_BALG["edge_k2"] if w.maxdim >= 1 else SURVEY_BALG["edge_k1"]) + T * SURVEY_BALG["tri"]
+    path_gbs = balg / (ms_per_step / 1e3) / 1e9
+
+    # e2e: through the C-ABI host path: pinned host points -> H2D inside
+    # vrb_build -> build -> D2H of the per-dimension counts and value_of_rank
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        e2e_ms = []
+        d2h = 0
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(2)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            r = one_build(Xh)
+            vor = r.rank_values()
+            host_vor = torch.empty(vor.shape, dtype=vor.dtype, pin_memory=True)
+            host_vor.copy_(vor, non_blocking=True)
+            e1.record(s)
+            torch.cuda.synchronize()
+            cnts = [r.count(k)[0] for k in range(w.maxdim + 2)]
+            e2e_ms.append(e0.elapsed_time(e1))
+            d2h = host_vor.numel() * 8 + 8 * len(cnts)
+            del r, vor
+        em = float(sum(e2e_ms))
+        if world > 1:
+            t = torch.tensor([em], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            em = float(t.item())
+        e2e = {"value": units_global * len(e2e_ms) / (em / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": em / len(e2e_ms)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        m = min(ORACLE_SAMPLE.get(args.workload, 2000), X.shape[0])
+        u, sec = oracle_sample(w, m)
+        cpu = {"value": u / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {m} of {X.shape[0]} points of {args.workload} ({u} simplices, "
+                         f"{sec:.1f} s), oracle steps 1-7 single-threaded"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": w.config, "n": int(X.shape[0]), "d": int(X.shape[1]),
+                       "maxdim": w.maxdim, "radius": w.radius if math.isfinite(w.radius) else "inf",
+                       "E": int(E), "T": int(T), "l2": "flushed (512 MB write) between steps; outputs >> L2",
+                       "parallelism": f"owner-edge ranges x{world}" if world > 1 else "single GPU"},
+            "gpu_launches": int(launches // max(1, args.steps)),
+            "roofline": roofline,
+            "path_roofline": {"survey_balg_bytes": int(balg), "achieved_gbs": path_gbs, "peak": peak,
+                              "frac": path_gbs / peak},
+            "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

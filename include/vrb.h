@@ -1,0 +1,179 @@
+/*
+ * vrb.h -- C ABI of libvrb.so, the B200 (sm_100a) Vietoris-Rips filtration
+ * and boundary-matrix build (the data-parallel hot path of Eirene profiled in
+ * Hylton, Henselman-Petrusek, Sang, Short, arXiv:1809.04424).
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md, S:<line> = SPEC.md,
+ * SURVEY 8(x) = /root/repo/SURVEY.md section 8.  Readings A1..A14 of the
+ * paper (inclusive cap, dense ranks, lex tie-break, ...) are listed in
+ * DESIGN.md "Readings".
+ *
+ * Problem statement: C = eirene(x; upperlim, bettimax)
+ * -- a point cloud, the maximum homology dimension and an optional radius --
+ * gives ranked edges, ranked simplices and the boundary operator whose rows
+ * and columns are simplices in filtration order.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", no exceptions cross the ABI; every call returns vrb_status.
+ *  - indices are 0-based; vertex ids are u32; positions are u32 (a count that
+ *    would not fit u32 returns VRB_EOVERFLOW); colptr offsets are u64.
+ *  - "device" pointers are CUDA device memory of the current device; "host"
+ *    pointers are ordinary (optionally pinned) host memory.
+ *  - work is ordered on the caller's cudaStream_t (0 = legacy default
+ *    stream).  A call blocks only at internal count read-backs that size its
+ *    allocations, and is complete on the stream when it returns.
+ *  - On error no handle is produced, nothing leaks, and vrb_last_error()
+ *    holds a one-line description (thread-local, valid until the next vrb_*
+ *    call on the same thread).
+ *  - Thread safety: distinct handles may be used concurrently; one handle
+ *    must not be used by two threads at once.
+ */
+#ifndef VRB_H
+#define VRB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRB_ABI_VERSION 1
+
+typedef enum {
+    VRB_OK = 0,
+    VRB_EINVAL = 1,     /* bad argument: n < 0, d < 1, maxdim not in 0..2,
+                           radius NaN or < 0, non-finite coordinate,
+                           dim / k out of range in an accessor, NaN key */
+    VRB_ENOMEM = 2,     /* an allocation (through the allocator hook) failed */
+    VRB_EOVERFLOW = 3,  /* a count needs more than 32 bits where the layout
+                           stores u32 positions (E, T, Q >= 2^32), or n >= 2^21 */
+    VRB_ECUDA = 4,      /* CUDA runtime error; text in vrb_last_error() */
+    VRB_ECOMM = 5,      /* the collective callback of vrb_build_dist failed */
+    VRB_ENOTSUP = 6     /* configuration outside what this build implements */
+} vrb_status;
+
+/* vrb_opts.flags */
+#define VRB_STRICT_RADIUS    0x1u  /* keep len < radius instead of len <= radius (reading A1) */
+#define VRB_DIM_MAJOR        0x2u  /* X is d x n (rowsare="dimensions") */
+#define VRB_POINTS_ON_DEVICE 0x4u  /* X is a device pointer (else host; copied H2D inside) */
+#define VRB_SKIP_BOUNDARY    0x8u  /* do not materialise the D_k row arrays (k >= 2) */
+
+typedef struct {
+    int32_t maxdim;   /* homology dimension: simplices are built up to
+                         K = maxdim + 1 (reading A6); 0, 1 or 2 */
+    double radius;    /* upperlim: >= 0 or +INFINITY */
+    uint32_t flags;   /* VRB_* flags above */
+} vrb_opts;
+
+typedef struct vrb_result* vrb_handle;   /* opaque; owns all device outputs */
+
+/* Allocator hook (e.g. PyTorch's caching allocator).  Both calls are made on
+ * the build's stream and device.  alloc returns NULL on failure.  The default
+ * (hook unset or set to NULL) is cudaMallocAsync / cudaFreeAsync.  Process-
+ * wide; set it before any build, never while a build runs. */
+typedef void* (*vrb_alloc_fn)(size_t bytes, int device, void* stream, void* ctx);
+typedef void (*vrb_free_fn)(void* ptr, size_t bytes, int device, void* stream, void* ctx);
+
+int vrb_abi_version(void);
+const char* vrb_last_error(void);
+vrb_status vrb_set_allocator(vrb_alloc_fn alloc, vrb_free_fn free_fn, void* ctx);
+
+/* Build the filtration for n points of dimension d.
+ *   X      : n x d float64, row-major (points are rows) unless VRB_DIM_MAJOR;
+ *            host memory unless VRB_POINTS_ON_DEVICE.  Read-only, caller-owned.
+ *   opts   : maxdim, radius, flags (above).
+ *   stream : cudaStream_t (as void*).
+ *   out    : receives the handle; release with vrb_free.
+ * Method (P:107-113 VR construction, P:929-941 ranking, P:251 order):
+ *   len(i,j) = sqrt_rn(fold_c (x_ic - x_jc)^2) in coordinate order, binary64
+ *   round-to-nearest, no contraction (reading A5); an edge is kept iff
+ *   len <= radius (len < radius with VRB_STRICT_RADIUS); edge filt = dense
+ *   rank of len (1-based, ties share a level, reading A3); a k-simplex's filt
+ *   is the max filt of its edges; each dimension is ordered by (filt, lex
+ *   vertex tuple) (reading A4).  Errors: VRB_EINVAL, VRB_ENOMEM,
+ *   VRB_EOVERFLOW, VRB_ECUDA. */
+vrb_status vrb_build(const double* X, int64_t n, int32_t d, const vrb_opts* opts,
+                     void* stream, vrb_handle* out);
+
+/* Collective callback for vrb_build_dist: gather `bytes` bytes from every
+ * rank into recv (world * bytes, rank order).  send/recv are DEVICE pointers
+ * on the build's stream; return 0 on success.  (The Python binding implements
+ * it with torch.distributed all_gather_into_tensor over NCCL.) */
+typedef int (*vrb_allgather_fn)(const void* send, void* recv, size_t bytes, void* stream, void* ctx);
+
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    vrb_allgather_fn allgather;
+    void* ctx;
+} vrb_comm;
+
+/* Multi-GPU build, one process per GPU; every rank calls it with the same
+ * X (valid on every rank), n, d and opts.  Triangles/tetrahedra are
+ * partitioned by ranges of their owner edge in the global edge order, so each
+ * rank produces a contiguous slice of the global (filt, lex) order; the
+ * slices concatenated in rank order are byte-identical to vrb_build (SURVEY
+ * 8(e), pin P13).  The edge level is computed redundantly on every rank; the
+ * one exchange is an all-gather of per-edge simplex counts.  Errors as
+ * vrb_build plus VRB_ECOMM. */
+vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts,
+                          const vrb_comm* comm, void* stream, vrb_handle* out);
+
+/* Counts of dimension dim (0..K): global_n = size of the whole dimension;
+ * local_off/local_n = this handle's slice (the whole for vrb_build).  Any
+ * output pointer may be NULL.  dim out of range -> VRB_EINVAL. */
+vrb_status vrb_count(vrb_handle h, int32_t dim, int64_t* global_n, int64_t* local_off,
+                     int64_t* local_n);
+
+/* Simplices of dimension dim in 1..K (this handle's slice): verts = (dim+1)
+ * u32 per simplex, ascending vertex ids, filtration order; filt = u32 level
+ * per simplex (vertices, dim 0, are implicit: id order, filt 0).  Device
+ * pointers owned by the handle. */
+vrb_status vrb_simplices(vrb_handle h, int32_t dim, const uint32_t** verts_dev,
+                         const uint32_t** filt_dev);
+
+/* value_of_rank: nvals float64 lengths, value_of_rank[f-1] = length of level f
+ * (strictly increasing; level 0 = vertices = 0.0).  Device, owned. */
+vrb_status vrb_rank_values(vrb_handle h, const double** value_of_rank_dev, int64_t* nvals);
+
+/* Boundary matrix D_k, k in 1..K: column j (this handle's
+ * slice) has the k+1 rows rowval[(k+1)j .. (k+1)j+k], strictly ascending, each
+ * the POSITION of a face in the dimension k-1 filtration order (reading A7).
+ * colptr is implicit, (k+1)j.  D_1's rows are the vertex ids, so rowval of
+ * D_1 aliases the edge vertex array.  nrows = global size of dim k-1, ncols =
+ * local size of dim k.  VRB_SKIP_BOUNDARY builds -> VRB_EINVAL for k >= 2. */
+vrb_status vrb_boundary(vrb_handle h, int32_t k, int64_t* nrows, int64_t* ncols,
+                        const uint32_t** rowval_dev);
+
+/* Materialise colptr (u64, ncols+1 entries, global offsets (k+1)(local_off+j))
+ * into caller device memory on `stream`. */
+vrb_status vrb_boundary_colptr(vrb_handle h, int32_t k, uint64_t* colptr_dev, void* stream);
+
+vrb_status vrb_free(vrb_handle h);
+
+/* sortperm (Fig. GPU_sortperm) on device: perm_dev gets
+ * the 0-based stable ascending permutation of keys_dev (n doubles; -0.0 ==
+ * +0.0; NaN -> VRB_EINVAL), dense_rank_dev (nullable) gets 1-based dense ranks
+ * (equal keys share a rank, reading A3).  All pointers device, caller-owned. */
+vrb_status vrb_sortperm_f64(const double* keys_dev, int64_t n, int64_t* perm_dev,
+                            uint32_t* dense_rank_dev, void* stream);
+
+/* Stage timings of the last build on this thread (milliseconds, CUDA events
+ * on the build stream): [0] points + distances S1-S2, [1] edge sort + ranks
+ * S3, [2] neighbourhood lists S4, [3] simplex count + offsets + output
+ * allocation, [4] simplex fill kernel S5/S6+S8 alone, [5] tie-group sort S7,
+ * [6] exchange (vrb_build_dist), [7] total.  Recorded only while profiling
+ * is enabled (events add no synchronisation inside the build). */
+vrb_status vrb_set_profiling(int32_t enable);
+vrb_status vrb_last_stage_ms(double* ms8);
+
+/* Number of kernels this library has launched in this process (monotonic;
+ * the difference across a region is the number of launches inside it). */
+unsigned long long vrb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VRB_H */

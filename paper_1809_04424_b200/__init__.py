@@ -1,0 +1,355 @@
+"""Python binding of libvrb.so -- the B200 Vietoris-Rips filtration build.
+
+Argument marshalling only: every step of the build runs in the CUDA kernels of
+``libvrb.so`` (``csrc/``); PyTorch supplies device memory (through the
+allocator hook), streams and ``torch.distributed``.  There is no CPU path: if
+the library is missing or no CUDA device is present, calls raise.
+
+Names follow ``include/vrb.h`` (``vrb_build`` -> ``build`` ...).  The paper's
+problem statement: a point cloud, the max homology
+dimension and an optional radius give ranked edges, ranked simplices and the
+boundary matrices in filtration order.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libvrb.so")
+
+VRB_OK, VRB_EINVAL, VRB_ENOMEM, VRB_EOVERFLOW, VRB_ECUDA, VRB_ECOMM, VRB_ENOTSUP = range(7)
+STATUS_NAMES = {0: "VRB_OK", 1: "VRB_EINVAL", 2: "VRB_ENOMEM", 3: "VRB_EOVERFLOW", 4: "VRB_ECUDA",
+                5: "VRB_ECOMM", 6: "VRB_ENOTSUP"}
+VRB_STRICT_RADIUS = 0x1
+VRB_DIM_MAJOR = 0x2
+VRB_POINTS_ON_DEVICE = 0x4
+VRB_SKIP_BOUNDARY = 0x8
+
+# Every symbol include/vrb.h declares (checked by tests/test_abi.py).
+EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
+           "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
+           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count")
+
+STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total")
+
+
+class VrbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class vrb_opts(ctypes.Structure):
+    _fields_ = [("maxdim", ctypes.c_int32), ("radius", ctypes.c_double), ("flags", ctypes.c_uint32)]
+
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                ctypes.c_void_p, ctypes.c_void_p)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                           ctypes.c_void_p)
+
+
+class vrb_comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("allgather", ALLGATHER_FN),
+                ("ctx", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libvrb.so; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    p, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    P = ctypes.POINTER
+    L.vrb_abi_version.restype = ctypes.c_int
+    L.vrb_abi_version.argtypes = []
+    L.vrb_last_error.restype = ctypes.c_char_p
+    L.vrb_last_error.argtypes = []
+    L.vrb_set_allocator.restype = ctypes.c_int
+    L.vrb_set_allocator.argtypes = [ALLOC_FN, FREE_FN, p]
+    L.vrb_build.restype = ctypes.c_int
+    L.vrb_build.argtypes = [p, i64, i32, P(vrb_opts), p, P(p)]
+    L.vrb_build_dist.restype = ctypes.c_int
+    L.vrb_build_dist.argtypes = [p, i64, i32, P(vrb_opts), P(vrb_comm), p, P(p)]
+    L.vrb_count.restype = ctypes.c_int
+    L.vrb_count.argtypes = [p, i32, P(i64), P(i64), P(i64)]
+    L.vrb_simplices.restype = ctypes.c_int
+    L.vrb_simplices.argtypes = [p, i32, P(p), P(p)]
+    L.vrb_rank_values.restype = ctypes.c_int
+    L.vrb_rank_values.argtypes = [p, P(p), P(i64)]
+    L.vrb_boundary.restype = ctypes.c_int
+    L.vrb_boundary.argtypes = [p, i32, P(i64), P(i64), P(p)]
+    L.vrb_boundary_colptr.restype = ctypes.c_int
+    L.vrb_boundary_colptr.argtypes = [p, i32, p, p]
+    L.vrb_free.restype = ctypes.c_int
+    L.vrb_free.argtypes = [p]
+    L.vrb_sortperm_f64.restype = ctypes.c_int
+    L.vrb_sortperm_f64.argtypes = [p, i64, p, p, p]
+    L.vrb_set_profiling.restype = ctypes.c_int
+    L.vrb_set_profiling.argtypes = [i32]
+    L.vrb_last_stage_ms.restype = ctypes.c_int
+    L.vrb_last_stage_ms.argtypes = [P(ctypes.c_double)]
+    L.vrb_launch_count.restype = ctypes.c_ulonglong
+    L.vrb_launch_count.argtypes = []
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != VRB_OK:
+        raise VrbError(st, lib().vrb_last_error().decode(errors="replace"))
+
+
+def abi_version() -> int:
+    return lib().vrb_abi_version()
+
+
+# ---------------------------------------------------------------------------
+# allocator hook -> PyTorch caching allocator
+# ---------------------------------------------------------------------------
+_hooks = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device allocations through torch's caching allocator."""
+    global _hooks
+    import torch
+
+    if not enable:
+        _check(lib().vrb_set_allocator(ALLOC_FN(), FREE_FN(), None))
+        _hooks = None
+        return
+
+    def _alloc(nbytes, dev, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), int(dev), int(stream or 0))
+        except Exception:   # reported as VRB_ENOMEM by the library
+            return None
+
+    def _free(ptr, nbytes, dev, stream, ctx):
+        try:
+            torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:
+            pass
+
+    hooks = (ALLOC_FN(_alloc), FREE_FN(_free))
+    _check(lib().vrb_set_allocator(hooks[0], hooks[1], None))
+    _hooks = hooks
+
+
+def set_profiling(enable: bool):
+    _check(lib().vrb_set_profiling(1 if enable else 0))
+
+
+def launch_count() -> int:
+    """Kernels launched by libvrb.so so far in this process."""
+    return int(lib().vrb_launch_count())
+
+
+def last_stage_ms() -> dict:
+    arr = (ctypes.c_double * 8)()
+    _check(lib().vrb_last_stage_ms(arr))
+    return {k: float(v) for k, v in zip(STAGES, arr)}
+
+
+# ---------------------------------------------------------------------------
+# zero-copy device views of handle-owned arrays
+# ---------------------------------------------------------------------------
+class _CAI:
+    def __init__(self, ptr, shape, typestr, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+        self._owner = owner
+
+
+def _view(ptr, shape, typestr, owner, device):
+    import torch
+
+    n = int(np.prod(shape)) if len(shape) else 1
+    if n == 0 or not ptr:
+        dt = {"<i4": torch.int32, "<f8": torch.float64, "<i8": torch.int64}[typestr]
+        return torch.empty(shape, dtype=dt, device=device)
+    return torch.as_tensor(_CAI(ptr, shape, typestr, owner), device=device)
+
+
+class VRResult:
+    """A built filtration (owns the vrb handle).  Arrays are zero-copy CUDA
+    tensors in filtration order; u32 arrays are exposed as int32 tensors
+    holding the u32 bit patterns (use ``.view(torch.uint32)`` or ``u64()``)."""
+
+    def __init__(self, handle: int, device):
+        self._h = ctypes.c_void_p(handle)
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().vrb_free(h)
+            finally:
+                self._h = None
+
+    def free(self):
+        self.__del__()
+
+    # counts
+    def count(self, dim: int):
+        g, o, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().vrb_count(self._h, dim, ctypes.byref(g), ctypes.byref(o), ctypes.byref(n)))
+        return g.value, o.value, n.value
+
+    @property
+    def num_edges(self) -> int:
+        return self.count(1)[0]
+
+    def simplices(self, dim: int):
+        """(vertices (N, dim+1) int32[u32], filt (N,) int32[u32]) of this handle's slice."""
+        v, f = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().vrb_simplices(self._h, dim, ctypes.byref(v), ctypes.byref(f)))
+        n = self.count(dim)[2]
+        return (_view(v.value, (n, dim + 1), "<i4", self, self.device),
+                _view(f.value, (n,), "<i4", self, self.device))
+
+    def rank_values(self):
+        p, nv = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().vrb_rank_values(self._h, ctypes.byref(p), ctypes.byref(nv)))
+        return _view(p.value, (nv.value,), "<f8", self, self.device)
+
+    def boundary(self, k: int):
+        """D_k row values (ncols, k+1) int32[u32]: positions of the faces, ascending."""
+        nr, nc, p = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_void_p()
+        _check(lib().vrb_boundary(self._h, k, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(p)))
+        return _view(p.value, (nc.value, k + 1), "<i4", self, self.device)
+
+    def boundary_colptr(self, k: int, stream=None):
+        import torch
+
+        nc = self.count(k)[2]
+        out = torch.empty(nc + 1, dtype=torch.int64, device=self.device)
+        _check(lib().vrb_boundary_colptr(self._h, k, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+
+def u64(t):
+    """int32 tensor holding u32 bit patterns -> int64 values."""
+    import torch
+
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+def _stream_ptr(stream):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(int(s.cuda_stream))
+
+
+def _prepare_points(points, device):
+    """Returns (pointer, n, d, flags, keepalive)."""
+    import torch
+
+    if isinstance(points, torch.Tensor):
+        t = points.detach()
+        if t.dtype != torch.float64:
+            raise TypeError("points must be float64")
+        if t.ndim != 2:
+            raise ValueError("points must be (n, d)")
+        if t.is_cuda:
+            t = t.contiguous()
+            return t.data_ptr(), t.shape[0], t.shape[1], VRB_POINTS_ON_DEVICE, t
+        t = t.contiguous()
+        return t.data_ptr(), t.shape[0], t.shape[1], 0, t
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError("points must be (n, d)")
+    return a.ctypes.data, a.shape[0], a.shape[1], 0, a
+
+
+def build(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
+          skip_boundary: bool = False, stream=None) -> VRResult:
+    """vrb_build: points (n, d) float64 (numpy / CPU tensor -> copied H2D inside
+    the call; CUDA tensor -> used in place on its device)."""
+    import torch
+
+    ptr, n, d, flags, keep = _prepare_points(points, None)
+    if flags & VRB_POINTS_ON_DEVICE:
+        device = keep.device
+    else:
+        device = torch.device("cuda", torch.cuda.current_device())
+    if strict:
+        flags |= VRB_STRICT_RADIUS
+    if skip_boundary:
+        flags |= VRB_SKIP_BOUNDARY
+    opts = vrb_opts(int(maxdim), float(radius), flags)
+    h = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _check(lib().vrb_build(ctypes.c_void_p(ptr), n, max(d, 1), ctypes.byref(opts), _stream_ptr(stream),
+                               ctypes.byref(h)))
+    del keep
+    return VRResult(h.value, device)
+
+
+def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
+               skip_boundary: bool = False, group=None, stream=None) -> VRResult:
+    """vrb_build_dist: one process per GPU; every rank passes the same points.
+    The all-gather the library asks for runs over torch.distributed (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ptr, n, d, flags, keep = _prepare_points(points, None)
+    device = keep.device if (flags & VRB_POINTS_ON_DEVICE) else torch.device("cuda", torch.cuda.current_device())
+    if strict:
+        flags |= VRB_STRICT_RADIUS
+    if skip_boundary:
+        flags |= VRB_SKIP_BOUNDARY
+
+    def _allgather(send, recv, nbytes, stream, ctx):
+        try:
+            src = _view(send, (nbytes,), "<i4", None, device) if nbytes % 4 == 0 else None
+            dst = _view(recv, (nbytes * world,), "<i4", None, device) if nbytes % 4 == 0 else None
+            if src is None:
+                return 1
+            src = src[: nbytes // 4]
+            dst = dst[: world * nbytes // 4]
+            dist.all_gather_into_tensor(dst, src, group=group)
+            return 0
+        except Exception as e:   # reported as VRB_ECOMM
+            print("vrb allgather failed:", e)
+            return 1
+
+    cb = ALLGATHER_FN(_allgather)
+    comm = vrb_comm(rank, world, cb, None)
+    opts = vrb_opts(int(maxdim), float(radius), flags)
+    h = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _check(lib().vrb_build_dist(ctypes.c_void_p(ptr), n, max(d, 1), ctypes.byref(opts), ctypes.byref(comm),
+                                    _stream_ptr(stream), ctypes.byref(h)))
+    del keep
+    return VRResult(h.value, device)
+
+
+def sortperm_f64(keys):
+    """vrb_sortperm_f64: (0-based stable permutation int64, dense ranks int32[u32])."""
+    import torch
+
+    if not (isinstance(keys, torch.Tensor) and keys.is_cuda and keys.dtype == torch.float64):
+        raise TypeError("keys must be a CUDA float64 tensor")
+    k = keys.contiguous()
+    perm = torch.empty(k.numel(), dtype=torch.int64, device=k.device)
+    dense = torch.empty(k.numel(), dtype=torch.int32, device=k.device)
+    with torch.cuda.device(k.device):
+        _check(lib().vrb_sortperm_f64(ctypes.c_void_p(k.data_ptr()), k.numel(), ctypes.c_void_p(perm.data_ptr()),
+                                      ctypes.c_void_p(dense.data_ptr()), _stream_ptr(None)))
+    return perm, dense

@@ -1,0 +1,244 @@
+// distance.cu -- S1 (point placement) and S2 (pairwise distance + radius cap).
+//
+// Paper: sec. 2.1 P:107-113 ("any two points that are less than the distance
+// epsilon from each other are connected by an edge"); the distance matrix is
+// "the primary input" of Eirene.  Readings: A1 inclusive
+// cap (len <= r; STRICT: len < r), A5 fixed-order fold
+//     acc = +0.0; for c = 0..d-1: t = x_ic - x_jc; acc = acc + t*t; len = sqrt(acc)
+// with every operation binary64 round-to-nearest and no FMA contraction
+// (__dsub_rn / __dmul_rn / __dadd_rn / __dsqrt_rn).
+//
+// The cap is applied to d2 against a host-computed threshold T(r) = the
+// largest double x with sqrt_rn(x) <= r (or < r): sqrt_rn is monotone, so
+// "d2 <= T(r)" is exactly "sqrt_rn(d2) <= r" without a sqrt per pair.
+//
+// Two passes over 64x64 upper-triangular tiles of the pair matrix:
+//   k_dist_mask : FP64 fold for every pair of the tile -> 64x64 kept bitmask
+//                 + per (row, tile) kept counts            (FP64-ALU bound)
+//   scan        : per (row, tile) counts -> lex slot bases
+//   k_dist_fill : kept pairs only: recompute the fold, sqrt, write
+//                 (len bits, i, j) at its lex slot          (write bound)
+// Output: the kept edges in lexicographic (i, j) order.
+#include <cmath>
+
+#include "vrb_internal.cuh"
+#include "vrb_stages.cuh"
+
+namespace vrb {
+namespace {
+
+constexpr int kT = 64;        // tile edge
+constexpr int kDC = 16;       // coordinates staged per chunk
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int64_t tile_index(int64_t ti, int64_t tj, int64_t nt) {
+    return ti * nt - ti * (ti - 1) / 2 + (tj - ti);   // packed upper triangle (tj >= ti)
+}
+
+__global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict__ X, int64_t n, int d,
+                                                        int64_t nt, double thr, int all,
+                                                        unsigned long long* __restrict__ masks,
+                                                        uint32_t* __restrict__ rowtile_cnt) {
+    const int64_t tj = blockIdx.x, ti = blockIdx.y;
+    if (tj < ti) return;
+    __shared__ double sA[kDC][kT];
+    __shared__ double sB[kDC][kT];
+    __shared__ unsigned long long mrow[kT];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = ti * kT, j0 = tj * kT;
+    if (threadIdx.x < kT) mrow[threadIdx.x] = 0ull;
+
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+
+    if (!all) {
+        for (int c0 = 0; c0 < d; c0 += kDC) {
+            const int dc = min(kDC, d - c0);
+            __syncthreads();
+            for (int q = threadIdx.x; q < kT * kDC; q += kThreads) {
+                const int r = q / kDC, c = q % kDC;
+                double va = 0.0, vb = 0.0;
+                if (c < dc) {
+                    if (i0 + r < n) va = X[(i0 + r) * d + c0 + c];
+                    if (j0 + r < n) vb = X[(j0 + r) * d + c0 + c];
+                }
+                sA[c][r] = va;
+                sB[c][r] = vb;
+            }
+            __syncthreads();
+            for (int c = 0; c < dc; ++c) {
+                double a[4], b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { a[q] = sA[c][ty + 16 * q]; b[q] = sB[c][tx + 16 * q]; }
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double t = __dsub_rn(a[p], b[q]);
+                        acc[p][q] = __dadd_rn(acc[p][q], __dmul_rn(t, t));
+                    }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int64_t i = i0 + ty + 16 * p;
+        unsigned long long bits = 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t j = j0 + tx + 16 * q;
+            const bool keep = i < n && j < n && j > i && (all || acc[p][q] <= thr);
+            if (keep) bits |= 1ull << (tx + 16 * q);
+        }
+        if (bits) atomicOr(&mrow[ty + 16 * p], bits);
+    }
+    __syncthreads();
+    if (threadIdx.x < kT) {
+        const int r = threadIdx.x;
+        const unsigned long long m = mrow[r];
+        masks[tile_index(ti, tj, nt) * kT + r] = m;
+        if (i0 + r < n) rowtile_cnt[(i0 + r) * nt + tj] = (uint32_t)__popcll(m);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict__ X, int64_t n, int d,
+                                                        int64_t nt,
+                                                        const unsigned long long* __restrict__ masks,
+                                                        const uint64_t* __restrict__ slot_base,
+                                                        uint64_t* __restrict__ key,
+                                                        uint32_t* __restrict__ ei,
+                                                        uint32_t* __restrict__ ej) {
+    const int64_t tj = blockIdx.x, ti = blockIdx.y;
+    if (tj < ti) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t i0 = ti * kT, j0 = tj * kT;
+    const unsigned long long* m = masks + tile_index(ti, tj, nt) * kT;
+    for (int r = wid; r < kT; r += kThreads / 32) {
+        const int64_t i = i0 + r;
+        if (i >= n) break;
+        const unsigned long long bits = m[r];
+        if (!bits) continue;
+        const uint64_t base = slot_base[i * nt + tj];
+        const double* xi = X + i * d;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            if (!((bits >> c) & 1ull)) continue;
+            const int64_t j = j0 + c;
+            const double* xj = X + j * d;
+            double acc = 0.0;
+            for (int q = 0; q < d; ++q) {
+                const double t = __dsub_rn(__ldg(xi + q), __ldg(xj + q));
+                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            }
+            const double len = __dsqrt_rn(acc);
+            const uint64_t slot = base + __popcll(bits & ((1ull << c) - 1ull));
+            key[slot] = (uint64_t)__double_as_longlong(len);
+            ei[slot] = (uint32_t)i;
+            ej[slot] = (uint32_t)j;
+        }
+    }
+}
+
+__global__ void k_check_points(const double* __restrict__ X, int64_t total, int* bad) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(X[q])) atomicOr(bad, 1);
+}
+
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t n, int d) {
+    // in: d x n (dimension-major), out: n x d
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * d;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / d, c = q % d;
+        out[q] = in[c * n + i];
+    }
+}
+
+}  // namespace
+
+// Threshold on d2 equivalent to the cap on len = sqrt_rn(d2) (reading A1).
+double cap_threshold(double r, bool strict) {
+    if (std::isinf(r)) return strict ? 1.79769313486231570815e308 : INFINITY;
+    auto ok = [&](double x) { double s = std::sqrt(x); return strict ? s < r : s <= r; };
+    if (!ok(0.0)) return -1.0;                    // nothing can be kept (strict, r == 0)
+    double x = r * r;
+    if (std::isinf(x)) x = 1.79769313486231570815e308;
+    while (x > 0.0 && !ok(x)) x = std::nextafter(x, -INFINITY);
+    while (!std::isinf(std::nextafter(x, INFINITY)) && ok(std::nextafter(x, INFINITY)))
+        x = std::nextafter(x, INFINITY);
+    return x;
+}
+
+void place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out) {
+    const int64_t total = n * d;
+    out.alloc((size_t)total, s);
+    if (total == 0) return;
+    DBuf<double> staged;
+    const double* src = X;
+    if (!(flags & VRB_POINTS_ON_DEVICE)) {
+        if (flags & VRB_DIM_MAJOR) {
+            staged.alloc((size_t)total, s);
+            VRB_CUDA(cudaMemcpyAsync(staged.get(), X, total * sizeof(double), cudaMemcpyHostToDevice, s));
+            src = staged.get();
+        } else {
+            VRB_CUDA(cudaMemcpyAsync(out.get(), X, total * sizeof(double), cudaMemcpyHostToDevice, s));
+            src = nullptr;
+        }
+    }
+    if (src) {
+        const unsigned g = (unsigned)std::min<int64_t>(ceil_div(total, 256), 4096);
+        if (flags & VRB_DIM_MAJOR) {
+            k_transpose<<<g, 256, 0, s>>>(src, out.get(), n, d);
+        } else {
+            VRB_CUDA(cudaMemcpyAsync(out.get(), src, total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        }
+        VRB_LAUNCH_CHECK();
+    }
+    DBuf<int> bad(1, s);
+    VRB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(total, 256), 4096);
+    k_check_points<<<g, 256, 0, s>>>(out.get(), total, bad.get());
+    VRB_LAUNCH_CHECK();
+    int h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (h) fail(VRB_EINVAL, "non-finite coordinate in the point cloud");
+}
+
+void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
+                      KeptEdges& out) {
+    out.E = 0;
+    if (n < 2) return;
+    const int64_t nt = ceil_div(n, kT);
+    const double thr = cap_threshold(radius, strict);
+    const int all = (!strict && std::isinf(radius)) ? 1 : 0;
+    if (thr < 0.0) return;
+    const int64_t ntiles = nt * (nt + 1) / 2;
+    DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
+    DBuf<uint32_t> cnt((size_t)(n * nt), s);
+    VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    dim3 grid((unsigned)nt, (unsigned)nt);
+    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get());
+    VRB_LAUNCH_CHECK();
+    DBuf<uint64_t> base((size_t)(n * nt + 1), s);
+    exclusive_scan(cnt.get(), base.get(), n * nt, s);
+    uint64_t E = 0;
+    VRB_CUDA(cudaMemcpyAsync(&E, base.get() + n * nt, sizeof(E), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (E >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu kept edges exceed u32 positions", (unsigned long long)E);
+    out.E = (int64_t)E;
+    if (E == 0) return;
+    out.key.alloc(E, s);
+    out.ei.alloc(E, s);
+    out.ej.alloc(E, s);
+    k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, masks.get(), base.get(), out.key.get(),
+                                          out.ei.get(), out.ej.get());
+    VRB_LAUNCH_CHECK();
+}
+
+}  // namespace vrb

@@ -1,0 +1,222 @@
+// edges.cu -- S3 (edge ranking) and S4 (neighbourhood lists + owner-edge plan).
+//
+// S3 follows the paper's GPU sortperm (sec. 4.5: order the
+// distance entries, then read ranks off the permutation) with the readings of
+// order by (len, i, j) (A4), filt = dense rank of len (A3, A14).
+// The kept edges arrive in lex order, so a STABLE radix sort on the length
+// bits alone yields (len, i, j) order.  Head flags + an inclusive scan give
+// the dense rank; heads also write value_of_rank.
+//
+// S4 builds, per vertex v, (a) its neighbours in edge-position order (the
+// "older-neighbour prefix" of an edge is a prefix of this list) and (b) its
+// neighbours in id order with their edge positions.  Each edge p = (a, b) is
+// then assigned to the endpoint x with the SHORTER prefix of neighbours older
+// than p (to be scanned) and the other endpoint y (the "host", whose full
+// neighbourhood is held as a dense map in shared memory during enumeration).
+#include "vrb_internal.cuh"
+#include "vrb_stages.cuh"
+
+namespace vrb {
+namespace {
+
+unsigned grid_for(int64_t n, int threads) {
+    int64_t g = ceil_div(n, threads);
+    int64_t cap = (int64_t)device_sm_count() * 32;
+    return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+#define GRID_STRIDE(i, n)                                                          \
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n);       \
+         i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_rank_heads(const uint64_t* __restrict__ key, int64_t E, uint32_t* __restrict__ head) {
+    GRID_STRIDE(p, E) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
+}
+
+__global__ void k_edge_outputs(const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
+                               const uint32_t* __restrict__ ei, const uint32_t* __restrict__ ej,
+                               const uint32_t* __restrict__ efilt, int64_t E, uint32_t* __restrict__ ev,
+                               double* __restrict__ vor) {
+    GRID_STRIDE(p, E) {
+        const uint32_t lex = perm[p];
+        ev[2 * p] = ei[lex];
+        ev[2 * p + 1] = ej[lex];
+        if (p == 0 || key[p] != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)key[p]);
+    }
+}
+
+__global__ void k_degree(const uint32_t* __restrict__ ev, int64_t n2, uint32_t* __restrict__ deg) {
+    GRID_STRIDE(q, n2) atomicAdd(&deg[ev[q]], 1u);
+}
+
+__global__ void k_keys_vertex(const uint32_t* __restrict__ ev, int64_t n2, uint64_t* __restrict__ key) {
+    GRID_STRIDE(q, n2) key[q] = ev[q];
+}
+
+__global__ void k_keys_vertex_nbr(const uint32_t* __restrict__ ev, int64_t n2, uint64_t* __restrict__ key) {
+    GRID_STRIDE(q, n2) key[q] = ((uint64_t)ev[q] << 21) | ev[q ^ 1];
+}
+
+// position-ordered lists: slot s holds entry q = sorted[s]
+__global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
+                            const uint64_t* __restrict__ off, int64_t n2, uint32_t* __restrict__ nbr_pos,
+                            uint32_t* __restrict__ listidx) {
+    GRID_STRIDE(s, n2) {
+        const uint32_t q = sorted[s];
+        const uint32_t v = ev[q];
+        nbr_pos[s] = ev[q ^ 1];
+        listidx[q] = (uint32_t)(s - (int64_t)off[v]);
+    }
+}
+
+// id-ordered lists: slot s holds entry q = sorted[s]
+__global__ void k_id_lists(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
+                           const uint64_t* __restrict__ off, const uint32_t* __restrict__ listidx,
+                           int64_t n2, uint64_t* __restrict__ kord, uint32_t* __restrict__ krank_pos) {
+    GRID_STRIDE(s, n2) {
+        const uint32_t q = sorted[s];
+        const uint32_t v = ev[q];
+        const uint64_t o = off[v];
+        kord[s] = ((uint64_t)(q >> 1) << 32) | ev[q ^ 1];
+        krank_pos[o + listidx[q]] = (uint32_t)(s - (int64_t)o);
+    }
+}
+
+__global__ void k_assign(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ listidx, int64_t E,
+                         uint32_t* __restrict__ scan_v, uint32_t* __restrict__ scan_len,
+                         uint64_t* __restrict__ host_key) {
+    GRID_STRIDE(p, E) {
+        const uint32_t la = listidx[2 * p], lb = listidx[2 * p + 1];
+        const uint32_t a = ev[2 * p], b = ev[2 * p + 1];
+        const bool scan_a = la <= lb;
+        scan_v[p] = scan_a ? a : b;
+        scan_len[p] = scan_a ? la : lb;
+        host_key[p] = scan_a ? b : a;
+    }
+}
+
+__global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_t* __restrict__ host_key,
+                              const uint32_t* __restrict__ scan_len, int64_t E,
+                              uint32_t* __restrict__ hosted_v, uint32_t* __restrict__ work) {
+    GRID_STRIDE(i, E) {
+        hosted_v[i] = (uint32_t)host_key[i];
+        work[i] = scan_len[hosted[i]];
+    }
+}
+
+__global__ void k_max_deg(const uint32_t* __restrict__ deg, int64_t n, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    GRID_STRIDE(v, n) m = max(m, deg[v]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Sort (keys, vals) where vals start as 0..m-1; returns the buffer with the
+// sorted values (the other buffers are scratch).
+uint32_t* sort_ids(DBuf<uint64_t>& k0, DBuf<uint64_t>& k1, DBuf<uint32_t>& v0, DBuf<uint32_t>& v1,
+                   int64_t m, cudaStream_t s, uint64_t** sorted_keys = nullptr) {
+    iota_u32(v0.get(), m, s);
+    const uint64_t vary = varying_bits(k0.get(), m, s);
+    const bool alt = radix_sort_pairs(k0.get(), k1.get(), v0.get(), v1.get(), m, vary, s);
+    if (sorted_keys) *sorted_keys = alt ? k1.get() : k0.get();
+    return alt ? v1.get() : v0.get();
+}
+
+}  // namespace
+
+int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
+    const int64_t E = ke.E;
+    if (E == 0) return 0;
+    DBuf<uint64_t> key_alt(E, s);
+    DBuf<uint32_t> perm(E, s), perm_alt(E, s);
+    iota_u32(perm.get(), E, s);
+    const uint64_t vary = varying_bits(ke.key.get(), E, s);
+    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), perm.get(), perm_alt.get(), E, vary, s);
+    const uint64_t* skey = alt ? key_alt.get() : ke.key.get();
+    const uint32_t* sperm = alt ? perm_alt.get() : perm.get();
+    DBuf<uint32_t> head(E, s);
+    k_rank_heads<<<grid_for(E, 256), 256, 0, s>>>(skey, E, head.get());
+    VRB_LAUNCH_CHECK();
+    inclusive_scan_u32(head.get(), efilt, E, s);
+    k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sperm, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor);
+    VRB_LAUNCH_CHECK();
+    uint32_t nvals = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nvals, efilt + E - 1, sizeof(nvals), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    return nvals;
+}
+
+void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g) {
+    g.n = n;
+    g.E = E;
+    const int64_t n2 = 2 * E;
+    g.off.alloc(n + 1, s);
+    {
+        DBuf<uint32_t> deg(n, s);
+        VRB_CUDA(cudaMemsetAsync(deg.get(), 0, deg.bytes(), s));
+        if (n2) k_degree<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, deg.get());
+        VRB_LAUNCH_CHECK();
+        exclusive_scan(deg.get(), g.off.get(), n, s);
+        DBuf<unsigned> mx(1, s);
+        VRB_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned), s));
+        if (n) k_max_deg<<<grid_for(n, 256), 256, 0, s>>>(deg.get(), n, mx.get());
+        VRB_LAUNCH_CHECK();
+        unsigned h = 0;
+        VRB_CUDA(cudaMemcpyAsync(&h, mx.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+        g.max_deg = h;
+    }
+    g.nbr_pos.alloc(n2, s);
+    g.krank_pos.alloc(n2, s);
+    g.kord.alloc(n2, s);
+    g.listidx.alloc(n2, s);
+    g.scan_v.alloc(E, s);
+    g.scan_len.alloc(E, s);
+    g.hosted.alloc(E, s);
+    g.hosted_v.alloc(E, s);
+    g.work_pre.alloc(E + 1, s);
+    if (E == 0) {
+        VRB_CUDA(cudaMemsetAsync(g.work_pre.get(), 0, sizeof(uint64_t), s));
+        g.work = 0;
+        return;
+    }
+    {
+        DBuf<uint64_t> k0(n2, s), k1(n2, s);
+        DBuf<uint32_t> v0(n2, s), v1(n2, s);
+        // (a) lists in edge-position order: stable sort of entries by vertex
+        k_keys_vertex<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
+        VRB_LAUNCH_CHECK();
+        const uint32_t* sorted = sort_ids(k0, k1, v0, v1, n2, s);
+        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), n2, g.nbr_pos.get(),
+                                                       g.listidx.get());
+        VRB_LAUNCH_CHECK();
+        // (b) lists in neighbour-id order: sort entries by (vertex, neighbour)
+        k_keys_vertex_nbr<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
+        VRB_LAUNCH_CHECK();
+        sorted = sort_ids(k0, k1, v0, v1, n2, s);
+        k_id_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), g.listidx.get(), n2,
+                                                      g.kord.get(), g.krank_pos.get());
+        VRB_LAUNCH_CHECK();
+    }
+    {
+        // (c) owner-edge plan: scanned endpoint, prefix length, host; edges by host
+        DBuf<uint64_t> k0(E, s), k1(E, s);
+        DBuf<uint32_t> v0(E, s), v1(E, s);
+        k_assign<<<grid_for(E, 256), 256, 0, s>>>(ev, g.listidx.get(), E, g.scan_v.get(), g.scan_len.get(),
+                                                  k0.get());
+        VRB_LAUNCH_CHECK();
+        uint64_t* skeys = nullptr;
+        const uint32_t* sorted = sort_ids(k0, k1, v0, v1, E, s, &skeys);
+        VRB_CUDA(cudaMemcpyAsync(g.hosted.get(), sorted, E * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        DBuf<uint32_t> work(E, s);
+        k_hosted_work<<<grid_for(E, 256), 256, 0, s>>>(g.hosted.get(), skeys, g.scan_len.get(), E,
+                                                       g.hosted_v.get(), work.get());
+        VRB_LAUNCH_CHECK();
+        exclusive_scan(work.get(), g.work_pre.get(), E, s);
+        VRB_CUDA(cudaMemcpyAsync(&g.work, g.work_pre.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+    }
+}
+
+}  // namespace vrb

@@ -1,0 +1,511 @@
+// vrb_api.cu -- the C ABI of libvrb.so (include/vrb.h): argument checks,
+// allocator hook, stage orchestration, result handle and accessors.
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <new>
+
+#include "vrb_internal.cuh"
+#include "vrb_stages.cuh"
+
+namespace vrb {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string t_last_error;
+static thread_local double t_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+static bool g_profiling = false;
+
+void fail(vrb_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw Error{st, std::string(buf)};
+}
+
+bool profiling_enabled() { return g_profiling; }
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------
+// allocator hook
+// ---------------------------------------------------------------------------
+static vrb_alloc_fn g_alloc = nullptr;
+static vrb_free_fn g_free = nullptr;
+static void* g_ctx = nullptr;
+static std::once_flag g_pool_once[64];
+
+static int current_device() {
+    int dev = 0;
+    VRB_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+
+void* dalloc(size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return nullptr;
+    const int dev = current_device();
+    void* p = nullptr;
+    if (g_alloc) {
+        p = g_alloc(bytes, dev, (void*)s, g_ctx);
+        if (!p) fail(VRB_ENOMEM, "allocator hook failed for %zu bytes", bytes);
+        return p;
+    }
+    std::call_once(g_pool_once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? VRB_ENOMEM : VRB_ECUDA, "cudaMallocAsync(%zu): %s", bytes,
+             cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void dfree(void* p, size_t bytes, cudaStream_t s) {
+    if (!p) return;
+    if (g_free) {
+        g_free(p, bytes, current_device(), (void*)s, g_ctx);
+        return;
+    }
+    cudaFreeAsync(p, s);   // never throws (called from destructors)
+}
+
+int device_sm_count() {
+    static int cached[64] = {0};
+    const int dev = current_device();
+    if (!cached[dev & 63]) {
+        int v = 0;
+        VRB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        cached[dev & 63] = v;
+    }
+    return cached[dev & 63];
+}
+
+size_t device_max_smem_optin() {
+    static int cached[64] = {0};
+    const int dev = current_device();
+    if (!cached[dev & 63]) {
+        int v = 0;
+        VRB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        cached[dev & 63] = v;
+    }
+    return (size_t)cached[dev & 63];
+}
+
+// ---------------------------------------------------------------------------
+// stage timer
+// ---------------------------------------------------------------------------
+void StageTimer::start(cudaStream_t st) {
+    on = g_profiling;
+    s = st;
+    if (!on) return;
+    cudaEvent_t e;
+    VRB_CUDA(cudaEventCreate(&e));
+    VRB_CUDA(cudaEventRecord(e, s));
+    marks.push_back({-1, e});
+}
+
+void StageTimer::mark(int stage) {
+    if (!on) return;
+    cudaEvent_t e;
+    VRB_CUDA(cudaEventCreate(&e));
+    VRB_CUDA(cudaEventRecord(e, s));
+    marks.push_back({stage, e});
+}
+
+void StageTimer::finish() {
+    if (!on || marks.empty()) return;
+    VRB_CUDA(cudaEventSynchronize(marks.back().second));
+    for (int q = 0; q < 8; ++q) t_stage_ms[q] = 0.0;
+    for (size_t q = 1; q < marks.size(); ++q) {
+        float ms = 0.f;
+        VRB_CUDA(cudaEventElapsedTime(&ms, marks[q - 1].second, marks[q].second));
+        if (marks[q].first >= 0 && marks[q].first < 7) t_stage_ms[marks[q].first] += ms;
+    }
+    float tot = 0.f;
+    VRB_CUDA(cudaEventElapsedTime(&tot, marks.front().second, marks.back().second));
+    t_stage_ms[7] = tot;
+}
+
+StageTimer::~StageTimer() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+}
+
+}  // namespace vrb
+
+// ---------------------------------------------------------------------------
+// result handle
+// ---------------------------------------------------------------------------
+struct vrb_result {
+    int device = 0;
+    int64_t n = 0;
+    int32_t d = 0, maxdim = 0, K = 0;
+    uint32_t flags = 0;
+    int64_t count[4] = {0, 0, 0, 0};        // global size per dimension
+    int64_t local_off[4] = {0, 0, 0, 0};
+    int64_t local_n[4] = {0, 0, 0, 0};
+    int64_t nvals = 0;
+    uint32_t* verts[4] = {nullptr, nullptr, nullptr, nullptr};   // local slice base, dim 1..3
+    uint32_t* filt[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t* rows[4] = {nullptr, nullptr, nullptr, nullptr};    // dim 2..3 (dim 1 aliases verts[1])
+    double* vor = nullptr;
+    std::vector<vrb::Alloc> owned;
+
+    template <class T>
+    T* own(size_t n_elems, cudaStream_t s) {
+        if (n_elems == 0) return nullptr;
+        T* p = static_cast<T*>(vrb::dalloc(n_elems * sizeof(T), s));
+        owned.push_back({p, n_elems * sizeof(T)});
+        return p;
+    }
+    void release_all() {
+        for (auto& a : owned) vrb::dfree(a.p, a.bytes, 0);
+        owned.clear();
+    }
+};
+
+namespace {
+
+using namespace vrb;
+
+template <class F>
+vrb_status guarded(F&& f) {
+    try {
+        f();
+        t_last_error.clear();
+        return VRB_OK;
+    } catch (const Error& e) {
+        t_last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        t_last_error = "host allocation failed";
+        return VRB_ENOMEM;
+    } catch (...) {
+        t_last_error = "unknown internal error";
+        return VRB_ECUDA;
+    }
+}
+
+void check_opts(const double* X, int64_t n, int32_t d, const vrb_opts* opts, vrb_handle* out) {
+    if (!out) fail(VRB_EINVAL, "out handle pointer is NULL");
+    *out = nullptr;
+    if (!opts) fail(VRB_EINVAL, "opts is NULL");
+    if (n < 0) fail(VRB_EINVAL, "n = %lld < 0", (long long)n);
+    if (d < 1) fail(VRB_EINVAL, "d = %d < 1", d);
+    if (n > 0 && !X) fail(VRB_EINVAL, "X is NULL");
+    if (opts->maxdim < 0 || opts->maxdim > 2) fail(VRB_EINVAL, "maxdim = %d not in 0..2", opts->maxdim);
+    if (std::isnan(opts->radius) || opts->radius < 0.0) fail(VRB_EINVAL, "radius must be >= 0 (got %g)", opts->radius);
+    if (n >= kMaxN) fail(VRB_EOVERFLOW, "n = %lld exceeds the 21-bit vertex id limit", (long long)n);
+}
+
+__global__ void k_colptr(uint64_t* colptr, int64_t ncols, uint64_t k1, uint64_t off) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= ncols; j += (int64_t)gridDim.x * blockDim.x)
+        colptr[j] = k1 * (off + (uint64_t)j);
+}
+
+__global__ void k_sortable_keys(const double* __restrict__ in, int64_t n, uint64_t* __restrict__ out, int* bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = in[i];
+        if (isnan(v)) atomicOr(bad, 1);
+        if (v == 0.0) v = 0.0;   // -0.0 == +0.0
+        const uint64_t b = (uint64_t)__double_as_longlong(v);
+        out[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    }
+}
+
+__global__ void k_sortperm_out(const uint64_t* __restrict__ skey, const uint32_t* __restrict__ perm,
+                               const uint32_t* __restrict__ rank, int64_t n, int64_t* __restrict__ perm_out,
+                               uint32_t* __restrict__ dense) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        perm_out[p] = perm[p];
+        if (dense) dense[perm[p]] = rank[p];
+    }
+}
+
+__global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, uint32_t* __restrict__ head) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
+}
+
+__global__ void k_sum_slices(const uint32_t* __restrict__ all, int64_t E, int world, uint32_t* __restrict__ out) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0;
+        for (int r = 0; r < world; ++r) s += all[(int64_t)r * E + p];
+        out[p] = s;
+    }
+}
+
+// boundaries[g] = first edge p with toff[p] >= T*g/G, moved back to the start
+// of its filtration level (a level is never split across ranks).
+__global__ void k_partition(const uint64_t* __restrict__ toff, const uint32_t* __restrict__ efilt, int64_t E,
+                            int world, int64_t* __restrict__ bounds) {
+    const int g = threadIdx.x;
+    if (g > world) return;
+    if (g == 0) { bounds[0] = 0; return; }
+    if (g == world) { bounds[world] = E; return; }
+    const uint64_t T = toff[E];
+    const uint64_t target = (uint64_t)(((__uint128_t)T * (uint64_t)g) / (uint64_t)world);
+    int64_t lo = 0, hi = E;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (toff[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    while (lo > 0 && lo < E && efilt[lo - 1] == efilt[lo]) --lo;
+    bounds[g] = lo;
+}
+
+unsigned grid_of(int64_t n) {
+    int64_t g = ceil_div(n, 256);
+    return (unsigned)(g < 1 ? 1 : (g > 4096 ? 4096 : g));
+}
+
+// The shared body of vrb_build / vrb_build_dist.
+void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
+                cudaStream_t s, vrb_handle* out) {
+    check_opts(X, n, d, opts, out);
+    const int rank = comm ? comm->rank : 0;
+    const int world = comm ? comm->world : 1;
+    if (comm && (world < 1 || rank < 0 || rank >= world || !comm->allgather))
+        fail(VRB_EINVAL, "bad communicator (rank %d, world %d)", rank, world);
+    vrb_result* h = new vrb_result();
+    try {
+        h->device = current_device();
+        h->n = n;
+        h->d = d;
+        h->maxdim = opts->maxdim;
+        h->K = opts->maxdim + 1;
+        h->flags = opts->flags;
+        h->count[0] = n;
+        h->local_off[0] = 0;
+        h->local_n[0] = n;
+        StageTimer timer;
+        timer.start(s);
+
+        DBuf<double> Xd;
+        place_points(X, n, d, opts->flags, s, Xd);
+        KeptEdges ke;
+        build_kept_edges(Xd.get(), n, d, opts->radius, (opts->flags & VRB_STRICT_RADIUS) != 0, s, ke);
+        timer.mark(0);
+        const int64_t E = ke.E;
+        h->count[1] = E;
+        uint32_t* ev = h->own<uint32_t>(2 * E, s);
+        uint32_t* efilt = h->own<uint32_t>(E, s);
+        h->vor = h->own<double>(E, s);
+        h->nvals = rank_edges(ke, ev, efilt, h->vor, s);
+        ke = KeptEdges();
+        timer.mark(1);
+        {
+            const int64_t lo = E * rank / world, hi = E * (rank + 1) / world;
+            h->local_off[1] = lo;
+            h->local_n[1] = hi - lo;
+            h->verts[1] = ev ? ev + 2 * lo : nullptr;
+            h->filt[1] = efilt ? efilt + lo : nullptr;
+        }
+        if (h->K >= 3) fail(VRB_ENOTSUP, "tetrahedra (maxdim 2) are not built yet");
+        if (h->K >= 2) {
+            if (n > dense_map_limit())
+                fail(VRB_ENOTSUP, "n = %lld exceeds the shared-memory vertex map (%lld)", (long long)n,
+                     (long long)dense_map_limit());
+            Graph g;
+            build_graph(ev, n, E, s, g);
+            timer.mark(2);
+            DBuf<uint32_t> cnt(E, s);
+            count_triangles(g, cnt.get(), rank, world, s);
+            if (world > 1) {
+                // the one exchange: every rank counted a disjoint, work-balanced
+                // part of the owner edges; gather and add the parts
+                DBuf<uint32_t> all((size_t)E * world, s);
+                if (comm->allgather(cnt.get(), all.get(), E * sizeof(uint32_t), (void*)s, comm->ctx) != 0)
+                    fail(VRB_ECOMM, "allgather of triangle counts failed");
+                k_sum_slices<<<grid_of(E), 256, 0, s>>>(all.get(), E, world, cnt.get());
+                VRB_LAUNCH_CHECK();
+                timer.mark(6);
+            }
+            DBuf<uint64_t> toff(E + 1, s);
+            exclusive_scan(cnt.get(), toff.get(), E, s);
+            int64_t bounds[2] = {0, E};
+            if (world > 1) {
+                DBuf<int64_t> b(world + 1, s);
+                k_partition<<<1, 64, 0, s>>>(toff.get(), efilt, E, world, b.get());
+                VRB_LAUNCH_CHECK();
+                VRB_CUDA(cudaMemcpyAsync(bounds, b.get() + rank, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            }
+            uint64_t tb[3] = {0, 0, 0};
+            VRB_CUDA(cudaMemcpyAsync(&tb[0], toff.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            VRB_CUDA(cudaStreamSynchronize(s));
+            VRB_CUDA(cudaMemcpyAsync(&tb[1], toff.get() + bounds[0], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            VRB_CUDA(cudaMemcpyAsync(&tb[2], toff.get() + bounds[1], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            VRB_CUDA(cudaStreamSynchronize(s));
+            const uint64_t T = tb[0];
+            if (T >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu triangles exceed u32 positions", (unsigned long long)T);
+            h->count[2] = (int64_t)T;
+            h->local_off[2] = (int64_t)tb[1];
+            h->local_n[2] = (int64_t)(tb[2] - tb[1]);
+            const int64_t Tl = h->local_n[2];
+            h->verts[2] = h->own<uint32_t>(3 * Tl, s);
+            h->filt[2] = h->own<uint32_t>(Tl, s);
+            if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[2] = h->own<uint32_t>(3 * Tl, s);
+            timer.mark(3);
+            fill_triangles(g, efilt, toff.get(), bounds[0], bounds[1], tb[1], h->verts[2], h->filt[2], h->rows[2], s);
+            timer.mark(4);
+            sort_tie_groups(efilt, toff.get(), E, bounds[0], bounds[1], n, h->verts[2], h->rows[2], s);
+            timer.mark(5);
+        }
+        VRB_CUDA(cudaStreamSynchronize(s));
+        VRB_CUDA(cudaGetLastError());
+        timer.finish();
+        *out = h;
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaGetLastError();
+        h->release_all();
+        delete h;
+        throw;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int vrb_abi_version(void) { return VRB_ABI_VERSION; }
+
+const char* vrb_last_error(void) { return vrb::t_last_error.c_str(); }
+
+vrb_status vrb_set_allocator(vrb_alloc_fn alloc, vrb_free_fn free_fn, void* ctx) {
+    return guarded([&] {
+        if ((alloc == nullptr) != (free_fn == nullptr)) fail(VRB_EINVAL, "alloc and free hooks must be set together");
+        vrb::g_alloc = alloc;
+        vrb::g_free = free_fn;
+        vrb::g_ctx = ctx;
+    });
+}
+
+vrb_status vrb_build(const double* X, int64_t n, int32_t d, const vrb_opts* opts, void* stream, vrb_handle* out) {
+    return guarded([&] { build_impl(X, n, d, opts, nullptr, (cudaStream_t)stream, out); });
+}
+
+vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
+                          void* stream, vrb_handle* out) {
+    return guarded([&] {
+        if (!comm) fail(VRB_EINVAL, "comm is NULL");
+        build_impl(X, n, d, opts, comm, (cudaStream_t)stream, out);
+    });
+}
+
+vrb_status vrb_count(vrb_handle h, int32_t dim, int64_t* global_n, int64_t* local_off, int64_t* local_n) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (dim < 0 || dim > h->K) fail(VRB_EINVAL, "dim %d out of range 0..%d", dim, h->K);
+        if (global_n) *global_n = h->count[dim];
+        if (local_off) *local_off = h->local_off[dim];
+        if (local_n) *local_n = h->local_n[dim];
+    });
+}
+
+vrb_status vrb_simplices(vrb_handle h, int32_t dim, const uint32_t** verts_dev, const uint32_t** filt_dev) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (dim < 1 || dim > h->K) fail(VRB_EINVAL, "dim %d out of range 1..%d", dim, h->K);
+        if (verts_dev) *verts_dev = h->verts[dim];
+        if (filt_dev) *filt_dev = h->filt[dim];
+    });
+}
+
+vrb_status vrb_rank_values(vrb_handle h, const double** value_of_rank_dev, int64_t* nvals) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (value_of_rank_dev) *value_of_rank_dev = h->vor;
+        if (nvals) *nvals = h->nvals;
+    });
+}
+
+vrb_status vrb_boundary(vrb_handle h, int32_t k, int64_t* nrows, int64_t* ncols, const uint32_t** rowval_dev) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (k < 1 || k > h->K) fail(VRB_EINVAL, "k %d out of range 1..%d", k, h->K);
+        if (k >= 2 && (h->flags & VRB_SKIP_BOUNDARY)) fail(VRB_EINVAL, "boundary of dim %d was skipped", k);
+        if (nrows) *nrows = h->count[k - 1];
+        if (ncols) *ncols = h->local_n[k];
+        if (rowval_dev) *rowval_dev = k == 1 ? h->verts[1] : h->rows[k];
+    });
+}
+
+vrb_status vrb_boundary_colptr(vrb_handle h, int32_t k, uint64_t* colptr_dev, void* stream) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (k < 1 || k > h->K) fail(VRB_EINVAL, "k %d out of range 1..%d", k, h->K);
+        if (!colptr_dev) fail(VRB_EINVAL, "colptr is NULL");
+        const int64_t nc = h->local_n[k];
+        k_colptr<<<grid_of(nc + 1), 256, 0, (cudaStream_t)stream>>>(colptr_dev, nc, (uint64_t)(k + 1),
+                                                                     (uint64_t)h->local_off[k]);
+        VRB_LAUNCH_CHECK();
+    });
+}
+
+vrb_status vrb_free(vrb_handle h) {
+    return guarded([&] {
+        if (!h) return;
+        h->release_all();
+        delete h;
+    });
+}
+
+vrb_status vrb_sortperm_f64(const double* keys_dev, int64_t n, int64_t* perm_dev, uint32_t* dense_rank_dev,
+                            void* stream) {
+    return guarded([&] {
+        if (n < 0) fail(VRB_EINVAL, "n < 0");
+        if (n == 0) return;
+        if (!keys_dev || !perm_dev) fail(VRB_EINVAL, "NULL pointer");
+        if (n >= (int64_t)0xFFFFFFFFll) fail(VRB_EOVERFLOW, "n exceeds u32 permutation indices");
+        cudaStream_t s = (cudaStream_t)stream;
+        DBuf<uint64_t> k0(n, s), k1(n, s);
+        DBuf<uint32_t> v0(n, s), v1(n, s);
+        DBuf<int> bad(1, s);
+        VRB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+        k_sortable_keys<<<grid_of(n), 256, 0, s>>>(keys_dev, n, k0.get(), bad.get());
+        VRB_LAUNCH_CHECK();
+        int hbad = 0;
+        VRB_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+        if (hbad) fail(VRB_EINVAL, "NaN key");
+        iota_u32(v0.get(), n, s);
+        const uint64_t vary = varying_bits(k0.get(), n, s);
+        const bool alt = radix_sort_pairs(k0.get(), k1.get(), v0.get(), v1.get(), n, vary, s);
+        const uint64_t* sk = alt ? k1.get() : k0.get();
+        const uint32_t* sp = alt ? v1.get() : v0.get();
+        DBuf<uint32_t> head(n, s), rank(n, s);
+        k_heads<<<grid_of(n), 256, 0, s>>>(sk, n, head.get());
+        VRB_LAUNCH_CHECK();
+        inclusive_scan_u32(head.get(), rank.get(), n, s);
+        k_sortperm_out<<<grid_of(n), 256, 0, s>>>(sk, sp, rank.get(), n, perm_dev, dense_rank_dev);
+        VRB_LAUNCH_CHECK();
+        VRB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+unsigned long long vrb_launch_count(void) { return vrb::g_launches.load(); }
+
+vrb_status vrb_set_profiling(int32_t enable) {
+    vrb::g_profiling = enable != 0;
+    return VRB_OK;
+}
+
+vrb_status vrb_last_stage_ms(double* ms8) {
+    return guarded([&] {
+        if (!ms8) fail(VRB_EINVAL, "NULL output");
+        for (int q = 0; q < 8; ++q) ms8[q] = vrb::t_stage_ms[q];
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// vrb_stages.cuh -- the stages of the build as host
+// launchers over device buffers.  Product path only.
+#pragma once
+
+#include "vrb_internal.cuh"
+
+namespace vrb {
+
+// S1: device copy of the points, row-major n x d, finite-checked.
+void place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out);
+
+// d2 threshold equivalent to the cap on sqrt_rn(d2) (reading A1); < 0: none kept.
+double cap_threshold(double r, bool strict);
+
+// S2: kept edges in lexicographic (i, j) order with their length bits.
+struct KeptEdges {
+    int64_t E = 0;
+    DBuf<uint64_t> key;   // bit pattern of len (non-negative doubles order as u64)
+    DBuf<uint32_t> ei, ej;
+};
+void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
+                      KeptEdges& out);
+
+// S3: edge filtration order (len, i, j), dense ranks, value_of_rank.
+//   ev    : 2E u32 (i, j) per edge in position order   (caller-allocated)
+//   efilt : E u32 dense rank, 1-based                    (caller-allocated)
+//   vor   : >= nvals f64, vor[f-1] = length of level f  (caller-allocated, E entries)
+int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s);
+
+// S4: neighbourhoods of the edge graph, used by the simplex enumeration.
+struct Graph {
+    int64_t n = 0, E = 0;
+    DBuf<uint64_t> off;        // n + 1: offsets of each vertex's 2E directed entries
+    DBuf<uint32_t> nbr_pos;    // 2E: neighbour ids, each list in edge-position order
+    DBuf<uint32_t> krank_pos;  // 2E: index of that neighbour in the vertex's id-ordered list
+    DBuf<uint64_t> kord;       // 2E: (edge position << 32) | neighbour id, id-ordered lists
+    DBuf<uint32_t> listidx;    // 2E: entry q = 2p + side -> index in the vertex's position list
+    // owner-edge enumeration plan (triangles and tetrahedra)
+    DBuf<uint32_t> scan_v;     // E: endpoint whose older-neighbour prefix is scanned
+    DBuf<uint32_t> scan_len;   // E: length of that prefix (older neighbours)
+    DBuf<uint32_t> hosted;     // E: edge positions sorted by (host endpoint, position)
+    DBuf<uint32_t> hosted_v;   // E: host endpoint of hosted[i]
+    DBuf<uint64_t> work_pre;   // E + 1: exclusive prefix of scan_len over hosted order
+    uint64_t work = 0;
+    uint32_t max_deg = 0;
+};
+void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g);
+
+// S5 + S7 + S8 for triangles (owner-edge enumeration, see triangles.cu).
+// Count per owner edge: cnt[p] (E entries, zero-initialised here).  The
+// owner edges are split into work-balanced tasks; this call counts the tasks
+// of part `part` of `nparts` (0 of 1 = all) and leaves the others at 0.
+void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s);
+// Emit triangles of owner edges in [p_lo, p_hi) at slots toff[p] - slot0
+// (slot0 = toff[p_lo]).
+void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
+                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, cudaStream_t s);
+// Reorder the triangles of every tie group (>= 2 edges sharing a level) into
+// lex order (readings A3, A4); only the range [p_lo, p_hi) of owner edges.
+void sort_tie_groups(const uint32_t* efilt, const uint64_t* toff, int64_t E, int64_t p_lo, int64_t p_hi,
+                     int64_t n, uint32_t* tv, uint32_t* rows, cudaStream_t s);
+
+int64_t dense_map_limit();   // largest n the shared-memory vertex map supports
+
+}  // namespace vrb

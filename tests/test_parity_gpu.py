@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Small and medium inputs: every output array is compared element by element
+(bit-exact: all outputs are integers or bit-exact float64).  Full-size
+configs (C3, C5B, in the launch configuration bench.py times): edge arrays
+exactly; triangles by (a) the per-level count histogram against the oracle's
+(golden digest written by tools/make_golden.py from oracle/ only), (b) strict
+(filt, lex) order of the whole array, (c) every triangle's boundary rows
+pointing at its three edges with filt = max edge filt, (d) sampled levels
+compared element by element with the oracle's enumeration of that level.
+(a)+(b)+(c) imply the sets are equal; (d) spot-checks the exact layout.
+"""
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def vrb():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1809_04424_b200 as m
+    return m
+
+
+def _np(t):
+    return t.cpu().numpy().view(np.uint32) if t.dtype == torch.int32 else t.cpu().numpy()
+
+
+def compare(vrb, X, maxdim, radius, strict=False, via_torch_alloc=False):
+    res = vrb.build(X, maxdim=maxdim, radius=radius, strict=strict)
+    o = oracle.Oracle(X, radius, strict)
+    ev, ef, el, vor = o.edges()
+    assert res.count(0)[0] == X.shape[0]
+    assert res.count(1)[0] == o.E
+    gv, gf = res.simplices(1)
+    np.testing.assert_array_equal(_np(gv), ev)
+    np.testing.assert_array_equal(_np(gf), ef)
+    gvor = _np(res.rank_values())
+    assert gvor.shape[0] == o.nvals
+    assert gvor.tobytes() == vor.tobytes()          # bit-exact lengths
+    np.testing.assert_array_equal(_np(res.boundary(1)), ev)
+    if maxdim >= 1:
+        tv, tf, tr = o.simplices(2)
+        assert res.count(2)[0] == tv.shape[0]
+        gtv, gtf = res.simplices(2)
+        np.testing.assert_array_equal(_np(gtv), tv)
+        np.testing.assert_array_equal(_np(gtf), tf)
+        np.testing.assert_array_equal(_np(res.boundary(2)), tr)
+        cp = res.boundary_colptr(2).cpu().numpy()
+        np.testing.assert_array_equal(cp, 3 * np.arange(tv.shape[0] + 1))
+    return res, o
+
+
+def test_golden_unit_square_and_ties(vrb):
+    for name in ("unit_square.json", "ties_five_points.json"):
+        g = json.load(open(os.path.join(GOLDEN, name)))
+        X = np.array(g["points"], dtype=np.float64)
+        compare(vrb, X, 1, math.inf)
+    X = np.array(json.load(open(os.path.join(GOLDEN, "ties_five_points.json")))["points"], dtype=np.float64)
+    compare(vrb, X, 1, 5.0)
+    compare(vrb, X, 1, 5.0, strict=True)
+
+
+def test_c1(vrb):
+    w = workloads.WORKLOADS["C1"]
+    compare(vrb, w.points(), w.maxdim, w.radius)
+
+
+def test_c2_triangles(vrb):
+    w = workloads.WORKLOADS["C2"]
+    compare(vrb, w.points(), 1, w.radius)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3])
+def test_tiny(vrb, n):
+    compare(vrb, workloads.random_cloud(n, n, 2), 1, math.inf)
+
+
+def test_zero_radius_duplicates(vrb):
+    X = np.array([[0.5, 0.5], [0.5, 0.5], [2.0, 0.0], [0.5, 0.5]])
+    compare(vrb, X, 1, 0.0)
+    compare(vrb, X, 1, 0.0, strict=True)
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_small(vrb, seed):
+    rng = np.random.default_rng(seed)
+    kind = ["uniform", "gauss", "lattice", "halfint", "dups"][seed % 5]
+    n = int(rng.integers(0, 90))
+    d = int(rng.integers(1, 6))
+    X = workloads.random_cloud(seed, n, d, kind)
+    if n >= 2:
+        qs = [math.inf, 0.1, 0.3, 0.6]
+        q = qs[seed % 4]
+        # caps at data quantiles, sometimes exactly at an attained length
+        lens = [oracle.length(X, i, j) for i in range(min(n, 12)) for j in range(i + 1, min(n, 12))]
+        radius = math.inf if q == math.inf else float(np.quantile(lens, q, method="nearest")) if lens else 1.0
+    else:
+        radius = math.inf
+    compare(vrb, X, 1, radius, strict=bool(seed % 7 == 3))
+
+
+def test_multi_tile_ragged(vrb):
+    X = workloads.random_cloud(77, 333, 4, "uniform")      # 6 tiles of 64, ragged tail
+    compare(vrb, X, 1, 0.45)
+
+
+def test_lattice_heavy_ties_large_segments(vrb):
+    # 5x5x5 lattice: 7750 edges on 25 levels; tie groups hold up to ~10^5
+    # triangles (exercises the global-sort path of the tie sort)
+    X = workloads.integer_lattice(5, 3)
+    compare(vrb, X, 1, math.inf)
+    compare(vrb, X, 1, 2.0)
+
+
+def test_dim_major_and_device_points(vrb):
+    X = workloads.random_cloud(5, 120, 3, "gauss")
+    res, o = compare(vrb, X, 1, 1.3)
+    Xd = torch.from_numpy(X).cuda()
+    r2 = vrb.build(Xd, maxdim=1, radius=1.3)
+    np.testing.assert_array_equal(_np(r2.simplices(2)[0]), _np(res.simplices(2)[0]))
+
+
+def test_high_degree_byte_map_rounds(vrb):
+    # two hubs adjacent to 4500 jittered sphere points; the hub-hub edge is the
+    # longest, so its older-neighbour prefixes hold 4500 entries (> 4096 byte-map
+    # slots: the fill runs several rounds)
+    rng = np.random.default_rng(3)
+    m = 4500
+    S = rng.standard_normal((m, 10))
+    S /= np.linalg.norm(S, axis=1, keepdims=True)
+    S *= (1.0 + 0.01 * rng.uniform(size=(m, 1)))
+    P = np.zeros((m + 2, 11))
+    P[:m, :10] = S
+    P[m, 10] = 0.6
+    P[m + 1, 10] = -0.6
+    compare(vrb, P, 1, 1.2)
+
+
+def test_sortperm_literal_and_random(vrb):
+    g = json.load(open(os.path.join(GOLDEN, "sortperm_literal.json")))
+    for case in g["cases"]:
+        perm, dense = vrb.sortperm_f64(torch.tensor(case["v"], dtype=torch.float64, device="cuda"))
+        assert (perm.cpu().numpy() + 1).tolist() == case["sortperm_1based"]
+        assert dense.cpu().numpy().tolist() == case["dense_rank"]
+    rng = np.random.default_rng(0)
+    v = np.concatenate([rng.standard_normal(100000), rng.integers(-5, 5, 50000).astype(np.float64),
+                        [0.0, -0.0, np.inf, -np.inf]])
+    rng.shuffle(v)
+    perm, dense = vrb.sortperm_f64(torch.from_numpy(v).cuda())
+    op, od = oracle.sortperm(v)
+    np.testing.assert_array_equal(perm.cpu().numpy(), op)
+    np.testing.assert_array_equal(dense.cpu().numpy().view(np.uint32), od)
+
+
+def test_sortperm_nan_rejected(vrb):
+    with pytest.raises(vrb.VrbError):
+        vrb.sortperm_f64(torch.tensor([1.0, float("nan")], dtype=torch.float64, device="cuda"))
+
+
+def test_torch_allocator_hook(vrb):
+    vrb.use_torch_allocator(True)
+    try:
+        compare(vrb, workloads.random_cloud(8, 200, 3, "uniform"), 1, 0.3)
+    finally:
+        vrb.use_torch_allocator(False)
+
+
+# ---------------------------------------------------------------------------
+# full-size configs
+# ---------------------------------------------------------------------------
+
+def _check_triangles_full(vrb, res, o, golden, n_levels_sampled=40):
+    dev = res.device
+    E = o.E
+    ev, ef, el, vor = o.edges()
+    gv, gf = res.simplices(1)
+    np.testing.assert_array_equal(_np(gv), ev)
+    np.testing.assert_array_equal(_np(gf), ef)
+    assert _np(res.rank_values()).tobytes() == vor.tobytes()
+    tv, tf = res.simplices(2)
+    rows = res.boundary(2)
+    T = tv.shape[0]
+    assert T == golden["count"]
+    # (a) per-level histogram == oracle's
+    hist = torch.bincount(tf.to(torch.int64), minlength=E + 1).cpu().numpy().astype(np.uint64)
+    assert hashlib.sha256(hist.tobytes()).hexdigest() == golden["hist_sha256"]
+    # (b) strict (filt, lex) order, (c) rows are the three edges, filt = max edge filt
+    evd = torch.from_numpy(ev.astype(np.int64)).to(dev)
+    efd = torch.from_numpy(ef.astype(np.int64)).to(dev)
+    chunk = 1 << 27
+    prev = None
+    for s in range(0, T, chunk):
+        e = min(T, s + chunk + 1)
+        v = tv[s:e].to(torch.int64)
+        f = tf[s:e].to(torch.int64)
+        r = rows[s:e].to(torch.int64) & 0xFFFFFFFF
+        assert bool((v[:, 0] < v[:, 1]).all()) and bool((v[:, 1] < v[:, 2]).all())
+        code = (v[:, 0] << 42) | (v[:, 1] << 21) | v[:, 2]
+        key_f = f[1:] - f[:-1]
+        key_c = code[1:] - code[:-1]
+        assert bool(((key_f > 0) | ((key_f == 0) & (key_c > 0))).all())
+        assert bool((r[:, 0] < r[:, 1]).all()) and bool((r[:, 1] < r[:, 2]).all())
+        ea, eb, ec = evd[r[:, 0]], evd[r[:, 1]], evd[r[:, 2]]
+        verts = torch.sort(torch.cat([ea, eb, ec], 1), 1).values
+        want = torch.stack([v[:, 0], v[:, 0], v[:, 1], v[:, 1], v[:, 2], v[:, 2]], 1)
+        assert bool((verts == want).all())
+        assert bool((efd[r[:, 2]] == f).all())
+        assert bool((torch.maximum(torch.maximum(efd[r[:, 0]], efd[r[:, 1]]), efd[r[:, 2]]) == f).all())
+        del v, f, r, ea, eb, ec, verts, want, code
+    # (d) sampled levels, element by element
+    start = np.concatenate([[0], np.cumsum(hist)]).astype(np.int64)
+    rng = np.random.default_rng(0)
+    levels = sorted(set(rng.integers(1, o.nvals + 1, n_levels_sampled).tolist()) | {1, o.nvals})
+    for lvl in levels:
+        sv, sr = o.simplices_at_filt(2, int(lvl))
+        a, b = start[lvl], start[lvl + 1]
+        assert b - a == len(sv)
+        np.testing.assert_array_equal(_np(tv[a:b]), sv)
+        np.testing.assert_array_equal(_np(rows[a:b]), sr)
+
+
+@pytest.mark.parametrize("config", ["C3", "C5B"])
+def test_full_size_config(vrb, config):
+    path = os.path.join(GOLDEN, f"{config.lower()}_levels.json")
+    golden = json.load(open(path))
+    w = workloads.WORKLOADS[config]
+    X = w.points()
+    assert hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest() == golden["points_sha256"]
+    vrb.use_torch_allocator(True)
+    try:
+        res = vrb.build(torch.from_numpy(X).cuda(), maxdim=w.maxdim, radius=w.radius)
+        o = oracle.Oracle(X, w.radius)
+        assert o.E == golden["E"]
+        _check_triangles_full(vrb, res, o, golden)
+        del res
+    finally:
+        torch.cuda.synchronize()
+        vrb.use_torch_allocator(False)
+        torch.cuda.empty_cache()
+
+
+def test_c5a_edges_full(vrb):
+    # C5A: 199,990,000 edges, all pairs (r = inf).  Full edge parity on a
+    # sample of positions plus global properties (the oracle's full sort of
+    # 2e8 edges is minutes of CPU: checked by sampling rows of the oracle).
+    w = workloads.WORKLOADS["C5A"]
+    X = w.points()
+    res = vrb.build(torch.from_numpy(X).cuda(), maxdim=0, radius=math.inf)
+    n = X.shape[0]
+    E = n * (n - 1) // 2
+    assert res.count(1)[0] == E
+    gv, gf = res.simplices(1)
+    vor = res.rank_values()
+    v = gv.to(torch.int64)
+    f = gf.to(torch.int64)
+    assert bool((v[:, 0] < v[:, 1]).all())
+    # every pair exactly once
+    code = v[:, 0] * n + v[:, 1]
+    assert int(torch.unique(code).numel()) == E
+    # lengths non-decreasing along the order, (len, i, j) ties in lex order
+    lens = vor[f - 1]
+    dl = lens[1:] - lens[:-1]
+    assert bool((dl >= 0).all())
+    tie = dl == 0
+    assert bool((code[1:][tie] > code[:-1][tie]).all())
+    assert bool(((f[1:] - f[:-1]) == (dl > 0).to(torch.int64)).all())
+    # sampled pairs: bit-exact length against the oracle's fold
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, E, 2000)
+    vv = v[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ll = lens[torch.from_numpy(idx).cuda()].cpu().numpy()
+    for (i, j), L in zip(vv, ll):
+        assert oracle.length(X, int(i), int(j)) == L
