@@ -13,6 +13,8 @@
 // then assigned to the endpoint x with the SHORTER prefix of neighbours older
 // than p (to be scanned) and the other endpoint y (the "host", whose full
 // neighbourhood is held as a dense map in shared memory during enumeration).
+#include <cstdlib>
+
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
 
@@ -59,26 +61,31 @@ __global__ void k_keys_vertex_nbr(const uint32_t* __restrict__ ev, int64_t n2, u
 
 // position-ordered lists: slot s holds entry q = sorted[s]
 __global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
-                            const uint64_t* __restrict__ off, int64_t n2, uint32_t* __restrict__ nbr_pos,
-                            uint32_t* __restrict__ listidx) {
+                            const uint64_t* __restrict__ off, int64_t n2, uint32_t* __restrict__ nkr,
+                            uint32_t* __restrict__ np, uint32_t* __restrict__ listidx) {
     GRID_STRIDE(s, n2) {
         const uint32_t q = sorted[s];
         const uint32_t v = ev[q];
-        nbr_pos[s] = ev[q ^ 1];
+        nkr[s] = ev[q ^ 1];
+        np[s] = q >> 1;
         listidx[q] = (uint32_t)(s - (int64_t)off[v]);
     }
 }
 
-// id-ordered lists: slot s holds entry q = sorted[s]
-__global__ void k_id_lists(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
+// id-ordered lists: slot s holds entry q = sorted[s]; its rank s - off[v] is
+// recorded at the entry's slot of the position-ordered list
+__global__ void k_id_ranks(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
                            const uint64_t* __restrict__ off, const uint32_t* __restrict__ listidx,
-                           int64_t n2, uint64_t* __restrict__ kord, uint32_t* __restrict__ krank_pos) {
+                           int64_t n2, int packed, uint32_t* __restrict__ nkr, uint32_t* __restrict__ nr) {
     GRID_STRIDE(s, n2) {
         const uint32_t q = sorted[s];
-        const uint32_t v = ev[q];
-        const uint64_t o = off[v];
-        kord[s] = ((uint64_t)(q >> 1) << 32) | ev[q ^ 1];
-        krank_pos[o + listidx[q]] = (uint32_t)(s - (int64_t)o);
+        const uint64_t o = off[ev[q]];
+        const uint32_t r = (uint32_t)(s - (int64_t)o);
+        const uint64_t slot = o + listidx[q];
+        if (packed)
+            nkr[slot] |= r << 16;
+        else
+            nr[slot] = r;
     }
 }
 
@@ -91,7 +98,8 @@ __global__ void k_assign(const uint32_t* __restrict__ ev, const uint32_t* __rest
         const bool scan_a = la <= lb;
         scan_v[p] = scan_a ? a : b;
         scan_len[p] = scan_a ? la : lb;
-        host_key[p] = scan_a ? b : a;
+        // sort key: host, then longest prefix first (LPT order inside a host)
+        host_key[p] = ((uint64_t)(scan_a ? b : a) << 32) | (uint32_t)~(scan_a ? la : lb);
     }
 }
 
@@ -99,7 +107,7 @@ __global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_
                               const uint32_t* __restrict__ scan_len, int64_t E,
                               uint32_t* __restrict__ hosted_v, uint32_t* __restrict__ work) {
     GRID_STRIDE(i, E) {
-        hosted_v[i] = (uint32_t)host_key[i];
+        hosted_v[i] = (uint32_t)(host_key[i] >> 32);
         work[i] = scan_len[hosted[i]];
     }
 }
@@ -167,9 +175,14 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         VRB_CUDA(cudaStreamSynchronize(s));
         g.max_deg = h;
     }
-    g.nbr_pos.alloc(n2, s);
-    g.krank_pos.alloc(n2, s);
-    g.kord.alloc(n2, s);
+    // packed (krank << 16 | k) lists when ids and ranks fit 16 bits; the wide
+    // layout can be forced for testing with VRB_FORCE_WIDE_LISTS=1
+    const char* force_wide = std::getenv("VRB_FORCE_WIDE_LISTS");
+    g.packed = n <= 65536 && g.max_deg <= 65536 && !(force_wide && force_wide[0] == '1');
+    // +4 entries: the enumeration kernels read lists in aligned 16-byte groups
+    g.nkr.alloc(n2 + 4, s);
+    if (!g.packed) g.nr.alloc(n2 + 4, s);
+    g.np.alloc(n2 + 4, s);
     g.listidx.alloc(n2, s);
     g.scan_v.alloc(E, s);
     g.scan_len.alloc(E, s);
@@ -188,15 +201,15 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         k_keys_vertex<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
         VRB_LAUNCH_CHECK();
         const uint32_t* sorted = sort_ids(k0, k1, v0, v1, n2, s);
-        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), n2, g.nbr_pos.get(),
+        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
                                                        g.listidx.get());
         VRB_LAUNCH_CHECK();
-        // (b) lists in neighbour-id order: sort entries by (vertex, neighbour)
+        // (b) ranks in neighbour-id order: sort entries by (vertex, neighbour)
         k_keys_vertex_nbr<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
         VRB_LAUNCH_CHECK();
         sorted = sort_ids(k0, k1, v0, v1, n2, s);
-        k_id_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), g.listidx.get(), n2,
-                                                      g.kord.get(), g.krank_pos.get());
+        k_id_ranks<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), g.listidx.get(), n2,
+                                                      g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
         VRB_LAUNCH_CHECK();
     }
     {

@@ -34,24 +34,26 @@
 namespace vrb {
 namespace {
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 16;               // max warps per CTA (fewer when the map is large)
 constexpr int kThreads = kWarps * 32;
-constexpr int kBM = 4096;        // byte-map entries per warp (apex ranks per round)
-constexpr int kU = 4;            // loads in flight per lane in the prefix scan
+constexpr int kBits = 4096;      // apex ranks per round (bitmap bits per warp)
+constexpr int kWords = kBits / 32;
+constexpr int kWin = 512;        // triangles staged per output window
 
 struct TriArgs {
     int64_t n, E;
     const uint64_t* off;
-    const uint32_t* nbr_pos;
-    const uint32_t* krank_pos;
-    const uint64_t* kord;
+    const uint32_t* nkr;     // packed ? (krank << 16 | k) : k, position-ordered lists
+    const uint32_t* nr;      // krank when !packed
+    const uint32_t* np;      // edge position of each list entry
+    int packed;
     const uint32_t* scan_v;
     const uint32_t* scan_len;
     const uint32_t* hosted;
     const uint32_t* hosted_v;
     const uint64_t* work_pre;
     uint64_t chunk;
-    int64_t ntasks;          // tasks of the whole work
+    int64_t ntasks;             // tasks of the whole work
     int64_t task_lo, task_hi;   // this launch's task range
     unsigned long long* task_counter;
     // count
@@ -89,117 +91,297 @@ __device__ __forceinline__ void sort3(uint32_t& a, uint32_t& b, uint32_t& c) {
     if (a > b) { t = a; a = b; b = t; }
 }
 
+// Prefix streaming: lane-owned 16-byte aligned groups of 4 consecutive list
+// entries.  `mis` = entries before the list start inside the first group.
+// Entry e of group i is list index t = 4 i + e - mis (valid iff 0 <= t < len).
+__device__ __forceinline__ const uint4* aligned_groups(const uint32_t* lst, int& mis) {
+    mis = (int)((reinterpret_cast<uintptr_t>(lst) >> 2) & 3);
+    return reinterpret_cast<const uint4*>(lst - mis);
+}
+
+__device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
+    return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
+}
+
 // Warp: count apexes of owner edge p (host y's map in smem).
 __device__ __forceinline__ uint32_t warp_count(const TriArgs& A, const uint32_t* __restrict__ map,
                                                uint32_t p, uint32_t x, uint32_t len) {
     const int lane = threadIdx.x & 31;
-    const uint32_t* __restrict__ lst = A.nbr_pos + A.off[x];
+    int mis;
+    const uint4* g = aligned_groups(A.nkr + A.off[x], mis);
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    const int ngroups = (int)((len + mis + 3) >> 2);
     uint32_t c = 0;
-    for (uint32_t t0 = 0; t0 < len; t0 += 32 * kU) {
-        uint32_t k[kU];
+    for (int i0 = 0; i0 < ngroups; i0 += 64) {
+        uint4 q[2];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint32_t t = t0 + u * 32 + lane;
-            k[u] = t < len ? __ldg(lst + t) : NONE32;
+        for (int u = 0; u < 2; ++u) {
+            const int i = i0 + u * 32 + lane;
+            q[u] = i < ngroups ? __ldg(g + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < kU; ++u) c += (k[u] != NONE32 && map[k[u]] < p) ? 1u : 0u;
+        for (int u = 0; u < 2; ++u) {
+            const int i = i0 + u * 32 + lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int t = 4 * i + e - mis;
+                if (t >= 0 && t < (int)len && map[pick(q[u], e) & kmask] < p) ++c;
+            }
+        }
     }
     return __reduce_add_sync(0xffffffffu, c);
 }
 
-// Warp: emit the triangles of owner edge p in apex-id order.
+// Per-warp shared scratch of the fill kernel.
+struct WarpScratch {
+    uint8_t flag[kBits];     // valid apexes of this round, by rank in x's id-ordered list (0/1)
+    uint32_t bits[kWords];   // the same as a bitmap
+    uint32_t wpre[kWords];   // exclusive prefix popcount per bitmap word
+    uint32_t rec[kWin];      // staged window: apex k (low 16 bits) | prefix index t (high 16 bits)
+};
+
+// Warp: emit the triangles of owner edge p = (y, x) in apex-id order.
+//  mark    : stream x's older-neighbour prefix; for every apex k with
+//            pos_y[k] < p set flag[krank(k)] = 1 (krank = rank of k in x's
+//            id-ordered list; plain byte stores, lanes never collide)
+//  bitmap  : 16-byte reads of the flags -> 16-bit masks (multiply bit-gather),
+//            flags cleared on the way; exclusive prefix popcount per word
+//  emit    : stream the prefix again; a valid apex's output slot is
+//            prefix(word) + popc(word below its bit); stage (k, t) at that slot
+//            of the current window
+//  flush   : one lane per triangle of the window: vertices sort3(y, x, k),
+//            rows (min, max)(pos(x,k), pos(y,k)), p, filt -- streaming stores
+// Only the packed layout (n, deg <= 65536) is handled here; the caller picks
+// warp_fill_wide otherwise.
 __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __restrict__ map,
-                                          uint8_t* __restrict__ bm, uint32_t& stamp, uint32_t p,
-                                          uint32_t y, uint32_t x, uint32_t len) {
+                                          WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                          uint32_t len) {
     const int lane = threadIdx.x & 31;
     const uint64_t offx = A.off[x];
     const uint32_t degx = (uint32_t)(A.off[x + 1] - offx);
-    const uint32_t* __restrict__ lst = A.nbr_pos + offx;
-    const uint32_t* __restrict__ krk = A.krank_pos + offx;
-    const uint64_t* __restrict__ kord = A.kord + offx;
+    int mis;
+    const uint4* gk = aligned_groups(A.nkr + offx, mis);
+    const uint32_t* __restrict__ npx = A.np + offx;
+    const int ngroups = (int)((len + mis + 3) >> 2);
     const uint32_t filt = A.efilt[p];
     uint64_t slot = A.toff[p] - A.slot0;
-    for (uint32_t R = 0; R < degx; R += kBM) {
-        if (++stamp == 256) {     // wrap: clear this warp's byte map
-            for (int q = lane; q < kBM / 4; q += 32) reinterpret_cast<uint32_t*>(bm)[q] = 0u;
-            stamp = 1;
-            __syncwarp();
-        }
-        const uint8_t st = (uint8_t)stamp;
-        // mark valid apexes by their rank in x's id-ordered list
-        for (uint32_t t0 = 0; t0 < len; t0 += 32 * kU) {
-            uint32_t k[kU], r[kU];
+    for (uint32_t R = 0; R < degx; R += kBits) {
+        const uint32_t lim = min((uint32_t)kBits, degx - R);
+        // ---- mark
+        for (int i0 = 0; i0 < ngroups; i0 += 64) {
+            uint4 q[2];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const uint32_t t = t0 + u * 32 + lane;
-                k[u] = t < len ? __ldg(lst + t) : NONE32;
-                r[u] = t < len ? __ldg(krk + t) : NONE32;
+            for (int u = 0; u < 2; ++u) {
+                const int i = i0 + 32 * u + lane;
+                q[u] = i < ngroups ? __ldg(gk + i) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
             }
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const uint32_t rr = r[u] - R;
-                if (k[u] != NONE32 && rr < (uint32_t)kBM && map[k[u]] < p) bm[rr] = st;
+            for (int u = 0; u < 2; ++u) {
+                const int i = i0 + 32 * u + lane;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int t = 4 * i + e - mis;
+                    const uint32_t w = pick(q[u], e);
+                    const uint32_t r = (w >> 16) - R;
+                    const bool ok = t >= 0 && t < (int)len && r < (uint32_t)kBits;
+                    if (ok && map[w & 0xFFFFu] < p) W->flag[r] = 1;
+                }
             }
         }
         __syncwarp();
-        // read back in id order and write
-        const uint32_t lim = min((uint32_t)kBM, degx - R);
-        for (uint32_t w0 = 0; w0 < lim; w0 += 128) {
-            const uint32_t idx = w0 + 4 * lane;
-            uint32_t m4 = 0;
-            if (idx < lim) {
-                const uint32_t word = reinterpret_cast<const uint32_t*>(bm)[idx >> 2];
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (((word >> (8 * b)) & 0xFF) == st && idx + b < lim) m4 |= 1u << b;
+        // ---- flags -> bitmap (16 flags per lane per step), clearing the flags
+        const uint32_t lim32 = (lim + 31) & ~31u;   // whole bitmap words (flags past lim are 0)
+        for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
+            const uint32_t b = b0 + 16 * lane;
+            if (b < lim32) {
+                uint4* f = reinterpret_cast<uint4*>(W->flag + b);
+                const uint4 qf = *f;
+                *f = make_uint4(0, 0, 0, 0);
+                const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
+                                     (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
+                reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
             }
-            const uint32_t c = __popc(m4);
-            uint32_t incl = c;
+        }
+        __syncwarp();
+        // ---- exclusive prefix popcount per word (lane owns words 4 lane .. 4 lane + 3)
+        const uint32_t nwords = (lim + 31) >> 5;
+        uint32_t c[4], tot = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t wd = 4 * lane + j;
+            c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
+            tot += c[j];
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { W->wpre[4 * lane + j] = run; run += c[j]; }
+        __syncwarp();
+        // ---- emit + flush, one window of kWin triangles per pass over the prefix
+        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
+            for (int i0 = 0; i0 < ngroups; i0 += 64) {
+                uint4 q[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + 32 * u + lane;
+                    q[u] = i < ngroups ? __ldg(gk + i)
+                                       : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + 32 * u + lane;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int t = 4 * i + e - mis;
+                        const uint32_t w = pick(q[u], e);
+                        const uint32_t k = w & 0xFFFFu;
+                        const uint32_t r = (w >> 16) - R;
+                        const bool ok = t >= 0 && t < (int)len && r < (uint32_t)kBits;
+                        if (ok && map[k] < p) {
+                            const uint32_t pos =
+                                W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
+                            if (pos < (uint32_t)kWin) W->rec[pos] = k | ((uint32_t)t << 16);
+                        }
+                    }
+                }
             }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            uint64_t s = slot + (incl - c);
-            while (m4) {
-                const int b = __ffs(m4) - 1;
-                m4 &= m4 - 1;
-                const uint64_t kp = __ldg(reinterpret_cast<const unsigned long long*>(kord) + R + idx + b);
-                const uint32_t k = (uint32_t)kp;
-                const uint32_t px = (uint32_t)(kp >> 32);
+            __syncwarp();
+            const uint32_t m = min((uint32_t)kWin, count - w0);
+            const uint64_t s0 = slot + w0;
+            for (uint32_t j = lane; j < m; j += 32) {
+                const uint32_t rc = W->rec[j];
+                const uint32_t k = rc & 0xFFFFu;
+                const uint32_t px = __ldg(npx + (rc >> 16));
                 const uint32_t py = map[k];
                 uint32_t a0 = y, a1 = x, a2 = k;
                 sort3(a0, a1, a2);
-                uint32_t* tv = A.tv + 3 * s;
-                tv[0] = a0; tv[1] = a1; tv[2] = a2;
-                A.tf[s] = filt;
+                uint32_t* tv = A.tv + 3 * (s0 + j);
+                __stcs(tv, a0);
+                __stcs(tv + 1, a1);
+                __stcs(tv + 2, a2);
                 if (A.rows) {
-                    uint32_t* rw = A.rows + 3 * s;
-                    rw[0] = min(px, py); rw[1] = max(px, py); rw[2] = p;
+                    uint32_t* rw = A.rows + 3 * (s0 + j);
+                    __stcs(rw, min(px, py));
+                    __stcs(rw + 1, max(px, py));
+                    __stcs(rw + 2, p);
                 }
-                ++s;
+                __stcs(A.tf + s0 + j, filt);
             }
-            slot += total;
+            __syncwarp();
+        }
+        slot += count;
+    }
+}
+
+// The same for the wide layout (separate krank array; any n and degree):
+// simpler, unstaged window loop with 32-bit records.
+__device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t* __restrict__ map,
+                                               WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                               uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t offx = A.off[x];
+    const uint32_t degx = (uint32_t)(A.off[x + 1] - offx);
+    const uint32_t* __restrict__ lk = A.nkr + offx;
+    const uint32_t* __restrict__ lr = A.nr + offx;
+    const uint32_t* __restrict__ npx = A.np + offx;
+    const uint32_t filt = A.efilt[p];
+    uint64_t slot = A.toff[p] - A.slot0;
+    const uint32_t win = kWin / 2;   // rec holds (k, t) as two words
+    for (uint32_t R = 0; R < degx; R += kBits) {
+        const uint32_t lim = min((uint32_t)kBits, degx - R);
+        for (uint32_t t = lane; t < len; t += 32) {
+            const uint32_t r = __ldg(lr + t) - R;
+            if (r < (uint32_t)kBits && map[__ldg(lk + t)] < p) W->flag[r] = 1;
         }
         __syncwarp();
+        const uint32_t lim32 = (lim + 31) & ~31u;
+        for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
+            const uint32_t b = b0 + 16 * lane;
+            if (b < lim32) {
+                uint4* f = reinterpret_cast<uint4*>(W->flag + b);
+                const uint4 qf = *f;
+                *f = make_uint4(0, 0, 0, 0);
+                const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
+                                     (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
+                reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
+            }
+        }
+        __syncwarp();
+        const uint32_t nwords = (lim + 31) >> 5;
+        uint32_t c[4], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t wd = 4 * lane + j;
+            c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
+            tot += c[j];
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { W->wpre[4 * lane + j] = run; run += c[j]; }
+        __syncwarp();
+        for (uint32_t w0 = 0; w0 < count; w0 += win) {
+            for (uint32_t t = lane; t < len; t += 32) {
+                const uint32_t r = __ldg(lr + t) - R;
+                const uint32_t k = __ldg(lk + t);
+                if (r < (uint32_t)kBits && map[k] < p) {
+                    const uint32_t pos = W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
+                    if (pos < win) { W->rec[2 * pos] = k; W->rec[2 * pos + 1] = t; }
+                }
+            }
+            __syncwarp();
+            const uint32_t m = min(win, count - w0);
+            const uint64_t s0 = slot + w0;
+            for (uint32_t j = lane; j < m; j += 32) {
+                const uint32_t k = W->rec[2 * j];
+                const uint32_t px = __ldg(npx + W->rec[2 * j + 1]);
+                const uint32_t py = map[k];
+                uint32_t a0 = y, a1 = x, a2 = k;
+                sort3(a0, a1, a2);
+                uint32_t* tv = A.tv + 3 * (s0 + j);
+                __stcs(tv, a0);
+                __stcs(tv + 1, a1);
+                __stcs(tv + 2, a2);
+                if (A.rows) {
+                    uint32_t* rw = A.rows + 3 * (s0 + j);
+                    __stcs(rw, min(px, py));
+                    __stcs(rw + 1, max(px, py));
+                    __stcs(rw + 2, p);
+                }
+                __stcs(A.tf + s0 + j, filt);
+            }
+            __syncwarp();
+        }
+        slot += count;
     }
 }
 
 template <bool kFill>
-__global__ void __launch_bounds__(kThreads) k_triangles(TriArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
-    uint8_t* bm_all = smem + ((A.n * 4 + 15) / 16) * 16;
+    WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem + ((A.n * 4 + 15) / 16) * 16);
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
+    __shared__ unsigned s_next;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t* bm = bm_all + (size_t)wid * kBM;
-    uint32_t stamp = 0;
-    for (int64_t q = threadIdx.x; q < A.n; q += kThreads) map[q] = NONE32;
-    if (kFill)
-        for (int q = threadIdx.x; q < kWarps * kBM / 4; q += kThreads) reinterpret_cast<uint32_t*>(bm_all)[q] = 0u;
+    const int nthreads = blockDim.x;
+    for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
+    if (kFill)   // the flags are cleared after every use, so they must start at 0
+        for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WarpScratch) / 4); q += nthreads)
+            reinterpret_cast<uint32_t*>(scratch)[q] = 0u;
     __syncthreads();
     for (;;) {
         if (threadIdx.x == 0) {
@@ -223,55 +405,67 @@ __global__ void __launch_bounds__(kThreads) k_triangles(TriArgs A) {
                 const uint32_t y = A.hosted_v[seg];
                 s_y = y;
                 s_end = upper_bound_u32(A.hosted_v, seg, hi, y);
+                s_next = 0;
             }
             __syncthreads();
             const uint32_t y = s_y;
             const int64_t end = s_end;
             const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
-            for (uint64_t t = oy + threadIdx.x; t < oy1; t += kThreads) {
-                const uint64_t kp = A.kord[t];
-                map[(uint32_t)kp] = (uint32_t)(kp >> 32);
-            }
+            const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
             __syncthreads();
-            for (int64_t e = seg + wid; e < end; e += kWarps) {
+            // edges of this host, longest prefix first, grabbed dynamically
+            for (;;) {
+                unsigned my = 0;
+                if (lane == 0) my = atomicAdd(&s_next, 1u);
+                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+                if (e >= end) break;
                 const uint32_t p = A.hosted[e];
                 if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
                 const uint32_t len = A.scan_len[p];
-                if (len == 0) {
-                    if (!kFill && lane == 0) A.cnt[p] = 0;
-                    continue;
-                }
+                if (len == 0) continue;
                 const uint32_t x = A.scan_v[p];
                 if (kFill) {
-                    warp_fill(A, map, bm, stamp, p, y, x, len);
+                    if (A.packed)
+                        warp_fill(A, map, scratch + wid, p, y, x, len);
+                    else
+                        warp_fill_wide(A, map, scratch + wid, p, y, x, len);
                 } else {
                     const uint32_t c = warp_count(A, map, p, x, len);
                     if (lane == 0) A.cnt[p] = c;
                 }
             }
             __syncthreads();
-            for (uint64_t t = oy + threadIdx.x; t < oy1; t += kThreads) map[(uint32_t)A.kord[t]] = NONE32;
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
             __syncthreads();
             seg = end;
         }
     }
 }
 
-size_t smem_bytes(int64_t n, bool fill) {
-    return (size_t)((n * 4 + 15) / 16) * 16 + (fill ? (size_t)kWarps * kBM : 0);
+size_t map_bytes(int64_t n) { return (size_t)((n * 4 + 15) / 16) * 16; }
+
+// warps per CTA: 16, or fewer when the vertex map leaves too little shared memory
+int fill_warps(int64_t n) {
+    const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(n) - 1024;
+    const int64_t w = avail / (int64_t)sizeof(WarpScratch);
+    return (int)std::max<int64_t>(0, std::min<int64_t>(kWarps, w));
 }
 
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
-    const size_t smem = smem_bytes(A.n, fill);
+    const int warps = fill ? fill_warps(A.n) : kWarps;
+    if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
+    const int threads = warps * 32;
+    const size_t smem = map_bytes(A.n) + (fill ? (size_t)warps * sizeof(WarpScratch) : 0);
     const int nsm = device_sm_count();
     int per_sm = 1;
     if (fill) {
         VRB_CUDA(cudaFuncSetAttribute(k_triangles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<true>, kThreads, smem));
+        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<true>, threads, smem));
     } else {
         VRB_CUDA(cudaFuncSetAttribute(k_triangles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<false>, kThreads, smem));
+        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<false>, threads, smem));
     }
     if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
     const int64_t nctas = (int64_t)nsm * per_sm;
@@ -291,9 +485,9 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     A.task_counter = counter.get();
     const unsigned grid = (unsigned)std::min<int64_t>(nctas, A.task_hi - A.task_lo);
     if (fill)
-        k_triangles<true><<<grid, kThreads, smem, s>>>(A);
+        k_triangles<true><<<grid, threads, smem, s>>>(A);
     else
-        k_triangles<false><<<grid, kThreads, smem, s>>>(A);
+        k_triangles<false><<<grid, threads, smem, s>>>(A);
     VRB_LAUNCH_CHECK();
 }
 
@@ -302,9 +496,10 @@ TriArgs graph_args(const Graph& g) {
     A.n = g.n;
     A.E = g.E;
     A.off = g.off.get();
-    A.nbr_pos = g.nbr_pos.get();
-    A.krank_pos = g.krank_pos.get();
-    A.kord = g.kord.get();
+    A.nkr = g.nkr.get();
+    A.nr = g.nr.get();
+    A.np = g.np.get();
+    A.packed = g.packed ? 1 : 0;
     A.scan_v = g.scan_v.get();
     A.scan_len = g.scan_len.get();
     A.hosted = g.hosted.get();
@@ -317,7 +512,7 @@ TriArgs graph_args(const Graph& g) {
 
 int64_t dense_map_limit() {
     const int64_t smem = (int64_t)device_max_smem_optin();
-    return (smem - (int64_t)kWarps * kBM - 64) / 4;
+    return (smem - 4 * (int64_t)sizeof(WarpScratch) - 1024) / 4;   // >= 4 warps of fill scratch
 }
 
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s) {

@@ -31,14 +31,18 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
 struct Graph {
     int64_t n = 0, E = 0;
     DBuf<uint64_t> off;        // n + 1: offsets of each vertex's 2E directed entries
-    DBuf<uint32_t> nbr_pos;    // 2E: neighbour ids, each list in edge-position order
-    DBuf<uint32_t> krank_pos;  // 2E: index of that neighbour in the vertex's id-ordered list
-    DBuf<uint64_t> kord;       // 2E: (edge position << 32) | neighbour id, id-ordered lists
+    // per vertex, its neighbours in EDGE-POSITION order (the older-neighbour
+    // prefix of an edge is a prefix of this list):
+    DBuf<uint32_t> nkr;        // 2E: packed ? (krank << 16 | k) : k
+    DBuf<uint32_t> nr;         // 2E: krank (only when !packed)
+    DBuf<uint32_t> np;         // 2E: position of the entry's edge
+    bool packed = false;       // n <= 65536 and every degree <= 65536
+    //   krank = index of k in the vertex's neighbour-ID-ordered list
     DBuf<uint32_t> listidx;    // 2E: entry q = 2p + side -> index in the vertex's position list
     // owner-edge enumeration plan (triangles and tetrahedra)
     DBuf<uint32_t> scan_v;     // E: endpoint whose older-neighbour prefix is scanned
     DBuf<uint32_t> scan_len;   // E: length of that prefix (older neighbours)
-    DBuf<uint32_t> hosted;     // E: edge positions sorted by (host endpoint, position)
+    DBuf<uint32_t> hosted;     // E: edge positions sorted by (host endpoint, longest prefix first)
     DBuf<uint32_t> hosted_v;   // E: host endpoint of hosted[i]
     DBuf<uint64_t> work_pre;   // E + 1: exclusive prefix of scan_len over hosted order
     uint64_t work = 0;

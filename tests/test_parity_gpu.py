@@ -150,6 +150,21 @@ def test_high_degree_byte_map_rounds(vrb):
     compare(vrb, P, 1, 1.2)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_wide_list_layout(vrb, seed, monkeypatch):
+    # the unpacked neighbour-list layout used when n or a degree exceeds 65536,
+    # forced on small inputs
+    monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
+    kind = ["uniform", "lattice", "halfint", "dups"][seed % 4]
+    X = workloads.random_cloud(300 + seed, 40 + 20 * seed, 3, kind)
+    compare(vrb, X, 1, [0.5, 1.6, 1.2, 0.4][seed % 4])
+
+
+def test_wide_list_layout_multi_round(vrb, monkeypatch):
+    monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
+    test_high_degree_byte_map_rounds(vrb)
+
+
 def test_sortperm_literal_and_random(vrb):
     g = json.load(open(os.path.join(GOLDEN, "sortperm_literal.json")))
     for case in g["cases"]:

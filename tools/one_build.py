@@ -11,7 +11,8 @@ import workloads  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5B"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 w = workloads.WORKLOADS[cfg]
-X = torch.from_numpy(w.points()).cuda()
+npts = int(sys.argv[3]) if len(sys.argv) > 3 else None   # optional: first npts points only
+X = torch.from_numpy(w.points()[:npts]).cuda()
 vrb.use_torch_allocator(True)
 for _ in range(reps):
     r = vrb.build(X, maxdim=w.maxdim, radius=w.radius)
