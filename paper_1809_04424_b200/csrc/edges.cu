@@ -104,11 +104,15 @@ __global__ void k_assign(const uint32_t* __restrict__ ev, const uint32_t* __rest
 }
 
 __global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_t* __restrict__ host_key,
-                              const uint32_t* __restrict__ scan_len, int64_t E,
-                              uint32_t* __restrict__ hosted_v, uint32_t* __restrict__ work) {
+                              const uint32_t* __restrict__ scan_v, const uint32_t* __restrict__ scan_len,
+                              const uint64_t* __restrict__ off, int64_t E, uint32_t* __restrict__ hosted_v,
+                              uint4* __restrict__ plan, uint32_t* __restrict__ work) {
     GRID_STRIDE(i, E) {
+        const uint32_t p = hosted[i];
+        const uint32_t x = scan_v[p], len = scan_len[p];
         hosted_v[i] = (uint32_t)(host_key[i] >> 32);
-        work[i] = scan_len[hosted[i]];
+        plan[i] = make_uint4(p, x, len, (uint32_t)(off[x + 1] - off[x]));
+        work[i] = len;
     }
 }
 
@@ -186,7 +190,7 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     g.listidx.alloc(n2, s);
     g.scan_v.alloc(E, s);
     g.scan_len.alloc(E, s);
-    g.hosted.alloc(E, s);
+    g.plan.alloc(E, s);
     g.hosted_v.alloc(E, s);
     g.work_pre.alloc(E + 1, s);
     if (E == 0) {
@@ -221,10 +225,9 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         VRB_LAUNCH_CHECK();
         uint64_t* skeys = nullptr;
         const uint32_t* sorted = sort_ids(k0, k1, v0, v1, E, s, &skeys);
-        VRB_CUDA(cudaMemcpyAsync(g.hosted.get(), sorted, E * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         DBuf<uint32_t> work(E, s);
-        k_hosted_work<<<grid_for(E, 256), 256, 0, s>>>(g.hosted.get(), skeys, g.scan_len.get(), E,
-                                                       g.hosted_v.get(), work.get());
+        k_hosted_work<<<grid_for(E, 256), 256, 0, s>>>(sorted, skeys, g.scan_v.get(), g.scan_len.get(), g.off.get(),
+                                                       E, g.hosted_v.get(), g.plan.get(), work.get());
         VRB_LAUNCH_CHECK();
         exclusive_scan(work.get(), g.work_pre.get(), E, s);
         VRB_CUDA(cudaMemcpyAsync(&g.work, g.work_pre.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));

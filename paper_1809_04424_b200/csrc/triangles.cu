@@ -18,14 +18,20 @@
 // final slot -- no sort of the 2e9 triangles of C5B.  Owner edges sharing a
 // level (ties) get their small ranges re-sorted by lex afterwards (segsort.cu).
 //
-// Kernel shape.  Edges are grouped by a "host" endpoint y; a CTA loads the
+// Kernel shape.  Edges are grouped by a "host" endpoint y; a CTA holds the
 // whole neighbourhood of y as a dense shared-memory map pos_y[k] (n u32) and
-// its warps take the host's owner edges one at a time.  For edge p = (y, x)
-// a warp streams the older-neighbour PREFIX of x (x's neighbours in position
-// order, cut at p; the endpoint with the shorter prefix is scanned) and tests
-// pos_y[k] < p.  Count: popc of ballots.  Fill: valid apexes are marked in a
-// per-warp byte map indexed by the apex's rank in x's id-ordered list, which is
-// then read back in id order (the lex order) and written coalesced.
+// its warps take the host's owner edges one at a time (longest first, grabbed
+// dynamically).  For edge p = (y, x) a warp streams the older-neighbour PREFIX
+// of x (x's neighbours in position order, cut at p; the endpoint with the
+// shorter prefix is scanned) and tests pos_y[k] < p.
+//   count: per-lane counters, one warp reduction.
+//   fill : the valid apexes' ranks in x's ID-ordered list are flagged, the
+//          flags are folded into a bitmap with per-word prefix popcounts, and
+//          each valid apex computes its own output slot (#valid apexes of
+//          smaller id) -- a counting sort by apex id with no data movement.
+//          Prefixes up to kRegEntries stay in registers between the passes.
+//          A window of kWin slots is staged in shared memory and written with
+//          one lane per triangle (streaming stores).
 #include <algorithm>
 
 #include "vrb_internal.cuh"
@@ -36,9 +42,10 @@ namespace {
 
 constexpr int kWarps = 16;               // max warps per CTA (fewer when the map is large)
 constexpr int kThreads = kWarps * 32;
-constexpr int kBits = 4096;      // apex ranks per round (bitmap bits per warp)
+constexpr int kBits = 2048;              // apex ranks per round (flags / bitmap bits per warp)
 constexpr int kWords = kBits / 32;
-constexpr int kWin = 512;        // triangles staged per output window
+constexpr int kWin = 512;                // triangles staged per output window
+constexpr int kRegGroups = 4;            // uint4 groups per lane kept in registers
 
 struct TriArgs {
     int64_t n, E;
@@ -47,9 +54,7 @@ struct TriArgs {
     const uint32_t* nr;      // krank when !packed
     const uint32_t* np;      // edge position of each list entry
     int packed;
-    const uint32_t* scan_v;
-    const uint32_t* scan_len;
-    const uint32_t* hosted;
+    const uint4* plan;       // per hosted slot: (p, x, prefix length, deg x)
     const uint32_t* hosted_v;
     const uint64_t* work_pre;
     uint64_t chunk;
@@ -103,24 +108,26 @@ __device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
 }
 
+__device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
+
 // Warp: count apexes of owner edge p (host y's map in smem).
 __device__ __forceinline__ uint32_t warp_count(const TriArgs& A, const uint32_t* __restrict__ map,
-                                               uint32_t p, uint32_t x, uint32_t len) {
+                                               uint32_t p, uint64_t offx, uint32_t len) {
     const int lane = threadIdx.x & 31;
     int mis;
-    const uint4* g = aligned_groups(A.nkr + A.off[x], mis);
+    const uint4* g = aligned_groups(A.nkr + offx, mis);
     const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
     const int ngroups = (int)((len + mis + 3) >> 2);
     uint32_t c = 0;
-    for (int i0 = 0; i0 < ngroups; i0 += 64) {
-        uint4 q[2];
+    for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
+        uint4 q[kRegGroups];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRegGroups; ++u) {
             const int i = i0 + u * 32 + lane;
-            q[u] = i < ngroups ? __ldg(g + i) : make_uint4(0, 0, 0, 0);
+            q[u] = i < ngroups ? __ldg(g + i) : no_group();
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRegGroups; ++u) {
             const int i = i0 + u * 32 + lane;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -137,162 +144,162 @@ struct WarpScratch {
     uint8_t flag[kBits];     // valid apexes of this round, by rank in x's id-ordered list (0/1)
     uint32_t bits[kWords];   // the same as a bitmap
     uint32_t wpre[kWords];   // exclusive prefix popcount per bitmap word
-    uint32_t rec[kWin];      // staged window: apex k (low 16 bits) | prefix index t (high 16 bits)
+    uint32_t rk[kWin];       // staged window: apex k
+    uint32_t rpx[kWin];      //               pos(x, k)
 };
 
-// Warp: emit the triangles of owner edge p = (y, x) in apex-id order.
-//  mark    : stream x's older-neighbour prefix; for every apex k with
-//            pos_y[k] < p set flag[krank(k)] = 1 (krank = rank of k in x's
-//            id-ordered list; plain byte stores, lanes never collide)
-//  bitmap  : 16-byte reads of the flags -> 16-bit masks (multiply bit-gather),
-//            flags cleared on the way; exclusive prefix popcount per word
-//  emit    : stream the prefix again; a valid apex's output slot is
-//            prefix(word) + popc(word below its bit); stage (k, t) at that slot
-//            of the current window
-//  flush   : one lane per triangle of the window: vertices sort3(y, x, k),
-//            rows (min, max)(pos(x,k), pos(y,k)), p, filt -- streaming stores
-// Only the packed layout (n, deg <= 65536) is handled here; the caller picks
-// warp_fill_wide otherwise.
+// Fold the round's flags into the bitmap (16 flags per lane per step; the
+// flags are cleared on the way) and compute exclusive per-word prefix
+// popcounts.  Returns the number of valid apexes of the round.
+__device__ __forceinline__ uint32_t fold_flags(WarpScratch* __restrict__ W, uint32_t lim) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lim32 = (lim + 31) & ~31u;   // whole bitmap words (flags past lim are 0)
+    for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
+        const uint32_t b = b0 + 16 * lane;
+        if (b < lim32) {
+            uint4* f = reinterpret_cast<uint4*>(W->flag + b);
+            const uint4 qf = *f;
+            *f = make_uint4(0, 0, 0, 0);
+            const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
+                                 (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
+            reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
+        }
+    }
+    __syncwarp();
+    const uint32_t nwords = lim32 >> 5;   // lane owns words 2 lane, 2 lane + 1
+    const uint32_t c0 = 2u * lane < nwords ? __popc(W->bits[2 * lane]) : 0u;
+    const uint32_t c1 = 2u * lane + 1 < nwords ? __popc(W->bits[2 * lane + 1]) : 0u;
+    const uint32_t tot = c0 + c1;
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    W->wpre[2 * lane] = incl - tot;
+    W->wpre[2 * lane + 1] = incl - tot + c0;
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// One lane per triangle of the staged window [s0, s0 + m).
+__device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* __restrict__ map,
+                                             const WarpScratch* __restrict__ W, uint32_t m, uint64_t s0,
+                                             uint32_t p, uint32_t y, uint32_t x, uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = lane; j < m; j += 32) {
+        const uint32_t k = W->rk[j];
+        const uint32_t px = W->rpx[j];
+        const uint32_t py = map[k];
+        uint32_t a0 = y, a1 = x, a2 = k;
+        sort3(a0, a1, a2);
+        uint32_t* tv = A.tv + 3 * (s0 + j);
+        __stcs(tv, a0);
+        __stcs(tv + 1, a1);
+        __stcs(tv + 2, a2);
+        if (A.rows) {
+            uint32_t* rw = A.rows + 3 * (s0 + j);
+            __stcs(rw, min(px, py));
+            __stcs(rw + 1, max(px, py));
+            __stcs(rw + 2, p);
+        }
+        __stcs(A.tf + s0 + j, filt);
+    }
+}
+
+// Warp: emit the triangles of owner edge p = (y, x) in apex-id order (packed
+// lists: k and krank in one word).
 __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __restrict__ map,
                                           WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                          uint32_t len) {
+                                          uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                          uint32_t filt) {
     const int lane = threadIdx.x & 31;
-    const uint64_t offx = A.off[x];
-    const uint32_t degx = (uint32_t)(A.off[x + 1] - offx);
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
-    const uint32_t* __restrict__ npx = A.np + offx;
+    const uint4* gp = reinterpret_cast<const uint4*>(A.np + offx - mis);
     const int ngroups = (int)((len + mis + 3) >> 2);
-    const uint32_t filt = A.efilt[p];
-    uint64_t slot = A.toff[p] - A.slot0;
+    const bool inreg = ngroups <= 32 * kRegGroups;
+    uint4 qk[kRegGroups], qp[kRegGroups];
+    if (inreg) {
+#pragma unroll
+        for (int u = 0; u < kRegGroups; ++u) {
+            const int i = u * 32 + lane;
+            qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+            qp[u] = i < ngroups ? __ldg(gp + i) : no_group();
+        }
+    }
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = min((uint32_t)kBits, degx - R);
         // ---- mark
-        for (int i0 = 0; i0 < ngroups; i0 += 64) {
-            uint4 q[2];
+        for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
+            if (!inreg) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int i = i0 + 32 * u + lane;
-                q[u] = i < ngroups ? __ldg(gk + i) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                for (int u = 0; u < kRegGroups; ++u) {
+                    const int i = i0 + u * 32 + lane;
+                    qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int i = i0 + 32 * u + lane;
+            for (int u = 0; u < kRegGroups; ++u) {
+                const int i = i0 + u * 32 + lane;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int t = 4 * i + e - mis;
-                    const uint32_t w = pick(q[u], e);
+                    const uint32_t w = pick(qk[u], e);
                     const uint32_t r = (w >> 16) - R;
-                    const bool ok = t >= 0 && t < (int)len && r < (uint32_t)kBits;
-                    if (ok && map[w & 0xFFFFu] < p) W->flag[r] = 1;
+                    if (t >= 0 && t < (int)len && r < (uint32_t)kBits && map[w & 0xFFFFu] < p) W->flag[r] = 1;
                 }
             }
         }
         __syncwarp();
-        // ---- flags -> bitmap (16 flags per lane per step), clearing the flags
-        const uint32_t lim32 = (lim + 31) & ~31u;   // whole bitmap words (flags past lim are 0)
-        for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
-            const uint32_t b = b0 + 16 * lane;
-            if (b < lim32) {
-                uint4* f = reinterpret_cast<uint4*>(W->flag + b);
-                const uint4 qf = *f;
-                *f = make_uint4(0, 0, 0, 0);
-                const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
-                                     (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
-                reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
-            }
-        }
-        __syncwarp();
-        // ---- exclusive prefix popcount per word (lane owns words 4 lane .. 4 lane + 3)
-        const uint32_t nwords = (lim + 31) >> 5;
-        uint32_t c[4], tot = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t wd = 4 * lane + j;
-            c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
-            tot += c[j];
-        }
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t run = incl - tot;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { W->wpre[4 * lane + j] = run; run += c[j]; }
-        __syncwarp();
-        // ---- emit + flush, one window of kWin triangles per pass over the prefix
+        const uint32_t count = fold_flags(W, lim);
+        // ---- emit: valid <=> its rank bit is set; slot = #valid of smaller rank
         for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
-            for (int i0 = 0; i0 < ngroups; i0 += 64) {
-                uint4 q[2];
+            for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
+                if (!inreg) {
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int i = i0 + 32 * u + lane;
-                    q[u] = i < ngroups ? __ldg(gk + i)
-                                       : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                    for (int u = 0; u < kRegGroups; ++u) {
+                        const int i = i0 + u * 32 + lane;
+                        qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                        qp[u] = i < ngroups ? __ldg(gp + i) : no_group();
+                    }
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int i = i0 + 32 * u + lane;
+                for (int u = 0; u < kRegGroups; ++u) {
+                    const int i = i0 + u * 32 + lane;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int t = 4 * i + e - mis;
-                        const uint32_t w = pick(q[u], e);
-                        const uint32_t k = w & 0xFFFFu;
+                        const uint32_t w = pick(qk[u], e);
                         const uint32_t r = (w >> 16) - R;
-                        const bool ok = t >= 0 && t < (int)len && r < (uint32_t)kBits;
-                        if (ok && map[k] < p) {
-                            const uint32_t pos =
-                                W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
-                            if (pos < (uint32_t)kWin) W->rec[pos] = k | ((uint32_t)t << 16);
+                        if (t < 0 || t >= (int)len || r >= (uint32_t)kBits) continue;
+                        const uint32_t wd = W->bits[r >> 5];
+                        if (!((wd >> (r & 31)) & 1u)) continue;
+                        const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
+                        if (pos < (uint32_t)kWin) {
+                            W->rk[pos] = w & 0xFFFFu;
+                            W->rpx[pos] = pick(qp[u], e);
                         }
                     }
                 }
             }
             __syncwarp();
-            const uint32_t m = min((uint32_t)kWin, count - w0);
-            const uint64_t s0 = slot + w0;
-            for (uint32_t j = lane; j < m; j += 32) {
-                const uint32_t rc = W->rec[j];
-                const uint32_t k = rc & 0xFFFFu;
-                const uint32_t px = __ldg(npx + (rc >> 16));
-                const uint32_t py = map[k];
-                uint32_t a0 = y, a1 = x, a2 = k;
-                sort3(a0, a1, a2);
-                uint32_t* tv = A.tv + 3 * (s0 + j);
-                __stcs(tv, a0);
-                __stcs(tv + 1, a1);
-                __stcs(tv + 2, a2);
-                if (A.rows) {
-                    uint32_t* rw = A.rows + 3 * (s0 + j);
-                    __stcs(rw, min(px, py));
-                    __stcs(rw + 1, max(px, py));
-                    __stcs(rw + 2, p);
-                }
-                __stcs(A.tf + s0 + j, filt);
-            }
+            flush_window(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt);
             __syncwarp();
         }
         slot += count;
     }
 }
 
-// The same for the wide layout (separate krank array; any n and degree):
-// simpler, unstaged window loop with 32-bit records.
+// The same for the wide layout (separate krank array; any n and degree).
 __device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t* __restrict__ map,
                                                WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                               uint32_t len) {
+                                               uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                               uint32_t filt) {
     const int lane = threadIdx.x & 31;
-    const uint64_t offx = A.off[x];
-    const uint32_t degx = (uint32_t)(A.off[x + 1] - offx);
     const uint32_t* __restrict__ lk = A.nkr + offx;
     const uint32_t* __restrict__ lr = A.nr + offx;
-    const uint32_t* __restrict__ npx = A.np + offx;
-    const uint32_t filt = A.efilt[p];
-    uint64_t slot = A.toff[p] - A.slot0;
-    const uint32_t win = kWin / 2;   // rec holds (k, t) as two words
+    const uint32_t* __restrict__ lp = A.np + offx;
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = min((uint32_t)kBits, degx - R);
         for (uint32_t t = lane; t < len; t += 32) {
@@ -300,68 +307,21 @@ __device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t*
             if (r < (uint32_t)kBits && map[__ldg(lk + t)] < p) W->flag[r] = 1;
         }
         __syncwarp();
-        const uint32_t lim32 = (lim + 31) & ~31u;
-        for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
-            const uint32_t b = b0 + 16 * lane;
-            if (b < lim32) {
-                uint4* f = reinterpret_cast<uint4*>(W->flag + b);
-                const uint4 qf = *f;
-                *f = make_uint4(0, 0, 0, 0);
-                const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
-                                     (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
-                reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
-            }
-        }
-        __syncwarp();
-        const uint32_t nwords = (lim + 31) >> 5;
-        uint32_t c[4], tot = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t wd = 4 * lane + j;
-            c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
-            tot += c[j];
-        }
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t run = incl - tot;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { W->wpre[4 * lane + j] = run; run += c[j]; }
-        __syncwarp();
-        for (uint32_t w0 = 0; w0 < count; w0 += win) {
+        const uint32_t count = fold_flags(W, lim);
+        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
             for (uint32_t t = lane; t < len; t += 32) {
                 const uint32_t r = __ldg(lr + t) - R;
-                const uint32_t k = __ldg(lk + t);
-                if (r < (uint32_t)kBits && map[k] < p) {
-                    const uint32_t pos = W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
-                    if (pos < win) { W->rec[2 * pos] = k; W->rec[2 * pos + 1] = t; }
+                if (r >= (uint32_t)kBits) continue;
+                const uint32_t wd = W->bits[r >> 5];
+                if (!((wd >> (r & 31)) & 1u)) continue;
+                const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
+                if (pos < (uint32_t)kWin) {
+                    W->rk[pos] = __ldg(lk + t);
+                    W->rpx[pos] = __ldg(lp + t);
                 }
             }
             __syncwarp();
-            const uint32_t m = min(win, count - w0);
-            const uint64_t s0 = slot + w0;
-            for (uint32_t j = lane; j < m; j += 32) {
-                const uint32_t k = W->rec[2 * j];
-                const uint32_t px = __ldg(npx + W->rec[2 * j + 1]);
-                const uint32_t py = map[k];
-                uint32_t a0 = y, a1 = x, a2 = k;
-                sort3(a0, a1, a2);
-                uint32_t* tv = A.tv + 3 * (s0 + j);
-                __stcs(tv, a0);
-                __stcs(tv + 1, a1);
-                __stcs(tv + 2, a2);
-                if (A.rows) {
-                    uint32_t* rw = A.rows + 3 * (s0 + j);
-                    __stcs(rw, min(px, py));
-                    __stcs(rw + 1, max(px, py));
-                    __stcs(rw + 2, p);
-                }
-                __stcs(A.tf + s0 + j, filt);
-            }
+            flush_window(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt);
             __syncwarp();
         }
         slot += count;
@@ -383,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
         for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WarpScratch) / 4); q += nthreads)
             reinterpret_cast<uint32_t*>(scratch)[q] = 0u;
     __syncthreads();
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
     for (;;) {
         if (threadIdx.x == 0) {
             const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
@@ -411,7 +372,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
             const uint32_t y = s_y;
             const int64_t end = s_end;
             const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
-            const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
             __syncthreads();
             // edges of this host, longest prefix first, grabbed dynamically
@@ -420,18 +380,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
                 if (lane == 0) my = atomicAdd(&s_next, 1u);
                 const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
                 if (e >= end) break;
-                const uint32_t p = A.hosted[e];
-                if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
-                const uint32_t len = A.scan_len[p];
+                const uint4 pl = A.plan[e];   // (p, x, len, deg x)
+                const uint32_t p = pl.x, x = pl.y, len = pl.z;
                 if (len == 0) continue;
-                const uint32_t x = A.scan_v[p];
+                if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
+                const uint64_t offx = A.off[x];
                 if (kFill) {
+                    const uint64_t slot = A.toff[p] - A.slot0;
+                    const uint32_t filt = A.efilt[p];
                     if (A.packed)
-                        warp_fill(A, map, scratch + wid, p, y, x, len);
+                        warp_fill(A, map, scratch + wid, p, y, x, len, offx, pl.w, slot, filt);
                     else
-                        warp_fill_wide(A, map, scratch + wid, p, y, x, len);
+                        warp_fill_wide(A, map, scratch + wid, p, y, x, len, offx, pl.w, slot, filt);
                 } else {
-                    const uint32_t c = warp_count(A, map, p, x, len);
+                    const uint32_t c = warp_count(A, map, p, offx, len);
                     if (lane == 0) A.cnt[p] = c;
                 }
             }
@@ -500,9 +462,7 @@ TriArgs graph_args(const Graph& g) {
     A.nr = g.nr.get();
     A.np = g.np.get();
     A.packed = g.packed ? 1 : 0;
-    A.scan_v = g.scan_v.get();
-    A.scan_len = g.scan_len.get();
-    A.hosted = g.hosted.get();
+    A.plan = g.plan.get();
     A.hosted_v = g.hosted_v.get();
     A.work_pre = g.work_pre.get();
     return A;

@@ -42,8 +42,9 @@ struct Graph {
     // owner-edge enumeration plan (triangles and tetrahedra)
     DBuf<uint32_t> scan_v;     // E: endpoint whose older-neighbour prefix is scanned
     DBuf<uint32_t> scan_len;   // E: length of that prefix (older neighbours)
-    DBuf<uint32_t> hosted;     // E: edge positions sorted by (host endpoint, longest prefix first)
-    DBuf<uint32_t> hosted_v;   // E: host endpoint of hosted[i]
+    DBuf<uint4> plan;          // E: per hosted slot (edge position p, scanned x, prefix length, deg x),
+                               //    slots sorted by (host endpoint, longest prefix first)
+    DBuf<uint32_t> hosted_v;   // E: host endpoint of each hosted slot
     DBuf<uint64_t> work_pre;   // E + 1: exclusive prefix of scan_len over hosted order
     uint64_t work = 0;
     uint32_t max_deg = 0;
