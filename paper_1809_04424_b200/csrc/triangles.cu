@@ -42,9 +42,10 @@ namespace {
 
 constexpr int kWarps = 16;               // max warps per CTA (fewer when the map is large)
 constexpr int kThreads = kWarps * 32;
-constexpr int kBits = 2048;              // apex ranks per round (flags / bitmap bits per warp)
+constexpr int kBits = 4096;              // apex ranks per round (flags / bitmap bits per warp)
 constexpr int kWords = kBits / 32;
-constexpr int kWin = 512;                // triangles staged per output window
+static_assert(kWords % 32 == 0, "bitmap words must split evenly over the lanes");
+constexpr int kWin = 1024;               // triangles staged per output window (packed records)
 constexpr int kRegGroups = 4;            // uint4 groups per lane kept in registers
 
 struct TriArgs {
@@ -108,6 +109,22 @@ __device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
 }
 
+// Prefetch the 128-byte lines of a list prefix into L2 (one line per lane).
+__device__ __forceinline__ void prefetch_l2(const uint32_t* lst, uint32_t len, int lane) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(lst) & ~(uintptr_t)127;
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(lst + len);
+    for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a < a1; a += 128 * 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
+// Entries of group i that lie inside the prefix [0, len): a 4-bit mask.
+__device__ __forceinline__ uint32_t group_mask(int i, int mis, uint32_t len) {
+    const int t0 = 4 * i - mis;
+    const int lo = max(0, -t0);
+    const int hi = min(4, (int)len - t0);
+    return hi > lo ? ((1u << hi) - (1u << lo)) : 0u;
+}
+
 __device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
 
 // Warp: count apexes of owner edge p (host y's map in smem).
@@ -144,8 +161,8 @@ struct WarpScratch {
     uint8_t flag[kBits];     // valid apexes of this round, by rank in x's id-ordered list (0/1)
     uint32_t bits[kWords];   // the same as a bitmap
     uint32_t wpre[kWords];   // exclusive prefix popcount per bitmap word
-    uint32_t rk[kWin];       // staged window: apex k
-    uint32_t rpx[kWin];      //               pos(x, k)
+    uint32_t rec[kWin];      // staged window: packed: apex k | prefix index t << 16;
+                             //                wide:   (k, t) word pairs, kWin / 2 slots
 };
 
 // Fold the round's flags into the bitmap (16 flags per lane per step; the
@@ -166,44 +183,78 @@ __device__ __forceinline__ uint32_t fold_flags(WarpScratch* __restrict__ W, uint
         }
     }
     __syncwarp();
-    const uint32_t nwords = lim32 >> 5;   // lane owns words 2 lane, 2 lane + 1
-    const uint32_t c0 = 2u * lane < nwords ? __popc(W->bits[2 * lane]) : 0u;
-    const uint32_t c1 = 2u * lane + 1 < nwords ? __popc(W->bits[2 * lane + 1]) : 0u;
-    const uint32_t tot = c0 + c1;
+    constexpr int kWpl = kWords / 32;      // bitmap words per lane (lane owns kWpl consecutive words)
+    const uint32_t nwords = lim32 >> 5;
+    uint32_t c[kWpl], tot = 0;
+#pragma unroll
+    for (int j = 0; j < kWpl; ++j) {
+        const uint32_t wd = kWpl * lane + j;
+        c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
+        tot += c[j];
+    }
     uint32_t incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
     }
-    W->wpre[2 * lane] = incl - tot;
-    W->wpre[2 * lane + 1] = incl - tot + c0;
+    uint32_t run = incl - tot;
+#pragma unroll
+    for (int j = 0; j < kWpl; ++j) { W->wpre[kWpl * lane + j] = run; run += c[j]; }
     __syncwarp();
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-// One lane per triangle of the staged window [s0, s0 + m).
+// One lane per triangle of the staged window [s0, s0 + m): record -> (k, t),
+// pos(x, k) = np[offx + t] (the prefix just streamed: an L1/L2 hit),
+// pos(y, k) = map[k].
+template <bool kPacked>
 __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* __restrict__ map,
                                              const WarpScratch* __restrict__ W, uint32_t m, uint64_t s0,
-                                             uint32_t p, uint32_t y, uint32_t x, uint32_t filt) {
+                                             uint32_t p, uint32_t y, uint32_t x, uint32_t filt,
+                                             const uint32_t* __restrict__ npx) {
     const int lane = threadIdx.x & 31;
-    for (uint32_t j = lane; j < m; j += 32) {
-        const uint32_t k = W->rk[j];
-        const uint32_t px = W->rpx[j];
-        const uint32_t py = map[k];
-        uint32_t a0 = y, a1 = x, a2 = k;
-        sort3(a0, a1, a2);
-        uint32_t* tv = A.tv + 3 * (s0 + j);
-        __stcs(tv, a0);
-        __stcs(tv + 1, a1);
-        __stcs(tv + 2, a2);
-        if (A.rows) {
-            uint32_t* rw = A.rows + 3 * (s0 + j);
-            __stcs(rw, min(px, py));
-            __stcs(rw + 1, max(px, py));
-            __stcs(rw + 2, p);
+    constexpr int kU = 4;   // gathers in flight per lane
+    for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
+        uint32_t kk[kU], px[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t j = j0 + 32 * q + lane;
+            kk[q] = 0;
+            px[q] = 0;
+            if (j < m) {
+                uint32_t t;
+                if (kPacked) {
+                    const uint32_t rc = W->rec[j];
+                    kk[q] = rc & 0xFFFFu;
+                    t = rc >> 16;
+                } else {
+                    kk[q] = W->rec[2 * j];
+                    t = W->rec[2 * j + 1];
+                }
+                px[q] = __ldg(npx + t);
+            }
         }
-        __stcs(A.tf + s0 + j, filt);
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t j = j0 + 32 * q + lane;
+            if (j >= m) continue;
+            const uint32_t k = kk[q];
+            const uint32_t py = map[k];
+            uint32_t a0 = y, a1 = x, a2 = k;
+            sort3(a0, a1, a2);
+            uint32_t* tv = A.tv + 3 * (s0 + j);
+            __stcs(tv, a0);
+            __stcs(tv + 1, a1);
+            __stcs(tv + 2, a2);
+            if (A.rows) {
+                uint32_t* rw = A.rows + 3 * (s0 + j);
+                __stcs(rw, min(px[q], py));
+                __stcs(rw + 1, max(px[q], py));
+                __stcs(rw + 2, p);
+            }
+            __stcs(A.tf + s0 + j, filt);
+        }
     }
 }
 
@@ -216,28 +267,79 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
-    const uint4* gp = reinterpret_cast<const uint4*>(A.np + offx - mis);
+    const uint32_t* __restrict__ npx = A.np + offx;
     const int ngroups = (int)((len + mis + 3) >> 2);
-    const bool inreg = ngroups <= 32 * kRegGroups;
-    uint4 qk[kRegGroups], qp[kRegGroups];
-    if (inreg) {
+    if (ngroups <= 32 * kRegGroups) {
+        // ---------- register-resident prefix (<= 512 entries)
+        const int nu = (ngroups + 31) >> 5;   // warp-uniform number of group slots in use
+        uint4 qk[kRegGroups];
 #pragma unroll
         for (int u = 0; u < kRegGroups; ++u) {
             const int i = u * 32 + lane;
-            qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
-            qp[u] = i < ngroups ? __ldg(gp + i) : no_group();
+            if (u < nu) qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
         }
-    }
-    for (uint32_t R = 0; R < degx; R += kBits) {
-        const uint32_t lim = min((uint32_t)kBits, degx - R);
-        // ---- mark
-        for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
-            if (!inreg) {
+        // validity does not depend on the round: test once, keep a 16-bit mask
+        uint32_t vm = 0;
+#pragma unroll
+        for (int u = 0; u < kRegGroups; ++u) {
+            if (u < nu) {
+                const int i = u * 32 + lane;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int t = 4 * i + e - mis;
+                    const uint32_t w = pick(qk[u], e);
+                    if (t >= 0 && t < (int)len && map[w & 0xFFFFu] < p) vm |= 1u << (4 * u + e);
+                }
+            }
+        }
+        for (uint32_t R = 0; R < degx; R += kBits) {
+            const uint32_t lim = min((uint32_t)kBits, degx - R);
+#pragma unroll
+            for (int u = 0; u < kRegGroups; ++u) {
+                if (u < nu) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t r = (pick(qk[u], e) >> 16) - R;
+                        if (((vm >> (4 * u + e)) & 1u) && r < (uint32_t)kBits) W->flag[r] = 1;
+                    }
+                }
+            }
+            __syncwarp();
+            const uint32_t count = fold_flags(W, lim);
+            for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
 #pragma unroll
                 for (int u = 0; u < kRegGroups; ++u) {
-                    const int i = i0 + u * 32 + lane;
-                    qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                    if (u < nu) {
+                        const int i = u * 32 + lane;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t w = pick(qk[u], e);
+                            const uint32_t r = (w >> 16) - R;
+                            if (((vm >> (4 * u + e)) & 1u) && r < (uint32_t)kBits) {
+                                const uint32_t pos = W->wpre[r >> 5] +
+                                                     __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
+                                if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)(4 * i + e - mis) << 16);
+                            }
+                        }
+                    }
                 }
+                __syncwarp();
+                flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
+                __syncwarp();
+            }
+            slot += count;
+        }
+        return;
+    }
+    // ---------- long prefix: stream it in chunks of 512 entries per pass
+    for (uint32_t R = 0; R < degx; R += kBits) {
+        const uint32_t lim = min((uint32_t)kBits, degx - R);
+        for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
+            uint4 qk[kRegGroups];
+#pragma unroll
+            for (int u = 0; u < kRegGroups; ++u) {
+                const int i = i0 + u * 32 + lane;
+                qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
             }
 #pragma unroll
             for (int u = 0; u < kRegGroups; ++u) {
@@ -253,16 +355,13 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
         }
         __syncwarp();
         const uint32_t count = fold_flags(W, lim);
-        // ---- emit: valid <=> its rank bit is set; slot = #valid of smaller rank
         for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
             for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
-                if (!inreg) {
+                uint4 qk[kRegGroups];
 #pragma unroll
-                    for (int u = 0; u < kRegGroups; ++u) {
-                        const int i = i0 + u * 32 + lane;
-                        qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
-                        qp[u] = i < ngroups ? __ldg(gp + i) : no_group();
-                    }
+                for (int u = 0; u < kRegGroups; ++u) {
+                    const int i = i0 + u * 32 + lane;
+                    qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
                 }
 #pragma unroll
                 for (int u = 0; u < kRegGroups; ++u) {
@@ -276,15 +375,12 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                         const uint32_t wd = W->bits[r >> 5];
                         if (!((wd >> (r & 31)) & 1u)) continue;
                         const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
-                        if (pos < (uint32_t)kWin) {
-                            W->rk[pos] = w & 0xFFFFu;
-                            W->rpx[pos] = pick(qp[u], e);
-                        }
+                        if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)t << 16);
                     }
                 }
             }
             __syncwarp();
-            flush_window(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt);
+            flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
             __syncwarp();
         }
         slot += count;
@@ -299,7 +395,8 @@ __device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t*
     const int lane = threadIdx.x & 31;
     const uint32_t* __restrict__ lk = A.nkr + offx;
     const uint32_t* __restrict__ lr = A.nr + offx;
-    const uint32_t* __restrict__ lp = A.np + offx;
+    const uint32_t* __restrict__ npx = A.np + offx;
+    const uint32_t win = kWin / 2;
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = min((uint32_t)kBits, degx - R);
         for (uint32_t t = lane; t < len; t += 32) {
@@ -308,20 +405,20 @@ __device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t*
         }
         __syncwarp();
         const uint32_t count = fold_flags(W, lim);
-        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
+        for (uint32_t w0 = 0; w0 < count; w0 += win) {
             for (uint32_t t = lane; t < len; t += 32) {
                 const uint32_t r = __ldg(lr + t) - R;
                 if (r >= (uint32_t)kBits) continue;
                 const uint32_t wd = W->bits[r >> 5];
                 if (!((wd >> (r & 31)) & 1u)) continue;
                 const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
-                if (pos < (uint32_t)kWin) {
-                    W->rk[pos] = __ldg(lk + t);
-                    W->rpx[pos] = __ldg(lp + t);
+                if (pos < win) {
+                    W->rec[2 * pos] = __ldg(lk + t);
+                    W->rec[2 * pos + 1] = t;
                 }
             }
             __syncwarp();
-            flush_window(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt);
+            flush_window<false>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
             __syncwarp();
         }
         slot += count;
@@ -374,28 +471,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
             const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
             __syncthreads();
-            // edges of this host, longest prefix first, grabbed dynamically
-            for (;;) {
+            // Edges of this host, longest prefix first, grabbed dynamically and
+            // software-pipelined two deep: while edge e0 is processed, the
+            // plan of e2 and the offsets of e1 are in flight.
+            auto grab = [&]() -> int64_t {
                 unsigned my = 0;
                 if (lane == 0) my = atomicAdd(&s_next, 1u);
-                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
-                if (e >= end) break;
-                const uint4 pl = A.plan[e];   // (p, x, len, deg x)
-                const uint32_t p = pl.x, x = pl.y, len = pl.z;
-                if (len == 0) continue;
-                if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
-                const uint64_t offx = A.off[x];
-                if (kFill) {
-                    const uint64_t slot = A.toff[p] - A.slot0;
-                    const uint32_t filt = A.efilt[p];
-                    if (A.packed)
-                        warp_fill(A, map, scratch + wid, p, y, x, len, offx, pl.w, slot, filt);
-                    else
-                        warp_fill_wide(A, map, scratch + wid, p, y, x, len, offx, pl.w, slot, filt);
-                } else {
-                    const uint32_t c = warp_count(A, map, p, offx, len);
-                    if (lane == 0) A.cnt[p] = c;
+                return seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+            };
+            auto plan_of = [&](int64_t e) -> uint4 {
+                uint4 pl = e < end ? A.plan[e] : make_uint4(0, 0, 0, 0);
+                if (kFill && ((int64_t)pl.x < A.p_lo || (int64_t)pl.x >= A.p_hi)) pl.z = 0;
+                return pl;
+            };
+            int64_t e0 = grab();
+            uint4 pl0 = plan_of(e0);
+            int64_t e1 = grab();
+            uint4 pl1 = plan_of(e1);
+            uint64_t off0 = pl0.z ? A.off[pl0.y] : 0, off1 = pl1.z ? A.off[pl1.y] : 0;
+            uint64_t slot0 = 0, slot1 = 0;
+            uint32_t filt0 = 0, filt1 = 0;
+            if (kFill) {
+                if (pl0.z) { slot0 = A.toff[pl0.x] - A.slot0; filt0 = A.efilt[pl0.x]; }
+                if (pl1.z) { slot1 = A.toff[pl1.x] - A.slot0; filt1 = A.efilt[pl1.x]; }
+            }
+            while (e0 < end) {
+                const int64_t e2 = grab();
+                const uint4 pl2 = plan_of(e2);
+                if (pl0.z) {
+                    const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
+                    if (kFill) {
+                        if (A.packed)
+                            warp_fill(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                        else
+                            warp_fill_wide(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    } else {
+                        const uint32_t c = warp_count(A, map, p, off0, len);
+                        if (lane == 0) A.cnt[p] = c;
+                    }
                 }
+                uint64_t off2 = pl2.z ? A.off[pl2.y] : 0, slot2 = 0;
+                uint32_t filt2 = 0;
+                if (kFill && pl2.z) { slot2 = A.toff[pl2.x] - A.slot0; filt2 = A.efilt[pl2.x]; }
+                e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1;
+                e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2;
             }
             __syncthreads();
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;

@@ -135,18 +135,19 @@ def test_dim_major_and_device_points(vrb):
 
 
 def test_high_degree_byte_map_rounds(vrb):
-    # two hubs adjacent to 4500 jittered sphere points; the hub-hub edge is the
-    # longest, so its older-neighbour prefixes hold 4500 entries (> 4096 byte-map
-    # slots: the fill runs several rounds)
+    # two hubs adjacent to 4500 jittered points of a high-dimensional sphere
+    # (mutually almost never adjacent); the hub-hub edge is the longest, so its
+    # older-neighbour prefixes hold 4500 entries (> 4096 ranks per round: the
+    # fill runs several rounds, and a long prefix is streamed in chunks)
     rng = np.random.default_rng(3)
-    m = 4500
-    S = rng.standard_normal((m, 10))
+    m, dim = 4500, 200
+    S = rng.standard_normal((m, dim))
     S /= np.linalg.norm(S, axis=1, keepdims=True)
     S *= (1.0 + 0.01 * rng.uniform(size=(m, 1)))
-    P = np.zeros((m + 2, 11))
-    P[:m, :10] = S
-    P[m, 10] = 0.6
-    P[m + 1, 10] = -0.6
+    P = np.zeros((m + 2, dim + 1))
+    P[:m, :dim] = S
+    P[m, dim] = 0.6
+    P[m + 1, dim] = -0.6
     compare(vrb, P, 1, 1.2)
 
 
