@@ -46,7 +46,8 @@ constexpr int kBits = 4096;              // apex ranks per round (flags / bitmap
 constexpr int kWords = kBits / 32;
 static_assert(kWords % 32 == 0, "bitmap words must split evenly over the lanes");
 constexpr int kWin = 1024;               // triangles staged per output window (packed records)
-constexpr int kRegGroups = 4;            // uint4 groups per lane kept in registers
+constexpr int kRegGroups = 4;            // uint4 groups per lane in flight when streaming
+constexpr int kRegSlots = 8;             // uint4 groups per lane kept in registers (1024 entries)
 
 struct TriArgs {
     int64_t n, E;
@@ -269,19 +270,19 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
     const uint32_t* __restrict__ npx = A.np + offx;
     const int ngroups = (int)((len + mis + 3) >> 2);
-    if (ngroups <= 32 * kRegGroups) {
-        // ---------- register-resident prefix (<= 512 entries)
+    if (ngroups <= 32 * kRegSlots && degx <= (uint32_t)kBits) {
+        // ---------- register-resident prefix (<= 1024 entries), one round
         const int nu = (ngroups + 31) >> 5;   // warp-uniform number of group slots in use
-        uint4 qk[kRegGroups];
+        uint4 qk[kRegSlots];
 #pragma unroll
-        for (int u = 0; u < kRegGroups; ++u) {
+        for (int u = 0; u < kRegSlots; ++u) {
             const int i = u * 32 + lane;
             if (u < nu) qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
         }
-        // validity does not depend on the round: test once, keep a 16-bit mask
+        // valid apexes: 4 bits per slot
         uint32_t vm = 0;
 #pragma unroll
-        for (int u = 0; u < kRegGroups; ++u) {
+        for (int u = 0; u < kRegSlots; ++u) {
             if (u < nu) {
                 const int i = u * 32 + lane;
 #pragma unroll
@@ -292,42 +293,56 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                 }
             }
         }
-        for (uint32_t R = 0; R < degx; R += kBits) {
-            const uint32_t lim = min((uint32_t)kBits, degx - R);
 #pragma unroll
-            for (int u = 0; u < kRegGroups; ++u) {
+        for (int u = 0; u < kRegSlots; ++u)
+            if (u < nu)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((vm >> (4 * u + e)) & 1u) W->flag[pick(qk[u], e) >> 16] = 1;
+        __syncwarp();
+        const uint32_t count = fold_flags(W, degx);
+        if (count <= (uint32_t)kWin) {
+#pragma unroll
+            for (int u = 0; u < kRegSlots; ++u) {
                 if (u < nu) {
+                    const uint32_t tb = (uint32_t)(4 * (u * 32 + lane) - mis);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const uint32_t r = (pick(qk[u], e) >> 16) - R;
-                        if (((vm >> (4 * u + e)) & 1u) && r < (uint32_t)kBits) W->flag[r] = 1;
+                        if ((vm >> (4 * u + e)) & 1u) {
+                            const uint32_t w = pick(qk[u], e);
+                            const uint32_t r = w >> 16;
+                            const uint32_t pos = W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u));
+                            W->rec[pos] = (w & 0xFFFFu) | ((tb + e) << 16);
+                        }
                     }
                 }
             }
             __syncwarp();
-            const uint32_t count = fold_flags(W, lim);
-            for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
+            flush_window<true>(A, map, W, count, slot, p, y, x, filt, npx);
+            __syncwarp();
+            return;
+        }
+        // more than one window: the bitmap is already built; windows below
+        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
 #pragma unroll
-                for (int u = 0; u < kRegGroups; ++u) {
-                    if (u < nu) {
-                        const int i = u * 32 + lane;
+            for (int u = 0; u < kRegSlots; ++u) {
+                if (u < nu) {
+                    const uint32_t tb = (uint32_t)(4 * (u * 32 + lane) - mis);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
+                    for (int e = 0; e < 4; ++e) {
+                        if ((vm >> (4 * u + e)) & 1u) {
                             const uint32_t w = pick(qk[u], e);
-                            const uint32_t r = (w >> 16) - R;
-                            if (((vm >> (4 * u + e)) & 1u) && r < (uint32_t)kBits) {
-                                const uint32_t pos = W->wpre[r >> 5] +
-                                                     __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
-                                if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)(4 * i + e - mis) << 16);
-                            }
+                            const uint32_t r = w >> 16;
+                            const uint32_t pos =
+                                W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
+                            if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((tb + e) << 16);
                         }
                     }
                 }
-                __syncwarp();
-                flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
-                __syncwarp();
             }
-            slot += count;
+            __syncwarp();
+            flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
+            __syncwarp();
         }
         return;
     }
