@@ -13,6 +13,7 @@
 // then assigned to the endpoint x with the SHORTER prefix of neighbours older
 // than p (to be scanned) and the other endpoint y (the "host", whose full
 // neighbourhood is held as a dense map in shared memory during enumeration).
+#include <algorithm>
 #include <cstdlib>
 
 #include "vrb_internal.cuh"
@@ -86,6 +87,58 @@ __global__ void k_id_ranks(const uint32_t* __restrict__ sorted, const uint32_t* 
             nkr[slot] |= r << 16;
         else
             nr[slot] = r;
+    }
+}
+
+// krank by counting (n <= kRankBitmapMax): one CTA per vertex v marks its
+// neighbours in an n-bit shared bitmap; krank(k) = #neighbours with smaller id
+// = prefix popcount of the bitmap below bit k.
+constexpr int64_t kRankBitmapMax = 262144;
+
+__global__ void __launch_bounds__(256) k_ranks_bitmap(const uint64_t* __restrict__ off, int64_t n, int packed,
+                                                      uint32_t* __restrict__ nkr, uint32_t* __restrict__ nr) {
+    extern __shared__ uint32_t sm[];
+    const int64_t nw = (n + 31) >> 5;
+    uint32_t* bm = sm;
+    uint32_t* wp = sm + nw;
+    __shared__ uint32_t warp_tot[8];
+    for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+        const uint64_t o0 = off[v], o1 = off[v + 1];
+        if (o1 == o0) continue;
+        for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) bm[w] = 0u;
+        __syncthreads();
+        for (uint64_t t = o0 + threadIdx.x; t < o1; t += blockDim.x) {
+            const uint32_t k = nkr[t];
+            atomicOr(&bm[k >> 5], 1u << (k & 31));
+        }
+        __syncthreads();
+        // exclusive prefix popcount over the words: thread owns a contiguous run
+        const int64_t per = (nw + blockDim.x - 1) / blockDim.x;
+        const int64_t w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+        uint32_t tot = 0;
+        for (int64_t w = w0; w < w1; ++w) tot += __popc(bm[w]);
+        uint32_t x = tot;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 1; q < 32; q <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, q);
+            if (lane >= q) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        uint32_t run = x - tot;
+        for (int w = 0; w < wid; ++w) run += warp_tot[w];
+        for (int64_t w = w0; w < w1; ++w) { wp[w] = run; run += __popc(bm[w]); }
+        __syncthreads();
+        for (uint64_t t = o0 + threadIdx.x; t < o1; t += blockDim.x) {
+            const uint32_t k = nkr[t];
+            const uint32_t r = wp[k >> 5] + __popc(bm[k >> 5] & ((1u << (k & 31)) - 1u));
+            if (packed)
+                nkr[t] = k | (r << 16);
+            else
+                nr[t] = r;
+        }
+        __syncthreads();
     }
 }
 
@@ -208,13 +261,23 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
                                                        g.listidx.get());
         VRB_LAUNCH_CHECK();
-        // (b) ranks in neighbour-id order: sort entries by (vertex, neighbour)
-        k_keys_vertex_nbr<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
-        VRB_LAUNCH_CHECK();
-        sorted = sort_ids(k0, k1, v0, v1, n2, s);
-        k_id_ranks<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), g.listidx.get(), n2,
-                                                      g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
-        VRB_LAUNCH_CHECK();
+        // (b) ranks in neighbour-id order
+        const char* force_sort = std::getenv("VRB_FORCE_SORT_RANKS");   // testing knob
+        if (n <= kRankBitmapMax && !(force_sort && force_sort[0] == '1')) {
+            const size_t smem = (size_t)2 * ((n + 31) >> 5) * sizeof(uint32_t);
+            VRB_CUDA(cudaFuncSetAttribute(k_ranks_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)device_sm_count() * 8);
+            k_ranks_bitmap<<<grid, 256, smem, s>>>(g.off.get(), n, g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
+            VRB_LAUNCH_CHECK();
+        } else {
+            // large n: sort entries by (vertex, neighbour)
+            k_keys_vertex_nbr<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
+            VRB_LAUNCH_CHECK();
+            sorted = sort_ids(k0, k1, v0, v1, n2, s);
+            k_id_ranks<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), g.listidx.get(), n2,
+                                                          g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
+            VRB_LAUNCH_CHECK();
+        }
     }
     {
         // (c) owner-edge plan: scanned endpoint, prefix length, host; edges by host

@@ -1,15 +1,20 @@
-// radix_sort.cu -- stable LSD radix sort of (u64 key, u32 value) pairs.
+// radix_sort.cu -- stable LSD radix sort of (u64 key, u32 value) pairs,
+// onesweep style (one kernel per 8-bit digit pass).
 //
-// One pass per 8-bit digit that actually varies across the keys (digits with
-// no varying bit are skipped; see varying_bits()).  Each pass is
-//   k_digit_hist  : per-tile 256-bin histogram          (reads keys)
-//   exclusive_scan: digit-major offsets over all tiles   (tiny)
-//   k_scatter     : stable in-tile ranking (warp match_any + per-warp digit
-//                   counters, warps combined in order) and scatter
-// Stability: items of a tile are ranked in index order (round, warp, lane),
-// tiles in index order via the digit-major scan.  This is the sort behind the
-// edge ranking (paper sec. 4.5: sortperm over the distance entries
-// on the GPU) and behind the CSR builds.
+//   k_histograms : ONE read of the keys builds the 256-bin histogram of every
+//                  digit that varies (per-CTA shared histograms, atomics)
+//   k_scan_bins  : exclusive scan per digit pass (256 entries each, tiny)
+//   k_onesweep   : per pass; CTAs take tiles in order (atomic tile counter);
+//                  stable in-tile ranking (warps own contiguous item runs,
+//                  match_any per round); per-digit global offsets by decoupled
+//                  look-back over earlier tiles; a shared-memory exchange turns
+//                  the scatter into contiguous per-digit runs.
+// Digits with no varying bit (varying_bits()) are skipped.  Stability: items
+// of a tile are ranked in index order, tiles in index order.  This sort is
+// the GPU sortperm of the edge lengths (paper sec. 4.5) and the
+// grouping step of the neighbourhood-list builds.
+#include <vector>
+
 #include "vrb_internal.cuh"
 
 namespace vrb {
@@ -17,73 +22,161 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;
+constexpr int kItems = 16;                   // per thread
+constexpr int kTile = kThreads * kItems;     // 4096 items per tile
+constexpr int kWarpItems = 32 * kItems;      // contiguous items per warp
 constexpr int kBins = 256;
 
-__global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t* __restrict__ keys, int64_t n,
-                                                         int shift, int64_t ntiles,
-                                                         uint32_t* __restrict__ counts) {
-    __shared__ uint32_t hist[kWarps][kBins];
-    for (int q = threadIdx.x; q < kWarps * kBins; q += kThreads) (&hist[0][0])[q] = 0;
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kThreads) k_histograms(const uint64_t* __restrict__ keys, int64_t n,
+                                                         uint32_t digit_mask, unsigned long long* __restrict__ hist) {
+    __shared__ uint32_t h[8][kBins];
+    for (int q = threadIdx.x; q < 8 * kBins; q += kThreads) (&h[0][0])[q] = 0;
     __syncthreads();
-    const int wid = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-#pragma unroll 4
-    for (int it = 0; it < kItems; ++it) {
-        int64_t i = base + (int64_t)it * kThreads + threadIdx.x;
-        if (i < n) atomicAdd(&hist[wid][(keys[i] >> shift) & 0xFF], 1u);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+            if ((digit_mask >> d) & 1u) atomicAdd(&h[d][(k >> (8 * d)) & 0xFF], 1u);
     }
     __syncthreads();
-    const int d = threadIdx.x;   // kThreads == kBins
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) t += hist[w][d];
-    counts[(int64_t)d * ntiles + blockIdx.x] = t;
+    for (int q = threadIdx.x; q < 8 * kBins; q += kThreads) {
+        const int d = q / kBins;
+        if (((digit_mask >> d) & 1u) && (&h[0][0])[q]) atomicAdd(&hist[q], (unsigned long long)(&h[0][0])[q]);
+    }
 }
 
-__global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict__ keys_in,
-                                                      const uint32_t* __restrict__ vals_in,
-                                                      uint64_t* __restrict__ keys_out,
-                                                      uint32_t* __restrict__ vals_out, int64_t n,
-                                                      int shift, int64_t ntiles,
-                                                      const uint64_t* __restrict__ offsets) {
-    __shared__ uint64_t run[kBins];            // running global offset per digit
-    __shared__ uint64_t wcnt[kWarps][kBins];   // per-warp digit counts -> offsets
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    run[threadIdx.x] = offsets[(int64_t)threadIdx.x * ntiles + blockIdx.x];
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int it = 0; it < kItems; ++it) {
-        for (int q = threadIdx.x; q < kWarps * kBins; q += kThreads) (&wcnt[0][0])[q] = 0;
-        __syncthreads();
-        const int64_t i = base + (int64_t)it * kThreads + threadIdx.x;
-        const bool valid = i < n;
-        uint64_t key = valid ? keys_in[i] : 0;
-        uint32_t val = valid ? vals_in[i] : 0;
-        const uint32_t digit = valid ? (uint32_t)((key >> shift) & 0xFF) : (uint32_t)(kBins + lane);
-        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
-        const uint32_t rank = __popc(peers & lt_mask);
-        if (valid && rank == 0) wcnt[wid][digit] = __popc(peers);
-        __syncthreads();
-        {   // combine warps in order, per digit
-            const int d = threadIdx.x;
-            uint64_t r = run[d];
+// exclusive scan of each digit's 256 bins (one warp per digit)
+__global__ void k_scan_bins(unsigned long long* __restrict__ hist) {
+    const int d = blockIdx.x, lane = threadIdx.x;
+    unsigned long long* h = hist + d * kBins;
+    unsigned long long carry = 0;
+    for (int b0 = 0; b0 < kBins; b0 += 32) {
+        const unsigned long long v = h[b0 + lane];
+        unsigned long long x = v;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                uint64_t c = wcnt[w][d];
-                wcnt[w][d] = r;
-                r += c;
-            }
-            run[d] = r;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        __syncthreads();
-        if (valid) {
-            const uint64_t dst = wcnt[wid][digit] + rank;
-            keys_out[dst] = key;
-            vals_out[dst] = val;
+        h[b0 + lane] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+struct SweepSmem {
+    uint64_t key[kTile];
+    uint32_t val[kTile];
+    uint32_t woff[kWarps][kBins];   // per-warp digit counts -> tile-local start per warp
+    uint32_t tstart[kBins];         // tile-local start of each digit
+    unsigned long long gstart[kBins];   // global position of the tile's run of each digit
+    uint32_t wsum[kWarps];
+    uint32_t tile_id;
+};
+
+__global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t* __restrict__ keys_in,
+                                                       const uint32_t* __restrict__ vals_in,
+                                                       uint64_t* __restrict__ keys_out,
+                                                       uint32_t* __restrict__ vals_out, int64_t n, int shift,
+                                                       const unsigned long long* __restrict__ pass_base,
+                                                       unsigned long long* __restrict__ status,
+                                                       unsigned* __restrict__ tile_counter) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SweepSmem& S = *reinterpret_cast<SweepSmem*>(smem_raw);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) S.tile_id = atomicAdd(tile_counter, 1u);
+    for (int q = threadIdx.x; q < kWarps * kBins; q += kThreads) (&S.woff[0][0])[q] = 0;
+    __syncthreads();
+    const uint32_t tile = S.tile_id;
+    const int64_t tile_base = (int64_t)tile * kTile;
+    const int64_t base = tile_base + (int64_t)wid * kWarpItems;
+    const int tile_n = (int)min((int64_t)kTile, n - tile_base);
+    // ---- load: warp w owns items [base, base + 512) in rounds of 32 lanes
+    uint64_t k[kItems];
+    uint32_t v[kItems], rk[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        k[r] = i < n ? keys_in[i] : 0ull;
+        v[r] = i < n ? vals_in[i] : 0u;
+    }
+    // ---- stable warp-local ranks (rounds in order, lanes in order)
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        const bool ok = i < n;
+        const uint32_t dg = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : (uint32_t)(kBins + lane);
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t before = ok ? S.woff[wid][dg] : 0u;
+        __syncwarp();
+        rk[r] = before + __popc(peers & lt);
+        if (ok && (peers & lt) == 0) S.woff[wid][dg] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // ---- digit d (thread d): warps in order -> per-warp starts; tile count
+    const int d = threadIdx.x;   // kThreads == kBins
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = S.woff[w][d];
+        S.woff[w][d] = cnt;
+        cnt += c;
+    }
+    // publish the tile aggregate early, then look back over earlier tiles
+    unsigned long long* st = status + (int64_t)tile * kBins + d;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+        atomicExch(st, kFlagPre | cnt);
+    } else {
+        atomicExch(st, kFlagAgg | cnt);
+        for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
+            const volatile unsigned long long* sp = status + j * kBins + d;
+            unsigned long long s;
+            do { s = *sp; } while ((s & (kFlagAgg | kFlagPre)) == 0);
+            excl += s & kValMask;
+            if (s & kFlagPre) break;
         }
-        __syncthreads();
+        atomicExch(st, kFlagPre | (excl + cnt));
+    }
+    S.gstart[d] = pass_base[d] + excl;
+    // tile-local starts: exclusive scan of cnt over the 256 digits
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) S.wsum[wid] = x;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w)
+        if (w < wid) wpre += S.wsum[w];
+    S.tstart[d] = wpre + x - cnt;
+    __syncthreads();
+    // ---- exchange through shared memory in tile order
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        if (i < n) {
+            const uint32_t dg = (uint32_t)((k[r] >> shift) & 0xFF);
+            const uint32_t pos = S.tstart[dg] + S.woff[wid][dg] + rk[r];
+            S.key[pos] = k[r];
+            S.val[pos] = v[r];
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < tile_n; q += kThreads) {
+        const uint64_t kk = S.key[q];
+        const uint32_t dg = (uint32_t)((kk >> shift) & 0xFF);
+        const unsigned long long dst = S.gstart[dg] + (uint32_t)(q - S.tstart[dg]);
+        keys_out[dst] = kk;
+        vals_out[dst] = S.val[q];
     }
 }
 
@@ -92,24 +185,38 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
 bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
                       int64_t n, uint64_t varying, cudaStream_t s) {
     if (n <= 1 || varying == 0) return false;
+    uint32_t digit_mask = 0;
+    for (int d = 0; d < 8; ++d)
+        if ((varying >> (8 * d)) & 0xFFull) digit_mask |= 1u << d;
     const int64_t ntiles = ceil_div(n, kTile);
-    DBuf<uint32_t> counts((size_t)kBins * ntiles, s);
-    DBuf<uint64_t> offsets((size_t)kBins * ntiles + 1, s);
+    DBuf<unsigned long long> hist(8 * kBins, s);
+    VRB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.bytes(), s));
+    const unsigned hg = (unsigned)std::min<int64_t>(ceil_div(n, kThreads), (int64_t)device_sm_count() * 8);
+    k_histograms<<<hg, kThreads, 0, s>>>(keys, n, digit_mask, hist.get());
+    VRB_LAUNCH_CHECK();
+    k_scan_bins<<<8, 32, 0, s>>>(hist.get());
+    VRB_LAUNCH_CHECK();
+    const int npass = __builtin_popcount(digit_mask);
+    DBuf<unsigned long long> status((size_t)ntiles * kBins * npass, s);
+    DBuf<unsigned> counters(npass, s);
+    VRB_CUDA(cudaMemsetAsync(status.get(), 0, status.bytes(), s));
+    VRB_CUDA(cudaMemsetAsync(counters.get(), 0, counters.bytes(), s));
+    const size_t smem = sizeof(SweepSmem);
+    VRB_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool alt = false;
-    for (int digit = 0; digit < 8; ++digit) {
-        const int shift = 8 * digit;
-        if (((varying >> shift) & 0xFFull) == 0) continue;
+    int pass = 0;
+    for (int d = 0; d < 8; ++d) {
+        if (!((digit_mask >> d) & 1u)) continue;
         uint64_t* kin = alt ? keys_alt : keys;
         uint64_t* kout = alt ? keys : keys_alt;
         uint32_t* vin = alt ? vals_alt : vals;
         uint32_t* vout = alt ? vals : vals_alt;
-        k_digit_hist<<<(unsigned)ntiles, kThreads, 0, s>>>(kin, n, shift, ntiles, counts.get());
-        VRB_LAUNCH_CHECK();
-        exclusive_scan(counts.get(), offsets.get(), (int64_t)kBins * ntiles, s);
-        k_scatter<<<(unsigned)ntiles, kThreads, 0, s>>>(kin, vin, kout, vout, n, shift, ntiles,
-                                                       offsets.get());
+        k_onesweep<<<(unsigned)ntiles, kThreads, smem, s>>>(kin, vin, kout, vout, n, 8 * d, hist.get() + d * kBins,
+                                                            status.get() + (size_t)pass * ntiles * kBins,
+                                                            counters.get() + pass);
         VRB_LAUNCH_CHECK();
         alt = !alt;
+        ++pass;
     }
     return alt;
 }

@@ -161,6 +161,17 @@ def test_wide_list_layout(vrb, seed, monkeypatch):
     compare(vrb, X, 1, [0.5, 1.6, 1.2, 0.4][seed % 4])
 
 
+@pytest.mark.parametrize("wide", ["0", "1"])
+def test_sorted_rank_path(vrb, monkeypatch, wide):
+    # neighbour ranks by the (vertex, neighbour) radix sort, used when n is too
+    # large for the per-vertex bitmap, forced on small inputs
+    monkeypatch.setenv("VRB_FORCE_SORT_RANKS", "1")
+    monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", wide)
+    for seed in range(4):
+        X = workloads.random_cloud(700 + seed, 150, 3, ["uniform", "lattice"][seed % 2])
+        compare(vrb, X, 1, [0.4, 1.5][seed % 2])
+
+
 def test_wide_list_layout_multi_round(vrb, monkeypatch):
     monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
     test_high_degree_byte_map_rounds(vrb)
