@@ -33,6 +33,7 @@
 //          A window of kWin slots is staged in shared memory and written with
 //          one lane per triangle (streaming stores).
 #include <algorithm>
+#include <cstdlib>
 
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
@@ -40,14 +41,13 @@
 namespace vrb {
 namespace {
 
-constexpr int kWarps = 16;               // max warps per CTA (fewer when the map is large)
+constexpr int kWarps = 32;               // max warps per CTA (fewer when the map is large)
 constexpr int kThreads = kWarps * 32;
-constexpr int kBits = 4096;              // apex ranks per round (flags / bitmap bits per warp)
+constexpr int kBits = 4096;              // apex ranks per round (bitmap bits per warp)
 constexpr int kWords = kBits / 32;
 static_assert(kWords % 32 == 0, "bitmap words must split evenly over the lanes");
-constexpr int kWin = 1024;               // triangles staged per output window (packed records)
+constexpr int kWin = 512;                // triangles staged per output window (packed records)
 constexpr int kRegGroups = 4;            // uint4 groups per lane in flight when streaming
-constexpr int kRegSlots = 8;             // uint4 groups per lane kept in registers (1024 entries)
 
 struct TriArgs {
     int64_t n, E;
@@ -73,6 +73,7 @@ struct TriArgs {
     uint32_t* tv;
     uint32_t* tf;
     uint32_t* rows;
+    int debug;   // ablation knob (VRB_DEBUG_FILL): 1 = stop after mark, 2 = skip the flush
 };
 
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t v) {
@@ -157,35 +158,30 @@ __device__ __forceinline__ uint32_t warp_count(const TriArgs& A, const uint32_t*
     return __reduce_add_sync(0xffffffffu, c);
 }
 
-// Per-warp shared scratch of the fill kernel.
+// Per-warp shared scratch of the fill kernel (3 KB: 32 warps + the vertex
+// map fit one SM).
 struct WarpScratch {
-    uint8_t flag[kBits];     // valid apexes of this round, by rank in x's id-ordered list (0/1)
-    uint32_t bits[kWords];   // the same as a bitmap
+    uint32_t bits[kWords];   // valid apexes of this round, bitmap by rank in x's id-ordered list
     uint32_t wpre[kWords];   // exclusive prefix popcount per bitmap word
     uint32_t rec[kWin];      // staged window: packed: apex k | prefix index t << 16;
                              //                wide:   (k, t) word pairs, kWin / 2 slots
 };
 
-// Fold the round's flags into the bitmap (16 flags per lane per step; the
-// flags are cleared on the way) and compute exclusive per-word prefix
-// popcounts.  Returns the number of valid apexes of the round.
-__device__ __forceinline__ uint32_t fold_flags(WarpScratch* __restrict__ W, uint32_t lim) {
+// Clear the bitmap words of a round of lim ranks (before marking).
+__device__ __forceinline__ void clear_bits(WarpScratch* __restrict__ W, uint32_t lim) {
     const int lane = threadIdx.x & 31;
-    const uint32_t lim32 = (lim + 31) & ~31u;   // whole bitmap words (flags past lim are 0)
-    for (uint32_t b0 = 0; b0 < lim32; b0 += 512) {
-        const uint32_t b = b0 + 16 * lane;
-        if (b < lim32) {
-            uint4* f = reinterpret_cast<uint4*>(W->flag + b);
-            const uint4 qf = *f;
-            *f = make_uint4(0, 0, 0, 0);
-            const uint32_t m16 = ((qf.x * 0x01020408u) >> 24) | (((qf.y * 0x01020408u) >> 24) << 4) |
-                                 (((qf.z * 0x01020408u) >> 24) << 8) | (((qf.w * 0x01020408u) >> 24) << 12);
-            reinterpret_cast<uint16_t*>(W->bits)[b >> 4] = (uint16_t)m16;
-        }
-    }
+    const uint32_t nwords = (lim + 31) >> 5;
+    for (uint32_t w = lane; w < nwords; w += 32) W->bits[w] = 0u;
+    __syncwarp();
+}
+
+// Exclusive per-word prefix popcounts of the round's bitmap (lim ranks);
+// returns the number of valid apexes of the round.
+__device__ __forceinline__ uint32_t rank_bits(WarpScratch* __restrict__ W, uint32_t lim) {
+    const int lane = threadIdx.x & 31;
     __syncwarp();
     constexpr int kWpl = kWords / 32;      // bitmap words per lane (lane owns kWpl consecutive words)
-    const uint32_t nwords = lim32 >> 5;
+    const uint32_t nwords = (lim + 31) >> 5;
     uint32_t c[kWpl], tot = 0;
 #pragma unroll
     for (int j = 0; j < kWpl; ++j) {
@@ -206,16 +202,16 @@ __device__ __forceinline__ uint32_t fold_flags(WarpScratch* __restrict__ W, uint
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-// One lane per triangle of the staged window [s0, s0 + m): record -> (k, t),
-// pos(x, k) = np[offx + t] (the prefix just streamed: an L1/L2 hit),
-// pos(y, k) = map[k].
+// Write the staged window [s0, s0 + m), one lane per triangle, kU position
+// gathers in flight per lane: record -> (k, t); pos(x, k) = np[offx + t] (the
+// prefix just streamed: L1/L2), pos(y, k) = map[k].
 template <bool kPacked>
 __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* __restrict__ map,
                                              const WarpScratch* __restrict__ W, uint32_t m, uint64_t s0,
                                              uint32_t p, uint32_t y, uint32_t x, uint32_t filt,
                                              const uint32_t* __restrict__ npx) {
     const int lane = threadIdx.x & 31;
-    constexpr int kU = 4;   // gathers in flight per lane
+    constexpr int kU = 4;
     for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
         uint32_t kk[kU], px[kU];
 #pragma unroll
@@ -259,8 +255,17 @@ __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* _
     }
 }
 
-// Warp: emit the triangles of owner edge p = (y, x) in apex-id order (packed
-// lists: k and krank in one word).
+// Warp: emit the triangles of owner edge p = (y, x) in apex-id order.
+//  mark : stream x's older-neighbour prefix (kRegGroups 16-byte groups per
+//         lane in flight); every apex k with pos_y[k] < p sets bit krank(k)
+//         of the warp's bitmap (shared atomic OR: as cheap as a byte store on
+//         B200, measured by tools/micro/smem_atomics.cu)
+//  rank : exclusive per-word prefix popcounts
+//  emit : stream the prefix again (L1/L2-hot); a valid apex's slot is
+//         prefix(word) + popc(word below its bit); stage (k, t) in the window
+//  flush: one lane per triangle (flush_window)
+// kBits ranks per round (rounds only when deg x > kBits), kWin slots per window.
+template <bool kPacked>
 __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __restrict__ map,
                                           WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
                                           uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
@@ -268,93 +273,21 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
+    const uint4* gr = kPacked ? nullptr : reinterpret_cast<const uint4*>(A.nr + offx - mis);
     const uint32_t* __restrict__ npx = A.np + offx;
     const int ngroups = (int)((len + mis + 3) >> 2);
-    if (ngroups <= 32 * kRegSlots && degx <= (uint32_t)kBits) {
-        // ---------- register-resident prefix (<= 1024 entries), one round
-        const int nu = (ngroups + 31) >> 5;   // warp-uniform number of group slots in use
-        uint4 qk[kRegSlots];
-#pragma unroll
-        for (int u = 0; u < kRegSlots; ++u) {
-            const int i = u * 32 + lane;
-            if (u < nu) qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
-        }
-        // valid apexes: 4 bits per slot
-        uint32_t vm = 0;
-#pragma unroll
-        for (int u = 0; u < kRegSlots; ++u) {
-            if (u < nu) {
-                const int i = u * 32 + lane;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int t = 4 * i + e - mis;
-                    const uint32_t w = pick(qk[u], e);
-                    if (t >= 0 && t < (int)len && map[w & 0xFFFFu] < p) vm |= 1u << (4 * u + e);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kRegSlots; ++u)
-            if (u < nu)
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if ((vm >> (4 * u + e)) & 1u) W->flag[pick(qk[u], e) >> 16] = 1;
-        __syncwarp();
-        const uint32_t count = fold_flags(W, degx);
-        if (count <= (uint32_t)kWin) {
-#pragma unroll
-            for (int u = 0; u < kRegSlots; ++u) {
-                if (u < nu) {
-                    const uint32_t tb = (uint32_t)(4 * (u * 32 + lane) - mis);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if ((vm >> (4 * u + e)) & 1u) {
-                            const uint32_t w = pick(qk[u], e);
-                            const uint32_t r = w >> 16;
-                            const uint32_t pos = W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u));
-                            W->rec[pos] = (w & 0xFFFFu) | ((tb + e) << 16);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            flush_window<true>(A, map, W, count, slot, p, y, x, filt, npx);
-            __syncwarp();
-            return;
-        }
-        // more than one window: the bitmap is already built; windows below
-        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
-#pragma unroll
-            for (int u = 0; u < kRegSlots; ++u) {
-                if (u < nu) {
-                    const uint32_t tb = (uint32_t)(4 * (u * 32 + lane) - mis);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if ((vm >> (4 * u + e)) & 1u) {
-                            const uint32_t w = pick(qk[u], e);
-                            const uint32_t r = w >> 16;
-                            const uint32_t pos =
-                                W->wpre[r >> 5] + __popc(W->bits[r >> 5] & ((1u << (r & 31)) - 1u)) - w0;
-                            if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((tb + e) << 16);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
-            __syncwarp();
-        }
-        return;
-    }
-    // ---------- long prefix: stream it in chunks of 512 entries per pass
+    const uint32_t win = kPacked ? (uint32_t)kWin : (uint32_t)kWin / 2;
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = min((uint32_t)kBits, degx - R);
+        clear_bits(W, lim);
+        // ---- mark
         for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
-            uint4 qk[kRegGroups];
+            uint4 qk[kRegGroups], qr[kRegGroups];
 #pragma unroll
             for (int u = 0; u < kRegGroups; ++u) {
                 const int i = i0 + u * 32 + lane;
                 qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                if (!kPacked) qr[u] = i < ngroups ? __ldg(gr + i) : no_group();
             }
 #pragma unroll
             for (int u = 0; u < kRegGroups; ++u) {
@@ -363,20 +296,24 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                 for (int e = 0; e < 4; ++e) {
                     const int t = 4 * i + e - mis;
                     const uint32_t w = pick(qk[u], e);
-                    const uint32_t r = (w >> 16) - R;
-                    if (t >= 0 && t < (int)len && r < (uint32_t)kBits && map[w & 0xFFFFu] < p) W->flag[r] = 1;
+                    const uint32_t k = kPacked ? (w & 0xFFFFu) : w;
+                    const uint32_t r = (kPacked ? (w >> 16) : pick(qr[u], e)) - R;
+                    if (t >= 0 && t < (int)len && r < (uint32_t)kBits && map[k] < p)
+                        atomicOr(&W->bits[r >> 5], 1u << (r & 31));
                 }
             }
         }
-        __syncwarp();
-        const uint32_t count = fold_flags(W, lim);
-        for (uint32_t w0 = 0; w0 < count; w0 += kWin) {
+        const uint32_t count = rank_bits(W, lim);
+        if (A.debug == 1) { slot += count; continue; }
+        // ---- emit + flush, one window per pass over the prefix
+        for (uint32_t w0 = 0; w0 < count; w0 += win) {
             for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
-                uint4 qk[kRegGroups];
+                uint4 qk[kRegGroups], qr[kRegGroups];
 #pragma unroll
                 for (int u = 0; u < kRegGroups; ++u) {
                     const int i = i0 + u * 32 + lane;
                     qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                    if (!kPacked) qr[u] = i < ngroups ? __ldg(gr + i) : no_group();
                 }
 #pragma unroll
                 for (int u = 0; u < kRegGroups; ++u) {
@@ -385,55 +322,24 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                     for (int e = 0; e < 4; ++e) {
                         const int t = 4 * i + e - mis;
                         const uint32_t w = pick(qk[u], e);
-                        const uint32_t r = (w >> 16) - R;
+                        const uint32_t r = (kPacked ? (w >> 16) : pick(qr[u], e)) - R;
                         if (t < 0 || t >= (int)len || r >= (uint32_t)kBits) continue;
                         const uint32_t wd = W->bits[r >> 5];
                         if (!((wd >> (r & 31)) & 1u)) continue;
                         const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
-                        if (pos < (uint32_t)kWin) W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)t << 16);
+                        if (pos >= win) continue;
+                        if (kPacked) {
+                            W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)t << 16);
+                        } else {
+                            W->rec[2 * pos] = w;
+                            W->rec[2 * pos + 1] = (uint32_t)t;
+                        }
                     }
                 }
             }
             __syncwarp();
-            flush_window<true>(A, map, W, min((uint32_t)kWin, count - w0), slot + w0, p, y, x, filt, npx);
-            __syncwarp();
-        }
-        slot += count;
-    }
-}
-
-// The same for the wide layout (separate krank array; any n and degree).
-__device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t* __restrict__ map,
-                                               WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                               uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
-                                               uint32_t filt) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t* __restrict__ lk = A.nkr + offx;
-    const uint32_t* __restrict__ lr = A.nr + offx;
-    const uint32_t* __restrict__ npx = A.np + offx;
-    const uint32_t win = kWin / 2;
-    for (uint32_t R = 0; R < degx; R += kBits) {
-        const uint32_t lim = min((uint32_t)kBits, degx - R);
-        for (uint32_t t = lane; t < len; t += 32) {
-            const uint32_t r = __ldg(lr + t) - R;
-            if (r < (uint32_t)kBits && map[__ldg(lk + t)] < p) W->flag[r] = 1;
-        }
-        __syncwarp();
-        const uint32_t count = fold_flags(W, lim);
-        for (uint32_t w0 = 0; w0 < count; w0 += win) {
-            for (uint32_t t = lane; t < len; t += 32) {
-                const uint32_t r = __ldg(lr + t) - R;
-                if (r >= (uint32_t)kBits) continue;
-                const uint32_t wd = W->bits[r >> 5];
-                if (!((wd >> (r & 31)) & 1u)) continue;
-                const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
-                if (pos < win) {
-                    W->rec[2 * pos] = __ldg(lk + t);
-                    W->rec[2 * pos + 1] = t;
-                }
-            }
-            __syncwarp();
-            flush_window<false>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
+            if (A.debug != 2)
+                flush_window<kPacked>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
             __syncwarp();
         }
         slot += count;
@@ -441,7 +347,7 @@ __device__ __forceinline__ void warp_fill_wide(const TriArgs& A, const uint32_t*
 }
 
 template <bool kFill>
-__global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
+__global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
     WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem + ((A.n * 4 + 15) / 16) * 16);
@@ -517,9 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_triangles(TriArgs A) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
                     if (kFill) {
                         if (A.packed)
-                            warp_fill(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                            warp_fill<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                         else
-                            warp_fill_wide(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                            warp_fill<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                     } else {
                         const uint32_t c = warp_count(A, map, p, off0, len);
                         if (lane == 0) A.cnt[p] = c;
@@ -550,7 +456,9 @@ int fill_warps(int64_t n) {
 
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
-    const int warps = fill ? fill_warps(A.n) : kWarps;
+    // fill: one 32-warp CTA per SM (the vertex map + 3 KB per warp); count:
+    // 16-warp CTAs, two per SM (shorter per-host barrier tails)
+    const int warps = fill ? fill_warps(A.n) : kWarps / 2;
     if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
     const size_t smem = map_bytes(A.n) + (fill ? (size_t)warps * sizeof(WarpScratch) : 0);
@@ -630,6 +538,8 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.tv = tv;
     A.tf = tf;
     A.rows = rows;
+    const char* dbg = std::getenv("VRB_DEBUG_FILL");   // ablation timing only; breaks outputs
+    A.debug = dbg ? std::atoi(dbg) : 0;
     launch(A, true, g.work, 0, 1, s);
 }
 
