@@ -1,0 +1,501 @@
+// tetrahedra.cu -- S6 (tetrahedron enumeration), S7 and S8 for dimension 3.
+//
+// Definition ("a solid tetrahedra is constructed if all its face
+// triangles have been created"; readings A3/A4/A7): {a,b,c,d} is a
+// tetrahedron iff its six edges are kept; filt = max edge filt; dimension 3
+// is ordered by (filt, lex); its D_3 column holds the positions of its four
+// face triangles in the dimension-2 order, ascending.
+//
+// Owner-edge order, as for triangles (triangles.cu): the owner of a
+// tetrahedron is its edge of largest position p = (y, x).  Its other two
+// vertices k < l are both in S(p) = {k : pos(x,k) < p, pos(y,k) < p} (the
+// apex set of p's triangles) and are adjacent with pos(k,l) < p.  For a fixed
+// owner, (k, l) lex order is the lex order of the sorted 4-tuple, so a count
+// pass, an exclusive scan and a fill pass place every tetrahedron directly;
+// tie levels are re-sorted afterwards (segsort.cu).
+//
+// Per owner edge (one warp, the host y's position map in shared memory):
+//   S     : x's older-neighbour prefix -> bitmap by rank in x's id list ->
+//           S sorted by id, with pos(x,k), in shared memory; S's vertices
+//           also flagged in an n-bit vertex bitmap
+//   pairs : for each k in S (ascending), stream k's neighbours older than p
+//           (a prefix of k's position-ordered list, found by binary search);
+//           l in S with l > k (vertex bitmap, then binary search in S for its
+//           index) marks bit idx(l) of a small bitmap; its popcount ranks give
+//           the (k, l) emission order
+//   D_3   : faces (y,x,k), (y,x,l) are p's own triangles (direct index when
+//           p's level is a single edge); faces (y,k,l), (x,k,l) are found by
+//           binary search in the triangle range of their owner edge.
+#include <algorithm>
+
+#include "vrb_internal.cuh"
+#include "vrb_stages.cuh"
+
+namespace vrb {
+namespace {
+
+constexpr int kWarps = 16;
+constexpr int kThreads = kWarps * 32;
+constexpr int kBits = 4096;     // ranks of x's id list per round
+constexpr int kWords = kBits / 32;
+constexpr int kS = 1024;        // max |S(p)| handled (else VRB_ENOTSUP)
+
+struct TetArgs {
+    int64_t n, E;
+    const uint64_t* off;
+    const uint32_t* nkr;
+    const uint32_t* nr;
+    const uint32_t* np;
+    int packed;
+    const uint4* plan;
+    const uint32_t* hosted_v;
+    const uint64_t* work_pre;
+    uint64_t chunk;
+    int64_t ntasks, task_lo, task_hi;
+    unsigned long long* task_counter;
+    unsigned* overflow;       // set when |S(p)| > kS
+    // triangles (dimension 2, global arrays)
+    const uint64_t* toff;     // E + 1
+    const uint64_t* tlo;      // E: start of the triangle range of p's level
+    const uint64_t* thi;      // E: end of it
+    const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
+    // count
+    uint32_t* cnt;
+    // fill
+    const uint32_t* efilt;
+    const uint64_t* qoff;
+    int64_t p_lo, p_hi;
+    uint64_t slot0;
+    uint32_t* qv;
+    uint32_t* qf;
+    uint32_t* rows;
+};
+
+struct TetScratch {
+    uint32_t bits[kWords];
+    uint32_t wpre[kWords];
+    uint32_t Sk[kS];          // S sorted by id
+    uint32_t Spx[kS];         // pos(x, k)
+    uint32_t lbits[kS / 32];  // l in S (by index) adjacent to the current k through an older edge
+    uint32_t lpre[kS / 32];
+    uint32_t lpos[kS];        // pos(k, l) for the marked l
+};
+
+__device__ __forceinline__ int64_t lb_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t v) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int64_t ub_u32(const uint32_t* a, int64_t lo, int64_t hi, uint32_t v) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// first index in [lo, hi) of the ascending u32 array a with a[i] >= v
+__device__ __forceinline__ uint32_t lb_u32(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t v) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void sort3v(uint32_t& a, uint32_t& b, uint32_t& c) {
+    uint32_t t;
+    if (a > b) { t = a; a = b; b = t; }
+    if (b > c) { t = b; b = c; c = t; }
+    if (a > b) { t = a; a = b; b = t; }
+}
+
+__device__ __forceinline__ void sort4v(uint32_t* v) {
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j)
+            if (v[j - 1] > v[j]) { const uint32_t t = v[j]; v[j] = v[j - 1]; v[j - 1] = t; }
+}
+
+// Position of triangle {a, b, c} (a < b < c) whose owner edge is f: binary
+// search by lex triple inside the (lex-sorted) triangle range of f's level.
+__device__ __forceinline__ uint32_t tri_pos(const TetArgs& A, uint32_t f, uint32_t a, uint32_t b, uint32_t c) {
+    uint64_t lo = A.tlo[f], hi = A.thi[f];
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const uint32_t* t = A.tv + 3 * mid;
+        const uint32_t t0 = t[0], t1 = t[1], t2 = t[2];
+        const bool less = t0 < a || (t0 == a && (t1 < b || (t1 == b && t2 < c)));
+        if (less) lo = mid + 1; else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+// Warp: S(p) sorted by id into W->Sk / W->Spx, flags S in the vertex bitmap.
+// Returns |S| (may exceed kS: caller checks).
+__device__ uint32_t build_S(const TetArgs& A, const uint32_t* __restrict__ map, TetScratch* __restrict__ W,
+                           uint32_t* __restrict__ vbits, uint32_t p, uint32_t x, uint32_t len, uint64_t offx,
+                           uint32_t degx) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t* lk = A.nkr + offx;
+    const uint32_t* lr = A.nr + offx;
+    const uint32_t* lp = A.np + offx;
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    uint32_t total = 0;
+    for (uint32_t R = 0; R < degx; R += kBits) {
+        const uint32_t lim = min((uint32_t)kBits, degx - R);
+        const uint32_t nwords = (lim + 31) >> 5;
+        for (uint32_t w = lane; w < nwords; w += 32) W->bits[w] = 0u;
+        __syncwarp();
+        for (uint32_t t = lane; t < len; t += 32) {
+            const uint32_t w = __ldg(lk + t);
+            const uint32_t k = w & kmask;
+            const uint32_t r = (A.packed ? (w >> 16) : __ldg(lr + t)) - R;
+            if (r < (uint32_t)kBits && map[k] < p) atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+        }
+        __syncwarp();
+        // prefix popcount, 4 words per lane
+        uint32_t c[kWords / 32], tot = 0;
+#pragma unroll
+        for (int j = 0; j < kWords / 32; ++j) {
+            const uint32_t wd = (kWords / 32) * lane + j;
+            c[j] = wd < nwords ? __popc(W->bits[wd]) : 0u;
+            tot += c[j];
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int j = 0; j < kWords / 32; ++j) { W->wpre[(kWords / 32) * lane + j] = run; run += c[j]; }
+        const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        for (uint32_t t = lane; t < len; t += 32) {
+            const uint32_t w = __ldg(lk + t);
+            const uint32_t r = (A.packed ? (w >> 16) : __ldg(lr + t)) - R;
+            if (r >= (uint32_t)kBits) continue;
+            const uint32_t wd = W->bits[r >> 5];
+            if (!((wd >> (r & 31)) & 1u)) continue;
+            const uint32_t idx = total + W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u));
+            if (idx < (uint32_t)kS) {
+                const uint32_t k = w & kmask;
+                W->Sk[idx] = k;
+                W->Spx[idx] = __ldg(lp + t);
+                atomicOr(&vbits[k >> 5], 1u << (k & 31));
+            }
+        }
+        __syncwarp();
+        total += count;
+    }
+    return total;
+}
+
+__device__ void clear_S(TetScratch* __restrict__ W, uint32_t* __restrict__ vbits, uint32_t m) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = lane; i < m; i += 32) {
+        const uint32_t k = W->Sk[i];
+        atomicAnd(&vbits[k >> 5], ~(1u << (k & 31)));
+    }
+    __syncwarp();
+}
+
+// For k = Sk[ki]: mark l in S, l > k, pos(k,l) < p; returns #marked and
+// fills lpre.
+__device__ uint32_t mark_l(const TetArgs& A, TetScratch* __restrict__ W, const uint32_t* __restrict__ vbits,
+                           uint32_t p, uint32_t ki, uint32_t m) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t k = W->Sk[ki];
+    const uint64_t ok0 = A.off[k], ok1 = A.off[k + 1];
+    const uint32_t* npk = A.np + ok0;
+    // k's neighbours older than p: a prefix of its position-ordered list
+    uint32_t plen = 0;
+    if (lane == 0) plen = lb_u32(npk, 0, (uint32_t)(ok1 - ok0), p);
+    plen = __shfl_sync(0xffffffffu, plen, 0);
+    const uint32_t nw = (m + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) W->lbits[w] = 0u;
+    __syncwarp();
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    const uint32_t* lk = A.nkr + ok0;
+    for (uint32_t t = lane; t < plen; t += 32) {
+        const uint32_t l = __ldg(lk + t) & kmask;
+        if (l <= k || !((vbits[l >> 5] >> (l & 31)) & 1u)) continue;
+        const uint32_t j = lb_u32(W->Sk, ki + 1, m, l);
+        if (j < m && W->Sk[j] == l) {
+            atomicOr(&W->lbits[j >> 5], 1u << (j & 31));
+            W->lpos[j] = __ldg(npk + t);
+        }
+    }
+    __syncwarp();
+    uint32_t tot = 0;
+    for (uint32_t w = lane; w < nw; w += 32) tot += __popc(W->lbits[w]);
+    // words in order: lane w holds word w (nw <= 32)
+    const uint32_t c = lane < (int)nw ? __popc(W->lbits[lane]) : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane < (int)nw) W->lpre[lane] = incl - c;
+    __syncwarp();
+    (void)tot;
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* map = reinterpret_cast<uint32_t*>(smem);
+    const int64_t nvw = (A.n + 31) >> 5;
+    const size_t map_b = (size_t)((A.n * 4 + 15) / 16) * 16;
+    const size_t vb_b = (size_t)((nvw * 4 + 15) / 16) * 16;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nthreads = blockDim.x;
+    uint32_t* vbits = reinterpret_cast<uint32_t*>(smem + map_b + (size_t)wid * vb_b);
+    TetScratch* W = reinterpret_cast<TetScratch*>(smem + map_b + (size_t)(nthreads / 32) * vb_b) + wid;
+    __shared__ int64_t s_lo, s_hi, s_end;
+    __shared__ uint32_t s_y;
+    __shared__ unsigned s_next;
+    for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
+    for (int64_t q = lane; q < nvw; q += 32) vbits[q] = 0u;
+    __syncthreads();
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
+            if (task >= A.task_hi) {
+                s_lo = s_hi = -1;
+            } else {
+                s_lo = lb_u64(A.work_pre, 0, A.E + 1, (uint64_t)task * A.chunk);
+                s_hi = task == A.ntasks - 1 ? A.E : lb_u64(A.work_pre, 0, A.E + 1, (uint64_t)(task + 1) * A.chunk);
+                if (s_lo > A.E) s_lo = A.E;
+                if (s_hi > A.E) s_hi = A.E;
+            }
+        }
+        __syncthreads();
+        const int64_t lo = s_lo, hi = s_hi;
+        __syncthreads();
+        if (lo < 0) break;
+        for (int64_t seg = lo; seg < hi;) {
+            if (threadIdx.x == 0) {
+                const uint32_t y = A.hosted_v[seg];
+                s_y = y;
+                s_end = ub_u32(A.hosted_v, seg, hi, y);
+                s_next = 0;
+            }
+            __syncthreads();
+            const uint32_t y = s_y;
+            const int64_t end = s_end;
+            const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
+            __syncthreads();
+            for (;;) {
+                unsigned my = 0;
+                if (lane == 0) my = atomicAdd(&s_next, 1u);
+                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+                if (e >= end) break;
+                const uint4 pl = A.plan[e];
+                const uint32_t p = pl.x, x = pl.y, len = pl.z;
+                if (len < 2) continue;
+                if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
+                const uint64_t offx = A.off[x];
+                const uint32_t m = build_S(A, map, W, vbits, p, x, len, offx, pl.w);
+                if (m > (uint32_t)kS) {
+                    if (lane == 0) atomicOr(A.overflow, 1u);
+                    clear_S(W, vbits, kS);
+                    continue;
+                }
+                uint64_t slot = 0;
+                uint32_t filt = 0;
+                bool direct = false;
+                uint64_t tbase = 0;
+                if (kFill) {
+                    slot = A.qoff[p] - A.slot0;
+                    filt = A.efilt[p];
+                    tbase = A.toff[p];
+                    direct = A.tlo[p] == tbase && A.thi[p] == A.toff[p + 1];   // p alone at its level
+                }
+                uint32_t total = 0;
+                for (uint32_t ki = 0; ki + 1 < m; ++ki) {
+                    const uint32_t c = mark_l(A, W, vbits, p, ki, m);
+                    if (kFill && c) {
+                        const uint32_t k = W->Sk[ki];
+                        const uint32_t pxk = W->Spx[ki];
+                        const uint32_t pyk = map[k];
+                        const uint32_t f_yxk = direct ? (uint32_t)(tbase + ki) : 0u;
+                        for (uint32_t j = ki + 1 + lane; j < m; j += 32) {
+                            const uint32_t wd = W->lbits[j >> 5];
+                            if (!((wd >> (j & 31)) & 1u)) continue;
+                            const uint32_t l = W->Sk[j];
+                            const uint64_t s = slot + total + W->lpre[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u));
+                            const uint32_t pxl = W->Spx[j], pyl = map[l], pkl = W->lpos[j];
+                            uint32_t v[4] = {y, x, k, l};
+                            sort4v(v);
+                            uint32_t* qv = A.qv + 4 * s;
+                            qv[0] = v[0]; qv[1] = v[1]; qv[2] = v[2]; qv[3] = v[3];
+                            A.qf[s] = filt;
+                            if (A.rows) {
+                                uint32_t a, b, cc;
+                                // (y, x, k) and (y, x, l): owned by p
+                                uint32_t r[4];
+                                if (direct) {
+                                    r[0] = f_yxk;
+                                    r[1] = (uint32_t)(tbase + j);
+                                } else {
+                                    a = y; b = x; cc = k; sort3v(a, b, cc);
+                                    r[0] = tri_pos(A, p, a, b, cc);
+                                    a = y; b = x; cc = l; sort3v(a, b, cc);
+                                    r[1] = tri_pos(A, p, a, b, cc);
+                                }
+                                // (y, k, l): owner = max of pos(y,k), pos(y,l), pos(k,l)
+                                a = y; b = k; cc = l; sort3v(a, b, cc);
+                                r[2] = tri_pos(A, max(max(pyk, pyl), pkl), a, b, cc);
+                                // (x, k, l)
+                                a = x; b = k; cc = l; sort3v(a, b, cc);
+                                r[3] = tri_pos(A, max(max(pxk, pxl), pkl), a, b, cc);
+                                sort4v(r);
+                                uint32_t* rw = A.rows + 4 * s;
+                                rw[0] = r[0]; rw[1] = r[1]; rw[2] = r[2]; rw[3] = r[3];
+                            }
+                        }
+                    }
+                    total += c;
+                    __syncwarp();
+                }
+                if (!kFill && lane == 0) A.cnt[p] = total;
+                clear_S(W, vbits, m);
+            }
+            __syncthreads();
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
+            __syncthreads();
+            seg = end;
+        }
+    }
+}
+
+__global__ void k_level_ranges(const uint32_t* __restrict__ efilt, const uint64_t* __restrict__ toff, int64_t E,
+                               uint64_t* __restrict__ tlo, uint64_t* __restrict__ thi) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
+        if (p > 0 && efilt[p - 1] == efilt[p]) continue;   // not a level start
+        int64_t q = p + 1;
+        while (q < E && efilt[q] == efilt[p]) ++q;
+        for (int64_t r = p; r < q; ++r) {
+            tlo[r] = toff[p];
+            thi[r] = toff[q];
+        }
+    }
+}
+
+size_t tet_smem(int64_t n, int warps) {
+    const int64_t nvw = (n + 31) >> 5;
+    return (size_t)((n * 4 + 15) / 16) * 16 + (size_t)warps * ((size_t)((nvw * 4 + 15) / 16) * 16) +
+           (size_t)warps * sizeof(TetScratch);
+}
+
+int tet_warps(int64_t n) {
+    const int64_t avail = (int64_t)device_max_smem_optin() - 1024;
+    for (int w = kWarps; w >= 4; w /= 2)
+        if ((int64_t)tet_smem(n, w) <= avail) return w;
+    return 0;
+}
+
+void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
+    const int warps = tet_warps(A.n);
+    if (warps < 4) fail(VRB_ENOTSUP, "tetrahedron kernel: n = %lld leaves no shared memory", (long long)A.n);
+    const int threads = warps * 32;
+    const size_t smem = tet_smem(A.n, warps);
+    if (fill)
+        VRB_CUDA(cudaFuncSetAttribute(k_tets<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    else
+        VRB_CUDA(cudaFuncSetAttribute(k_tets<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    uint64_t chunk = work / 8192 + 1;
+    if (chunk < 16384) chunk = 16384;
+    A.chunk = chunk;
+    A.ntasks = (int64_t)((work + chunk - 1) / chunk);
+    if (A.ntasks < 1) A.ntasks = 1;
+    A.task_lo = A.ntasks * part / nparts;
+    A.task_hi = A.ntasks * (part + 1) / nparts;
+    if (A.task_lo >= A.task_hi) return;
+    DBuf<unsigned long long> counter(1, s);
+    DBuf<unsigned> overflow(1, s);
+    VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
+    VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
+    A.task_counter = counter.get();
+    A.overflow = overflow.get();
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count(), A.task_hi - A.task_lo);
+    if (fill)
+        k_tets<true><<<grid, threads, smem, s>>>(A);
+    else
+        k_tets<false><<<grid, threads, smem, s>>>(A);
+    VRB_LAUNCH_CHECK();
+    unsigned h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, overflow.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (h) fail(VRB_ENOTSUP, "an edge owns more than %d triangles; tetrahedra not supported for this input", kS);
+}
+
+TetArgs tet_args(const Graph& g, const TriLevels& L) {
+    TetArgs A{};
+    A.n = g.n;
+    A.E = g.E;
+    A.off = g.off.get();
+    A.nkr = g.nkr.get();
+    A.nr = g.nr.get();
+    A.np = g.np.get();
+    A.packed = g.packed ? 1 : 0;
+    A.plan = g.plan.get();
+    A.hosted_v = g.hosted_v.get();
+    A.work_pre = g.work_pre.get();
+    A.toff = L.toff;
+    A.tlo = L.tlo.get();
+    A.thi = L.thi.get();
+    A.tv = L.tv;
+    return A;
+}
+
+}  // namespace
+
+void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, const uint32_t* tv, cudaStream_t s,
+                     TriLevels& L) {
+    L.toff = toff;
+    L.tv = tv;
+    L.tlo.alloc(E, s);
+    L.thi.alloc(E, s);
+    if (E == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
+    k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get());
+    VRB_LAUNCH_CHECK();
+}
+
+void count_tets(const Graph& g, const TriLevels& L, uint32_t* cnt, int part, int nparts, cudaStream_t s) {
+    if (g.E == 0) return;
+    VRB_CUDA(cudaMemsetAsync(cnt, 0, g.E * sizeof(uint32_t), s));
+    if (g.work == 0) return;
+    TetArgs A = tet_args(g, L);
+    A.cnt = cnt;
+    launch_tets(A, false, g.work, part, nparts, s);
+}
+
+void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const uint64_t* qoff, int64_t p_lo,
+               int64_t p_hi, uint64_t slot0, uint32_t* qv, uint32_t* qf, uint32_t* rows, cudaStream_t s) {
+    if (g.E == 0 || g.work == 0 || p_lo >= p_hi) return;
+    TetArgs A = tet_args(g, L);
+    A.efilt = efilt;
+    A.qoff = qoff;
+    A.p_lo = p_lo;
+    A.p_hi = p_hi;
+    A.slot0 = slot0;
+    A.qv = qv;
+    A.qf = qf;
+    A.rows = rows;
+    launch_tets(A, true, g.work, 0, 1, s);
+}
+
+}  // namespace vrb

@@ -269,6 +269,26 @@ unsigned grid_of(int64_t n) {
     return (unsigned)(g < 1 ? 1 : (g > 4096 ? 4096 : g));
 }
 
+// Owner-edge range [b[0], b[1]) of `rank`: level-aligned split of the
+// simplex offsets off (E + 1 entries) into `world` equal parts.
+void partition_range(const uint64_t* off, const uint32_t* efilt, int64_t E, int world, int rank, cudaStream_t s,
+                     int64_t* b) {
+    DBuf<int64_t> bd(world + 1, s);
+    k_partition<<<1, 64, 0, s>>>(off, efilt, E, world, bd.get());
+    VRB_LAUNCH_CHECK();
+    VRB_CUDA(cudaMemcpyAsync(b, bd.get() + rank, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+}
+
+// total = off[E], lo = off[b[0]], hi = off[b[1]]
+void read_offsets(const uint64_t* off, int64_t E, const int64_t* b, cudaStream_t s, uint64_t& total, uint64_t& lo,
+                  uint64_t& hi) {
+    VRB_CUDA(cudaMemcpyAsync(&total, off + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(&lo, off + b[0], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(&hi, off + b[1], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+}
+
 // The shared body of vrb_build / vrb_build_dist.
 void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
                 cudaStream_t s, vrb_handle* out) {
@@ -311,7 +331,6 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             h->verts[1] = ev ? ev + 2 * lo : nullptr;
             h->filt[1] = efilt ? efilt + lo : nullptr;
         }
-        if (h->K >= 3) fail(VRB_ENOTSUP, "tetrahedra (maxdim 2) are not built yet");
         if (h->K >= 2) {
             if (n > dense_map_limit())
                 fail(VRB_ENOTSUP, "n = %lld exceeds the shared-memory vertex map (%lld)", (long long)n,
@@ -319,11 +338,12 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             Graph g;
             build_graph(ev, n, E, s, g);
             timer.mark(2);
+            // ---- triangles: count per owner edge (work split over the ranks), offsets
             DBuf<uint32_t> cnt(E, s);
             count_triangles(g, cnt.get(), rank, world, s);
             if (world > 1) {
-                // the one exchange: every rank counted a disjoint, work-balanced
-                // part of the owner edges; gather and add the parts
+                // the exchange: every rank counted a disjoint, work-balanced part
+                // of the owner edges; gather and add the parts
                 DBuf<uint32_t> all((size_t)E * world, s);
                 if (comm->allgather(cnt.get(), all.get(), E * sizeof(uint32_t), (void*)s, comm->ctx) != 0)
                     fail(VRB_ECOMM, "allgather of triangle counts failed");
@@ -333,33 +353,73 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             }
             DBuf<uint64_t> toff(E + 1, s);
             exclusive_scan(cnt.get(), toff.get(), E, s);
-            int64_t bounds[2] = {0, E};
-            if (world > 1) {
-                DBuf<int64_t> b(world + 1, s);
-                k_partition<<<1, 64, 0, s>>>(toff.get(), efilt, E, world, b.get());
-                VRB_LAUNCH_CHECK();
-                VRB_CUDA(cudaMemcpyAsync(bounds, b.get() + rank, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-            }
-            uint64_t tb[3] = {0, 0, 0};
-            VRB_CUDA(cudaMemcpyAsync(&tb[0], toff.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-            VRB_CUDA(cudaStreamSynchronize(s));
-            VRB_CUDA(cudaMemcpyAsync(&tb[1], toff.get() + bounds[0], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-            VRB_CUDA(cudaMemcpyAsync(&tb[2], toff.get() + bounds[1], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-            VRB_CUDA(cudaStreamSynchronize(s));
-            const uint64_t T = tb[0];
+            // owner-edge range of this rank (whole levels); with tetrahedra every
+            // rank needs all triangles (face positions of D_3)
+            int64_t tb_[2] = {0, E};
+            if (world > 1 && h->K == 2) partition_range(toff.get(), efilt, E, world, rank, s, tb_);
+            uint64_t T = 0, t0 = 0, t1 = 0;
+            read_offsets(toff.get(), E, tb_, s, T, t0, t1);
             if (T >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu triangles exceed u32 positions", (unsigned long long)T);
             h->count[2] = (int64_t)T;
-            h->local_off[2] = (int64_t)tb[1];
-            h->local_n[2] = (int64_t)(tb[2] - tb[1]);
+            h->local_off[2] = (int64_t)t0;
+            h->local_n[2] = (int64_t)(t1 - t0);
             const int64_t Tl = h->local_n[2];
-            h->verts[2] = h->own<uint32_t>(3 * Tl, s);
-            h->filt[2] = h->own<uint32_t>(Tl, s);
-            if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[2] = h->own<uint32_t>(3 * Tl, s);
+            uint32_t* tv = h->own<uint32_t>(3 * Tl, s);
+            uint32_t* tf = h->own<uint32_t>(Tl, s);
+            uint32_t* trows = nullptr;
+            if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * Tl, s);
             timer.mark(3);
-            fill_triangles(g, efilt, toff.get(), bounds[0], bounds[1], tb[1], h->verts[2], h->filt[2], h->rows[2], s);
+            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, s);
             timer.mark(4);
-            sort_tie_groups(efilt, toff.get(), E, bounds[0], bounds[1], n, h->verts[2], h->rows[2], s);
+            sort_tie_groups(2, efilt, toff.get(), E, tb_[0], tb_[1], n, tv, trows, s);
             timer.mark(5);
+            h->verts[2] = tv;
+            h->filt[2] = tf;
+            h->rows[2] = trows;
+            if (h->K >= 3) {
+                // ---- tetrahedra (all triangles are on this rank)
+                TriLevels L;
+                triangle_levels(efilt, toff.get(), E, tv, s, L);
+                DBuf<uint32_t> qc(E, s);
+                count_tets(g, L, qc.get(), rank, world, s);
+                if (world > 1) {
+                    DBuf<uint32_t> all((size_t)E * world, s);
+                    if (comm->allgather(qc.get(), all.get(), E * sizeof(uint32_t), (void*)s, comm->ctx) != 0)
+                        fail(VRB_ECOMM, "allgather of tetrahedron counts failed");
+                    k_sum_slices<<<grid_of(E), 256, 0, s>>>(all.get(), E, world, qc.get());
+                    VRB_LAUNCH_CHECK();
+                }
+                DBuf<uint64_t> qoff(E + 1, s);
+                exclusive_scan(qc.get(), qoff.get(), E, s);
+                int64_t qb[2] = {0, E};
+                if (world > 1) partition_range(qoff.get(), efilt, E, world, rank, s, qb);
+                uint64_t Q = 0, q0 = 0, q1 = 0;
+                read_offsets(qoff.get(), E, qb, s, Q, q0, q1);
+                if (Q >= 0xFFFFFFFFull)
+                    fail(VRB_EOVERFLOW, "%llu tetrahedra exceed u32 positions", (unsigned long long)Q);
+                h->count[3] = (int64_t)Q;
+                h->local_off[3] = (int64_t)q0;
+                h->local_n[3] = (int64_t)(q1 - q0);
+                const int64_t Ql = h->local_n[3];
+                h->verts[3] = h->own<uint32_t>(4 * Ql, s);
+                h->filt[3] = h->own<uint32_t>(Ql, s);
+                if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[3] = h->own<uint32_t>(4 * Ql, s);
+                fill_tets(g, L, efilt, qoff.get(), qb[0], qb[1], q0, h->verts[3], h->filt[3], h->rows[3], s);
+                sort_tie_groups(3, efilt, qoff.get(), E, qb[0], qb[1], n, h->verts[3], h->rows[3], s);
+                timer.mark(4);
+                // triangles: this rank reports its slice of the (replicated) dimension 2
+                if (world > 1) {
+                    int64_t tp[2] = {0, E};
+                    partition_range(toff.get(), efilt, E, world, rank, s, tp);
+                    uint64_t Tt, a0, a1;
+                    read_offsets(toff.get(), E, tp, s, Tt, a0, a1);
+                    h->local_off[2] = (int64_t)a0;
+                    h->local_n[2] = (int64_t)(a1 - a0);
+                    h->verts[2] = tv + 3 * a0;
+                    h->filt[2] = tf + a0;
+                    h->rows[2] = trows ? trows + 3 * a0 : nullptr;
+                }
+            }
         }
         VRB_CUDA(cudaStreamSynchronize(s));
         VRB_CUDA(cudaGetLastError());

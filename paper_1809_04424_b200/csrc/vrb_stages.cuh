@@ -60,10 +60,24 @@ void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaSt
 // (slot0 = toff[p_lo]).
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
                     uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, cudaStream_t s);
-// Reorder the triangles of every tie group (>= 2 edges sharing a level) into
-// lex order (readings A3, A4); only the range [p_lo, p_hi) of owner edges.
-void sort_tie_groups(const uint32_t* efilt, const uint64_t* toff, int64_t E, int64_t p_lo, int64_t p_hi,
-                     int64_t n, uint32_t* tv, uint32_t* rows, cudaStream_t s);
+// Reorder the k-simplices (k = 2, 3) of every tie group (>= 2 edges sharing a
+// level) into lex order (readings A3, A4); only owner edges in [p_lo, p_hi).
+// off = per-owner-edge simplex offsets (E + 1); verts/rows: (k+1) u32 each.
+void sort_tie_groups(int k, const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi,
+                     int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s);
+
+// S6 + S7 + S8 for tetrahedra (tetrahedra.cu).  Needs the complete triangle
+// arrays of dimension 2 (face positions for D_3).
+struct TriLevels {
+    const uint64_t* toff = nullptr;   // E + 1 triangle offsets per owner edge
+    const uint32_t* tv = nullptr;     // 3T vertices (global order)
+    DBuf<uint64_t> tlo, thi;          // E: triangle range of each edge's filtration level
+};
+void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, const uint32_t* tv, cudaStream_t s,
+                     TriLevels& L);
+void count_tets(const Graph& g, const TriLevels& L, uint32_t* cnt, int part, int nparts, cudaStream_t s);
+void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const uint64_t* qoff, int64_t p_lo,
+               int64_t p_hi, uint64_t slot0, uint32_t* qv, uint32_t* qf, uint32_t* rows, cudaStream_t s);
 
 int64_t dense_map_limit();   // largest n the shared-memory vertex map supports
 

@@ -61,6 +61,15 @@ def compare(vrb, X, maxdim, radius, strict=False, via_torch_alloc=False):
         np.testing.assert_array_equal(_np(res.boundary(2)), tr)
         cp = res.boundary_colptr(2).cpu().numpy()
         np.testing.assert_array_equal(cp, 3 * np.arange(tv.shape[0] + 1))
+    if maxdim >= 2:
+        qv, qf, qr = o.simplices(3)
+        assert res.count(3)[0] == qv.shape[0]
+        gqv, gqf = res.simplices(3)
+        np.testing.assert_array_equal(_np(gqv), qv)
+        np.testing.assert_array_equal(_np(gqf), qf)
+        np.testing.assert_array_equal(_np(res.boundary(3)), qr)
+        cp = res.boundary_colptr(3).cpu().numpy()
+        np.testing.assert_array_equal(cp, 4 * np.arange(qv.shape[0] + 1))
     return res, o
 
 
@@ -82,6 +91,36 @@ def test_c1(vrb):
 def test_c2_triangles(vrb):
     w = workloads.WORKLOADS["C2"]
     compare(vrb, w.points(), 1, w.radius)
+
+
+def test_c2_tetrahedra(vrb):
+    w = workloads.WORKLOADS["C2"]
+    compare(vrb, w.points(), w.maxdim, w.radius)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_small_tetrahedra(vrb, seed):
+    rng = np.random.default_rng(5000 + seed)
+    kind = ["uniform", "gauss", "lattice", "halfint", "dups"][seed % 5]
+    n = int(rng.integers(0, 45))
+    d = int(rng.integers(1, 5))
+    X = workloads.random_cloud(5000 + seed, n, d, kind)
+    radius = [math.inf, 0.5, 1.0, 1.5, 2.0][seed % 5]
+    compare(vrb, X, 2, radius, strict=bool(seed % 6 == 1))
+
+
+def test_lattice_tetrahedra_ties(vrb):
+    # 4x4x4 lattice: heavy length ties in dimension 3 too
+    X = workloads.integer_lattice(4, 3)
+    compare(vrb, X, 2, math.inf)
+    compare(vrb, X, 2, 1.8)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_wide_list_layout_tetrahedra(vrb, seed, monkeypatch):
+    monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
+    X = workloads.random_cloud(900 + seed, 60, 3, ["uniform", "lattice"][seed % 2])
+    compare(vrb, X, 2, [0.6, 1.5][seed % 2])
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 3])
@@ -312,3 +351,68 @@ def test_c5a_edges_full(vrb):
     ll = lens[torch.from_numpy(idx).cuda()].cpu().numpy()
     for (i, j), L in zip(vv, ll):
         assert oracle.length(X, int(i), int(j)) == L
+
+
+def test_full_size_c4_tetrahedra(vrb):
+    # C4: 5000-point noisy sphere, cap 0.40, maxdim 2: edges and triangles
+    # element by element; 4.3e8 tetrahedra by (a) the per-level histogram
+    # (golden digest from oracle/), (b) strict (filt, lex) order, (c) every D_3
+    # row is a face triangle of the column with filt <= and the last row's filt
+    # equal to the column's, (d) sampled levels element by element.
+    path = os.path.join(GOLDEN, "c4_levels.json")
+    golden = json.load(open(path))
+    w = workloads.WORKLOADS["C4"]
+    X = w.points()
+    assert hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest() == golden["points_sha256"]
+    vrb.use_torch_allocator(True)
+    try:
+        res = vrb.build(torch.from_numpy(X).cuda(), maxdim=2, radius=w.radius)
+        o = oracle.Oracle(X, w.radius)
+        ev, ef, el, vor = o.edges()
+        np.testing.assert_array_equal(_np(res.simplices(1)[0]), ev)
+        np.testing.assert_array_equal(_np(res.simplices(1)[1]), ef)
+        tv, tf, tr = o.simplices(2)
+        np.testing.assert_array_equal(_np(res.simplices(2)[0]), tv)
+        np.testing.assert_array_equal(_np(res.simplices(2)[1]), tf)
+        np.testing.assert_array_equal(_np(res.boundary(2)), tr)
+        qv, qf = res.simplices(3)
+        qr = res.boundary(3)
+        Q = qv.shape[0]
+        assert Q == golden["count"]
+        hist = torch.bincount(qf.to(torch.int64), minlength=o.E + 1).cpu().numpy().astype(np.uint64)
+        assert hashlib.sha256(hist.tobytes()).hexdigest() == golden["hist_sha256"]
+        dev = res.device
+        tvd = torch.from_numpy(tv.astype(np.int64)).to(dev)
+        tfd = torch.from_numpy(tf.astype(np.int64)).to(dev)
+        chunk = 1 << 26
+        for s in range(0, Q, chunk):
+            e = min(Q, s + chunk + 1)
+            v = qv[s:e].to(torch.int64)
+            f = qf[s:e].to(torch.int64)
+            r = qr[s:e].to(torch.int64) & 0xFFFFFFFF
+            assert bool((v[:, :-1] < v[:, 1:]).all())
+            code = (v[:, 0] << 48) | (v[:, 1] << 32) | (v[:, 2] << 16) | v[:, 3]
+            df, dc = f[1:] - f[:-1], code[1:] - code[:-1]
+            assert bool(((df > 0) | ((df == 0) & (dc > 0))).all())
+            assert bool((r[:, :-1] < r[:, 1:]).all())
+            # each row is the face of the column missing one vertex
+            for c in range(4):
+                face = tvd[r[:, c]]                                  # (m, 3)
+                inside = (face.unsqueeze(2) == v.unsqueeze(1)).any(2).all(1)
+                assert bool(inside.all())
+            assert bool((tfd[r[:, 3]] == f).all())
+            assert bool((torch.maximum(tfd[r].max(1).values, tfd[r[:, 3]]) == f).all())
+            del v, f, r, code
+        start = np.concatenate([[0], np.cumsum(hist)]).astype(np.int64)
+        rng = np.random.default_rng(4)
+        levels = sorted(set(rng.integers(1, o.nvals + 1, 25).tolist()))
+        for lvl in levels:
+            sv, _ = o.simplices_at_filt(3, int(lvl))
+            a, b = start[lvl], start[lvl + 1]
+            assert b - a == len(sv)
+            np.testing.assert_array_equal(_np(qv[a:b]), sv)
+        del res
+    finally:
+        torch.cuda.synchronize()
+        vrb.use_torch_allocator(False)
+        torch.cuda.empty_cache()

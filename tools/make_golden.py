@@ -54,8 +54,8 @@ def digest(config: str, k: int = 2) -> dict:
 
 
 if __name__ == "__main__":
-    for cfg in sys.argv[1:] or ["C3", "C5B"]:
-        d = digest(cfg)
+    for cfg in sys.argv[1:] or ["C3", "C5B", "C4"]:
+        d = digest(cfg, k=3 if workloads.WORKLOADS[cfg].maxdim >= 2 else 2)
         path = os.path.join(ROOT, "tests", "golden", f"{cfg.lower()}_levels.json")
         with open(path, "w") as f:
             json.dump(d, f, indent=1)
