@@ -300,10 +300,26 @@ def build(points, maxdim: int = 1, radius: float = math.inf, strict: bool = Fals
     return VRResult(h.value, device)
 
 
+def allgather_bytes(src, dst, group=None):
+    """dst (world * nbytes, uint8) <- all-gather of src (nbytes, uint8) over the
+    process group: NCCL on device tensors directly, other backends (gloo)
+    through host memory.  Used by the collective callback of build_dist."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" or src.device.type == "cpu":
+        dist.all_gather_into_tensor(dst, src, group=group)
+        return
+    hs = src.cpu()
+    hd = torch.empty(dst.numel(), dtype=dst.dtype)
+    dist.all_gather_into_tensor(hd, hs, group=group)
+    dst.copy_(hd)
+
+
 def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
                skip_boundary: bool = False, group=None, stream=None) -> VRResult:
     """vrb_build_dist: one process per GPU; every rank passes the same points.
-    The all-gather the library asks for runs over torch.distributed (NCCL)."""
+    The all-gather the library asks for runs over torch.distributed."""
     import torch
     import torch.distributed as dist
 
@@ -315,15 +331,12 @@ def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool =
     if skip_boundary:
         flags |= VRB_SKIP_BOUNDARY
 
-    def _allgather(send, recv, nbytes, stream, ctx):
+    def _allgather(send, recv, nbytes, stream_, ctx):
         try:
-            src = _view(send, (nbytes,), "<i4", None, device) if nbytes % 4 == 0 else None
-            dst = _view(recv, (nbytes * world,), "<i4", None, device) if nbytes % 4 == 0 else None
-            if src is None:
-                return 1
-            src = src[: nbytes // 4]
-            dst = dst[: world * nbytes // 4]
-            dist.all_gather_into_tensor(dst, src, group=group)
+            src = torch.as_tensor(_CAI(send, (nbytes,), "|u1", None), device=device)
+            dst = torch.as_tensor(_CAI(recv, (nbytes * world,), "|u1", None), device=device)
+            allgather_bytes(src, dst, group)
+            torch.cuda.current_stream(device).synchronize()
             return 0
         except Exception as e:   # reported as VRB_ECOMM
             print("vrb allgather failed:", e)
