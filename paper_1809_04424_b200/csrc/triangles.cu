@@ -265,11 +265,11 @@ __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* _
 //         prefix(word) + popc(word below its bit); stage (k, t) in the window
 //  flush: one lane per triangle (flush_window)
 // kBits ranks per round (rounds only when deg x > kBits), kWin slots per window.
-template <bool kPacked>
-__device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __restrict__ map,
-                                          WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                          uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
-                                          uint32_t filt) {
+template <bool kPacked, bool kOneRound>
+__device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t* __restrict__ map,
+                                               WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                               uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                               uint32_t filt) {
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
@@ -278,7 +278,7 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
     const int ngroups = (int)((len + mis + 3) >> 2);
     const uint32_t win = kPacked ? (uint32_t)kWin : (uint32_t)kWin / 2;
     for (uint32_t R = 0; R < degx; R += kBits) {
-        const uint32_t lim = min((uint32_t)kBits, degx - R);
+        const uint32_t lim = kOneRound ? degx : min((uint32_t)kBits, degx - R);
         clear_bits(W, lim);
         // ---- mark
         for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
@@ -294,11 +294,11 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                 const int i = i0 + u * 32 + lane;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int t = 4 * i + e - mis;
+                    const uint32_t t = (uint32_t)(4 * i + e - mis);
                     const uint32_t w = pick(qk[u], e);
                     const uint32_t k = kPacked ? (w & 0xFFFFu) : w;
                     const uint32_t r = (kPacked ? (w >> 16) : pick(qr[u], e)) - R;
-                    if (t >= 0 && t < (int)len && r < (uint32_t)kBits && map[k] < p)
+                    if (t < len && (kOneRound || r < (uint32_t)kBits) && map[k] < p)
                         atomicOr(&W->bits[r >> 5], 1u << (r & 31));
                 }
             }
@@ -320,19 +320,20 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
                     const int i = i0 + u * 32 + lane;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int t = 4 * i + e - mis;
+                        const uint32_t t = (uint32_t)(4 * i + e - mis);
                         const uint32_t w = pick(qk[u], e);
                         const uint32_t r = (kPacked ? (w >> 16) : pick(qr[u], e)) - R;
-                        if (t < 0 || t >= (int)len || r >= (uint32_t)kBits) continue;
+                        if (t >= len || (!kOneRound && r >= (uint32_t)kBits)) continue;
                         const uint32_t wd = W->bits[r >> 5];
+                        const uint32_t below = wd & ((2u << (r & 31)) - 1u);   // bits <= r
                         if (!((wd >> (r & 31)) & 1u)) continue;
-                        const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((1u << (r & 31)) - 1u)) - w0;
+                        const uint32_t pos = W->wpre[r >> 5] + __popc(below) - 1u - w0;
                         if (pos >= win) continue;
                         if (kPacked) {
-                            W->rec[pos] = (w & 0xFFFFu) | ((uint32_t)t << 16);
+                            W->rec[pos] = (w & 0xFFFFu) | (t << 16);
                         } else {
                             W->rec[2 * pos] = w;
-                            W->rec[2 * pos + 1] = (uint32_t)t;
+                            W->rec[2 * pos + 1] = t;
                         }
                     }
                 }
@@ -343,7 +344,19 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
             __syncwarp();
         }
         slot += count;
+        if (kOneRound) break;
     }
+}
+
+template <bool kPacked>
+__device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __restrict__ map,
+                                          WarpScratch* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                          uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                          uint32_t filt) {
+    if (degx <= (uint32_t)kBits)
+        warp_fill_impl<kPacked, true>(A, map, W, p, y, x, len, offx, degx, slot, filt);
+    else
+        warp_fill_impl<kPacked, false>(A, map, W, p, y, x, len, offx, degx, slot, filt);
 }
 
 template <bool kFill>
