@@ -38,7 +38,7 @@ constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBits = 4096;     // ranks of x's id list per round
 constexpr int kWords = kBits / 32;
-constexpr int kS = 1024;        // max |S(p)| handled (else VRB_ENOTSUP)
+constexpr int kS = 512;         // max |S(p)| handled (else VRB_ENOTSUP)
 
 struct TetArgs {
     int64_t n, E;
@@ -59,6 +59,9 @@ struct TetArgs {
     const uint64_t* tlo;      // E: start of the triangle range of p's level
     const uint64_t* thi;      // E: end of it
     const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
+    const unsigned long long* hkeys;   // triangle lex code -> position (open addressing)
+    const uint32_t* hvals;
+    uint64_t hmask;
     // count
     uint32_t* cnt;
     // fill
@@ -106,6 +109,24 @@ __device__ __forceinline__ uint32_t lb_u32(const uint32_t* a, uint32_t lo, uint3
     return lo;
 }
 
+// Warp-cooperative lower bound in an ascending u32 array: 32 probes per
+// round, so ~log32(n) dependent loads instead of log2(n).
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t idx = min(hi - 1, lo + (uint32_t)(lane + 1) * step - 1);
+        const bool less = __ldg(a + idx) < v;
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, less));
+        const uint32_t nlo = lo + c * step;
+        hi = min(hi, nlo + step);
+        lo = min(nlo, hi);
+    }
+    const bool less = lo + lane < hi && __ldg(a + lo + lane) < v;
+    return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
 __device__ __forceinline__ void sort3v(uint32_t& a, uint32_t& b, uint32_t& c) {
     uint32_t t;
     if (a > b) { t = a; a = b; b = t; }
@@ -133,6 +154,41 @@ __device__ __forceinline__ uint32_t tri_pos(const TetArgs& A, uint32_t f, uint32
         if (less) lo = mid + 1; else hi = mid;
     }
     return (uint32_t)lo;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 33; z *= 0xff51afd7ed558ccdull;
+    z ^= z >> 33; z *= 0xc4ceb9fe1a85ec53ull;
+    z ^= z >> 33;
+    return z;
+}
+
+__device__ __forceinline__ uint64_t tri_code(uint32_t a, uint32_t b, uint32_t c) {
+    return ((uint64_t)a << 42) | ((uint64_t)b << 21) | (uint64_t)c;
+}
+
+// Position of triangle {a < b < c}: hash lookup (the key is always present).
+__device__ __forceinline__ uint32_t tri_lookup(const TetArgs& A, uint32_t a, uint32_t b, uint32_t c) {
+    const uint64_t code = tri_code(a, b, c);
+    uint64_t h = mix64(code) & A.hmask;
+    for (;;) {
+        const unsigned long long k = __ldg(A.hkeys + h);
+        if (k == code) return __ldg(A.hvals + h);
+        h = (h + 1) & A.hmask;
+    }
+}
+
+__global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, unsigned long long* __restrict__ keys,
+                           uint32_t* __restrict__ vals, uint64_t mask) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t code = tri_code(tv[3 * q], tv[3 * q + 1], tv[3 * q + 2]);
+        uint64_t h = mix64(code) & mask;
+        for (;;) {
+            const unsigned long long prev = atomicCAS(keys + h, ~0ull, (unsigned long long)code);
+            if (prev == ~0ull || prev == code) { vals[h] = (uint32_t)q; break; }
+            h = (h + 1) & mask;
+        }
+    }
 }
 
 // Warp: S(p) sorted by id into W->Sk / W->Spx, flags S in the vertex bitmap.
@@ -209,15 +265,13 @@ __device__ void clear_S(TetScratch* __restrict__ W, uint32_t* __restrict__ vbits
 // For k = Sk[ki]: mark l in S, l > k, pos(k,l) < p; returns #marked and
 // fills lpre.
 __device__ uint32_t mark_l(const TetArgs& A, TetScratch* __restrict__ W, const uint32_t* __restrict__ vbits,
-                           uint32_t p, uint32_t ki, uint32_t m) {
+                           const uint32_t* __restrict__ vpre, uint32_t p, uint32_t ki, uint32_t m) {
     const int lane = threadIdx.x & 31;
     const uint32_t k = W->Sk[ki];
     const uint64_t ok0 = A.off[k], ok1 = A.off[k + 1];
     const uint32_t* npk = A.np + ok0;
     // k's neighbours older than p: a prefix of its position-ordered list
-    uint32_t plen = 0;
-    if (lane == 0) plen = lb_u32(npk, 0, (uint32_t)(ok1 - ok0), p);
-    plen = __shfl_sync(0xffffffffu, plen, 0);
+    const uint32_t plen = warp_lower_bound(npk, (uint32_t)(ok1 - ok0), p);
     const uint32_t nw = (m + 31) >> 5;
     for (uint32_t w = lane; w < nw; w += 32) W->lbits[w] = 0u;
     __syncwarp();
@@ -225,12 +279,11 @@ __device__ uint32_t mark_l(const TetArgs& A, TetScratch* __restrict__ W, const u
     const uint32_t* lk = A.nkr + ok0;
     for (uint32_t t = lane; t < plen; t += 32) {
         const uint32_t l = __ldg(lk + t) & kmask;
-        if (l <= k || !((vbits[l >> 5] >> (l & 31)) & 1u)) continue;
-        const uint32_t j = lb_u32(W->Sk, ki + 1, m, l);
-        if (j < m && W->Sk[j] == l) {
-            atomicOr(&W->lbits[j >> 5], 1u << (j & 31));
-            W->lpos[j] = __ldg(npk + t);
-        }
+        const uint32_t vw = vbits[l >> 5];
+        if (l <= k || !((vw >> (l & 31)) & 1u)) continue;
+        const uint32_t j = vpre[l >> 5] + __popc(vw & ((1u << (l & 31)) - 1u));   // index of l in S
+        atomicOr(&W->lbits[j >> 5], 1u << (j & 31));
+        W->lpos[j] = __ldg(npk + t);
     }
     __syncwarp();
     uint32_t tot = 0;
@@ -258,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
     const size_t vb_b = (size_t)((nvw * 4 + 15) / 16) * 16;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nthreads = blockDim.x;
-    uint32_t* vbits = reinterpret_cast<uint32_t*>(smem + map_b + (size_t)wid * vb_b);
-    TetScratch* W = reinterpret_cast<TetScratch*>(smem + map_b + (size_t)(nthreads / 32) * vb_b) + wid;
+    uint32_t* vbits = reinterpret_cast<uint32_t*>(smem + map_b + (size_t)wid * 2 * vb_b);
+    uint32_t* vpre = vbits + vb_b / 4;
+    TetScratch* W = reinterpret_cast<TetScratch*>(smem + map_b + (size_t)(nthreads / 32) * 2 * vb_b) + wid;
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
     __shared__ unsigned s_next;
@@ -312,6 +366,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                     clear_S(W, vbits, kS);
                     continue;
                 }
+                {   // vpre[w] = #S members in words < w (index of a member = its rank by id)
+                    const uint32_t per = (uint32_t)((nvw + 31) >> 5);
+                    const uint32_t w0 = lane * per, w1 = min((uint32_t)nvw, w0 + per);
+                    uint32_t tot = 0;
+                    for (uint32_t w = w0; w < w1; ++w) tot += __popc(vbits[w]);
+                    uint32_t incl = tot;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    uint32_t run = incl - tot;
+                    for (uint32_t w = w0; w < w1; ++w) { vpre[w] = run; run += __popc(vbits[w]); }
+                    __syncwarp();
+                }
                 uint64_t slot = 0;
                 uint32_t filt = 0;
                 bool direct = false;
@@ -324,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                 }
                 uint32_t total = 0;
                 for (uint32_t ki = 0; ki + 1 < m; ++ki) {
-                    const uint32_t c = mark_l(A, W, vbits, p, ki, m);
+                    const uint32_t c = mark_l(A, W, vbits, vpre, p, ki, m);
                     if (kFill && c) {
                         const uint32_t k = W->Sk[ki];
                         const uint32_t pxk = W->Spx[ki];
@@ -350,16 +419,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                                     r[1] = (uint32_t)(tbase + j);
                                 } else {
                                     a = y; b = x; cc = k; sort3v(a, b, cc);
-                                    r[0] = tri_pos(A, p, a, b, cc);
+                                    r[0] = tri_lookup(A, a, b, cc);
                                     a = y; b = x; cc = l; sort3v(a, b, cc);
-                                    r[1] = tri_pos(A, p, a, b, cc);
+                                    r[1] = tri_lookup(A, a, b, cc);
                                 }
-                                // (y, k, l): owner = max of pos(y,k), pos(y,l), pos(k,l)
-                                a = y; b = k; cc = l; sort3v(a, b, cc);
-                                r[2] = tri_pos(A, max(max(pyk, pyl), pkl), a, b, cc);
-                                // (x, k, l)
-                                a = x; b = k; cc = l; sort3v(a, b, cc);
-                                r[3] = tri_pos(A, max(max(pxk, pxl), pkl), a, b, cc);
+                                a = y; b = k; cc = l; sort3v(a, b, cc);   // (y, k, l)
+                                r[2] = tri_lookup(A, a, b, cc);
+                                a = x; b = k; cc = l; sort3v(a, b, cc);   // (x, k, l)
+                                r[3] = tri_lookup(A, a, b, cc);
+                                (void)pxk; (void)pxl; (void)pyk; (void)pyl; (void)pkl;
                                 sort4v(r);
                                 uint32_t* rw = A.rows + 4 * s;
                                 rw[0] = r[0]; rw[1] = r[1]; rw[2] = r[2]; rw[3] = r[3];
@@ -395,7 +463,7 @@ __global__ void k_level_ranges(const uint32_t* __restrict__ efilt, const uint64_
 
 size_t tet_smem(int64_t n, int warps) {
     const int64_t nvw = (n + 31) >> 5;
-    return (size_t)((n * 4 + 15) / 16) * 16 + (size_t)warps * ((size_t)((nvw * 4 + 15) / 16) * 16) +
+    return (size_t)((n * 4 + 15) / 16) * 16 + (size_t)warps * 2 * ((size_t)((nvw * 4 + 15) / 16) * 16) +
            (size_t)warps * sizeof(TetScratch);
 }
 
@@ -457,6 +525,9 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.tlo = L.tlo.get();
     A.thi = L.thi.get();
     A.tv = L.tv;
+    A.hkeys = L.hkeys.get();
+    A.hvals = L.hvals.get();
+    A.hmask = L.hmask;
     return A;
 }
 
@@ -472,6 +543,21 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
     k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get());
     VRB_LAUNCH_CHECK();
+    // triangle position hash (load factor <= 1/2)
+    uint64_t T = 0;
+    VRB_CUDA(cudaMemcpyAsync(&T, toff + E, sizeof(T), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    uint64_t cap = 1024;
+    while (cap < 2 * T) cap <<= 1;
+    L.hmask = cap - 1;
+    L.hkeys.alloc(cap, s);
+    L.hvals.alloc(cap, s);
+    VRB_CUDA(cudaMemsetAsync(L.hkeys.get(), 0xFF, L.hkeys.bytes(), s));
+    if (T) {
+        const unsigned gh = (unsigned)std::min<int64_t>(ceil_div((int64_t)T, 256), (int64_t)device_sm_count() * 16);
+        k_tri_hash<<<gh, 256, 0, s>>>(tv, (int64_t)T, L.hkeys.get(), L.hvals.get(), L.hmask);
+        VRB_LAUNCH_CHECK();
+    }
 }
 
 void count_tets(const Graph& g, const TriLevels& L, uint32_t* cnt, int part, int nparts, cudaStream_t s) {
