@@ -59,8 +59,7 @@ struct TetArgs {
     const uint64_t* tlo;      // E: start of the triangle range of p's level
     const uint64_t* thi;      // E: end of it
     const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
-    const unsigned long long* hkeys;   // triangle lex code -> position (open addressing)
-    const uint32_t* hvals;
+    const ulonglong2* hslots;   // triangle lex code -> position: slot = (code, position), open addressing
     uint64_t hmask;
     // count
     uint32_t* cnt;
@@ -82,6 +81,7 @@ struct TetScratch {
     uint32_t lbits[kS / 32];  // l in S (by index) adjacent to the current k through an older edge
     uint32_t lpre[kS / 32];
     uint32_t lpos[kS];        // pos(k, l) for the marked l
+    uint32_t plen[kS];        // #neighbours of Sk[i] older than p (prefix of its position list)
 };
 
 __device__ __forceinline__ int64_t lb_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t v) {
@@ -172,20 +172,20 @@ __device__ __forceinline__ uint32_t tri_lookup(const TetArgs& A, uint32_t a, uin
     const uint64_t code = tri_code(a, b, c);
     uint64_t h = mix64(code) & A.hmask;
     for (;;) {
-        const unsigned long long k = __ldg(A.hkeys + h);
-        if (k == code) return __ldg(A.hvals + h);
+        const ulonglong2 sl = __ldg(A.hslots + h);   // key and position in one 16-byte slot
+        if (sl.x == code) return (uint32_t)sl.y;
         h = (h + 1) & A.hmask;
     }
 }
 
-__global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, unsigned long long* __restrict__ keys,
-                           uint32_t* __restrict__ vals, uint64_t mask) {
+__global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
+                           uint64_t mask) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t code = tri_code(tv[3 * q], tv[3 * q + 1], tv[3 * q + 2]);
         uint64_t h = mix64(code) & mask;
         for (;;) {
-            const unsigned long long prev = atomicCAS(keys + h, ~0ull, (unsigned long long)code);
-            if (prev == ~0ull || prev == code) { vals[h] = (uint32_t)q; break; }
+            const unsigned long long prev = atomicCAS(&slots[h].x, ~0ull, (unsigned long long)code);
+            if (prev == ~0ull || prev == code) { slots[h].y = (unsigned long long)q; break; }
             h = (h + 1) & mask;
         }
     }
@@ -271,7 +271,8 @@ __device__ uint32_t mark_l(const TetArgs& A, TetScratch* __restrict__ W, const u
     const uint64_t ok0 = A.off[k], ok1 = A.off[k + 1];
     const uint32_t* npk = A.np + ok0;
     // k's neighbours older than p: a prefix of its position-ordered list
-    const uint32_t plen = warp_lower_bound(npk, (uint32_t)(ok1 - ok0), p);
+    const uint32_t plen = W->plen[ki];
+    (void)ok1;
     const uint32_t nw = (m + 31) >> 5;
     for (uint32_t w = lane; w < nw; w += 32) W->lbits[w] = 0u;
     __syncwarp();
@@ -365,6 +366,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                     if (lane == 0) atomicOr(A.overflow, 1u);
                     clear_S(W, vbits, kS);
                     continue;
+                }
+                // older-neighbour prefix length of every k in S, one lane per k
+                for (uint32_t i = lane; i < m; i += 32) {
+                    const uint32_t k = W->Sk[i];
+                    const uint64_t o0 = A.off[k], o1 = A.off[k + 1];
+                    W->plen[i] = lb_u32(A.np + o0, 0, (uint32_t)(o1 - o0), p);
                 }
                 {   // vpre[w] = #S members in words < w (index of a member = its rank by id)
                     const uint32_t per = (uint32_t)((nvw + 31) >> 5);
@@ -525,8 +532,7 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.tlo = L.tlo.get();
     A.thi = L.thi.get();
     A.tv = L.tv;
-    A.hkeys = L.hkeys.get();
-    A.hvals = L.hvals.get();
+    A.hslots = L.hslots.get();
     A.hmask = L.hmask;
     return A;
 }
@@ -548,14 +554,13 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
     VRB_CUDA(cudaMemcpyAsync(&T, toff + E, sizeof(T), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     uint64_t cap = 1024;
-    while (cap < 2 * T) cap <<= 1;
+    while (cap < T + T / 2) cap <<= 1;   // load factor in (1/3, 2/3]
     L.hmask = cap - 1;
-    L.hkeys.alloc(cap, s);
-    L.hvals.alloc(cap, s);
-    VRB_CUDA(cudaMemsetAsync(L.hkeys.get(), 0xFF, L.hkeys.bytes(), s));
+    L.hslots.alloc(cap, s);
+    VRB_CUDA(cudaMemsetAsync(L.hslots.get(), 0xFF, L.hslots.bytes(), s));
     if (T) {
         const unsigned gh = (unsigned)std::min<int64_t>(ceil_div((int64_t)T, 256), (int64_t)device_sm_count() * 16);
-        k_tri_hash<<<gh, 256, 0, s>>>(tv, (int64_t)T, L.hkeys.get(), L.hvals.get(), L.hmask);
+        k_tri_hash<<<gh, 256, 0, s>>>(tv, (int64_t)T, L.hslots.get(), L.hmask);
         VRB_LAUNCH_CHECK();
     }
 }

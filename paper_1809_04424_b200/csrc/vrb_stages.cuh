@@ -72,8 +72,7 @@ struct TriLevels {
     const uint64_t* toff = nullptr;   // E + 1 triangle offsets per owner edge
     const uint32_t* tv = nullptr;     // 3T vertices (global order)
     DBuf<uint64_t> tlo, thi;          // E: triangle range of each edge's filtration level
-    DBuf<unsigned long long> hkeys;   // triangle lex code -> position, open addressing
-    DBuf<uint32_t> hvals;
+    DBuf<ulonglong2> hslots;          // (triangle lex code, position), open addressing
     uint64_t hmask = 0;
 };
 void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, const uint32_t* tv, cudaStream_t s,
