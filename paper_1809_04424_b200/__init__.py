@@ -19,7 +19,9 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libvrb.so")
+# VRB_LIB_PATH: an alternative build of the same library (tools/variants.py
+# experiment builds); the default is the in-tree libvrb.so
+LIB_PATH = os.environ.get("VRB_LIB_PATH") or os.path.join(_PKG, "libvrb.so")
 
 VRB_OK, VRB_EINVAL, VRB_ENOMEM, VRB_EOVERFLOW, VRB_ECUDA, VRB_ECOMM, VRB_ENOTSUP = range(7)
 STATUS_NAMES = {0: "VRB_OK", 1: "VRB_EINVAL", 2: "VRB_ENOMEM", 3: "VRB_EOVERFLOW", 4: "VRB_ECUDA",

@@ -41,14 +41,19 @@ def _headers():
     return hs
 
 
-def build(verbose: bool = False, extra: list[str] | None = None, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, extra: list[str] | None = None, force: bool = False,
+          out: str | None = None, objdir: str | None = None) -> str:
+    """Compile every csrc/*.cu and link libvrb.so (or `out`, with objects in
+    `objdir`: experiment variants built with extra -D flags)."""
+    OUT_ = out or OUT
+    OBJ_ = objdir or OBJ
+    os.makedirs(OBJ_, exist_ok=True)
     srcs = _sources()
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     flags = NVCC_FLAGS + list(extra or [])
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(OBJ_, os.path.basename(src)[:-3] + ".o")
         if (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(src)
                 and os.path.getmtime(obj) >= hdr_mtime):
             return obj
@@ -64,15 +69,15 @@ def build(verbose: bool = False, extra: list[str] | None = None, force: bool = F
 
     with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    if (force or not os.path.exists(OUT)
-            or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs)):
-        tmp = OUT + f".tmp{os.getpid()}"
+    if (force or not os.path.exists(OUT_)
+            or os.path.getmtime(OUT_) < max(os.path.getmtime(o) for o in objs)):
+        tmp = OUT_ + f".tmp{os.getpid()}"
         cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, OUT)
-    return OUT
+        os.replace(tmp, OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":

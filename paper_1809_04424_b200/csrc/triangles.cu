@@ -34,6 +34,7 @@
 //          one lane per triangle (streaming stores).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
@@ -46,8 +47,25 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBits = 4096;              // apex ranks per round (bitmap bits per warp)
 constexpr int kWords = kBits / 32;
 static_assert(kWords % 32 == 0, "bitmap words must split evenly over the lanes");
-constexpr int kWin = 512;                // triangles staged per output window (packed records)
+#ifndef VRB_TRI_WIN
+#define VRB_TRI_WIN 512
+#endif
+#ifndef VRB_TRI_MODE
+#define VRB_TRI_MODE 0
+#endif
+#ifndef VRB_TRI_BITSP
+#define VRB_TRI_BITSP 2048
+#endif
+#ifndef VRB_TRI_WINP
+#define VRB_TRI_WINP 512
+#endif
+constexpr int kWin = VRB_TRI_WIN;        // triangles staged per output window (packed records)
 constexpr int kRegGroups = 4;            // uint4 groups per lane in flight when streaming
+// packed lists (n, degrees <= 65536): the valid apexes are emitted from the
+// bitmap itself, so rounds are smaller and windows never re-stream the prefix
+constexpr int kBitsP = VRB_TRI_BITSP;    // apex ranks per round
+constexpr int kWordsP = kBitsP / 32;
+constexpr int kWinP = VRB_TRI_WINP;      // slots per window
 
 struct TriArgs {
     int64_t n, E;
@@ -111,51 +129,31 @@ __device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
 }
 
-// Prefetch the 128-byte lines of a list prefix into L2 (one line per lane).
-__device__ __forceinline__ void prefetch_l2(const uint32_t* lst, uint32_t len, int lane) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(lst) & ~(uintptr_t)127;
-    const uintptr_t a1 = reinterpret_cast<uintptr_t>(lst + len);
-    for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a < a1; a += 128 * 32)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-}
-
-// Entries of group i that lie inside the prefix [0, len): a 4-bit mask.
-__device__ __forceinline__ uint32_t group_mask(int i, int mis, uint32_t len) {
-    const int t0 = 4 * i - mis;
-    const int lo = max(0, -t0);
-    const int hi = min(4, (int)len - t0);
-    return hi > lo ? ((1u << hi) - (1u << lo)) : 0u;
-}
-
 __device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
 
-// Warp: count apexes of owner edge p (host y's map in smem).
-__device__ __forceinline__ uint32_t warp_count(const TriArgs& A, const uint32_t* __restrict__ map,
-                                               uint32_t p, uint64_t offx, uint32_t len) {
+// Stream the groups of a list prefix: G uint4 groups per lane in flight;
+// f(word, t) for every entry t in [0, len).
+template <int G, class F>
+__device__ __forceinline__ void stream_prefix(const uint4* __restrict__ g, int ngroups, int mis, uint32_t len,
+                                              F&& f) {
     const int lane = threadIdx.x & 31;
-    int mis;
-    const uint4* g = aligned_groups(A.nkr + offx, mis);
-    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
-    const int ngroups = (int)((len + mis + 3) >> 2);
-    uint32_t c = 0;
-    for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
-        uint4 q[kRegGroups];
+    for (int i0 = 0; i0 < ngroups; i0 += 32 * G) {
+        uint4 q[G];
 #pragma unroll
-        for (int u = 0; u < kRegGroups; ++u) {
+        for (int u = 0; u < G; ++u) {
             const int i = i0 + u * 32 + lane;
             q[u] = i < ngroups ? __ldg(g + i) : no_group();
         }
 #pragma unroll
-        for (int u = 0; u < kRegGroups; ++u) {
+        for (int u = 0; u < G; ++u) {
             const int i = i0 + u * 32 + lane;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int t = 4 * i + e - mis;
-                if (t >= 0 && t < (int)len && map[pick(q[u], e) & kmask] < p) ++c;
+                const uint32_t t = (uint32_t)(4 * i + e - mis);
+                if (t < len) f(pick(q[u], e), t);
             }
         }
     }
-    return __reduce_add_sync(0xffffffffu, c);
 }
 
 // Per-warp shared scratch of the fill kernel (3 KB: 32 warps + the vertex
@@ -167,8 +165,17 @@ struct WarpScratch {
                              //                wide:   (k, t) word pairs, kWin / 2 slots
 };
 
+// Per-warp shared scratch of the packed fill (5.6 KB).
+struct WarpScratchP {
+    uint32_t bits[kWordsP];  // valid apexes of this round, bitmap by rank in x's id-ordered list
+    uint32_t wpre[kWordsP];  // exclusive prefix popcount per bitmap word
+    uint16_t tk[kBitsP];     // prefix index t of the valid apex of rank r (set while marking)
+    uint16_t rec[kWinP];     // staged window: prefix index t per slot
+};
+
 // Clear the bitmap words of a round of lim ranks (before marking).
-__device__ __forceinline__ void clear_bits(WarpScratch* __restrict__ W, uint32_t lim) {
+template <class WS>
+__device__ __forceinline__ void clear_bits(WS* __restrict__ W, uint32_t lim) {
     const int lane = threadIdx.x & 31;
     const uint32_t nwords = (lim + 31) >> 5;
     for (uint32_t w = lane; w < nwords; w += 32) W->bits[w] = 0u;
@@ -177,10 +184,11 @@ __device__ __forceinline__ void clear_bits(WarpScratch* __restrict__ W, uint32_t
 
 // Exclusive per-word prefix popcounts of the round's bitmap (lim ranks);
 // returns the number of valid apexes of the round.
-__device__ __forceinline__ uint32_t rank_bits(WarpScratch* __restrict__ W, uint32_t lim) {
+template <int kNW, class WS>
+__device__ __forceinline__ uint32_t rank_bits(WS* __restrict__ W, uint32_t lim) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
-    constexpr int kWpl = kWords / 32;      // bitmap words per lane (lane owns kWpl consecutive words)
+    constexpr int kWpl = kNW / 32;         // bitmap words per lane (lane owns kWpl consecutive words)
     const uint32_t nwords = (lim + 31) >> 5;
     uint32_t c[kWpl], tot = 0;
 #pragma unroll
@@ -281,6 +289,15 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
         const uint32_t lim = kOneRound ? degx : min((uint32_t)kBits, degx - R);
         clear_bits(W, lim);
         // ---- mark
+        if constexpr (kPacked) {
+            auto mark = [&](uint32_t w, uint32_t) {
+                const uint32_t r = (w >> 16) - R;
+                if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
+                    atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+            };
+            if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
+            else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
+        } else
         for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
             uint4 qk[kRegGroups], qr[kRegGroups];
 #pragma unroll
@@ -303,10 +320,22 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
                 }
             }
         }
-        const uint32_t count = rank_bits(W, lim);
+        const uint32_t count = rank_bits<kWords>(W, lim);
         if (A.debug == 1) { slot += count; continue; }
         // ---- emit + flush, one window per pass over the prefix
         for (uint32_t w0 = 0; w0 < count; w0 += win) {
+            if constexpr (kPacked) {
+                auto emit = [&](uint32_t w, uint32_t t) {
+                    const uint32_t r = (w >> 16) - R;
+                    if (!kOneRound && r >= (uint32_t)kBits) return;
+                    const uint32_t wd = W->bits[r >> 5];
+                    if (!((wd >> (r & 31)) & 1u)) return;
+                    const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((2u << (r & 31)) - 1u)) - 1u - w0;
+                    if (pos < win) W->rec[pos] = (w & 0xFFFFu) | (t << 16);
+                };
+                if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, emit);
+                else stream_prefix<kRegGroups>(gk, ngroups, mis, len, emit);
+            } else
             for (int i0 = 0; i0 < ngroups; i0 += 32 * kRegGroups) {
                 uint4 qk[kRegGroups], qr[kRegGroups];
 #pragma unroll
@@ -359,11 +388,126 @@ __device__ __forceinline__ void warp_fill(const TriArgs& A, const uint32_t* __re
         warp_fill_impl<kPacked, false>(A, map, W, p, y, x, len, offx, degx, slot, filt);
 }
 
-template <bool kFill>
+// Warp: count the apexes of owner edge p (host y's map in smem).
+template <bool kPacked>
+__device__ __forceinline__ uint32_t warp_count_apexes(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t p,
+                                                      uint64_t offx, uint32_t len) {
+    int mis;
+    const uint4* g = aligned_groups(A.nkr + offx, mis);
+    const int ngroups = (int)((len + mis + 3) >> 2);
+    uint32_t c = 0;
+    auto test = [&](uint32_t w, uint32_t) { c += map[kPacked ? (w & 0xFFFFu) : w] < p; };
+    if (ngroups <= 32)
+        stream_prefix<1>(g, ngroups, mis, len, test);
+    else
+        stream_prefix<kRegGroups>(g, ngroups, mis, len, test);
+    return __reduce_add_sync(0xffffffffu, c);
+}
+
+// Packed fill of owner edge p = (y, x).
+//  mark : stream x's older-neighbour prefix (one group per lane when short,
+//         kRegGroups when long); a valid apex k (pos_y[k] < p) of rank r in
+//         x's id-ordered list sets bit r and records its prefix index tk[r]
+//  rank : exclusive per-word prefix popcounts (slot of bit r = wpre + popc below)
+//  emit : walk the set bits (lane owns words lane, lane + 32, ...), staging
+//         rec[slot] = tk[r] for the slots of the current window -- no second
+//         pass over the prefix
+//  flush: one lane per triangle: k = nkr[offx + t] & 0xFFFF and
+//         pos(x, k) = np[offx + t] (the prefix just streamed), pos(y, k) = map[k]
+template <bool kOneRound>
+__device__ __forceinline__ void warp_fill_packed(const TriArgs& A, const uint32_t* __restrict__ map,
+                                                 WarpScratchP* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                                 uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                                 uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    int mis;
+    const uint4* gk = aligned_groups(A.nkr + offx, mis);
+    const uint32_t* __restrict__ nkx = A.nkr + offx;
+    const uint32_t* __restrict__ npx = A.np + offx;
+    const int ngroups = (int)((len + mis + 3) >> 2);
+    for (uint32_t R = 0; R < degx; R += kBitsP) {
+        const uint32_t lim = kOneRound ? degx : min((uint32_t)kBitsP, degx - R);
+        clear_bits(W, lim);
+        auto mark = [&](uint32_t w, uint32_t t) {
+            const uint32_t r = (w >> 16) - R;
+            if ((kOneRound || r < (uint32_t)kBitsP) && map[w & 0xFFFFu] < p) {
+                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+                W->tk[r] = (uint16_t)t;
+            }
+        };
+        if (ngroups <= 32)
+            stream_prefix<1>(gk, ngroups, mis, len, mark);
+        else
+            stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
+        const uint32_t count = rank_bits<kWordsP>(W, lim);
+        if (A.debug == 1) { slot += count; if (kOneRound) break; continue; }
+        const uint32_t nwords = (lim + 31) >> 5;
+        for (uint32_t w0 = 0; w0 < count; w0 += kWinP) {
+            const uint32_t w1 = w0 + kWinP;
+            for (uint32_t wd = lane; wd < nwords; wd += 32) {
+                uint32_t b = W->bits[wd];
+                uint32_t s = W->wpre[wd];
+                if (s >= w1 || s + __popc(b) <= w0) continue;
+                while (b) {
+                    const int bit = __ffs(b) - 1;
+                    b &= b - 1;
+                    if (s >= w0 && s < w1) W->rec[s - w0] = W->tk[32 * wd + bit];
+                    ++s;
+                }
+            }
+            __syncwarp();
+            const uint32_t m = min((uint32_t)kWinP, count - w0);
+            if (A.debug != 2) {
+                const uint64_t s0 = slot + w0;
+                constexpr int kU = 4;
+                for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
+                    uint32_t kw[kU], px[kU];
+#pragma unroll
+                    for (int q = 0; q < kU; ++q) {
+                        const uint32_t j = j0 + 32 * q + lane;
+                        kw[q] = 0;
+                        px[q] = 0;
+                        if (j < m) {
+                            const uint32_t t = W->rec[j];
+                            kw[q] = __ldg(nkx + t);
+                            px[q] = __ldg(npx + t);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < kU; ++q) {
+                        const uint32_t j = j0 + 32 * q + lane;
+                        if (j >= m) continue;
+                        const uint32_t k = kw[q] & 0xFFFFu;
+                        const uint32_t py = map[k];
+                        uint32_t a0 = y, a1 = x, a2 = k;
+                        sort3(a0, a1, a2);
+                        uint32_t* tv = A.tv + 3 * (s0 + j);
+                        __stcs(tv, a0);
+                        __stcs(tv + 1, a1);
+                        __stcs(tv + 2, a2);
+                        if (A.rows) {
+                            uint32_t* rw = A.rows + 3 * (s0 + j);
+                            __stcs(rw, min(px[q], py));
+                            __stcs(rw + 1, max(px[q], py));
+                            __stcs(rw + 2, p);
+                        }
+                        __stcs(A.tf + s0 + j, filt);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        slot += count;
+        if (kOneRound) break;
+    }
+}
+
+template <bool kFill, bool kPacked>
 __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
-    WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem + ((A.n * 4 + 15) / 16) * 16);
+    using WS = typename std::conditional<kPacked && VRB_TRI_MODE == 1, WarpScratchP, WarpScratch>::type;
+    WS* scratch = reinterpret_cast<WS*>(smem + ((A.n * 4 + 15) / 16) * 16);
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
     __shared__ unsigned s_next;
@@ -371,10 +515,10 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
     const int nthreads = blockDim.x;
     for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
     if (kFill)   // the flags are cleared after every use, so they must start at 0
-        for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WarpScratch) / 4); q += nthreads)
+        for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WS) / 4); q += nthreads)
             reinterpret_cast<uint32_t*>(scratch)[q] = 0u;
     __syncthreads();
-    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    const uint32_t kmask = kPacked ? 0xFFFFu : 0xFFFFFFFFu;
     for (;;) {
         if (threadIdx.x == 0) {
             const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
@@ -434,13 +578,17 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
                 const uint4 pl2 = plan_of(e2);
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if (kFill) {
-                        if (A.packed)
-                            warp_fill<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    if constexpr (kFill && kPacked && VRB_TRI_MODE == 0) {
+                        warp_fill<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    } else if constexpr (kFill && kPacked) {
+                        if (pl0.w <= (uint32_t)kBitsP)
+                            warp_fill_packed<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                         else
-                            warp_fill<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                            warp_fill_packed<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    } else if constexpr (kFill) {
+                        warp_fill<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                     } else {
-                        const uint32_t c = warp_count(A, map, p, off0, len);
+                        const uint32_t c = warp_count_apexes<kPacked>(A, map, p, off0, len);
                         if (lane == 0) A.cnt[p] = c;
                     }
                 }
@@ -460,32 +608,37 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
 
 size_t map_bytes(int64_t n) { return (size_t)((n * 4 + 15) / 16) * 16; }
 
-// warps per CTA: 16, or fewer when the vertex map leaves too little shared memory
-int fill_warps(int64_t n) {
+// warps per CTA of the fill: up to kWarps, fewer when the vertex map leaves
+// too little shared memory
+int fill_warps(int64_t n, bool packed) {
     const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(n) - 1024;
-    const int64_t w = avail / (int64_t)sizeof(WarpScratch);
+    const int64_t w = avail / (int64_t)(packed && VRB_TRI_MODE == 1 ? sizeof(WarpScratchP) : sizeof(WarpScratch));
     return (int)std::max<int64_t>(0, std::min<int64_t>(kWarps, w));
+}
+
+template <bool kFill, bool kPacked>
+void launch_k(const TriArgs& A, int threads, size_t smem, int64_t nctas_cap, cudaStream_t s) {
+    VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    int per_sm = 0;
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked>, threads, smem));
+    if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count() * per_sm, nctas_cap);
+    k_triangles<kFill, kPacked><<<grid, threads, smem, s>>>(A);
+    VRB_LAUNCH_CHECK();
 }
 
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
-    // fill: one 32-warp CTA per SM (the vertex map + 3 KB per warp); count:
+    const bool packed = A.packed != 0;
+    // fill: one CTA per SM (the vertex map + per-warp scratch); count:
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
-    const int warps = fill ? fill_warps(A.n) : kWarps / 2;
+    const int warps = fill ? fill_warps(A.n, packed) : kWarps / 2;
     if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
-    const size_t smem = map_bytes(A.n) + (fill ? (size_t)warps * sizeof(WarpScratch) : 0);
-    const int nsm = device_sm_count();
-    int per_sm = 1;
-    if (fill) {
-        VRB_CUDA(cudaFuncSetAttribute(k_triangles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<true>, threads, smem));
-    } else {
-        VRB_CUDA(cudaFuncSetAttribute(k_triangles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<false>, threads, smem));
-    }
-    if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
-    const int64_t nctas = (int64_t)nsm * per_sm;
+    const size_t smem =
+        map_bytes(A.n) +
+        (fill ? (size_t)warps * (packed && VRB_TRI_MODE == 1 ? sizeof(WarpScratchP) : sizeof(WarpScratch)) : 0);
     // Task size depends on the work only (identical on every rank, so a
     // partition of the task range is a partition of the owner edges):
     // ~8k tasks, but not below ~64k candidate tests each.
@@ -500,12 +653,14 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     DBuf<unsigned long long> counter(1, s);
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     A.task_counter = counter.get();
-    const unsigned grid = (unsigned)std::min<int64_t>(nctas, A.task_hi - A.task_lo);
-    if (fill)
-        k_triangles<true><<<grid, threads, smem, s>>>(A);
-    else
-        k_triangles<false><<<grid, threads, smem, s>>>(A);
-    VRB_LAUNCH_CHECK();
+    const int64_t cap = A.task_hi - A.task_lo;
+    if (fill) {
+        if (packed) launch_k<true, true>(A, threads, smem, cap, s);
+        else launch_k<true, false>(A, threads, smem, cap, s);
+    } else {
+        if (packed) launch_k<false, true>(A, threads, smem, cap, s);
+        else launch_k<false, false>(A, threads, smem, cap, s);
+    }
 }
 
 TriArgs graph_args(const Graph& g) {
@@ -527,7 +682,7 @@ TriArgs graph_args(const Graph& g) {
 
 int64_t dense_map_limit() {
     const int64_t smem = (int64_t)device_max_smem_optin();
-    return (smem - 4 * (int64_t)sizeof(WarpScratch) - 1024) / 4;   // >= 4 warps of fill scratch
+    return (smem - 4 * (int64_t)std::max(sizeof(WarpScratch), sizeof(WarpScratchP)) - 1024) / 4;   // >= 4 warps of fill scratch
 }
 
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s) {
