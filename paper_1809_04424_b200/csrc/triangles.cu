@@ -29,9 +29,11 @@
 //          flags are folded into a bitmap with per-word prefix popcounts, and
 //          each valid apex computes its own output slot (#valid apexes of
 //          smaller id) -- a counting sort by apex id with no data movement.
-//          Prefixes up to kRegEntries stay in registers between the passes.
-//          A window of kWin slots is staged in shared memory and written with
-//          one lane per triangle (streaming stores).
+//          The emit pass streams the prefix again together with its edge
+//          positions (coalesced 16-byte groups) and stages (k, pos(x, k)) for
+//          a window of slots in shared memory; the flush writes the window
+//          one lane per triangle with streaming stores and no global gathers.
+//          Streams run 4/2/1 groups per lane so short prefixes waste few lanes.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -50,22 +52,18 @@ static_assert(kWords % 32 == 0, "bitmap words must split evenly over the lanes")
 #ifndef VRB_TRI_WIN
 #define VRB_TRI_WIN 512
 #endif
+// VRB_TRI_MODE selects the packed-list fill (experiment knob, tools/variants.py):
+//   3 (default) warp_fill_kp: the emit streams the prefix with its edge
+//     positions and stages (k, pos(x, k)), so the flush needs no gathers
+//   0 warp_fill (the wide-list algorithm): staged (k, t), pos(x, k) gathered
 #ifndef VRB_TRI_MODE
-#define VRB_TRI_MODE 0
+#define VRB_TRI_MODE 3
 #endif
-#ifndef VRB_TRI_BITSP
-#define VRB_TRI_BITSP 2048
-#endif
-#ifndef VRB_TRI_WINP
-#define VRB_TRI_WINP 512
+#ifndef VRB_TRI_WIN3
+#define VRB_TRI_WIN3 512
 #endif
 constexpr int kWin = VRB_TRI_WIN;        // triangles staged per output window (packed records)
 constexpr int kRegGroups = 4;            // uint4 groups per lane in flight when streaming
-// packed lists (n, degrees <= 65536): the valid apexes are emitted from the
-// bitmap itself, so rounds are smaller and windows never re-stream the prefix
-constexpr int kBitsP = VRB_TRI_BITSP;    // apex ranks per round
-constexpr int kWordsP = kBitsP / 32;
-constexpr int kWinP = VRB_TRI_WINP;      // slots per window
 
 struct TriArgs {
     int64_t n, E;
@@ -129,20 +127,51 @@ __device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
 }
 
+#ifndef VRB_TRI_HINT
+#define VRB_TRI_HINT 0
+#endif
+// Neighbour-list loads: with VRB_TRI_HINT the lines are kept in L2 with the
+// evict_last policy (the lists are re-read by many owner edges while the
+// output stream passes through L2 with evict-first stores).
+__device__ __forceinline__ uint4 ld_list(const uint4* a) {
+#if VRB_TRI_HINT
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(a), "l"(pol));
+    return v;
+#else
+    return __ldg(a);
+#endif
+}
+__device__ __forceinline__ uint32_t ld_list(const uint32_t* a) {
+#if VRB_TRI_HINT
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+#else
+    return __ldg(a);
+#endif
+}
+
 __device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
 
 // Stream the groups of a list prefix: G uint4 groups per lane in flight;
 // f(word, t) for every entry t in [0, len).
 template <int G, class F>
-__device__ __forceinline__ void stream_prefix(const uint4* __restrict__ g, int ngroups, int mis, uint32_t len,
-                                              F&& f) {
+__device__ __forceinline__ void stream_range(const uint4* __restrict__ g, int start, int stop, int ngroups, int mis,
+                                             uint32_t len, F&& f) {
     const int lane = threadIdx.x & 31;
-    for (int i0 = 0; i0 < ngroups; i0 += 32 * G) {
+    for (int i0 = start; i0 < stop; i0 += 32 * G) {
         uint4 q[G];
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             const int i = i0 + u * 32 + lane;
-            q[u] = i < ngroups ? __ldg(g + i) : no_group();
+            q[u] = i < ngroups ? ld_list(g + i) : no_group();
         }
 #pragma unroll
         for (int u = 0; u < G; ++u) {
@@ -155,6 +184,25 @@ __device__ __forceinline__ void stream_prefix(const uint4* __restrict__ g, int n
         }
     }
 }
+#ifndef VRB_TRI_TAIL
+#define VRB_TRI_TAIL 1
+#endif
+// The whole prefix: 4-group iterations while >= 128 groups remain, then
+// 2- and 1-group iterations (VRB_TRI_TAIL), so at most 127 entry slots per
+// lane-sweep are idle; without VRB_TRI_TAIL one 1- or G-group stride.
+template <int G, class F>
+__device__ __forceinline__ void stream_prefix(const uint4* __restrict__ g, int ngroups, int mis, uint32_t len,
+                                              F&& f) {
+#if VRB_TRI_TAIL
+    const int f4 = (ngroups / 128) * 128;
+    const int f2 = f4 + ((ngroups - f4) / 64) * 64;
+    stream_range<4>(g, 0, f4, ngroups, mis, len, f);
+    stream_range<2>(g, f4, f2, ngroups, mis, len, f);
+    stream_range<1>(g, f2, ngroups, ngroups, mis, len, f);
+#else
+    stream_range<G>(g, 0, ngroups, ngroups, mis, len, f);
+#endif
+}
 
 // Per-warp shared scratch of the fill kernel (3 KB: 32 warps + the vertex
 // map fit one SM).
@@ -165,13 +213,49 @@ struct WarpScratch {
                              //                wide:   (k, t) word pairs, kWin / 2 slots
 };
 
-// Per-warp shared scratch of the packed fill (5.6 KB).
-struct WarpScratchP {
-    uint32_t bits[kWordsP];  // valid apexes of this round, bitmap by rank in x's id-ordered list
-    uint32_t wpre[kWordsP];  // exclusive prefix popcount per bitmap word
-    uint16_t tk[kBitsP];     // prefix index t of the valid apex of rank r (set while marking)
-    uint16_t rec[kWinP];     // staged window: prefix index t per slot
+// Per-warp shared scratch of the (k, pos) fill (VRB_TRI_MODE 3).
+constexpr int kWin3 = VRB_TRI_WIN3;      // slots per window
+struct WarpScratch3 {
+    uint32_t bits[kWords];   // valid apexes of this round, bitmap by rank in x's id-ordered list
+    uint32_t wpre[kWords];   // exclusive prefix popcount per bitmap word
+    uint2 rec[kWin3];        // staged window: (apex k, pos(x, k)) per slot
 };
+
+// Stream two parallel list prefixes (same layout): f(word_a, word_b, t).
+template <int G, class F>
+__device__ __forceinline__ void stream_range2(const uint4* __restrict__ ga, const uint4* __restrict__ gb, int start,
+                                              int stop, int ngroups, int mis, uint32_t len, F&& f) {
+    const int lane = threadIdx.x & 31;
+    for (int i0 = start; i0 < stop; i0 += 32 * G) {
+        uint4 qa[G], qb[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int i = i0 + u * 32 + lane;
+            qa[u] = i < ngroups ? ld_list(ga + i) : no_group();
+            qb[u] = i < ngroups ? ld_list(gb + i) : no_group();
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int i = i0 + u * 32 + lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t t = (uint32_t)(4 * i + e - mis);
+                if (t < len) f(pick(qa[u], e), pick(qb[u], e), t);
+            }
+        }
+    }
+}
+template <int G, class F>
+__device__ __forceinline__ void stream_prefix2(const uint4* __restrict__ ga, const uint4* __restrict__ gb, int ngroups,
+                                               int mis, uint32_t len, F&& f) {
+#if VRB_TRI_TAIL
+    const int f2 = (ngroups / 64) * 64;
+    stream_range2<2>(ga, gb, 0, f2, ngroups, mis, len, f);
+    stream_range2<1>(ga, gb, f2, ngroups, ngroups, mis, len, f);
+#else
+    stream_range2<G>(ga, gb, 0, ngroups, ngroups, mis, len, f);
+#endif
+}
 
 // Clear the bitmap words of a round of lim ranks (before marking).
 template <class WS>
@@ -210,6 +294,68 @@ __device__ __forceinline__ uint32_t rank_bits(WS* __restrict__ W, uint32_t lim) 
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+#ifndef VRB_TRI_VEC
+#define VRB_TRI_VEC 0
+#endif
+// Write the window's m triangles at slots [s0, s0 + m): get(j) -> (k, pos(x, k)),
+// pos(y, k) = map[k].  Slots are taken four at a time per lane where the
+// slot index is a multiple of 4, so every output array gets 16-byte
+// streaming stores (3 for the vertices, 3 for the D_2 rows, 1 for filt);
+// the unaligned head and the tail are written one triangle per lane.
+template <class Get>
+__device__ __forceinline__ void flush_vec(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t m, uint64_t s0,
+                                          uint32_t p, uint32_t y, uint32_t x, uint32_t filt, Get&& get) {
+    const int lane = threadIdx.x & 31;
+    auto one = [&](uint32_t j) {
+        const uint2 kp = get(j);
+        const uint32_t k = kp.x, px = kp.y, py = map[k];
+        uint32_t a0 = y, a1 = x, a2 = k;
+        sort3(a0, a1, a2);
+        uint32_t* tv = A.tv + 3 * (s0 + j);
+        __stcs(tv, a0);
+        __stcs(tv + 1, a1);
+        __stcs(tv + 2, a2);
+        if (A.rows) {
+            uint32_t* rw = A.rows + 3 * (s0 + j);
+            __stcs(rw, min(px, py));
+            __stcs(rw + 1, max(px, py));
+            __stcs(rw + 2, p);
+        }
+        __stcs(A.tf + s0 + j, filt);
+    };
+    uint32_t h = (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u);
+    if (h > m) h = m;
+    if ((uint32_t)lane < h) one(lane);
+    const uint32_t nq = (m - h) >> 2;
+    for (uint32_t q = lane; q < nq; q += 32) {
+        const uint32_t j = h + 4 * q;
+        uint2 kp[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kp[e] = get(j + e);
+        uint32_t v[12], r[12];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t k = kp[e].x, px = kp[e].y, py = map[k];
+            uint32_t a0 = y, a1 = x, a2 = k;
+            sort3(a0, a1, a2);
+            v[3 * e] = a0; v[3 * e + 1] = a1; v[3 * e + 2] = a2;
+            r[3 * e] = min(px, py); r[3 * e + 1] = max(px, py); r[3 * e + 2] = p;
+        }
+        uint4* tv = reinterpret_cast<uint4*>(A.tv + 3 * (s0 + j));
+        __stcs(tv, make_uint4(v[0], v[1], v[2], v[3]));
+        __stcs(tv + 1, make_uint4(v[4], v[5], v[6], v[7]));
+        __stcs(tv + 2, make_uint4(v[8], v[9], v[10], v[11]));
+        if (A.rows) {
+            uint4* rw = reinterpret_cast<uint4*>(A.rows + 3 * (s0 + j));
+            __stcs(rw, make_uint4(r[0], r[1], r[2], r[3]));
+            __stcs(rw + 1, make_uint4(r[4], r[5], r[6], r[7]));
+            __stcs(rw + 2, make_uint4(r[8], r[9], r[10], r[11]));
+        }
+        __stcs(reinterpret_cast<uint4*>(A.tf + s0 + j), make_uint4(filt, filt, filt, filt));
+    }
+    for (uint32_t j = h + 4 * nq + lane; j < m; j += 32) one(j);
+}
+
 // Write the staged window [s0, s0 + m), one lane per triangle, kU position
 // gathers in flight per lane: record -> (k, t); pos(x, k) = np[offx + t] (the
 // prefix just streamed: L1/L2), pos(y, k) = map[k].
@@ -237,7 +383,7 @@ __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* _
                     kk[q] = W->rec[2 * j];
                     t = W->rec[2 * j + 1];
                 }
-                px[q] = __ldg(npx + t);
+                px[q] = ld_list(npx + t);
             }
         }
 #pragma unroll
@@ -303,7 +449,7 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
 #pragma unroll
             for (int u = 0; u < kRegGroups; ++u) {
                 const int i = i0 + u * 32 + lane;
-                qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                qk[u] = i < ngroups ? ld_list(gk + i) : no_group();
                 if (!kPacked) qr[u] = i < ngroups ? __ldg(gr + i) : no_group();
             }
 #pragma unroll
@@ -341,7 +487,7 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
 #pragma unroll
                 for (int u = 0; u < kRegGroups; ++u) {
                     const int i = i0 + u * 32 + lane;
-                    qk[u] = i < ngroups ? __ldg(gk + i) : no_group();
+                    qk[u] = i < ngroups ? ld_list(gk + i) : no_group();
                     if (!kPacked) qr[u] = i < ngroups ? __ldg(gr + i) : no_group();
                 }
 #pragma unroll
@@ -368,8 +514,16 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
                 }
             }
             __syncwarp();
-            if (A.debug != 2)
-                flush_window<kPacked>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
+            if (A.debug != 2) {
+                if constexpr (kPacked && VRB_TRI_VEC) {
+                    flush_vec(A, map, min(win, count - w0), slot + w0, p, y, x, filt, [&](uint32_t j) {
+                        const uint32_t rc = W->rec[j];
+                        return make_uint2(rc & 0xFFFFu, ld_list(npx + (rc >> 16)));
+                    });
+                } else {
+                    flush_window<kPacked>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
+                }
+            }
             __syncwarp();
         }
         slot += count;
@@ -404,96 +558,70 @@ __device__ __forceinline__ uint32_t warp_count_apexes(const TriArgs& A, const ui
     return __reduce_add_sync(0xffffffffu, c);
 }
 
-// Packed fill of owner edge p = (y, x).
-//  mark : stream x's older-neighbour prefix (one group per lane when short,
-//         kRegGroups when long); a valid apex k (pos_y[k] < p) of rank r in
-//         x's id-ordered list sets bit r and records its prefix index tk[r]
-//  rank : exclusive per-word prefix popcounts (slot of bit r = wpre + popc below)
-//  emit : walk the set bits (lane owns words lane, lane + 32, ...), staging
-//         rec[slot] = tk[r] for the slots of the current window -- no second
-//         pass over the prefix
-//  flush: one lane per triangle: k = nkr[offx + t] & 0xFFFF and
-//         pos(x, k) = np[offx + t] (the prefix just streamed), pos(y, k) = map[k]
+// (k, pos) fill of owner edge p = (y, x) (packed lists).
+//  mark : as warp_fill_impl (bitmap by rank of the valid apexes)
+//  emit : re-stream the prefix together with its edge positions (both
+//         coalesced 16-byte groups) and stage (k, pos(x, k)) at the apex's slot
+//  flush: one lane per triangle, no global gathers: pos(y, k) = map[k]
 template <bool kOneRound>
-__device__ __forceinline__ void warp_fill_packed(const TriArgs& A, const uint32_t* __restrict__ map,
-                                                 WarpScratchP* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                                 uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
-                                                 uint32_t filt) {
+__device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* __restrict__ map,
+                                             WarpScratch3* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                             uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
+                                             uint32_t filt) {
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
-    const uint32_t* __restrict__ nkx = A.nkr + offx;
-    const uint32_t* __restrict__ npx = A.np + offx;
+    const uint4* gp = reinterpret_cast<const uint4*>(A.np + offx - mis);
     const int ngroups = (int)((len + mis + 3) >> 2);
-    for (uint32_t R = 0; R < degx; R += kBitsP) {
-        const uint32_t lim = kOneRound ? degx : min((uint32_t)kBitsP, degx - R);
+    for (uint32_t R = 0; R < degx; R += kBits) {
+        const uint32_t lim = kOneRound ? degx : min((uint32_t)kBits, degx - R);
         clear_bits(W, lim);
-        auto mark = [&](uint32_t w, uint32_t t) {
+        auto mark = [&](uint32_t w, uint32_t) {
             const uint32_t r = (w >> 16) - R;
-            if ((kOneRound || r < (uint32_t)kBitsP) && map[w & 0xFFFFu] < p) {
+            if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
                 atomicOr(&W->bits[r >> 5], 1u << (r & 31));
-                W->tk[r] = (uint16_t)t;
-            }
         };
-        if (ngroups <= 32)
-            stream_prefix<1>(gk, ngroups, mis, len, mark);
-        else
-            stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
-        const uint32_t count = rank_bits<kWordsP>(W, lim);
+        if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
+        else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
+        const uint32_t count = rank_bits<kWords>(W, lim);
         if (A.debug == 1) { slot += count; if (kOneRound) break; continue; }
-        const uint32_t nwords = (lim + 31) >> 5;
-        for (uint32_t w0 = 0; w0 < count; w0 += kWinP) {
-            const uint32_t w1 = w0 + kWinP;
-            for (uint32_t wd = lane; wd < nwords; wd += 32) {
-                uint32_t b = W->bits[wd];
-                uint32_t s = W->wpre[wd];
-                if (s >= w1 || s + __popc(b) <= w0) continue;
-                while (b) {
-                    const int bit = __ffs(b) - 1;
-                    b &= b - 1;
-                    if (s >= w0 && s < w1) W->rec[s - w0] = W->tk[32 * wd + bit];
-                    ++s;
-                }
-            }
+        for (uint32_t w0 = 0; w0 < count; w0 += kWin3) {
+            auto emit = [&](uint32_t w, uint32_t px, uint32_t) {
+                const uint32_t r = (w >> 16) - R;
+                if (!kOneRound && r >= (uint32_t)kBits) return;
+                const uint32_t wd = W->bits[r >> 5];
+                if (!((wd >> (r & 31)) & 1u)) return;
+                const uint32_t pos = W->wpre[r >> 5] + __popc(wd & ((2u << (r & 31)) - 1u)) - 1u - w0;
+                if (pos < (uint32_t)kWin3) W->rec[pos] = make_uint2(w & 0xFFFFu, px);
+            };
+            if (ngroups <= 32) stream_prefix2<1>(gk, gp, ngroups, mis, len, emit);
+            else stream_prefix2<2>(gk, gp, ngroups, mis, len, emit);
             __syncwarp();
-            const uint32_t m = min((uint32_t)kWinP, count - w0);
+            const uint32_t m = min((uint32_t)kWin3, count - w0);
             if (A.debug != 2) {
+#if VRB_TRI_VEC
+                flush_vec(A, map, m, slot + w0, p, y, x, filt, [&](uint32_t j) { return W->rec[j]; });
+#else
                 const uint64_t s0 = slot + w0;
-                constexpr int kU = 4;
-                for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
-                    uint32_t kw[kU], px[kU];
-#pragma unroll
-                    for (int q = 0; q < kU; ++q) {
-                        const uint32_t j = j0 + 32 * q + lane;
-                        kw[q] = 0;
-                        px[q] = 0;
-                        if (j < m) {
-                            const uint32_t t = W->rec[j];
-                            kw[q] = __ldg(nkx + t);
-                            px[q] = __ldg(npx + t);
-                        }
+                for (uint32_t j = lane; j < m; j += 32) {
+                    const uint2 rc = W->rec[j];
+                    const uint32_t k = rc.x, px = rc.y;
+                    const uint32_t py = map[k];
+                    uint32_t a0 = y, a1 = x, a2 = k;
+                    sort3(a0, a1, a2);
+                    uint32_t* tv = A.tv + 3 * (s0 + j);
+                    __stcs(tv, a0);
+                    __stcs(tv + 1, a1);
+                    __stcs(tv + 2, a2);
+                    if (A.rows) {
+                        uint32_t* rw = A.rows + 3 * (s0 + j);
+                        __stcs(rw, min(px, py));
+                        __stcs(rw + 1, max(px, py));
+                        __stcs(rw + 2, p);
                     }
-#pragma unroll
-                    for (int q = 0; q < kU; ++q) {
-                        const uint32_t j = j0 + 32 * q + lane;
-                        if (j >= m) continue;
-                        const uint32_t k = kw[q] & 0xFFFFu;
-                        const uint32_t py = map[k];
-                        uint32_t a0 = y, a1 = x, a2 = k;
-                        sort3(a0, a1, a2);
-                        uint32_t* tv = A.tv + 3 * (s0 + j);
-                        __stcs(tv, a0);
-                        __stcs(tv + 1, a1);
-                        __stcs(tv + 2, a2);
-                        if (A.rows) {
-                            uint32_t* rw = A.rows + 3 * (s0 + j);
-                            __stcs(rw, min(px[q], py));
-                            __stcs(rw + 1, max(px[q], py));
-                            __stcs(rw + 2, p);
-                        }
-                        __stcs(A.tf + s0 + j, filt);
-                    }
+                    __stcs(A.tf + s0 + j, filt);
                 }
+#endif
             }
             __syncwarp();
         }
@@ -506,7 +634,7 @@ template <bool kFill, bool kPacked>
 __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
-    using WS = typename std::conditional<kPacked && VRB_TRI_MODE == 1, WarpScratchP, WarpScratch>::type;
+    using WS = typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type;
     WS* scratch = reinterpret_cast<WS*>(smem + ((A.n * 4 + 15) / 16) * 16);
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
@@ -578,13 +706,13 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
                 const uint4 pl2 = plan_of(e2);
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kFill && kPacked && VRB_TRI_MODE == 0) {
-                        warp_fill<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
-                    } else if constexpr (kFill && kPacked) {
-                        if (pl0.w <= (uint32_t)kBitsP)
-                            warp_fill_packed<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    if constexpr (kFill && kPacked && VRB_TRI_MODE == 3) {
+                        if (pl0.w <= (uint32_t)kBits)
+                            warp_fill_kp<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                         else
-                            warp_fill_packed<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                            warp_fill_kp<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
+                    } else if constexpr (kFill && kPacked) {
+                        warp_fill<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                     } else if constexpr (kFill) {
                         warp_fill<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                     } else {
@@ -608,11 +736,15 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
 
 size_t map_bytes(int64_t n) { return (size_t)((n * 4 + 15) / 16) * 16; }
 
+size_t scratch_bytes(bool packed) {
+    return packed && VRB_TRI_MODE == 3 ? sizeof(WarpScratch3) : sizeof(WarpScratch);
+}
+
 // warps per CTA of the fill: up to kWarps, fewer when the vertex map leaves
 // too little shared memory
 int fill_warps(int64_t n, bool packed) {
     const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(n) - 1024;
-    const int64_t w = avail / (int64_t)(packed && VRB_TRI_MODE == 1 ? sizeof(WarpScratchP) : sizeof(WarpScratch));
+    const int64_t w = avail / (int64_t)scratch_bytes(packed);
     return (int)std::max<int64_t>(0, std::min<int64_t>(kWarps, w));
 }
 
@@ -638,7 +770,7 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     const int threads = warps * 32;
     const size_t smem =
         map_bytes(A.n) +
-        (fill ? (size_t)warps * (packed && VRB_TRI_MODE == 1 ? sizeof(WarpScratchP) : sizeof(WarpScratch)) : 0);
+        (fill ? (size_t)warps * scratch_bytes(packed) : 0);
     // Task size depends on the work only (identical on every rank, so a
     // partition of the task range is a partition of the owner edges):
     // ~8k tasks, but not below ~64k candidate tests each.
@@ -682,7 +814,7 @@ TriArgs graph_args(const Graph& g) {
 
 int64_t dense_map_limit() {
     const int64_t smem = (int64_t)device_max_smem_optin();
-    return (smem - 4 * (int64_t)std::max(sizeof(WarpScratch), sizeof(WarpScratchP)) - 1024) / 4;   // >= 4 warps of fill scratch
+    return (smem - 4 * (int64_t)std::max(sizeof(WarpScratch), scratch_bytes(true)) - 1024) / 4;   // >= 4 warps of fill scratch
 }
 
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s) {
