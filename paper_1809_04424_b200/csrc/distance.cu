@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
                                                         const uint64_t* __restrict__ slot_base,
                                                         uint64_t* __restrict__ key,
                                                         uint32_t* __restrict__ ei,
-                                                        uint32_t* __restrict__ ej) {
+                                                        uint32_t* __restrict__ ej,
+                                                        uint32_t* __restrict__ pij) {
     const int64_t tj = blockIdx.x, ti = blockIdx.y;
     if (tj < ti) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -138,8 +139,12 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
             const double len = __dsqrt_rn(acc);
             const uint64_t slot = base + __popcll(bits & ((1ull << c) - 1ull));
             key[slot] = (uint64_t)__double_as_longlong(len);
-            ei[slot] = (uint32_t)i;
-            ej[slot] = (uint32_t)j;
+            if (pij) {
+                pij[slot] = ((uint32_t)i << 16) | (uint32_t)j;
+            } else {
+                ei[slot] = (uint32_t)i;
+                ej[slot] = (uint32_t)j;
+            }
         }
     }
 }
@@ -234,10 +239,15 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     out.E = (int64_t)E;
     if (E == 0) return;
     out.key.alloc(E, s);
-    out.ei.alloc(E, s);
-    out.ej.alloc(E, s);
+    out.packed = n <= 65536;
+    if (out.packed) {
+        out.pij.alloc(E, s);
+    } else {
+        out.ei.alloc(E, s);
+        out.ej.alloc(E, s);
+    }
     k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, masks.get(), base.get(), out.key.get(),
-                                          out.ei.get(), out.ej.get());
+                                          out.ei.get(), out.ej.get(), out.pij.get());
     VRB_LAUNCH_CHECK();
 }
 

@@ -48,6 +48,18 @@ __global__ void k_edge_outputs(const uint64_t* __restrict__ key, const uint32_t*
     }
 }
 
+// packed ids (n <= 65536): the sorted values are (i << 16 | j) themselves
+__global__ void k_edge_outputs_packed(const uint64_t* __restrict__ key, const uint32_t* __restrict__ pij,
+                                      const uint32_t* __restrict__ efilt, int64_t E, uint2* __restrict__ ev,
+                                      double* __restrict__ vor) {
+    GRID_STRIDE(p, E) {
+        const uint32_t v = pij[p];
+        ev[p] = make_uint2(v >> 16, v & 0xFFFFu);
+        const uint64_t k = key[p];
+        if (p == 0 || k != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)k);
+    }
+}
+
 __global__ void k_degree(const uint32_t* __restrict__ ev, int64_t n2, uint32_t* __restrict__ deg) {
     GRID_STRIDE(q, n2) atomicAdd(&deg[ev[q]], 1u);
 }
@@ -194,17 +206,27 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
     const int64_t E = ke.E;
     if (E == 0) return 0;
     DBuf<uint64_t> key_alt(E, s);
-    DBuf<uint32_t> perm(E, s), perm_alt(E, s);
-    iota_u32(perm.get(), E, s);
+    // values: the packed (i, j) ids, or the lex index (permutation) for large n
+    DBuf<uint32_t> perm, perm_alt(E, s);
+    uint32_t* vals = ke.pij.get();
+    if (!ke.packed) {
+        perm.alloc(E, s);
+        iota_u32(perm.get(), E, s);
+        vals = perm.get();
+    }
     const uint64_t vary = varying_bits(ke.key.get(), E, s);
-    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), perm.get(), perm_alt.get(), E, vary, s);
+    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary, s);
     const uint64_t* skey = alt ? key_alt.get() : ke.key.get();
-    const uint32_t* sperm = alt ? perm_alt.get() : perm.get();
+    const uint32_t* sval = alt ? perm_alt.get() : vals;
     DBuf<uint32_t> head(E, s);
     k_rank_heads<<<grid_for(E, 256), 256, 0, s>>>(skey, E, head.get());
     VRB_LAUNCH_CHECK();
     inclusive_scan_u32(head.get(), efilt, E, s);
-    k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sperm, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor);
+    if (ke.packed)
+        k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, efilt, E, reinterpret_cast<uint2*>(ev),
+                                                               vor);
+    else
+        k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor);
     VRB_LAUNCH_CHECK();
     uint32_t nvals = 0;
     VRB_CUDA(cudaMemcpyAsync(&nvals, efilt + E - 1, sizeof(nvals), cudaMemcpyDeviceToHost, s));

@@ -22,8 +22,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;                   // per thread
-constexpr int kTile = kThreads * kItems;     // 4096 items per tile
+#ifndef VRB_SORT_ITEMS
+#define VRB_SORT_ITEMS 12
+#endif
+#ifndef VRB_SORT_MINB
+#define VRB_SORT_MINB 4
+#endif
+constexpr int kItems = VRB_SORT_ITEMS;       // per thread
+constexpr int kTile = kThreads * kItems;     // 3072 items per tile
 constexpr int kWarpItems = 32 * kItems;      // contiguous items per warp
 constexpr int kBins = 256;
 
@@ -77,7 +83,7 @@ struct SweepSmem {
     uint32_t tile_id;
 };
 
-__global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint64_t* __restrict__ keys_in,
                                                        const uint32_t* __restrict__ vals_in,
                                                        uint64_t* __restrict__ keys_out,
                                                        uint32_t* __restrict__ vals_out, int64_t n, int shift,

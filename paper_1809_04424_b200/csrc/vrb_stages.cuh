@@ -16,7 +16,8 @@ double cap_threshold(double r, bool strict);
 struct KeptEdges {
     int64_t E = 0;
     DBuf<uint64_t> key;   // bit pattern of len (non-negative doubles order as u64)
-    DBuf<uint32_t> ei, ej;
+    bool packed = false;  // n <= 65536: (i << 16 | j) in pij, else i, j in ei, ej
+    DBuf<uint32_t> ei, ej, pij;
 };
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
                       KeptEdges& out);
