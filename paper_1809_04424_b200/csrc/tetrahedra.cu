@@ -39,6 +39,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kBits = 4096;     // ranks of x's id list per round
 constexpr int kWords = kBits / 32;
 constexpr int kS = 512;         // max |S(p)| handled (else VRB_ENOTSUP)
+constexpr int64_t kDenseMaxN = 16384;   // n x n u32 edge-position table (<= 1 GiB)
 
 struct TetArgs {
     int64_t n, E;
@@ -61,6 +62,8 @@ struct TetArgs {
     const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
     const ulonglong2* hslots;   // triangle lex code -> position: slot = (code, position), open addressing
     uint64_t hmask;
+    const uint16_t* apex;       // per triangle: its vertex off the owner edge (null: use the hash)
+    const uint32_t* dense;      // n x n edge positions (NONE32 = no edge), or null
     // count
     uint32_t* cnt;
     // fill
@@ -178,6 +181,73 @@ __device__ __forceinline__ uint32_t tri_lookup(const TetArgs& A, uint32_t a, uin
     }
 }
 
+// Positions of two triangles at once: both first probes are issued before
+// either is resolved (two independent DRAM round trips in flight per lane).
+__device__ __forceinline__ void tri_lookup2(const TetArgs& A, uint64_t c1, uint64_t c2, uint32_t& p1, uint32_t& p2) {
+    uint64_t h1 = mix64(c1) & A.hmask, h2 = mix64(c2) & A.hmask;
+    ulonglong2 s1 = __ldg(A.hslots + h1), s2 = __ldg(A.hslots + h2);
+    while (s1.x != c1) { h1 = (h1 + 1) & A.hmask; s1 = __ldg(A.hslots + h1); }
+    while (s2.x != c2) { h2 = (h2 + 1) & A.hmask; s2 = __ldg(A.hslots + h2); }
+    p1 = (uint32_t)s1.y;
+    p2 = (uint32_t)s2.y;
+}
+
+__device__ __forceinline__ uint64_t tri_code_sorted(uint32_t a, uint32_t b, uint32_t c) {
+    sort3v(a, b, c);
+    return tri_code(a, b, c);
+}
+
+// Faces of a tetrahedron by owner-edge search.  The triangle with owner edge
+// f (its largest edge position) and apex a (its vertex off f): when f is alone
+// at its filtration level, f's triangles sit at [toff[f], toff[f+1]) in apex
+// order, so its position is toff[f] + #apexes of f below a -- an 8-ary search
+// in the (L2-resident) apex array: 7 independent probes per round, then one
+// 8-entry scan, so ~3 dependent L2 round trips for the usual range of <= 64.
+// A tie level is lex-sorted as a whole: binary search by triple in tv.
+struct FaceQuery {
+    uint32_t f, a, a0, a1, a2;
+};
+
+__device__ __forceinline__ FaceQuery face_query(uint32_t u, uint32_t v, uint32_t w, uint32_t puv, uint32_t puw,
+                                                uint32_t pvw) {
+    FaceQuery q{puv, w, u, v, w};
+    if (puw > q.f) { q.f = puw; q.a = v; }
+    if (pvw > q.f) { q.f = pvw; q.a = u; }
+    sort3v(q.a0, q.a1, q.a2);
+    return q;
+}
+
+// #entries of apex[lo, hi) below a (ascending run)
+__device__ __forceinline__ uint64_t apex_rank(const uint16_t* __restrict__ apex, uint64_t lo, uint64_t hi, uint32_t a) {
+    while (hi - lo > 8) {
+        const uint64_t step = (hi - lo + 7) >> 3;
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+            const uint64_t q = lo + (uint64_t)i * step;
+            if (q < hi) c += __ldg(apex + q) < a ? 1u : 0u;
+        }
+        // all probes before lo + c*step are below a; the answer is in [lo + c*step, lo + (c+1)*step)
+        const uint64_t nlo = lo + (uint64_t)c * step;
+        hi = min(hi, nlo + step);
+        lo = nlo;
+    }
+    uint64_t r = lo;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (lo + i < hi && __ldg(apex + lo + i) < a) ++r;
+    return r;
+}
+
+__device__ __forceinline__ void face_pos2(const TetArgs& A, const FaceQuery& q1, const FaceQuery& q2, uint32_t& r1,
+                                          uint32_t& r2) {
+    const uint64_t s1 = A.toff[q1.f], e1 = A.toff[q1.f + 1], s2 = A.toff[q2.f], e2 = A.toff[q2.f + 1];
+    const bool d1 = A.tlo[q1.f] == s1 && A.thi[q1.f] == e1;
+    const bool d2 = A.tlo[q2.f] == s2 && A.thi[q2.f] == e2;
+    r1 = d1 ? (uint32_t)apex_rank(A.apex, s1, e1, q1.a) : tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2);
+    r2 = d2 ? (uint32_t)apex_rank(A.apex, s2, e2, q2.a) : tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2);
+}
+
 __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
                            uint64_t mask) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
@@ -244,7 +314,7 @@ __device__ uint32_t build_S(const TetArgs& A, const uint32_t* __restrict__ map, 
                 const uint32_t k = w & kmask;
                 W->Sk[idx] = k;
                 W->Spx[idx] = __ldg(lp + t);
-                atomicOr(&vbits[k >> 5], 1u << (k & 31));
+                if (vbits) atomicOr(&vbits[k >> 5], 1u << (k & 31));
             }
         }
         __syncwarp();
@@ -402,45 +472,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                 for (uint32_t ki = 0; ki + 1 < m; ++ki) {
                     const uint32_t c = mark_l(A, W, vbits, vpre, p, ki, m);
                     if (kFill && c) {
-                        const uint32_t k = W->Sk[ki];
-                        const uint32_t pxk = W->Spx[ki];
-                        const uint32_t pyk = map[k];
-                        const uint32_t f_yxk = direct ? (uint32_t)(tbase + ki) : 0u;
-                        for (uint32_t j = ki + 1 + lane; j < m; j += 32) {
-                            const uint32_t wd = W->lbits[j >> 5];
-                            if (!((wd >> (j & 31)) & 1u)) continue;
-                            const uint32_t l = W->Sk[j];
-                            const uint64_t s = slot + total + W->lpre[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u));
-                            const uint32_t pxl = W->Spx[j], pyl = map[l], pkl = W->lpos[j];
-                            uint32_t v[4] = {y, x, k, l};
-                            sort4v(v);
-                            uint32_t* qv = A.qv + 4 * s;
-                            qv[0] = v[0]; qv[1] = v[1]; qv[2] = v[2]; qv[3] = v[3];
-                            A.qf[s] = filt;
-                            if (A.rows) {
-                                uint32_t a, b, cc;
-                                // (y, x, k) and (y, x, l): owned by p
-                                uint32_t r[4];
-                                if (direct) {
-                                    r[0] = f_yxk;
-                                    r[1] = (uint32_t)(tbase + j);
-                                } else {
-                                    a = y; b = x; cc = k; sort3v(a, b, cc);
-                                    r[0] = tri_lookup(A, a, b, cc);
-                                    a = y; b = x; cc = l; sort3v(a, b, cc);
-                                    r[1] = tri_lookup(A, a, b, cc);
-                                }
-                                a = y; b = k; cc = l; sort3v(a, b, cc);   // (y, k, l)
-                                r[2] = tri_lookup(A, a, b, cc);
-                                a = x; b = k; cc = l; sort3v(a, b, cc);   // (x, k, l)
-                                r[3] = tri_lookup(A, a, b, cc);
-                                (void)pxk; (void)pxl; (void)pyk; (void)pyl; (void)pkl;
-                                sort4v(r);
-                                uint32_t* rw = A.rows + 4 * s;
-                                rw[0] = r[0]; rw[1] = r[1]; rw[2] = r[2]; rw[3] = r[3];
+                    const uint32_t k = W->Sk[ki];
+                    const uint32_t f_yxk = direct ? (uint32_t)(tbase + ki) : 0u;
+                    const uint32_t nw = (m + 31) >> 5;
+                    // dense lanes: lane takes the i-th marked l (i = lane, lane + 32, ...)
+                    for (uint32_t i = lane; i < c; i += 32) {
+                        uint32_t w = 0;
+                        while (w + 1 < nw && W->lpre[w + 1] <= i) ++w;
+                        const uint32_t j = 32 * w + (uint32_t)__fns(W->lbits[w], 0, (int)(i - W->lpre[w] + 1));
+                        const uint32_t l = W->Sk[j];
+                        const uint64_t s = slot + total + i;
+                        uint32_t v[4] = {y, x, k, l};
+                        sort4v(v);
+                        uint4* qv = reinterpret_cast<uint4*>(A.qv + 4 * s);
+                        *qv = make_uint4(v[0], v[1], v[2], v[3]);
+                        A.qf[s] = filt;
+                        if (A.rows) {
+                            uint32_t r[4];
+                            if (direct) {
+                                r[0] = f_yxk;
+                                r[1] = (uint32_t)(tbase + j);
+                            } else if (A.apex) {
+                                uint32_t a0 = y, a1 = x, a2 = k;
+                                sort3v(a0, a1, a2);
+                                r[0] = tri_pos(A, p, a0, a1, a2);
+                                a0 = y; a1 = x; a2 = l;
+                                sort3v(a0, a1, a2);
+                                r[1] = tri_pos(A, p, a0, a1, a2);
+                            } else {
+                                tri_lookup2(A, tri_code_sorted(y, x, k), tri_code_sorted(y, x, l), r[0], r[1]);
                             }
+                            if (A.apex) {
+                                const uint32_t pkl = W->lpos[j];
+                                face_pos2(A, face_query(y, k, l, map[k], map[l], pkl),
+                                          face_query(x, k, l, W->Spx[ki], W->Spx[j], pkl), r[2], r[3]);
+                            } else {
+                                tri_lookup2(A, tri_code_sorted(y, k, l), tri_code_sorted(x, k, l), r[2], r[3]);
+                            }
+                            sort4v(r);
+                            *reinterpret_cast<uint4*>(A.rows + 4 * s) = make_uint4(r[0], r[1], r[2], r[3]);
                         }
                     }
+                }
                     total += c;
                     __syncwarp();
                 }
@@ -452,6 +525,161 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
             __syncthreads();
             seg = end;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Dense-table variant (n <= kDenseMaxN; needs the apex array).  The pairs
+// (k, l), k < l, of S(p) are tested directly -- pos(k, l) < p in an n x n
+// table of edge positions (L2-resident for the configs of interest) --
+// instead of streaming every k's older-neighbour prefix.  The pairs are
+// walked in row-major (k, l) order, 32 per warp step: a ballot and a
+// prefix popcount place each tetrahedron, so emission is in lex order and
+// the stores of a step are contiguous.
+// ---------------------------------------------------------------------------
+struct TetScratchD {
+    uint32_t bits[kWords];
+    uint32_t wpre[kWords];
+    uint32_t Sk[kS];          // S sorted by id
+    uint32_t Spx[kS];         // pos(x, k)
+};
+
+// row i of the upper-triangular pair index q (rows of m - 1 - i pairs)
+__device__ __forceinline__ void pair_of(uint32_t q, uint32_t m, uint32_t& i, uint32_t& j) {
+    const float b = (float)(2 * m - 1);
+    int ii = (int)((b - sqrtf(b * b - 8.0f * (float)q)) * 0.5f);
+    ii = max(0, min(ii, (int)m - 2));
+    auto start = [&](int r) { return (uint32_t)(r * (2 * (int)m - r - 1) / 2); };
+    while (ii > 0 && start(ii) > q) --ii;
+    while (ii + 1 < (int)m - 1 && start(ii + 1) <= q) ++ii;
+    i = (uint32_t)ii;
+    j = q - start(ii) + (uint32_t)ii + 1u;
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* map = reinterpret_cast<uint32_t*>(smem);
+    const size_t map_b = (size_t)((A.n * 4 + 15) / 16) * 16;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int nthreads = blockDim.x;
+    TetScratchD* W = reinterpret_cast<TetScratchD*>(smem + map_b) + wid;
+    TetScratch* WS = reinterpret_cast<TetScratch*>(W);   // build_S uses the bits/wpre/Sk/Spx prefix
+    __shared__ int64_t s_lo, s_hi, s_end;
+    __shared__ uint32_t s_y;
+    __shared__ unsigned s_next;
+    for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
+    __syncthreads();
+    const uint32_t kmask = A.packed ? 0xFFFFu : 0xFFFFFFFFu;
+    const uint64_t n = (uint64_t)A.n;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
+            if (task >= A.task_hi) {
+                s_lo = s_hi = -1;
+            } else {
+                s_lo = lb_u64(A.work_pre, 0, A.E + 1, (uint64_t)task * A.chunk);
+                s_hi = task == A.ntasks - 1 ? A.E : lb_u64(A.work_pre, 0, A.E + 1, (uint64_t)(task + 1) * A.chunk);
+                if (s_lo > A.E) s_lo = A.E;
+                if (s_hi > A.E) s_hi = A.E;
+            }
+        }
+        __syncthreads();
+        const int64_t lo = s_lo, hi = s_hi;
+        __syncthreads();
+        if (lo < 0) break;
+        for (int64_t seg = lo; seg < hi;) {
+            if (threadIdx.x == 0) {
+                const uint32_t y = A.hosted_v[seg];
+                s_y = y;
+                s_end = ub_u32(A.hosted_v, seg, hi, y);
+                s_next = 0;
+            }
+            __syncthreads();
+            const uint32_t y = s_y;
+            const int64_t end = s_end;
+            const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
+            __syncthreads();
+            for (;;) {
+                unsigned my = 0;
+                if (lane == 0) my = atomicAdd(&s_next, 1u);
+                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+                if (e >= end) break;
+                const uint4 pl = A.plan[e];
+                const uint32_t p = pl.x, x = pl.y, len = pl.z;
+                if (len < 2) continue;
+                if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
+                const uint32_t m = build_S(A, map, WS, nullptr, p, x, len, A.off[x], pl.w);
+                if (m > (uint32_t)kS) {
+                    if (lane == 0) atomicOr(A.overflow, 1u);
+                    continue;
+                }
+                uint64_t slot = 0, tbase = 0;
+                uint32_t filt = 0;
+                bool direct = false;
+                if (kFill) {
+                    slot = A.qoff[p] - A.slot0;
+                    filt = A.efilt[p];
+                    tbase = A.toff[p];
+                    direct = A.tlo[p] == tbase && A.thi[p] == A.toff[p + 1];
+                }
+                const uint32_t npairs = m * (m - 1) / 2;
+                uint32_t total = 0;
+                for (uint32_t q0 = 0; q0 < npairs; q0 += 32) {
+                    const uint32_t q = q0 + lane;
+                    uint32_t i = 0, j = 0, pkl = NONE32;
+                    if (q < npairs) {
+                        pair_of(q, m, i, j);
+                        pkl = __ldg(A.dense + (uint64_t)W->Sk[i] * n + W->Sk[j]);
+                    }
+                    const bool valid = pkl < p;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, valid);
+                    if (kFill && valid) {
+                        const uint32_t k = W->Sk[i], l = W->Sk[j];
+                        const uint64_t s = slot + total + __popc(bal & lt);
+                        uint32_t v[4] = {y, x, k, l};
+                        sort4v(v);
+                        __stcs(reinterpret_cast<uint4*>(A.qv + 4 * s), make_uint4(v[0], v[1], v[2], v[3]));
+                        __stcs(A.qf + s, filt);
+                        if (A.rows) {
+                            uint32_t r[4];
+                            if (direct) {
+                                r[0] = (uint32_t)(tbase + i);
+                                r[1] = (uint32_t)(tbase + j);
+                            } else {
+                                uint32_t a0 = y, a1 = x, a2 = k;
+                                sort3v(a0, a1, a2);
+                                r[0] = tri_pos(A, p, a0, a1, a2);
+                                a0 = y; a1 = x; a2 = l;
+                                sort3v(a0, a1, a2);
+                                r[1] = tri_pos(A, p, a0, a1, a2);
+                            }
+                            face_pos2(A, face_query(y, k, l, map[k], map[l], pkl),
+                                      face_query(x, k, l, W->Spx[i], W->Spx[j], pkl), r[2], r[3]);
+                            sort4v(r);
+                            __stcs(reinterpret_cast<uint4*>(A.rows + 4 * s), make_uint4(r[0], r[1], r[2], r[3]));
+                        }
+                    }
+                    total += __popc(bal);
+                }
+                if (!kFill && lane == 0) A.cnt[p] = total;
+                __syncwarp();
+            }
+            __syncthreads();
+            for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
+            __syncthreads();
+            seg = end;
+        }
+    }
+}
+
+__global__ void k_dense_positions(const uint32_t* __restrict__ ev, int64_t E, int64_t n, uint32_t* __restrict__ tab) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = ev[2 * p], b = ev[2 * p + 1];
+        tab[a * (uint64_t)n + b] = (uint32_t)p;
+        tab[b * (uint64_t)n + a] = (uint32_t)p;
     }
 }
 
@@ -481,7 +709,45 @@ int tet_warps(int64_t n) {
     return 0;
 }
 
+int tet_dense_warps(int64_t n) {
+    const int64_t avail = (int64_t)device_max_smem_optin() - 1024 - (int64_t)((n * 4 + 15) / 16) * 16;
+    return (int)std::min<int64_t>(32, avail / (int64_t)sizeof(TetScratchD));
+}
+
 void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
+    if (A.dense && tet_dense_warps(A.n) >= 8) {
+        const int warps = tet_dense_warps(A.n);
+        const size_t smem = (size_t)((A.n * 4 + 15) / 16) * 16 + (size_t)warps * sizeof(TetScratchD);
+        if (fill)
+            VRB_CUDA(cudaFuncSetAttribute(k_tets_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else
+            VRB_CUDA(cudaFuncSetAttribute(k_tets_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        uint64_t chunk = work / 8192 + 1;
+        if (chunk < 16384) chunk = 16384;
+        A.chunk = chunk;
+        A.ntasks = (int64_t)((work + chunk - 1) / chunk);
+        if (A.ntasks < 1) A.ntasks = 1;
+        A.task_lo = A.ntasks * part / nparts;
+        A.task_hi = A.ntasks * (part + 1) / nparts;
+        if (A.task_lo >= A.task_hi) return;
+        DBuf<unsigned long long> counter(1, s);
+        DBuf<unsigned> overflow(1, s);
+        VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
+        VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
+        A.task_counter = counter.get();
+        A.overflow = overflow.get();
+        const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count(), A.task_hi - A.task_lo);
+        if (fill)
+            k_tets_dense<true><<<grid, warps * 32, smem, s>>>(A);
+        else
+            k_tets_dense<false><<<grid, warps * 32, smem, s>>>(A);
+        VRB_LAUNCH_CHECK();
+        unsigned h = 0;
+        VRB_CUDA(cudaMemcpyAsync(&h, overflow.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+        if (h) fail(VRB_ENOTSUP, "an edge owns more than %d triangles; tetrahedra not supported for this input", kS);
+        return;
+    }
     const int warps = tet_warps(A.n);
     if (warps < 4) fail(VRB_ENOTSUP, "tetrahedron kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
@@ -533,6 +799,8 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.thi = L.thi.get();
     A.tv = L.tv;
     A.hslots = L.hslots.get();
+    A.apex = L.apex;
+    A.dense = L.dense.get();
     A.hmask = L.hmask;
     return A;
 }
@@ -549,6 +817,16 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
     k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get());
     VRB_LAUNCH_CHECK();
+    if (L.apex) {   // face positions by owner-edge search (face_pos2)
+        if (L.n <= kDenseMaxN) {   // pair tests through an n x n table of edge positions
+            L.dense.alloc((size_t)(L.n * L.n), s);
+            VRB_CUDA(cudaMemsetAsync(L.dense.get(), 0xFF, L.dense.bytes(), s));
+            const unsigned gd = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
+            k_dense_positions<<<gd, 256, 0, s>>>(L.ev, E, L.n, L.dense.get());
+            VRB_LAUNCH_CHECK();
+        }
+        return;
+    }
     // triangle position hash (load factor <= 1/2)
     uint64_t T = 0;
     VRB_CUDA(cudaMemcpyAsync(&T, toff + E, sizeof(T), cudaMemcpyDeviceToHost, s));

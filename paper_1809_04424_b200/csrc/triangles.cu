@@ -89,6 +89,7 @@ struct TriArgs {
     uint32_t* tv;
     uint32_t* tf;
     uint32_t* rows;
+    uint16_t* apex;   // K >= 3, n <= 65536: apex id of each triangle (its vertex off the owner edge)
     int debug;   // ablation knob (VRB_DEBUG_FILL): 1 = stop after mark, 2 = skip the flush
 };
 
@@ -322,6 +323,7 @@ __device__ __forceinline__ void flush_vec(const TriArgs& A, const uint32_t* __re
             __stcs(rw + 2, p);
         }
         __stcs(A.tf + s0 + j, filt);
+        if (A.apex) A.apex[s0 + j] = (uint16_t)k;
     };
     uint32_t h = (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u);
     if (h > m) h = m;
@@ -352,6 +354,9 @@ __device__ __forceinline__ void flush_vec(const TriArgs& A, const uint32_t* __re
             __stcs(rw + 2, make_uint4(r[8], r[9], r[10], r[11]));
         }
         __stcs(reinterpret_cast<uint4*>(A.tf + s0 + j), make_uint4(filt, filt, filt, filt));
+        if (A.apex)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) A.apex[s0 + j + e] = (uint16_t)kp[e].x;
     }
     for (uint32_t j = h + 4 * nq + lane; j < m; j += 32) one(j);
 }
@@ -405,6 +410,7 @@ __device__ __forceinline__ void flush_window(const TriArgs& A, const uint32_t* _
                 __stcs(rw + 2, p);
             }
             __stcs(A.tf + s0 + j, filt);
+            if (A.apex) A.apex[s0 + j] = (uint16_t)k;
         }
     }
 }
@@ -620,6 +626,7 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
                         __stcs(rw + 2, p);
                     }
                     __stcs(A.tf + s0 + j, filt);
+                    if (A.apex) A.apex[s0 + j] = (uint16_t)k;
                 }
 #endif
             }
@@ -827,7 +834,7 @@ void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaSt
 }
 
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
-                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, cudaStream_t s) {
+                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s) {
     if (g.E == 0 || g.work == 0 || p_lo >= p_hi) return;
     TriArgs A = graph_args(g);
     A.efilt = efilt;
@@ -838,6 +845,7 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.tv = tv;
     A.tf = tf;
     A.rows = rows;
+    A.apex = g.n <= 65536 ? apex : nullptr;
     const char* dbg = std::getenv("VRB_DEBUG_FILL");   // ablation timing only; breaks outputs
     A.debug = dbg ? std::atoi(dbg) : 0;
     launch(A, true, g.work, 0, 1, s);

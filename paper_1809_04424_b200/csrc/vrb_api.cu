@@ -368,8 +368,11 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             uint32_t* tf = h->own<uint32_t>(Tl, s);
             uint32_t* trows = nullptr;
             if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * Tl, s);
+            // apex of every triangle (tetrahedra: face positions by owner-edge search)
+            DBuf<uint16_t> tapex;
+            if (h->K >= 3 && n <= 65536) tapex.alloc((size_t)Tl, s);
             timer.mark(3);
-            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, s);
+            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s);
             timer.mark(4);
             sort_tie_groups(2, efilt, toff.get(), E, tb_[0], tb_[1], n, tv, trows, s);
             timer.mark(5);
@@ -379,6 +382,9 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             if (h->K >= 3) {
                 // ---- tetrahedra (all triangles are on this rank)
                 TriLevels L;
+                L.apex = tapex.get();
+                L.ev = ev;
+                L.n = n;
                 triangle_levels(efilt, toff.get(), E, tv, s, L);
                 DBuf<uint32_t> qc(E, s);
                 count_tets(g, L, qc.get(), rank, world, s);

@@ -58,9 +58,10 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
 // of part `part` of `nparts` (0 of 1 = all) and leaves the others at 0.
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s);
 // Emit triangles of owner edges in [p_lo, p_hi) at slots toff[p] - slot0
-// (slot0 = toff[p_lo]).
+// (slot0 = toff[p_lo]).  apex (nullable; n <= 65536): each triangle's vertex
+// off its owner edge, for the face-position search of tetrahedra.
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
-                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, cudaStream_t s);
+                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s);
 // Reorder the k-simplices (k = 2, 3) of every tie group (>= 2 edges sharing a
 // level) into lex order (readings A3, A4); only owner edges in [p_lo, p_hi).
 // off = per-owner-edge simplex offsets (E + 1); verts/rows: (k+1) u32 each.
@@ -72,6 +73,10 @@ void sort_tie_groups(int k, const uint32_t* efilt, const uint64_t* off, int64_t 
 struct TriLevels {
     const uint64_t* toff = nullptr;   // E + 1 triangle offsets per owner edge
     const uint32_t* tv = nullptr;     // 3T vertices (global order)
+    const uint16_t* apex = nullptr;   // T: apex of each triangle (owner-edge search); null -> hash
+    const uint32_t* ev = nullptr;     // 2E edge endpoints in position order
+    int64_t n = 0;
+    DBuf<uint32_t> dense;             // n x n edge positions (n <= 16384 with apex), NONE32 = no edge
     DBuf<uint64_t> tlo, thi;          // E: triangle range of each edge's filtration level
     DBuf<ulonglong2> hslots;          // (triangle lex code, position), open addressing
     uint64_t hmask = 0;
