@@ -236,6 +236,19 @@ def main():
                 counts = [r.count(k) for k in range(w.maxdim + 2)]
             del r
     vrb.set_profiling(False)
+    # F1 (outside the step): dimension-0 persistence of one build, device-timed
+    h0 = None
+    if world == 1:
+        r = one_build(Xd)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        _, _, ness = r.h0()
+        e1.record(s)
+        torch.cuda.synchronize()
+        h0 = {"ms": e0.elapsed_time(e1), "essential_bars": int(ness),
+              "finite_bars": int(counts[0][0] - ness) if counts else None}
+        del r
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
@@ -321,6 +334,7 @@ def main():
                               "frac": path_gbs / peak},
             "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
             "clocks": clocks.summary(),
+            "h0_barcodes": h0,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

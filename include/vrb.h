@@ -152,6 +152,25 @@ vrb_status vrb_boundary_colptr(vrb_handle h, int32_t k, uint64_t* colptr_dev, vo
 
 vrb_status vrb_free(vrb_handle h);
 
+/* Dimension-0 persistence from the ranked edges (Algorithm 1
+ * P:210-227 on D_1, Pers/Barcode P:251-260, Fig. 4 caption P:286, readings
+ * A8/A13).  Every vertex is born at filtration 0; edge position e pairs with
+ * a vertex row iff e joins two components of the edges before it, i.e. iff e
+ * is in the minimum spanning forest under the total (filt, lex) edge order.
+ *   forest_pos : device, handle-owned: the n_finite forest edge positions,
+ *                ascending (the D_1 pivot columns -- the columns "clear and
+ *                compress" removes from the next reduction)
+ *   death_filt : device, handle-owned: filt of those edges, so the finite
+ *                dim-0 bars are [0, death_filt[i]) (integer levels; real
+ *                values via vrb_rank_values; zero-length bars are included)
+ *   n_finite   : number of finite bars (= n - n_essential)
+ *   n_essential: number of [0, inf) bars = connected components at the cap
+ * Computed on the first call (O(log n) Boruvka rounds on `stream`), cached in
+ * the handle.  Any pointer may be NULL.  Handles of vrb_build_dist hold every
+ * edge on every rank, so each rank gets the whole (identical) result. */
+vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const uint32_t** death_filt,
+                  int64_t* n_finite, int64_t* n_essential);
+
 /* sortperm (Fig. GPU_sortperm) on device: perm_dev gets
  * the 0-based stable ascending permutation of keys_dev (n doubles; -0.0 ==
  * +0.0; NaN -> VRB_EINVAL), dense_rank_dev (nullable) gets 1-based dense ranks

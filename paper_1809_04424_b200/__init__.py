@@ -34,7 +34,7 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count")
+           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count", "vrb_h0")
 
 STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total")
 
@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
     L.vrb_last_stage_ms.argtypes = [P(ctypes.c_double)]
     L.vrb_launch_count.restype = ctypes.c_ulonglong
     L.vrb_launch_count.argtypes = []
+    L.vrb_h0.restype = ctypes.c_int
+    L.vrb_h0.argtypes = [p, p, P(p), P(p), P(i64), P(i64)]
     _lib = L
     return L
 
@@ -222,6 +224,18 @@ class VRResult:
         n = self.count(dim)[2]
         return (_view(v.value, (n, dim + 1), "<i4", self, self.device),
                 _view(f.value, (n,), "<i4", self, self.device))
+
+    def h0(self, stream=None):
+        """Dimension-0 persistence (vrb_h0): (forest_pos, death_filt,
+        n_essential).  forest_pos: ascending positions of the minimum-spanning-forest
+        edges (the D_1 pivot columns); death_filt: their filt, so the finite bars are
+        [0, death_filt[i]); n_essential: number of [0, inf) bars (components)."""
+        pos, dth = ctypes.c_void_p(), ctypes.c_void_p()
+        nf, ne = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().vrb_h0(self._h, _stream_ptr(stream), ctypes.byref(pos), ctypes.byref(dth),
+                            ctypes.byref(nf), ctypes.byref(ne)))
+        return (_view(pos.value, (nf.value,), "<i4", self, self.device),
+                _view(dth.value, (nf.value,), "<i4", self, self.device), ne.value)
 
     def rank_values(self):
         p, nv = ctypes.c_void_p(), ctypes.c_int64()

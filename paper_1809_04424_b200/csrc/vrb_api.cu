@@ -159,6 +159,12 @@ struct vrb_result {
     uint32_t* filt[4] = {nullptr, nullptr, nullptr, nullptr};
     uint32_t* rows[4] = {nullptr, nullptr, nullptr, nullptr};    // dim 2..3 (dim 1 aliases verts[1])
     double* vor = nullptr;
+    uint32_t* ev_all = nullptr;      // 2E edge vertices of every rank (position order)
+    uint32_t* efilt_all = nullptr;   // E edge filt
+    bool h0_done = false;            // vrb_h0 cache
+    int64_t h0_nf = 0;
+    uint32_t* h0_pos = nullptr;
+    uint32_t* h0_death = nullptr;
     std::vector<vrb::Alloc> owned;
 
     template <class T>
@@ -322,6 +328,8 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
         uint32_t* efilt = h->own<uint32_t>(E, s);
         h->vor = h->own<double>(E, s);
         h->nvals = rank_edges(ke, ev, efilt, h->vor, s);
+        h->ev_all = ev;
+        h->efilt_all = efilt;
         ke = KeptEdges();
         timer.mark(1);
         {
@@ -524,6 +532,35 @@ vrb_status vrb_free(vrb_handle h) {
         if (!h) return;
         h->release_all();
         delete h;
+    });
+}
+
+namespace {
+struct H0Alloc {
+    vrb_result* h;
+    cudaStream_t s;
+};
+uint32_t* h0_alloc(int64_t n, void* ctx) {
+    auto* a = static_cast<H0Alloc*>(ctx);
+    return a->h->own<uint32_t>((size_t)n, a->s);
+}
+}  // namespace
+
+vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const uint32_t** death_filt,
+                  int64_t* n_finite, int64_t* n_essential) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (!h->h0_done) {
+            const cudaStream_t s = (cudaStream_t)stream;
+            H0Alloc ctx{h, s};
+            h->h0_nf = vrb::h0_forest(h->ev_all, h->efilt_all, h->n, h->count[1], s, h0_alloc, &ctx, &h->h0_pos,
+                                      &h->h0_death);
+            h->h0_done = true;
+        }
+        if (forest_pos) *forest_pos = h->h0_pos;
+        if (death_filt) *death_filt = h->h0_death;
+        if (n_finite) *n_finite = h->h0_nf;
+        if (n_essential) *n_essential = h->n - h->h0_nf;
     });
 }
 

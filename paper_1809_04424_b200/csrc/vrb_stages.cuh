@@ -89,4 +89,10 @@ void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const 
 
 int64_t dense_map_limit();   // largest n the shared-memory vertex map supports
 
+// F1 (h0.cu): minimum spanning forest of the edges under the position order
+// (Boruvka); returns its size and (through alloc_out) its positions ascending
+// and their filt.
+int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t E, cudaStream_t s,
+                  uint32_t* (*alloc_out)(int64_t, void*), void* ctx, uint32_t** pos_out, uint32_t** death_out);   // largest n the shared-memory vertex map supports
+
 }  // namespace vrb
