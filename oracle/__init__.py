@@ -50,6 +50,10 @@ def _L():
         lib.or_sortperm.argtypes = [c_p, c_i64, c_p, c_p]
         lib.or_new.restype = c_p
         lib.or_new.argtypes = [c_p, c_i64, c_i32, c_d, c_i32]
+        lib.or_new_dm.restype = c_p
+        lib.or_new_dm.argtypes = [c_p, c_i64, c_d, c_i32]
+        lib.or_latlon2euc.restype = None
+        lib.or_latlon2euc.argtypes = [c_p, c_i64, c_p]
         lib.or_free.restype = None
         lib.or_free.argtypes = [c_p]
         lib.or_n_edges.restype = c_i64
@@ -86,6 +90,14 @@ def length(X: np.ndarray, i: int, j: int) -> float:
     return _L().or_length(_ptr(X), X.shape[1], i, j)
 
 
+def latlon2euc(latlon) -> np.ndarray:
+    """(n, 2) degrees (lat, lon) -> (n, 3) unit-sphere xyz."""
+    a = np.ascontiguousarray(latlon, dtype=np.float64).reshape(-1, 2)
+    out = np.empty((a.shape[0], 3), dtype=np.float64)
+    _L().or_latlon2euc(_ptr(a), a.shape[0], _ptr(out))
+    return out
+
+
 def sortperm(v) -> tuple[np.ndarray, np.ndarray]:
     """(0-based stable ascending permutation, 1-based dense ranks)."""
     v = np.ascontiguousarray(v, dtype=np.float64)
@@ -117,12 +129,22 @@ class Oracle:
     """Steps 1-4 on construction; steps 5-7 via ``simplices(k)``; step 8 via
     ``barcodes``.  ``X`` is (n, d) row-major float64 (points are rows)."""
 
-    def __init__(self, X: np.ndarray, radius: float = np.inf, strict: bool = False):
-        self.X = np.ascontiguousarray(X, dtype=np.float64)
-        if self.X.ndim != 2:
-            raise ValueError("X must be (n, d)")
-        self.n, self.d = self.X.shape
-        self._h = _L().or_new(_ptr(self.X), self.n, self.d, float(radius), int(bool(strict)))
+    def __init__(self, X: np.ndarray, radius: float = np.inf, strict: bool = False, D: np.ndarray = None):
+        """X: (n, d) point cloud; or X=None and D: (n, n) distance matrix (upper
+        triangle = edge lengths)."""
+        if D is not None:
+            self.D = np.ascontiguousarray(D, dtype=np.float64)
+            if self.D.ndim != 2 or self.D.shape[0] != self.D.shape[1]:
+                raise ValueError("D must be (n, n)")
+            self.n, self.d = self.D.shape[0], 0
+            self.X = np.zeros((self.n, 0))
+            self._h = _L().or_new_dm(_ptr(self.D), self.n, float(radius), int(bool(strict)))
+        else:
+            self.X = np.ascontiguousarray(X, dtype=np.float64)
+            if self.X.ndim != 2:
+                raise ValueError("X must be (n, d)")
+            self.n, self.d = self.X.shape
+            self._h = _L().or_new(_ptr(self.X), self.n, self.d, float(radius), int(bool(strict)))
         if not self._h:
             raise MemoryError("oracle allocation failed")
         self.E = _L().or_n_edges(self._h)

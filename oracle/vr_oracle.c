@@ -133,19 +133,24 @@ static int cmp_edge(const void* pa, const void* pb) {
 }
 
 /* Steps 1-4.  Returns NULL on allocation failure. */
-or_ctx* or_new(const double* X, int64_t n, int32_t d, double radius, int32_t strict) {
+/* Steps 1-4 from either a point cloud X (n x d) or a distance matrix D (n x n,
+ * D != NULL): "x is either a point cloud ... or a square symmetric matrix
+ * (typically a pairwise distance matrix)" (sec. 3).
+ * With D the length of edge (i, j), i < j, is the upper-triangle entry
+ * D[i][j] (+0.0, so a -0.0 entry is the length +0.0). */
+static or_ctx* or_new_impl(const double* X, const double* D, int64_t n, int32_t d, double radius, int32_t strict) {
     or_ctx* c = (or_ctx*)calloc(1, sizeof(or_ctx));
     if (!c) return NULL;
     c->n = n; c->d = d; c->radius = radius; c->strict = strict;
     c->X = (double*)malloc((size_t)(n * d ? n * d : 1) * sizeof(double));
-    memcpy(c->X, X, (size_t)(n * d) * sizeof(double));
+    if (X) memcpy(c->X, X, (size_t)(n * d) * sizeof(double));
 
     /* Steps 1-2: every pair i < j, keep iff len <= r (len < r when strict). */
     int64_t cap = 1024, E = 0;
     edge_rec* er = (edge_rec*)malloc((size_t)cap * sizeof(edge_rec));
     for (int64_t i = 0; i < n; ++i) {
         for (int64_t j = i + 1; j < n; ++j) {
-            double len = or_length(c->X, d, i, j);
+            double len = D ? D[i * n + j] + 0.0 : or_length(c->X, d, i, j);
             int keep = strict ? (len < radius) : (len <= radius);
             if (!keep) continue;
             if (E == cap) { cap *= 2; er = (edge_rec*)realloc(er, (size_t)cap * sizeof(edge_rec)); }
@@ -196,6 +201,27 @@ or_ctx* or_new(const double* X, int64_t n, int32_t d, double radius, int32_t str
             if (c->posmat[i * n + j] != NONE32) c->up_nbr[w++] = (uint32_t)j;
     }
     return c;
+}
+
+or_ctx* or_new(const double* X, int64_t n, int32_t d, double radius, int32_t strict) {
+    return or_new_impl(X, NULL, n, d, radius, strict);
+}
+
+or_ctx* or_new_dm(const double* D, int64_t n, double radius, int32_t strict) {
+    return or_new_impl(NULL, D, n, 0, radius, strict);
+}
+
+/* latlon2euc (sec. 3): spherical coordinates in degrees on the
+ * unit sphere -> Euclidean (cos(lat) cos(lon), cos(lat) sin(lon), sin(lat)).
+ * P:403-407 prints (34.983, 63.1333) -> (0.370265, 0.730885, 0.573333). */
+void or_latlon2euc(const double* latlon, int64_t n, double* xyz) {
+    const double deg = 3.14159265358979323846 / 180.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double la = latlon[2 * i] * deg, lo = latlon[2 * i + 1] * deg;
+        xyz[3 * i] = cos(la) * cos(lo);
+        xyz[3 * i + 1] = cos(la) * sin(lo);
+        xyz[3 * i + 2] = sin(la);
+    }
 }
 
 void or_free(or_ctx* c) {

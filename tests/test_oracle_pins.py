@@ -246,11 +246,14 @@ def test_capped_counts_by_linear_algebra(seed, n, r):
 # --------------------------------------------------------------------------
 
 def _brute(X, radius, strict, K):
-    n = X.shape[0]
+    return _brute_len(X.shape[0], lambda i, j: oracle.length(X, i, j), radius, strict, K)   # length pinned above (P1)
+
+
+def _brute_len(n, length_of, radius, strict, K):
     L = {}
     for i in range(n):
         for j in range(i + 1, n):
-            length = oracle.length(X, i, j)        # pinned above (P1)
+            length = length_of(i, j)
             if (length < radius) if strict else (length <= radius):
                 L[(i, j)] = length
     vals = sorted(set(L.values()))
@@ -468,3 +471,67 @@ def test_c2_mixture_counts_and_betti():
     assert o.simplices(2)[0].shape[0] == 129438
     assert o.simplices(3)[0].shape[0] == 645405
     assert _alive_at_cap(o.barcodes(2, method="clear"), 2) == (2, 3, 1)
+
+
+# --------------------------------------------------------------------------
+# distance-matrix input ("x is either a point cloud ... or a
+# square symmetric matrix (typically a pairwise distance matrix)")
+# and latlon2euc.
+# --------------------------------------------------------------------------
+
+def test_latlon2euc_printed_worldmap_columns():
+    g = _load("latlon2euc_worldmap.json")
+    xyz = oracle.latlon2euc(np.array(g["latlon"]))
+    np.testing.assert_allclose(xyz, np.array(g["xyz"]), atol=0.6 * 10.0 ** -g["decimals"], rtol=0)
+    np.testing.assert_allclose(np.linalg.norm(xyz, axis=1), 1.0, atol=1e-15)     # unit sphere
+
+
+def _dm_exact(X):
+    """Distance matrix of integer-coordinate points: d2 is an exact integer,
+    np.sqrt is IEEE correctly rounded, so the entries are the exact lengths."""
+    d2 = ((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)
+    return np.sqrt(d2)
+
+
+def test_dm_golden_unit_square_and_ties():
+    g = _load("unit_square.json")
+    X = np.array(g["points"], dtype=np.float64)
+    _check_complex(oracle.Oracle(None, _radius(g["radius"]), D=_dm_exact(X)), g, g["maxdim"])
+    g = _load("ties_five_points.json")
+    X = np.array(g["points"], dtype=np.float64)
+    _check_complex(oracle.Oracle(None, INF, D=_dm_exact(X)), g["full"], g["maxdim"])
+    for key in ("inclusive_r5", "strict_r5"):
+        c = g[key]
+        o = oracle.Oracle(None, c["radius"], strict=c["strict"], D=_dm_exact(X))
+        assert o.E == c["n_edges"]
+        assert o.barcodes(g["maxdim"]).tolist() == sorted(c["bars"])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_dm_hamming_bruteforce(seed):
+    # HIV-like input (P:520-521: Hamming distances of sequences): integer
+    # lengths, heavy ties; against brute force over all subsets
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.integers(0, 10))
+    seqs = rng.integers(0, 2, (n, 10))
+    D = (seqs[:, None, :] != seqs[None, :, :]).sum(-1).astype(np.float64)
+    radius = [INF, 3.0, 4.0, 5.0][seed % 4]
+    strict = seed % 3 == 0
+    out, filt, rows, vals = _brute_len(n, lambda i, j: D[i, j], radius, strict, 3)
+    o = oracle.Oracle(None, radius, strict, D=D)
+    ev, ef, el, vor = o.edges()
+    assert [tuple(e) for e in ev.tolist()] == out[1]
+    assert ef.tolist() == [filt[1][e] for e in out[1]]
+    assert vor.tolist() == vals
+    for k in (2, 3):
+        v, f, r = o.simplices(k)
+        assert [tuple(x) for x in v.tolist()] == out[k]
+        assert f.tolist() == [filt[k][x] for x in out[k]]
+        assert r.tolist() == rows[k]
+
+
+def test_dm_negative_zero_is_length_zero():
+    D = np.array([[0.0, -0.0], [-0.0, 0.0]])
+    o = oracle.Oracle(None, 0.0, D=D)
+    ev, ef, el, vor = o.edges()
+    assert o.E == 1 and np.signbit(el[0]) == 0 and el[0] == 0.0
