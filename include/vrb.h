@@ -152,6 +152,24 @@ vrb_status vrb_boundary_colptr(vrb_handle h, int32_t k, uint64_t* colptr_dev, vo
 
 vrb_status vrb_free(vrb_handle h);
 
+/* Build from a distance matrix ("x is either a
+ * point cloud ... or a square symmetric matrix (typically a pairwise distance
+ * matrix)"; HIV's Hamming matrix P:520-521).  Same outputs and opts as
+ * vrb_build, with S1-S2 replaced by: edge (i, j), i < j, has length
+ * D[i*n + j] (+0.0, so -0.0 is 0.0); kept iff length <= radius (< with
+ * VRB_STRICT_RADIUS).  D: n x n row-major f64, host (copied H2D) or device
+ * (VRB_POINTS_ON_DEVICE), caller-owned, read-only.  VRB_EINVAL if an
+ * off-diagonal entry is negative, NaN or infinite, if D[i][j] != D[j][i]
+ * (the diagonal is not read), or with VRB_DIM_MAJOR. */
+vrb_status vrb_build_dm(const double* D, int64_t n, const vrb_opts* opts, void* stream, vrb_handle* out);
+
+/* latlon2euc (sec. 3): latlon_dev n x 2 f64 (latitude, longitude
+ * in degrees, one point per row) -> xyz_dev n x 3 f64 on the unit sphere,
+ * (cos lat cos lon, cos lat sin lon, sin lat); device pointers, caller-owned;
+ * the result is complete when the call returns.  CUDA's sincos is within
+ * 1 ulp (not bit-identical to a host libm). */
+vrb_status vrb_latlon2euc(const double* latlon_dev, int64_t n, double* xyz_dev, void* stream);
+
 /* Dimension-0 persistence from the ranked edges (Algorithm 1
  * P:210-227 on D_1, Pers/Barcode P:251-260, Fig. 4 caption P:286, readings
  * A8/A13).  Every vertex is born at filtration 0; edge position e pairs with

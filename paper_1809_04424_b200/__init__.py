@@ -34,7 +34,8 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count", "vrb_h0")
+           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count", "vrb_h0", "vrb_build_dm",
+           "vrb_latlon2euc")
 
 STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total")
 
@@ -104,6 +105,10 @@ def lib() -> ctypes.CDLL:
     L.vrb_last_stage_ms.argtypes = [P(ctypes.c_double)]
     L.vrb_launch_count.restype = ctypes.c_ulonglong
     L.vrb_launch_count.argtypes = []
+    L.vrb_build_dm.restype = ctypes.c_int
+    L.vrb_build_dm.argtypes = [p, i64, P(vrb_opts), p, P(p)]
+    L.vrb_latlon2euc.restype = ctypes.c_int
+    L.vrb_latlon2euc.argtypes = [p, i64, p, p]
     L.vrb_h0.restype = ctypes.c_int
     L.vrb_h0.argtypes = [p, p, P(p), P(p), P(i64), P(i64)]
     _lib = L
@@ -314,6 +319,43 @@ def build(points, maxdim: int = 1, radius: float = math.inf, strict: bool = Fals
                                ctypes.byref(h)))
     del keep
     return VRResult(h.value, device)
+
+
+def build_dm(D, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
+             skip_boundary: bool = False, stream=None) -> VRResult:
+    """vrb_build_dm: D (n, n) float64 symmetric distance matrix (numpy / CPU
+    tensor -> copied H2D inside the call; CUDA tensor -> used in place)."""
+    import torch
+
+    ptr, n, n2, flags, keep = _prepare_points(D, None)
+    if n != n2:
+        raise ValueError("D must be square (n, n)")
+    device = keep.device if (flags & VRB_POINTS_ON_DEVICE) else torch.device("cuda", torch.cuda.current_device())
+    if strict:
+        flags |= VRB_STRICT_RADIUS
+    if skip_boundary:
+        flags |= VRB_SKIP_BOUNDARY
+    opts = vrb_opts(int(maxdim), float(radius), flags)
+    h = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        _check(lib().vrb_build_dm(ctypes.c_void_p(ptr), n, ctypes.byref(opts), _stream_ptr(stream), ctypes.byref(h)))
+    del keep
+    return VRResult(h.value, device)
+
+
+def latlon2euc(latlon, stream=None):
+    """vrb_latlon2euc: (n, 2) float64 CUDA tensor of (lat, lon) degrees -> (n, 3)
+    unit-sphere coordinates."""
+    import torch
+
+    if not (isinstance(latlon, torch.Tensor) and latlon.is_cuda and latlon.dtype == torch.float64):
+        raise TypeError("latlon must be a float64 CUDA tensor")
+    a = latlon.detach().contiguous().reshape(-1, 2)
+    out = torch.empty((a.shape[0], 3), dtype=torch.float64, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib().vrb_latlon2euc(ctypes.c_void_p(a.data_ptr()), a.shape[0], ctypes.c_void_p(out.data_ptr()),
+                                    _stream_ptr(stream)))
+    return out
 
 
 def allgather_bytes(src, dst, group=None):

@@ -164,7 +164,146 @@ __global__ void k_transpose(const double* __restrict__ in, double* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// F3: distance-matrix input ("a square symmetric matrix (typically a
+// pairwise distance matrix)").  Edge (i, j), i < j, has length D[i][j] + 0.0
+// (so -0.0 is +0.0).  Checked: off-diagonal entries finite, >= 0 and
+// D[i][j] == D[j][i] (32 x 32 tiles staged through shared memory so both
+// reads are coalesced); the diagonal is ignored.
+// ---------------------------------------------------------------------------
+__global__ void k_dm_check(const double* __restrict__ D, int64_t n, int* __restrict__ bad) {
+    __shared__ double tile[32][33];
+    const int64_t nt = (n + 31) / 32;
+    for (int64_t t = blockIdx.x; t < nt * nt; t += gridDim.x) {
+        const int64_t ti = t / nt, tj = t % nt;
+        if (tj < ti) continue;
+        // tile (tj, ti) transposed into shared memory
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t i = tj * 32 + r, j = ti * 32 + threadIdx.x;
+            tile[r][threadIdx.x] = (i < n && j < n) ? D[i * n + j] : 0.0;
+        }
+        __syncthreads();
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int64_t i = ti * 32 + r, j = tj * 32 + threadIdx.x;
+            if (i < n && j < n && i != j) {
+                const double a = D[i * n + j], b = tile[threadIdx.x][r];
+                if (!(a >= 0.0) || isinf(a) || a != b) atomicOr(bad, 1);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ bool dm_keep(double len, double r, int strict) { return strict ? len < r : len <= r; }
+
+// kept pairs j > i of row i (one warp per row)
+__global__ void k_dm_count(const double* __restrict__ D, int64_t n, double r, int strict, uint32_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
+        uint32_t c = 0;
+        for (int64_t j = i + 1 + lane; j < n; j += 32) c += dm_keep(D[i * n + j] + 0.0, r, strict) ? 1u : 0u;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) cnt[i] = c;
+    }
+}
+
+// kept pairs of row i in lex order at [off[i], off[i+1]) (ballot compaction)
+__global__ void k_dm_fill(const double* __restrict__ D, int64_t n, double r, int strict,
+                          const uint64_t* __restrict__ off, uint64_t* __restrict__ key, uint32_t* __restrict__ ei,
+                          uint32_t* __restrict__ ej, uint32_t* __restrict__ pij) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
+        uint64_t slot = off[i];
+        for (int64_t j0 = i + 1; j0 < n; j0 += 32) {
+            const int64_t j = j0 + lane;
+            const double len = j < n ? D[i * n + j] + 0.0 : 0.0;
+            const bool keep = j < n && dm_keep(len, r, strict);
+            const uint32_t b = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint64_t q = slot + __popc(b & ((1u << lane) - 1u));
+                key[q] = (uint64_t)__double_as_longlong(len);
+                if (pij) {
+                    pij[q] = ((uint32_t)i << 16) | (uint32_t)j;
+                } else {
+                    ei[q] = (uint32_t)i;
+                    ej[q] = (uint32_t)j;
+                }
+            }
+            slot += __popc(b);
+        }
+    }
+}
+
+// latlon2euc: degrees on the unit sphere -> xyz
+__global__ void k_latlon2euc(const double* __restrict__ ll, int64_t n, double* __restrict__ xyz) {
+    const double deg = 3.14159265358979323846 / 180.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double sla, cla, slo, clo;
+        sincos(__dmul_rn(ll[2 * i], deg), &sla, &cla);
+        sincos(__dmul_rn(ll[2 * i + 1], deg), &slo, &clo);
+        xyz[3 * i] = __dmul_rn(cla, clo);
+        xyz[3 * i + 1] = __dmul_rn(cla, slo);
+        xyz[3 * i + 2] = sla;
+    }
+}
+
 }  // namespace
+
+void latlon2euc(const double* latlon, int64_t n, double* xyz, cudaStream_t s) {
+    if (n <= 0) return;
+    k_latlon2euc<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4096), 256, 0, s>>>(latlon, n, xyz);
+    VRB_LAUNCH_CHECK();
+}
+
+void place_matrix(const double* D, int64_t n, uint32_t flags, cudaStream_t s, DBuf<double>& out) {
+    const int64_t total = n * n;
+    out.alloc((size_t)total, s);
+    if (total == 0) return;
+    VRB_CUDA(cudaMemcpyAsync(out.get(), D, total * sizeof(double),
+                             (flags & VRB_POINTS_ON_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    DBuf<int> bad(1, s);
+    VRB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    const int64_t nt = ceil_div(n, 32);
+    k_dm_check<<<(unsigned)std::min<int64_t>(nt * nt, (int64_t)device_sm_count() * 16), dim3(32, 8), 0, s>>>(
+        out.get(), n, bad.get());
+    VRB_LAUNCH_CHECK();
+    int h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (h) fail(VRB_EINVAL, "distance matrix: an off-diagonal entry is negative, non-finite or asymmetric");
+}
+
+void build_kept_edges_dm(const double* D, int64_t n, double radius, bool strict, cudaStream_t s, KeptEdges& out) {
+    out.E = 0;
+    if (n < 2) return;
+    DBuf<uint32_t> cnt(n, s);
+    DBuf<uint64_t> off(n + 1, s);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)device_sm_count() * 16);
+    k_dm_count<<<g, 256, 0, s>>>(D, n, radius, strict ? 1 : 0, cnt.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(cnt.get(), off.get(), n, s);
+    uint64_t E = 0;
+    VRB_CUDA(cudaMemcpyAsync(&E, off.get() + n, sizeof(E), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (E >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu kept edges exceed u32 positions", (unsigned long long)E);
+    out.E = (int64_t)E;
+    if (E == 0) return;
+    out.key.alloc(E, s);
+    out.packed = n <= 65536;
+    if (out.packed) {
+        out.pij.alloc(E, s);
+    } else {
+        out.ei.alloc(E, s);
+        out.ej.alloc(E, s);
+    }
+    k_dm_fill<<<g, 256, 0, s>>>(D, n, radius, strict ? 1 : 0, off.get(), out.key.get(), out.ei.get(), out.ej.get(),
+                                out.pij.get());
+    VRB_LAUNCH_CHECK();
+}
 
 // Threshold on d2 equivalent to the cap on len = sqrt_rn(d2) (reading A1).
 double cap_threshold(double r, bool strict) {

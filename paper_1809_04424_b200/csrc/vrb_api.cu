@@ -297,7 +297,7 @@ void read_offsets(const uint64_t* off, int64_t E, const int64_t* b, cudaStream_t
 
 // The shared body of vrb_build / vrb_build_dist.
 void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
-                cudaStream_t s, vrb_handle* out) {
+                cudaStream_t s, vrb_handle* out, bool matrix = false) {
     check_opts(X, n, d, opts, out);
     const int rank = comm ? comm->rank : 0;
     const int world = comm ? comm->world : 1;
@@ -318,9 +318,15 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
         timer.start(s);
 
         DBuf<double> Xd;
-        place_points(X, n, d, opts->flags, s, Xd);
         KeptEdges ke;
-        build_kept_edges(Xd.get(), n, d, opts->radius, (opts->flags & VRB_STRICT_RADIUS) != 0, s, ke);
+        if (matrix) {   // F3: X is an n x n distance matrix
+            place_matrix(X, n, opts->flags, s, Xd);
+            build_kept_edges_dm(Xd.get(), n, opts->radius, (opts->flags & VRB_STRICT_RADIUS) != 0, s, ke);
+        } else {
+            place_points(X, n, d, opts->flags, s, Xd);
+            build_kept_edges(Xd.get(), n, d, opts->radius, (opts->flags & VRB_STRICT_RADIUS) != 0, s, ke);
+        }
+        Xd.reset();
         timer.mark(0);
         const int64_t E = ke.E;
         h->count[1] = E;
@@ -467,6 +473,22 @@ vrb_status vrb_set_allocator(vrb_alloc_fn alloc, vrb_free_fn free_fn, void* ctx)
 
 vrb_status vrb_build(const double* X, int64_t n, int32_t d, const vrb_opts* opts, void* stream, vrb_handle* out) {
     return guarded([&] { build_impl(X, n, d, opts, nullptr, (cudaStream_t)stream, out); });
+}
+
+vrb_status vrb_build_dm(const double* D, int64_t n, const vrb_opts* opts, void* stream, vrb_handle* out) {
+    return guarded([&] {
+        if (opts && (opts->flags & VRB_DIM_MAJOR)) fail(VRB_EINVAL, "VRB_DIM_MAJOR does not apply to a distance matrix");
+        build_impl(D, n, 1, opts, nullptr, (cudaStream_t)stream, out, true);
+    });
+}
+
+vrb_status vrb_latlon2euc(const double* latlon_dev, int64_t n, double* xyz_dev, void* stream) {
+    return guarded([&] {
+        if (n < 0) fail(VRB_EINVAL, "n < 0");
+        if (n > 0 && (!latlon_dev || !xyz_dev)) fail(VRB_EINVAL, "NULL pointer");
+        vrb::latlon2euc(latlon_dev, n, xyz_dev, (cudaStream_t)stream);
+        VRB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    });
 }
 
 vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,

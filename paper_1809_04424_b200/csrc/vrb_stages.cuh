@@ -22,6 +22,14 @@ struct KeptEdges {
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
                       KeptEdges& out);
 
+// F3: distance-matrix input.  place_matrix copies (if host) and checks D
+// (n x n, off-diagonal finite, >= 0, symmetric; VRB_EINVAL otherwise);
+// build_kept_edges_dm keeps i < j with D[i][j] <= r (< r strict) in lex order.
+void place_matrix(const double* D, int64_t n, uint32_t flags, cudaStream_t s, DBuf<double>& out);
+void build_kept_edges_dm(const double* D, int64_t n, double radius, bool strict, cudaStream_t s, KeptEdges& out);
+// latlon2euc: latlon n x 2 degrees -> xyz n x 3 (device pointers).
+void latlon2euc(const double* latlon, int64_t n, double* xyz, cudaStream_t s);
+
 // S3: edge filtration order (len, i, j), dense ranks, value_of_rank.
 //   ev    : 2E u32 (i, j) per edge in position order   (caller-allocated)
 //   efilt : E u32 dense rank, 1-based                    (caller-allocated)
