@@ -181,6 +181,22 @@ __global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_
     }
 }
 
+// (k, pos) of every neighbour in neighbour-ID order (packed lists): one warp
+// per vertex scatters its position-ordered entries by their id rank
+__global__ void k_id_lists(const uint64_t* __restrict__ off, int64_t n, const uint32_t* __restrict__ nkr,
+                           const uint32_t* __restrict__ np, uint2* __restrict__ idl) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = w0; v < n; v += nw) {
+        const uint64_t o0 = off[v], o1 = off[v + 1];
+        for (uint64_t t = o0 + lane; t < o1; t += 32) {
+            const uint32_t w = nkr[t];
+            idl[o0 + (w >> 16)] = make_uint2(w & 0xFFFFu, np[t]);
+        }
+    }
+}
+
 __global__ void k_max_deg(const uint32_t* __restrict__ deg, int64_t n, unsigned* __restrict__ out) {
     unsigned m = 0;
     GRID_STRIDE(v, n) m = max(m, deg[v]);
@@ -300,6 +316,12 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
                                                           g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
             VRB_LAUNCH_CHECK();
         }
+    }
+    if (g.packed) {
+        g.idl.alloc(n2, s);
+        const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)device_sm_count() * 16);
+        k_id_lists<<<gw, 256, 0, s>>>(g.off.get(), n, g.nkr.get(), g.np.get(), g.idl.get());
+        VRB_LAUNCH_CHECK();
     }
     {
         // (c) owner-edge plan: scanned endpoint, prefix length, host; edges by host

@@ -90,6 +90,9 @@ struct TriArgs {
     uint32_t* tf;
     uint32_t* rows;
     uint16_t* apex;   // K >= 3, n <= 65536: apex id of each triangle (its vertex off the owner edge)
+    uint32_t* bm;              // apex bitmaps (count writes, fill reads), or null
+    const uint64_t* bmoff;     // per hosted slot: word offset of its bitmap
+    const uint2* idl;          // (k, pos) in neighbour-ID order
     int debug;   // ablation knob (VRB_DEBUG_FILL): 1 = stop after mark, 2 = skip the flush
 };
 
@@ -573,7 +576,7 @@ template <bool kOneRound>
 __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* __restrict__ map,
                                              WarpScratch3* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
                                              uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
-                                             uint32_t filt) {
+                                             uint32_t filt, const uint32_t* __restrict__ bmw = nullptr) {
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
@@ -581,14 +584,20 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
     const int ngroups = (int)((len + mis + 3) >> 2);
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = kOneRound ? degx : min((uint32_t)kBits, degx - R);
-        clear_bits(W, lim);
-        auto mark = [&](uint32_t w, uint32_t) {
-            const uint32_t r = (w >> 16) - R;
-            if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
-                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
-        };
-        if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
-        else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
+        if (bmw) {   // the count pass's apex bitmap replaces the mark
+            const uint32_t nw = (lim + 31) >> 5;
+            for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = __ldcs(bmw + (R >> 5) + w);
+            __syncwarp();
+        } else {
+            clear_bits(W, lim);
+            auto mark = [&](uint32_t w, uint32_t) {
+                const uint32_t r = (w >> 16) - R;
+                if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
+                    atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+            };
+            if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
+            else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
+        }
         const uint32_t count = rank_bits<kWords>(W, lim);
         if (A.debug == 1) { slot += count; if (kOneRound) break; continue; }
         for (uint32_t w0 = 0; w0 < count; w0 += kWin3) {
@@ -637,11 +646,143 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
     }
 }
 
-template <bool kFill, bool kPacked>
+// ---------------------------------------------------------------------------
+// Apex-bitmap path (single rank, packed lists, degrees <= kApexBitmapMaxDeg).
+// The count pass keeps what it computes: per owner edge, the bitmap of its
+// valid apexes by rank r in x's id-ordered list (ceil(deg x / 32) words,
+// written coalesced).  The fill then never touches the candidates again:
+// it loads the bitmap, prefix-popcounts its words, walks the set bits of a
+// window of slots (lane owns words lane, lane + 32, ...) staging r, and
+// flushes one lane per triangle with (k, pos(x, k)) = idl[off x + r] -- a
+// gather in rank order, so a warp's 32 loads fall in a few sectors.
+// ---------------------------------------------------------------------------
+#ifndef VRB_TRI_BMFILL
+#define VRB_TRI_BMFILL 1
+#endif
+// VRB_TRI_BMFILL: 2 = the bitmap replaces the mark of warp_fill_kp (the emit
+// streams the prefix with its positions); 1 = warp_fill_bm (emit by walking
+// the bitmap, (k, pos) gathered from the id-ordered lists)
+constexpr int kBmWords = (int)(kApexBitmapMaxDeg / 32);
+constexpr int kWinB = 512;
+struct WarpScratchC {              // count
+    uint32_t bits[kBmWords];
+};
+struct WarpScratchB {              // fill
+    uint32_t bits[kBmWords];
+    uint16_t wpre[kBmWords];
+    uint16_t rec[kWinB];
+};
+
+__device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32_t* __restrict__ map,
+                                                  WarpScratchC* __restrict__ W, uint32_t p, uint64_t offx,
+                                                  uint32_t len, uint32_t degx, int64_t e) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (degx + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
+    __syncwarp();
+    int mis;
+    const uint4* g = aligned_groups(A.nkr + offx, mis);
+    const int ngroups = (int)((len + mis + 3) >> 2);
+    auto mark = [&](uint32_t w, uint32_t) {
+        if (map[w & 0xFFFFu] < p) {
+            const uint32_t r = w >> 16;
+            atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+        }
+    };
+    stream_prefix<kRegGroups>(g, ngroups, mis, len, mark);
+    __syncwarp();
+    uint32_t* out = A.bm + A.bmoff[e];
+    uint32_t c = 0;
+    for (uint32_t w = lane; w < nw; w += 32) {
+        const uint32_t b = W->bits[w];
+        __stcg(out + w, b);
+        c += __popc(b);
+    }
+    return __reduce_add_sync(0xffffffffu, c);
+}
+
+__device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* __restrict__ map,
+                                             WarpScratchB* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                             uint64_t offx, uint32_t degx, int64_t e, uint64_t slot, uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (degx + 31) >> 5;
+    const uint32_t* in = A.bm + A.bmoff[e];
+    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = __ldcs(in + w);
+    __syncwarp();
+    // exclusive per-word prefix popcounts, lane owns kBmWords / 32 consecutive words
+    constexpr int kWpl = kBmWords / 32;
+    uint32_t c[kWpl], tot = 0;
+#pragma unroll
+    for (int j = 0; j < kWpl; ++j) {
+        const uint32_t wd = kWpl * lane + j;
+        c[j] = wd < nw ? __popc(W->bits[wd]) : 0u;
+        tot += c[j];
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    uint32_t run = incl - tot;
+#pragma unroll
+    for (int j = 0; j < kWpl; ++j) {
+        const uint32_t wd = kWpl * lane + j;
+        if (wd < nw) W->wpre[wd] = (uint16_t)run;
+        run += c[j];
+    }
+    const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    const uint2* __restrict__ idx = A.idl + offx;
+    for (uint32_t w0 = 0; w0 < count; w0 += kWinB) {
+        const uint32_t w1 = w0 + kWinB;
+        for (uint32_t wd = lane; wd < nw; wd += 32) {
+            uint32_t b = W->bits[wd];
+            uint32_t s = W->wpre[wd];
+            if (s >= w1 || s + __popc(b) <= w0) continue;
+            while (b) {
+                const int bit = __ffs(b) - 1;
+                b &= b - 1;
+                if (s >= w0 && s < w1) W->rec[s - w0] = (uint16_t)(32 * wd + bit);
+                ++s;
+            }
+        }
+        __syncwarp();
+        const uint32_t m = min((uint32_t)kWinB, count - w0);
+        if (A.debug != 2) {
+            const uint64_t s0 = slot + w0;
+            for (uint32_t j = lane; j < m; j += 32) {
+                const uint2 kp = __ldg(idx + W->rec[j]);
+                const uint32_t k = kp.x, px = kp.y, py = map[k];
+                uint32_t a0 = y, a1 = x, a2 = k;
+                sort3(a0, a1, a2);
+                uint32_t* tv = A.tv + 3 * (s0 + j);
+                __stcs(tv, a0);
+                __stcs(tv + 1, a1);
+                __stcs(tv + 2, a2);
+                if (A.rows) {
+                    uint32_t* rw = A.rows + 3 * (s0 + j);
+                    __stcs(rw, min(px, py));
+                    __stcs(rw + 1, max(px, py));
+                    __stcs(rw + 2, p);
+                }
+                __stcs(A.tf + s0 + j, filt);
+                if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <bool kFill, bool kPacked, bool kBm>
 __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
-    using WS = typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type;
+    using WS = typename std::conditional<
+        kBm,
+        typename std::conditional<kFill, typename std::conditional<VRB_TRI_BMFILL == 2, WarpScratch3, WarpScratchB>::type,
+                                  WarpScratchC>::type,
+        typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type;
     WS* scratch = reinterpret_cast<WS*>(smem + ((A.n * 4 + 15) / 16) * 16);
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
@@ -649,7 +790,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nthreads = blockDim.x;
     for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
-    if (kFill)   // the flags are cleared after every use, so they must start at 0
+    if (kFill && !kBm)   // the flags are cleared after every use, so they must start at 0
         for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WS) / 4); q += nthreads)
             reinterpret_cast<uint32_t*>(scratch)[q] = 0u;
     __syncthreads();
@@ -713,7 +854,18 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
                 const uint4 pl2 = plan_of(e2);
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kFill && kPacked && VRB_TRI_MODE == 3) {
+                    if constexpr (kBm && kFill && VRB_TRI_BMFILL == 2) {
+                        const uint32_t* bmw = A.bm + A.bmoff[e0];
+                        if (pl0.w <= (uint32_t)kBits)
+                            warp_fill_kp<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0, bmw);
+                        else
+                            warp_fill_kp<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0, bmw);
+                    } else if constexpr (kBm && kFill) {
+                        warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, e0, slot0, filt0);
+                    } else if constexpr (kBm) {
+                        const uint32_t c = warp_count_bm(A, map, scratch + wid, p, off0, len, pl0.w, e0);
+                        if (lane == 0) A.cnt[p] = c;
+                    } else if constexpr (kFill && kPacked && VRB_TRI_MODE == 3) {
                         if (pl0.w <= (uint32_t)kBits)
                             warp_fill_kp<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0);
                         else
@@ -755,29 +907,34 @@ int fill_warps(int64_t n, bool packed) {
     return (int)std::max<int64_t>(0, std::min<int64_t>(kWarps, w));
 }
 
-template <bool kFill, bool kPacked>
+template <bool kFill, bool kPacked, bool kBm>
 void launch_k(const TriArgs& A, int threads, size_t smem, int64_t nctas_cap, cudaStream_t s) {
-    VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked, kBm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     int per_sm = 0;
-    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked>, threads, smem));
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked, kBm>, threads, smem));
     if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count() * per_sm, nctas_cap);
-    k_triangles<kFill, kPacked><<<grid, threads, smem, s>>>(A);
+    k_triangles<kFill, kPacked, kBm><<<grid, threads, smem, s>>>(A);
     VRB_LAUNCH_CHECK();
 }
 
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
     const bool packed = A.packed != 0;
+    const bool bm = A.bm != nullptr;
     // fill: one CTA per SM (the vertex map + per-warp scratch); count:
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
-    const int warps = fill ? fill_warps(A.n, packed) : kWarps / 2;
+    int warps = fill ? fill_warps(A.n, packed) : kWarps / 2;
+    size_t per_warp = fill ? scratch_bytes(packed) : 0;
+    if (bm) {
+        per_warp = fill ? (VRB_TRI_BMFILL == 2 ? sizeof(WarpScratch3) : sizeof(WarpScratchB)) : sizeof(WarpScratchC);
+        const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(A.n) - 1024;
+        warps = (int)std::min<int64_t>(fill ? kWarps : kWarps / 2, avail / (int64_t)per_warp);
+    }
     if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
-    const size_t smem =
-        map_bytes(A.n) +
-        (fill ? (size_t)warps * scratch_bytes(packed) : 0);
+    const size_t smem = map_bytes(A.n) + (size_t)warps * per_warp;
     // Task size depends on the work only (identical on every rank, so a
     // partition of the task range is a partition of the owner edges):
     // ~8k tasks, but not below ~64k candidate tests each.
@@ -793,13 +950,21 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     A.task_counter = counter.get();
     const int64_t cap = A.task_hi - A.task_lo;
-    if (fill) {
-        if (packed) launch_k<true, true>(A, threads, smem, cap, s);
-        else launch_k<true, false>(A, threads, smem, cap, s);
+    if (bm) {
+        if (fill) launch_k<true, true, true>(A, threads, smem, cap, s);
+        else launch_k<false, true, true>(A, threads, smem, cap, s);
+    } else if (fill) {
+        if (packed) launch_k<true, true, false>(A, threads, smem, cap, s);
+        else launch_k<true, false, false>(A, threads, smem, cap, s);
     } else {
-        if (packed) launch_k<false, true>(A, threads, smem, cap, s);
-        else launch_k<false, false>(A, threads, smem, cap, s);
+        if (packed) launch_k<false, true, false>(A, threads, smem, cap, s);
+        else launch_k<false, false, false>(A, threads, smem, cap, s);
     }
+}
+
+__global__ void k_bm_words(const uint4* __restrict__ plan, int64_t E, uint32_t* __restrict__ words) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        words[e] = (plan[e].w + 31u) >> 5;
 }
 
 TriArgs graph_args(const Graph& g) {
@@ -814,6 +979,7 @@ TriArgs graph_args(const Graph& g) {
     A.plan = g.plan.get();
     A.hosted_v = g.hosted_v.get();
     A.work_pre = g.work_pre.get();
+    A.idl = g.idl.get();
     return A;
 }
 
@@ -833,8 +999,41 @@ void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaSt
     launch(A, false, g.work, part, nparts, s);
 }
 
+bool apex_bitmaps_apply(const Graph& g) {
+    const char* off = std::getenv("VRB_NO_APEX_BITMAPS");   // testing knob: force the re-enumerating fill
+    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && !(off && off[0] == '1');
+}
+
+void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words, cudaStream_t s) {
+    bmoff.alloc(g.E + 1, s);
+    words = 0;
+    if (g.E == 0) {
+        VRB_CUDA(cudaMemsetAsync(bmoff.get(), 0, sizeof(uint64_t), s));
+        return;
+    }
+    DBuf<uint32_t> w(g.E, s);
+    k_bm_words<<<(unsigned)std::min<int64_t>(ceil_div(g.E, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
+        g.plan.get(), g.E, w.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(w.get(), bmoff.get(), g.E, s);
+    VRB_CUDA(cudaMemcpyAsync(&words, bmoff.get() + g.E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+}
+
+void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint64_t* bmoff, cudaStream_t s) {
+    if (g.E == 0) return;
+    VRB_CUDA(cudaMemsetAsync(cnt, 0, g.E * sizeof(uint32_t), s));
+    if (g.work == 0) return;
+    TriArgs A = graph_args(g);
+    A.cnt = cnt;
+    A.bm = bm;
+    A.bmoff = bmoff;
+    launch(A, false, g.work, 0, 1, s);
+}
+
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
-                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s) {
+                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s,
+                    const uint32_t* bm, const uint64_t* bmoff) {
     if (g.E == 0 || g.work == 0 || p_lo >= p_hi) return;
     TriArgs A = graph_args(g);
     A.efilt = efilt;
@@ -846,6 +1045,8 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.tf = tf;
     A.rows = rows;
     A.apex = g.n <= 65536 ? apex : nullptr;
+    A.bm = const_cast<uint32_t*>(bm);
+    A.bmoff = bmoff;
     const char* dbg = std::getenv("VRB_DEBUG_FILL");   // ablation timing only; breaks outputs
     A.debug = dbg ? std::atoi(dbg) : 0;
     launch(A, true, g.work, 0, 1, s);

@@ -354,7 +354,17 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             timer.mark(2);
             // ---- triangles: count per owner edge (work split over the ranks), offsets
             DBuf<uint32_t> cnt(E, s);
-            count_triangles(g, cnt.get(), rank, world, s);
+            // single rank: the count pass keeps the apex bitmaps the fill emits from
+            DBuf<uint64_t> bmoff;
+            DBuf<uint32_t> bm;
+            if (world == 1 && apex_bitmaps_apply(g)) {
+                uint64_t words = 0;
+                apex_bitmap_offsets(g, bmoff, words, s);
+                bm.alloc(words ? words : 1, s);
+                count_triangles_bm(g, cnt.get(), bm.get(), bmoff.get(), s);
+            } else {
+                count_triangles(g, cnt.get(), rank, world, s);
+            }
             if (world > 1) {
                 // the exchange: every rank counted a disjoint, work-balanced part
                 // of the owner edges; gather and add the parts
@@ -386,7 +396,9 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             DBuf<uint16_t> tapex;
             if (h->K >= 3 && n <= 65536) tapex.alloc((size_t)Tl, s);
             timer.mark(3);
-            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s);
+            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s, bm.get(),
+                           bmoff.get());
+            bm.reset();
             timer.mark(4);
             sort_tie_groups(2, efilt, toff.get(), E, tb_[0], tb_[1], n, tv, trows, s);
             timer.mark(5);

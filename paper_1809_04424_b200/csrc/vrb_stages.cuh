@@ -48,6 +48,7 @@ struct Graph {
     bool packed = false;       // n <= 65536 and every degree <= 65536
     //   krank = index of k in the vertex's neighbour-ID-ordered list
     DBuf<uint32_t> listidx;    // 2E: entry q = 2p + side -> index in the vertex's position list
+    DBuf<uint2> idl;           // 2E (packed only): (k, pos of edge (v, k)) in neighbour-ID order
     // owner-edge enumeration plan (triangles and tetrahedra)
     DBuf<uint32_t> scan_v;     // E: endpoint whose older-neighbour prefix is scanned
     DBuf<uint32_t> scan_len;   // E: length of that prefix (older neighbours)
@@ -65,11 +66,20 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
 // owner edges are split into work-balanced tasks; this call counts the tasks
 // of part `part` of `nparts` (0 of 1 = all) and leaves the others at 0.
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s);
+// Apex bitmaps (single rank, packed lists, max degree <= kApexBitmapMaxDeg):
+// the count pass also stores, per hosted slot e, the bitmap of the valid apexes
+// by rank in the scanned endpoint's id-ordered list at bm + bmoff[e]
+// (ceil(deg x / 32) words); the fill then emits from the bitmaps.
+constexpr uint32_t kApexBitmapMaxDeg = 8192;
+bool apex_bitmaps_apply(const Graph& g);
+void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words, cudaStream_t s);
+void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint64_t* bmoff, cudaStream_t s);
 // Emit triangles of owner edges in [p_lo, p_hi) at slots toff[p] - slot0
 // (slot0 = toff[p_lo]).  apex (nullable; n <= 65536): each triangle's vertex
 // off its owner edge, for the face-position search of tetrahedra.
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
-                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s);
+                    uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s,
+                    const uint32_t* bm = nullptr, const uint64_t* bmoff = nullptr);
 // Reorder the k-simplices (k = 2, 3) of every tie group (>= 2 edges sharing a
 // level) into lex order (readings A3, A4); only owner edges in [p_lo, p_hi).
 // off = per-owner-edge simplex offsets (E + 1); verts/rows: (k+1) u32 each.

@@ -173,13 +173,18 @@ def test_dim_major_and_device_points(vrb):
     np.testing.assert_array_equal(_np(r2.simplices(2)[0]), _np(res.simplices(2)[0]))
 
 
-def test_high_degree_byte_map_rounds(vrb):
-    # two hubs adjacent to 4500 jittered points of a high-dimensional sphere
+def test_high_degree_over_apex_bitmap_limit(vrb):
+    # hub degree 9000 > 8192: the build falls back to the re-enumerating fill
+    test_high_degree_byte_map_rounds(vrb, m=9000)
+
+
+def test_high_degree_byte_map_rounds(vrb, m=4500):
+    # two hubs adjacent to m jittered points of a high-dimensional sphere
     # (mutually almost never adjacent); the hub-hub edge is the longest, so its
-    # older-neighbour prefixes hold 4500 entries (> 4096 ranks per round: the
+    # older-neighbour prefixes hold m entries (> 4096 ranks per round: the
     # fill runs several rounds, and a long prefix is streamed in chunks)
     rng = np.random.default_rng(3)
-    m, dim = 4500, 200
+    dim = 200
     S = rng.standard_normal((m, dim))
     S /= np.linalg.norm(S, axis=1, keepdims=True)
     S *= (1.0 + 0.01 * rng.uniform(size=(m, 1)))
@@ -214,6 +219,24 @@ def test_sorted_rank_path(vrb, monkeypatch, wide):
 def test_wide_list_layout_multi_round(vrb, monkeypatch):
     monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
     test_high_degree_byte_map_rounds(vrb)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fill_without_apex_bitmaps(vrb, monkeypatch, seed):
+    # the re-enumerating fill (multi-rank builds, degrees > 8192) on the
+    # single-rank configs: same bytes as with the count pass's apex bitmaps
+    monkeypatch.setenv("VRB_NO_APEX_BITMAPS", "1")
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(50, 700))
+    X = workloads.random_cloud(seed, n, 3, ["uniform", "lattice", "gauss"][seed % 3])
+    compare(vrb, X, 2 if seed % 2 else 1, [0.35, 1.5, 1.2][seed % 3])
+
+
+def test_fill_without_apex_bitmaps_high_degree(vrb, monkeypatch):
+    monkeypatch.setenv("VRB_NO_APEX_BITMAPS", "1")
+    test_high_degree_byte_map_rounds(vrb)
+    w = workloads.WORKLOADS["C2"]
+    compare(vrb, w.points(), w.maxdim, w.radius)
 
 
 def test_sortperm_literal_and_random(vrb):
