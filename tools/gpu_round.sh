@@ -19,3 +19,8 @@ done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_reference.json 2>&1; tail -1 gpurun_out/${TAG}_bench_reference.json
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_c5b.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python tools/launches.py gpurun_out/${TAG}_launches_c5b.csv 4 2>/dev/null | head -14
+# ncu --set full of the dominant kernel (the triangle fill) in the bench's launch configuration
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_triangles -s 2 -c 2 -o gpurun_out/${TAG}_fill python tools/one_build.py C5B 2 > gpurun_out/${TAG}_fill_ncu.log 2>&1
+echo "ncu full rc=$?"
+{ python tools/ncu_summary.py gpurun_out/${TAG}_fill.ncu-rep "" 8; python tools/ncu_lines.py gpurun_out/${TAG}_fill.ncu-rep "k_triangles<(bool)1" 40; } > gpurun_out/${TAG}_ncu_fill_c5b.txt 2>&1
+head -5 gpurun_out/${TAG}_ncu_fill_c5b.txt
