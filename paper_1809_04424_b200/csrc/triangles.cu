@@ -162,6 +162,23 @@ __device__ __forceinline__ uint32_t ld_list(const uint32_t* a) {
 #endif
 }
 
+#ifndef VRB_TRI_IDL_HINT
+#define VRB_TRI_IDL_HINT 0
+#endif
+// id-ordered list gathers of the bitmap fill: VRB_TRI_IDL_HINT keeps their
+// lines in L2 with the evict_last policy (the output stream is evict-first)
+__device__ __forceinline__ uint2 ld_idl(const uint2* a) {
+#if VRB_TRI_IDL_HINT
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(pol));
+    return v;
+#else
+    return __ldg(a);
+#endif
+}
+
 __device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
 
 // Stream the groups of a list prefix: G uint4 groups per lane in flight;
@@ -751,8 +768,23 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         const uint32_t m = min((uint32_t)kWinB, count - w0);
         if (A.debug != 2) {
             const uint64_t s0 = slot + w0;
-            for (uint32_t j = lane; j < m; j += 32) {
-                const uint2 kp = __ldg(idx + W->rec[j]);
+#ifndef VRB_TRI_BM_UNROLL
+#define VRB_TRI_BM_UNROLL 8
+#endif
+            // kU gathers in flight per lane before the first is used
+            constexpr int kU = VRB_TRI_BM_UNROLL;
+            for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
+                uint2 kq[kU];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const uint32_t j = j0 + 32 * q + lane;
+                    kq[q] = j < m ? ld_idl(idx + W->rec[j]) : make_uint2(0u, 0u);
+                }
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                const uint32_t j = j0 + 32 * q + lane;
+                if (j >= m) break;
+                const uint2 kp = kq[q];
                 const uint32_t k = kp.x, px = kp.y, py = map[k];
                 uint32_t a0 = y, a1 = x, a2 = k;
                 sort3(a0, a1, a2);
@@ -768,6 +800,7 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
                 }
                 __stcs(A.tf + s0 + j, filt);
                 if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+                }
             }
         }
         __syncwarp();
