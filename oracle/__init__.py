@@ -74,6 +74,8 @@ def _L():
         lib.or_simplices_at_filt.argtypes = [c_p, c_i32, ctypes.c_uint32, c_p, c_p, c_i64]
         lib.or_barcodes.restype = c_i64
         lib.or_barcodes.argtypes = [c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_i64]
+        lib.or_blockprodsum.restype = c_i64
+        lib.or_blockprodsum.argtypes = [c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]
         lib.or_reduce.restype = None
         lib.or_reduce.argtypes = [c_i64, c_i64, c_p, c_p, c_i32, c_p, c_p]
         _lib = lib
@@ -123,6 +125,25 @@ def reduce(nrows: int, columns, method: str = "col"):
     _L().or_reduce(nrows, len(columns), _ptr(colptr), _ptr(rowval), METHOD[method] & 1,
                    _ptr(piv), _ptr(zero))
     return piv[:nrows], zero[:len(columns)].astype(bool)
+
+
+def blockprodsum(nrows: int, D, C, E):
+    """S = D + C E over GF(2).  D (nrows x ncols), C (nrows x k),
+    E (k x ncols) given as (colptr int64, rowval uint32) CSC pairs with rows
+    ascending; returns S as (colptr int64 (ncols+1,), rowval uint32)."""
+    def arr(m):
+        cp = np.ascontiguousarray(m[0], dtype=np.int64)
+        rv = np.ascontiguousarray(m[1], dtype=np.uint32)
+        return cp, (rv if rv.size else np.zeros(1, dtype=np.uint32))
+    (dc, dr), (cc, cr), (ec, er) = arr(D), arr(C), arr(E)
+    nc = dc.shape[0] - 1
+    scp = np.empty(nc + 1, dtype=np.int64)
+    nnz = _L().or_blockprodsum(nrows, nc, _ptr(dc), _ptr(dr), _ptr(cc), _ptr(cr), _ptr(ec), _ptr(er),
+                               _ptr(scp), None)
+    srv = np.empty(max(nnz, 1), dtype=np.uint32)
+    _L().or_blockprodsum(nrows, nc, _ptr(dc), _ptr(dr), _ptr(cc), _ptr(cr), _ptr(ec), _ptr(er),
+                         _ptr(scp), _ptr(srv))
+    return scp, srv[:nnz]
 
 
 class Oracle:

@@ -570,6 +570,40 @@ void or_reduce(int64_t nr, int64_t nc, const int64_t* colptr, const uint32_t* ro
     free(R);
 }
 
+/* F4: blockprodsum (sec. 4.6, Fig. BlkProdSum): S = D + C E    */
+/* over GF(2) ("using the modulo-2 operation"), all CSC.   */
+/* Column j of S is the mod-2 sum of column j of D and the columns C[:, i]  */
+/* for every i in column j of E, written out as a dense 0/1 accumulator of  */
+/* nr entries per column (textbook, no blocking).  Returns nnz(S); the      */
+/* caller sizes s_rowval with an upper bound or calls twice (s_rowval NULL  */
+/* counts only).  s_colptr has nc + 1 entries; rows ascending.              */
+int64_t or_blockprodsum(int64_t nr, int64_t nc,
+                        const int64_t* d_colptr, const uint32_t* d_rowval,
+                        const int64_t* c_colptr, const uint32_t* c_rowval,
+                        const int64_t* e_colptr, const uint32_t* e_rowval,
+                        int64_t* s_colptr, uint32_t* s_rowval) {
+    uint8_t* acc = (uint8_t*)calloc((size_t)(nr ? nr : 1), 1);
+    int64_t nnz = 0;
+    if (s_colptr) s_colptr[0] = 0;
+    for (int64_t j = 0; j < nc; ++j) {
+        for (int64_t q = d_colptr[j]; q < d_colptr[j + 1]; ++q) acc[d_rowval[q]] ^= 1;
+        for (int64_t q = e_colptr[j]; q < e_colptr[j + 1]; ++q) {
+            uint32_t i = e_rowval[q];
+            for (int64_t t = c_colptr[i]; t < c_colptr[i + 1]; ++t) acc[c_rowval[t]] ^= 1;
+        }
+        for (int64_t r = 0; r < nr; ++r) {
+            if (acc[r]) {
+                if (s_rowval) s_rowval[nnz] = (uint32_t)r;
+                nnz++;
+                acc[r] = 0;
+            }
+        }
+        if (s_colptr) s_colptr[j + 1] = nnz;
+    }
+    free(acc);
+    return nnz;
+}
+
 /* Reduce D_k of the context; cleared[j] != 0 marks columns zeroed          */
 /* beforehand (clearing).                                            */
 static void reduce_dim(const or_ctx* c, int32_t k, int method, const uint8_t* cleared,

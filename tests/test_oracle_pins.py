@@ -535,3 +535,65 @@ def test_dm_negative_zero_is_length_zero():
     o = oracle.Oracle(None, 0.0, D=D)
     ev, ef, el, vor = o.edges()
     assert o.E == 1 and np.signbit(el[0]) == 0 and el[0] == 0.0
+
+
+# --------------------------------------------------------------------------
+# blockprodsum S = D + C E over GF(2) (sec. 4.6).
+# --------------------------------------------------------------------------
+
+def _rand_csc(rng, nr, nc, density):
+    cols = [np.flatnonzero(rng.random(nr) < density).astype(np.uint32) for _ in range(nc)]
+    cp = np.zeros(nc + 1, dtype=np.int64)
+    for j, c in enumerate(cols):
+        cp[j + 1] = cp[j] + len(c)
+    rv = np.concatenate(cols) if cols and cp[-1] else np.zeros(0, dtype=np.uint32)
+    return cp, rv
+
+
+def _dense(m, nr):
+    cp, rv = m
+    M = np.zeros((nr, len(cp) - 1), dtype=np.int64)
+    for j in range(len(cp) - 1):
+        M[rv[cp[j]:cp[j + 1]], j] = 1
+    return M
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_blockprodsum_matches_dense_mod2_algebra(seed):
+    rng = np.random.default_rng(8000 + seed)
+    nr, k, nc = (int(x) for x in rng.integers(1, 40, 3))
+    D, C, E = _rand_csc(rng, nr, nc, 0.2), _rand_csc(rng, nr, k, 0.15), _rand_csc(rng, k, nc, 0.2)
+    S = oracle.blockprodsum(nr, D, C, E)
+    ref = (_dense(D, nr) + _dense(C, nr) @ _dense(E, k)) % 2      # numpy integer algebra, then mod 2
+    np.testing.assert_array_equal(_dense(S, nr), ref)
+    for j in range(nc):                                            # rows strictly ascending
+        assert np.all(np.diff(S[1][S[0][j]:S[0][j + 1]].astype(np.int64)) > 0)
+
+
+def test_blockprodsum_identities_and_worker_partition():
+    rng = np.random.default_rng(8100)
+    nr, k, nc = 30, 20, 25
+    D, C, E = _rand_csc(rng, nr, nc, 0.3), _rand_csc(rng, nr, k, 0.3), _rand_csc(rng, k, nc, 0.3)
+    zeroE = (np.zeros(nc + 1, dtype=np.int64), np.zeros(0, dtype=np.uint32))
+    S = oracle.blockprodsum(nr, D, C, zeroE)                       # E = 0: S = D
+    np.testing.assert_array_equal(S[0], D[0]); np.testing.assert_array_equal(S[1], D[1])
+    I = (np.arange(k + 1, dtype=np.int64), np.arange(k, dtype=np.uint32))
+    zeroD = (np.zeros(nc + 1, dtype=np.int64), np.zeros(0, dtype=np.uint32))
+    S = oracle.blockprodsum(k, zeroD, I, E)                         # D = 0, C = I: S = E
+    np.testing.assert_array_equal(S[0], E[0]); np.testing.assert_array_equal(S[1], E[1])
+    S = oracle.blockprodsum(nr, D, C, E)
+    S2 = oracle.blockprodsum(nr, S, C, E)                           # (D + CE) + CE = D
+    np.testing.assert_array_equal(S2[0], D[0]); np.testing.assert_array_equal(S2[1], D[1])
+    # master/workers (Fig. BlkProdSum): column blocks computed
+    # separately, colptr "adjusted one after the other" on concatenation
+    cuts = [0, 7, 8, 19, nc]
+    parts_cp, parts_rv, base = [np.zeros(1, dtype=np.int64)], [], 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        Db = (D[0][a:b + 1] - D[0][a], D[1][D[0][a]:D[0][b]])
+        Eb = (E[0][a:b + 1] - E[0][a], E[1][E[0][a]:E[0][b]])
+        cp, rv = oracle.blockprodsum(nr, Db, C, Eb)
+        parts_cp.append(cp[1:] + base)
+        parts_rv.append(rv)
+        base += cp[-1]
+    np.testing.assert_array_equal(np.concatenate(parts_cp), S[0])
+    np.testing.assert_array_equal(np.concatenate(parts_rv), S[1])
