@@ -196,6 +196,26 @@ vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const
 vrb_status vrb_sortperm_f64(const double* keys_dev, int64_t n, int64_t* perm_dev,
                             uint32_t* dense_rank_dev, void* stream);
 
+/* blockprodsum (sec. 4.6, Fig. BlkProdSum): the
+ * Schur-complement product-sum of Eirene's reduction, S = D + C E over GF(2)
+ * ("using the modulo-2 operation"), all CSC with 0-based rows.
+ *   D : nrows x ncols   (d_colptr: ncols+1 u64, d_rowval: u32 < nrows)
+ *   C : nrows x k       (c_colptr: k+1 u64,     c_rowval: u32 < nrows)
+ *   E : k x ncols       (e_colptr: ncols+1 u64, e_rowval: u32 < k)
+ * Rows within an input column need not be sorted; duplicates cancel in
+ * pairs.  All pointers device, caller-owned, read-only.  The result is
+ * handle-owned: S's rows are ascending within each column; vrb_gf2_csc gives
+ * nnz, colptr (ncols+1 u64) and rowval (nnz u32).  VRB_EINVAL if an index is
+ * out of range; VRB_EOVERFLOW if the candidate count (nnz(D) + sum over E of
+ * the C columns it selects) reaches 2^32. */
+typedef struct vrb_gf2* vrb_gf2_handle;
+vrb_status vrb_gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t k, const uint64_t* d_colptr,
+                                const uint32_t* d_rowval, const uint64_t* c_colptr, const uint32_t* c_rowval,
+                                const uint64_t* e_colptr, const uint32_t* e_rowval, void* stream,
+                                vrb_gf2_handle* out);
+vrb_status vrb_gf2_csc(vrb_gf2_handle h, int64_t* nnz, const uint64_t** colptr_dev, const uint32_t** rowval_dev);
+vrb_status vrb_gf2_free(vrb_gf2_handle h);
+
 /* Stage timings of the last build on this thread (milliseconds, CUDA events
  * on the build stream): [0] points + distances S1-S2, [1] edge sort + ranks
  * S3, [2] neighbourhood lists S4, [3] simplex count + offsets + output

@@ -35,7 +35,7 @@ VRB_SKIP_BOUNDARY = 0x8
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
            "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count", "vrb_h0", "vrb_build_dm",
-           "vrb_latlon2euc")
+           "vrb_latlon2euc", "vrb_gf2_blockprodsum", "vrb_gf2_csc", "vrb_gf2_free")
 
 STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total")
 
@@ -109,6 +109,12 @@ def lib() -> ctypes.CDLL:
     L.vrb_build_dm.argtypes = [p, i64, P(vrb_opts), p, P(p)]
     L.vrb_latlon2euc.restype = ctypes.c_int
     L.vrb_latlon2euc.argtypes = [p, i64, p, p]
+    L.vrb_gf2_blockprodsum.restype = ctypes.c_int
+    L.vrb_gf2_blockprodsum.argtypes = [i64, i64, i64, p, p, p, p, p, p, p, P(p)]
+    L.vrb_gf2_csc.restype = ctypes.c_int
+    L.vrb_gf2_csc.argtypes = [p, P(i64), P(p), P(p)]
+    L.vrb_gf2_free.restype = ctypes.c_int
+    L.vrb_gf2_free.argtypes = [p]
     L.vrb_h0.restype = ctypes.c_int
     L.vrb_h0.argtypes = [p, p, P(p), P(p), P(i64), P(i64)]
     _lib = L
@@ -356,6 +362,52 @@ def latlon2euc(latlon, stream=None):
         _check(lib().vrb_latlon2euc(ctypes.c_void_p(a.data_ptr()), a.shape[0], ctypes.c_void_p(out.data_ptr()),
                                     _stream_ptr(stream)))
     return out
+
+
+class Gf2Matrix:
+    """A GF(2) CSC matrix owned by the library (vrb_gf2_blockprodsum result):
+    ``colptr`` (ncols+1,) int64 and ``rowval`` (nnz,) int32[u32] CUDA tensors."""
+
+    def __init__(self, handle: int, ncols: int, device):
+        self._h = ctypes.c_void_p(handle)
+        nnz, cp, rv = ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().vrb_gf2_csc(self._h, ctypes.byref(nnz), ctypes.byref(cp), ctypes.byref(rv)))
+        self.nnz = nnz.value
+        self.colptr = _view(cp.value, (ncols + 1,), "<i8", self, device)
+        self.rowval = _view(rv.value, (nnz.value,), "<i4", self, device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().vrb_gf2_free(h)
+            finally:
+                self._h = None
+
+
+def gf2_blockprodsum(nrows: int, D, C, E, stream=None) -> Gf2Matrix:
+    """vrb_gf2_blockprodsum: S = D + C E over GF(2).  D, C, E are
+    (colptr, rowval) pairs of CUDA tensors (int64 colptr, int32/uint32 rows)."""
+    import torch
+
+    def prep(m):
+        cp, rv = m
+        if not (cp.is_cuda and rv.is_cuda):
+            raise TypeError("CSC arrays must be CUDA tensors")
+        cp = cp.to(torch.int64).contiguous()
+        rv = rv.contiguous()
+        if rv.dtype not in (torch.int32, torch.uint32):
+            raise TypeError("row indices must be 32-bit")
+        return cp, rv
+
+    (dc, dr), (cc, cr), (ec, er) = prep(D), prep(C), prep(E)
+    ncols, k = dc.numel() - 1, cc.numel() - 1
+    h = ctypes.c_void_p()
+    with torch.cuda.device(dc.device):
+        _check(lib().vrb_gf2_blockprodsum(int(nrows), ncols, k, *(ctypes.c_void_p(t.data_ptr()) for t in
+                                                                  (dc, dr, cc, cr, ec, er)),
+                                          _stream_ptr(stream), ctypes.byref(h)))
+    return Gf2Matrix(h.value, ncols, dc.device)
 
 
 def allgather_bytes(src, dst, group=None):

@@ -598,6 +598,78 @@ vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const
     });
 }
 
+struct vrb_gf2 {
+    int64_t ncols = 0, nnz = 0;
+    uint64_t* colptr = nullptr;
+    uint32_t* rowval = nullptr;
+    std::vector<vrb::Alloc> owned;
+    void release_all() {
+        for (auto& a : owned) vrb::dfree(a.p, a.bytes, 0);
+        owned.clear();
+    }
+};
+
+namespace {
+struct Gf2Alloc {
+    vrb_gf2* g;
+    cudaStream_t s;
+};
+uint32_t* gf2_alloc_rows(int64_t n, void* ctx) {
+    auto* a = static_cast<Gf2Alloc*>(ctx);
+    auto* p = static_cast<uint32_t*>(vrb::dalloc((size_t)n * sizeof(uint32_t), a->s));
+    a->g->owned.push_back({p, (size_t)n * sizeof(uint32_t)});
+    return p;
+}
+}  // namespace
+
+vrb_status vrb_gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t k, const uint64_t* d_colptr,
+                                const uint32_t* d_rowval, const uint64_t* c_colptr, const uint32_t* c_rowval,
+                                const uint64_t* e_colptr, const uint32_t* e_rowval, void* stream,
+                                vrb_gf2_handle* out) {
+    return guarded([&] {
+        if (!out) fail(VRB_EINVAL, "out is NULL");
+        *out = nullptr;
+        if (nrows < 0 || ncols < 0 || k < 0) fail(VRB_EINVAL, "negative dimension");
+        if (nrows > 0xFFFFFFFFll || k > 0xFFFFFFFFll) fail(VRB_EOVERFLOW, "row indices must fit u32");
+        if (!d_colptr || !c_colptr || !e_colptr) fail(VRB_EINVAL, "NULL colptr");
+        const cudaStream_t s = (cudaStream_t)stream;
+        vrb_gf2* g = new vrb_gf2();
+        try {
+            g->ncols = ncols;
+            g->colptr = static_cast<uint64_t*>(vrb::dalloc((size_t)(ncols + 1) * sizeof(uint64_t), s));
+            g->owned.push_back({g->colptr, (size_t)(ncols + 1) * sizeof(uint64_t)});
+            VRB_CUDA(cudaMemsetAsync(g->colptr, 0, (size_t)(ncols + 1) * sizeof(uint64_t), s));
+            Gf2Alloc ctx{g, s};
+            g->nnz = vrb::gf2_blockprodsum(nrows, ncols, k, d_colptr, d_rowval, c_colptr, c_rowval, e_colptr,
+                                           e_rowval, s, g->colptr, gf2_alloc_rows, &ctx, &g->rowval);
+            VRB_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            g->release_all();
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+vrb_status vrb_gf2_csc(vrb_gf2_handle h, int64_t* nnz, const uint64_t** colptr_dev, const uint32_t** rowval_dev) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (nnz) *nnz = h->nnz;
+        if (colptr_dev) *colptr_dev = h->colptr;
+        if (rowval_dev) *rowval_dev = h->rowval;
+    });
+}
+
+vrb_status vrb_gf2_free(vrb_gf2_handle h) {
+    return guarded([&] {
+        if (!h) return;
+        h->release_all();
+        delete h;
+    });
+}
+
 vrb_status vrb_sortperm_f64(const double* keys_dev, int64_t n, int64_t* perm_dev, uint32_t* dense_rank_dev,
                             void* stream) {
     return guarded([&] {

@@ -107,6 +107,13 @@ void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const 
 
 int64_t dense_map_limit();   // largest n the shared-memory vertex map supports
 
+// F4 (gf2.cu): S = D + C E over GF(2); writes colptr_out (ncols + 1) and
+// returns nnz(S) with its rows allocated through alloc_rows.
+int64_t gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t kdim, const uint64_t* dcp, const uint32_t* drv,
+                         const uint64_t* ccp, const uint32_t* crv, const uint64_t* ecp, const uint32_t* erv,
+                         cudaStream_t s, uint64_t* colptr_out, uint32_t* (*alloc_rows)(int64_t, void*), void* ctx,
+                         uint32_t** rowval_out);
+
 // F1 (h0.cu): minimum spanning forest of the edges under the position order
 // (Boruvka); returns its size and (through alloc_out) its positions ascending
 // and their filt.
