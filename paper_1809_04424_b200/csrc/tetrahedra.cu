@@ -709,9 +709,14 @@ int tet_warps(int64_t n) {
     return 0;
 }
 
+#ifndef VRB_TET_CTA_WARPS
+#define VRB_TET_CTA_WARPS 8
+#endif
+// dense path: CTAs of up to VRB_TET_CTA_WARPS warps; two per SM when the map
+// is small (shorter per-host barrier tails: hosts own ~E/n edges each)
 int tet_dense_warps(int64_t n) {
     const int64_t avail = (int64_t)device_max_smem_optin() - 1024 - (int64_t)((n * 4 + 15) / 16) * 16;
-    return (int)std::min<int64_t>(32, avail / (int64_t)sizeof(TetScratchD));
+    return (int)std::min<int64_t>(VRB_TET_CTA_WARPS, avail / (int64_t)sizeof(TetScratchD));
 }
 
 void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
@@ -736,7 +741,13 @@ void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cuda
         VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
         A.task_counter = counter.get();
         A.overflow = overflow.get();
-        const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count(), A.task_hi - A.task_lo);
+        int per_sm = 1;
+        if (fill)
+            VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tets_dense<true>, warps * 32, smem));
+        else
+            VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tets_dense<false>, warps * 32, smem));
+        const unsigned grid =
+            (unsigned)std::min<int64_t>((int64_t)device_sm_count() * std::max(1, per_sm), A.task_hi - A.task_lo);
         if (fill)
             k_tets_dense<true><<<grid, warps * 32, smem, s>>>(A);
         else
