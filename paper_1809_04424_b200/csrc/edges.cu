@@ -39,24 +39,24 @@ __global__ void k_rank_heads(const uint64_t* __restrict__ key, int64_t E, uint32
 __global__ void k_edge_outputs(const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
                                const uint32_t* __restrict__ ei, const uint32_t* __restrict__ ej,
                                const uint32_t* __restrict__ efilt, int64_t E, uint32_t* __restrict__ ev,
-                               double* __restrict__ vor) {
+                               double* __restrict__ vor, uint64_t bias) {
     GRID_STRIDE(p, E) {
         const uint32_t lex = perm[p];
         ev[2 * p] = ei[lex];
         ev[2 * p + 1] = ej[lex];
-        if (p == 0 || key[p] != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)key[p]);
+        if (p == 0 || key[p] != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)(key[p] + bias));
     }
 }
 
 // packed ids (n <= 65536): the sorted values are (i << 16 | j) themselves
 __global__ void k_edge_outputs_packed(const uint64_t* __restrict__ key, const uint32_t* __restrict__ pij,
                                       const uint32_t* __restrict__ efilt, int64_t E, uint2* __restrict__ ev,
-                                      double* __restrict__ vor) {
+                                      double* __restrict__ vor, uint64_t bias) {
     GRID_STRIDE(p, E) {
         const uint32_t v = pij[p];
         ev[p] = make_uint2(v >> 16, v & 0xFFFFu);
         const uint64_t k = key[p];
-        if (p == 0 || k != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)k);
+        if (p == 0 || k != key[p - 1]) vor[efilt[p] - 1] = __longlong_as_double((long long)(k + bias));
     }
 }
 
@@ -230,8 +230,12 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
         iota_u32(perm.get(), E, s);
         vals = perm.get();
     }
-    const uint64_t vary = varying_bits(ke.key.get(), E, s);
-    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary, s);
+    // sort (len bits - min): only the digits of (max - min) vary
+    uint64_t kmin = 0;
+    const uint64_t vary = key_range(ke.key.get(), E, s, &kmin);
+    bool biased = false;
+    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary, s, kmin, &biased);
+    const uint64_t bias = biased ? kmin : 0ull;
     const uint64_t* skey = alt ? key_alt.get() : ke.key.get();
     const uint32_t* sval = alt ? perm_alt.get() : vals;
     DBuf<uint32_t> head(E, s);
@@ -240,9 +244,10 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
     inclusive_scan_u32(head.get(), efilt, E, s);
     if (ke.packed)
         k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, efilt, E, reinterpret_cast<uint2*>(ev),
-                                                               vor);
+                                                               vor, bias);
     else
-        k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor);
+        k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor,
+                                                        bias);
     VRB_LAUNCH_CHECK();
     uint32_t nvals = 0;
     VRB_CUDA(cudaMemcpyAsync(&nvals, efilt + E - 1, sizeof(nvals), cudaMemcpyDeviceToHost, s));

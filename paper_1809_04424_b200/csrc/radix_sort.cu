@@ -38,12 +38,13 @@ constexpr unsigned long long kFlagPre = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_histograms(const uint64_t* __restrict__ keys, int64_t n,
-                                                         uint32_t digit_mask, unsigned long long* __restrict__ hist) {
+                                                         uint32_t digit_mask, unsigned long long* __restrict__ hist,
+                                                         uint64_t bias) {
     __shared__ uint32_t h[8][kBins];
     for (int q = threadIdx.x; q < 8 * kBins; q += kThreads) (&h[0][0])[q] = 0;
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
+        const uint64_t k = keys[i] - bias;
 #pragma unroll
         for (int d = 0; d < 8; ++d)
             if ((digit_mask >> d) & 1u) atomicAdd(&h[d][(k >> (8 * d)) & 0xFF], 1u);
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
                                                        uint32_t* __restrict__ vals_out, int64_t n, int shift,
                                                        const unsigned long long* __restrict__ pass_base,
                                                        unsigned long long* __restrict__ status,
-                                                       unsigned* __restrict__ tile_counter) {
+                                                       unsigned* __restrict__ tile_counter, uint64_t bias) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SweepSmem& S = *reinterpret_cast<SweepSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t i = base + r * 32 + lane;
-        k[r] = i < n ? keys_in[i] : 0ull;
+        k[r] = i < n ? keys_in[i] - bias : 0ull;
         v[r] = i < n ? vals_in[i] : 0u;
     }
     // ---- stable warp-local ranks (rounds in order, lanes in order)
@@ -189,8 +190,10 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
 }  // namespace
 
 bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
-                      int64_t n, uint64_t varying, cudaStream_t s) {
+                      int64_t n, uint64_t varying, cudaStream_t s, uint64_t bias, bool* biased) {
+    if (biased) *biased = false;
     if (n <= 1 || varying == 0) return false;
+    if (biased) *biased = true;
     uint32_t digit_mask = 0;
     for (int d = 0; d < 8; ++d)
         if ((varying >> (8 * d)) & 0xFFull) digit_mask |= 1u << d;
@@ -198,7 +201,7 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
     DBuf<unsigned long long> hist(8 * kBins, s);
     VRB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.bytes(), s));
     const unsigned hg = (unsigned)std::min<int64_t>(ceil_div(n, kThreads), (int64_t)device_sm_count() * 8);
-    k_histograms<<<hg, kThreads, 0, s>>>(keys, n, digit_mask, hist.get());
+    k_histograms<<<hg, kThreads, 0, s>>>(keys, n, digit_mask, hist.get(), bias);
     VRB_LAUNCH_CHECK();
     k_scan_bins<<<8, 32, 0, s>>>(hist.get());
     VRB_LAUNCH_CHECK();
@@ -219,7 +222,7 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
         uint32_t* vout = alt ? vals : vals_alt;
         k_onesweep<<<(unsigned)ntiles, kThreads, smem, s>>>(kin, vin, kout, vout, n, 8 * d, hist.get() + d * kBins,
                                                             status.get() + (size_t)pass * ntiles * kBins,
-                                                            counters.get() + pass);
+                                                            counters.get() + pass, pass == 0 ? bias : 0ull);
         VRB_LAUNCH_CHECK();
         alt = !alt;
         ++pass;

@@ -115,12 +115,18 @@ void inclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream
 // Bitwise OR over i of (keys[i] ^ keys[0]): the key bits that vary.
 uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s);
 
+// (max - min) of the keys as a bit mask of its length (every key - min fits
+// in it); *kmin = min.  A sort of (key - kmin) needs only those digits.
+uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin);
+
 // Stable ascending LSD radix sort of (keys, vals) on the bit range [0, 64)
 // restricted to the 8-bit digits that contain a bit of `varying`.  Uses
 // (keys_alt, vals_alt) as ping-pong space; returns true if the sorted result
-// ended in the *_alt buffers.
+// ended in the *_alt buffers.  With bias != 0 the sort key is (key - bias):
+// the first pass subtracts it while loading, so the sorted keys are biased
+// (*biased = true) unless no pass ran.
 bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
-                      int64_t n, uint64_t varying, cudaStream_t s);
+                      int64_t n, uint64_t varying, cudaStream_t s, uint64_t bias = 0, bool* biased = nullptr);
 
 // Fill helpers
 void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s);
