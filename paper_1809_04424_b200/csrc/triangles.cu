@@ -684,9 +684,7 @@ constexpr int kWinB = 512;
 struct WarpScratchC {              // count
     uint32_t bits[kBmWords];
 };
-struct WarpScratchB {              // fill
-    uint32_t bits[kBmWords];
-    uint16_t wpre[kBmWords];
+struct WarpScratchB {              // fill: the staged window (apex ranks by slot)
     uint16_t rec[kWinB];
 };
 
@@ -720,51 +718,46 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
 
 __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* __restrict__ map,
                                              WarpScratchB* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
-                                             uint64_t offx, uint32_t degx, int64_t e, uint64_t slot, uint32_t filt) {
+                                             uint64_t offx, uint32_t degx, uint64_t bmo, uint64_t slot,
+                                             uint32_t filt) {
     const int lane = threadIdx.x & 31;
     const uint32_t nw = (degx + 31) >> 5;
-    const uint32_t* in = A.bm + A.bmoff[e];
-    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = __ldcs(in + w);
-    __syncwarp();
-    // exclusive per-word prefix popcounts, lane owns kBmWords / 32 consecutive words
-    constexpr int kWpl = kBmWords / 32;
-    uint32_t c[kWpl], tot = 0;
-#pragma unroll
-    for (int j = 0; j < kWpl; ++j) {
-        const uint32_t wd = kWpl * lane + j;
-        c[j] = wd < nw ? __popc(W->bits[wd]) : 0u;
-        tot += c[j];
-    }
-    uint32_t incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    uint32_t run = incl - tot;
-#pragma unroll
-    for (int j = 0; j < kWpl; ++j) {
-        const uint32_t wd = kWpl * lane + j;
-        if (wd < nw) W->wpre[wd] = (uint16_t)run;
-        run += c[j];
-    }
-    const uint32_t count = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
-    const uint2* __restrict__ idx = A.idl + offx;
-    for (uint32_t w0 = 0; w0 < count; w0 += kWinB) {
+    const uint32_t nchunks = (nw + 31) >> 5;
+    const uint32_t* __restrict__ in = A.bm + bmo;
+    const uint2* __restrict__ idx = A.idl + (A.debug == 3 ? 0 : offx);   // debug 3: ablation, one hot list
+    // Windows of kWinB slots.  Each pass walks the bitmap in chunks of 32
+    // words held in registers (lane = word): a warp scan of the popcounts
+    // gives every word's first slot, and each lane stages the ranks of its
+    // set bits that fall in the window.  The first pass also yields count.
+    uint32_t count = 0;
+    for (uint32_t w0 = 0; w0 == 0 || w0 < count; w0 += kWinB) {
         const uint32_t w1 = w0 + kWinB;
-        for (uint32_t wd = lane; wd < nw; wd += 32) {
-            uint32_t b = W->bits[wd];
-            uint32_t s = W->wpre[wd];
-            if (s >= w1 || s + __popc(b) <= w0) continue;
-            while (b) {
-                const int bit = __ffs(b) - 1;
-                b &= b - 1;
-                if (s >= w0 && s < w1) W->rec[s - w0] = (uint16_t)(32 * wd + bit);
-                ++s;
+        uint32_t carry = 0;
+        for (uint32_t ch = 0; ch < nchunks; ++ch) {
+            if (w0 > 0 && carry >= w1) break;
+            const uint32_t wd = 32 * ch + lane;
+            uint32_t b = wd < nw ? __ldg(in + wd) : 0u;
+            const uint32_t c = __popc(b);
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            uint32_t s = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+            if (s < w1 && s + c > w0) {
+                while (b) {
+                    const int bit = __ffs(b) - 1;
+                    b &= b - 1;
+                    if (s >= w0 && s < w1) W->rec[s - w0] = (uint16_t)(32 * wd + bit);
+                    ++s;
+                }
             }
         }
+        if (w0 == 0) count = carry;
         __syncwarp();
+        if (count == 0) break;
         const uint32_t m = min((uint32_t)kWinB, count - w0);
         if (A.debug != 2) {
             const uint64_t s0 = slot + w0;
@@ -878,13 +871,25 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
             uint64_t off0 = pl0.z ? A.off[pl0.y] : 0, off1 = pl1.z ? A.off[pl1.y] : 0;
             uint64_t slot0 = 0, slot1 = 0;
             uint32_t filt0 = 0, filt1 = 0;
+            uint64_t bmo0 = 0, bmo1 = 0;   // bitmap fill: word offsets of the pipelined edges' bitmaps
             if (kFill) {
                 if (pl0.z) { slot0 = A.toff[pl0.x] - A.slot0; filt0 = A.efilt[pl0.x]; }
                 if (pl1.z) { slot1 = A.toff[pl1.x] - A.slot0; filt1 = A.efilt[pl1.x]; }
+                if (kBm) {
+                    if (pl0.z) bmo0 = A.bmoff[e0];
+                    if (pl1.z) bmo1 = A.bmoff[e1];
+                }
             }
             while (e0 < end) {
                 const int64_t e2 = grab();
                 const uint4 pl2 = plan_of(e2);
+                if (kBm && kFill && pl1.z) {
+                    // pull the next edge's bitmap into L2 while this edge runs
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.bm + bmo1) & ~(uintptr_t)127;
+                    const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.bm + bmo1 + ((pl1.w + 31) >> 5));
+                    for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a < a1; a += 128 * 32)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                }
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
                     if constexpr (kBm && kFill && VRB_TRI_BMFILL == 2) {
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
                         else
                             warp_fill_kp<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0, bmw);
                     } else if constexpr (kBm && kFill) {
-                        warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, e0, slot0, filt0);
+                        warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0, filt0);
                     } else if constexpr (kBm) {
                         const uint32_t c = warp_count_bm(A, map, scratch + wid, p, off0, len, pl0.w, e0);
                         if (lane == 0) A.cnt[p] = c;
@@ -912,11 +917,15 @@ __global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangle
                         if (lane == 0) A.cnt[p] = c;
                     }
                 }
-                uint64_t off2 = pl2.z ? A.off[pl2.y] : 0, slot2 = 0;
+                uint64_t off2 = pl2.z ? A.off[pl2.y] : 0, slot2 = 0, bmo2 = 0;
                 uint32_t filt2 = 0;
-                if (kFill && pl2.z) { slot2 = A.toff[pl2.x] - A.slot0; filt2 = A.efilt[pl2.x]; }
-                e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1;
-                e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2;
+                if (kFill && pl2.z) {
+                    slot2 = A.toff[pl2.x] - A.slot0;
+                    filt2 = A.efilt[pl2.x];
+                    if (kBm) bmo2 = A.bmoff[e2];
+                }
+                e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1; bmo0 = bmo1;
+                e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2; bmo1 = bmo2;
             }
             __syncthreads();
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
