@@ -39,7 +39,7 @@ UNIT = "simplices/s"
 TRI_OUT_BYTES = 28
 # SURVEY 8(d) B_alg per unit for the whole path (sort-based accounting)
 SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44}
-ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 600, "C4": 1500, "C5A": 3000, "C5B": 3000}
+ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400}
 
 
 def _peaks():
