@@ -686,6 +686,8 @@ struct WarpScratchC {              // count
 };
 struct WarpScratchB {              // fill: the staged window (apex ranks by slot)
     uint16_t rec[kWinB];
+    alignas(16) uint32_t st[96];   // 32 triangles' vertices, then D_2 rows: re-cut into
+    alignas(16) uint32_t sr[96];   // 16-byte chunks for full-sector vector stores
 };
 
 __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32_t* __restrict__ map,
@@ -761,38 +763,74 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         const uint32_t m = min((uint32_t)kWinB, count - w0);
         if (A.debug != 2) {
             const uint64_t s0 = slot + w0;
-#ifndef VRB_TRI_BM_UNROLL
-#define VRB_TRI_BM_UNROLL 8
-#endif
-            // kU gathers in flight per lane before the first is used
-            constexpr int kU = VRB_TRI_BM_UNROLL;
-            for (uint32_t j0 = 0; j0 < m; j0 += 32 * kU) {
-                uint2 kq[kU];
-#pragma unroll
-                for (int q = 0; q < kU; ++q) {
-                    const uint32_t j = j0 + 32 * q + lane;
-                    kq[q] = j < m ? ld_idl(idx + W->rec[j]) : make_uint2(0u, 0u);
-                }
-#pragma unroll
-                for (int q = 0; q < kU; ++q) {
-                const uint32_t j = j0 + 32 * q + lane;
-                if (j >= m) break;
-                const uint2 kp = kq[q];
+            // one triangle: slot j of the window, (k, pos(x, k)) gathered
+            auto tri = [&](uint32_t j, uint2 kp, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0,
+                           uint32_t& r1) {
                 const uint32_t k = kp.x, px = kp.y, py = map[k];
-                uint32_t a0 = y, a1 = x, a2 = k;
+                a0 = y; a1 = x; a2 = k;
                 sort3(a0, a1, a2);
+                r0 = min(px, py);
+                r1 = max(px, py);
+                __stcs(A.tf + s0 + j, filt);
+                if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+            };
+            auto scalar = [&](uint32_t j, uint2 kp) {
+                uint32_t a0, a1, a2, r0, r1;
+                tri(j, kp, a0, a1, a2, r0, r1);
                 uint32_t* tv = A.tv + 3 * (s0 + j);
                 __stcs(tv, a0);
                 __stcs(tv + 1, a1);
                 __stcs(tv + 2, a2);
                 if (A.rows) {
                     uint32_t* rw = A.rows + 3 * (s0 + j);
-                    __stcs(rw, min(px, py));
-                    __stcs(rw + 1, max(px, py));
+                    __stcs(rw, r0);
+                    __stcs(rw + 1, r1);
                     __stcs(rw + 2, p);
                 }
-                __stcs(A.tf + s0 + j, filt);
-                if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+            };
+            // head: slots before the first multiple of 4 (16-byte aligned triples)
+            const uint32_t h = min(m, (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u));
+            if ((uint32_t)lane < h) scalar(lane, ld_idl(idx + W->rec[lane]));
+#ifndef VRB_TRI_BM_UNROLL
+#define VRB_TRI_BM_UNROLL 8
+#endif
+            // groups of 32 triangles (384 bytes of vertices, 384 of rows): staged in
+            // shared memory and stored as 24 16-byte chunks each -- every L2 sector
+            // is written whole by one instruction; kU groups of gathers in flight
+            constexpr int kU = VRB_TRI_BM_UNROLL;
+            for (uint32_t g0 = h; g0 < m; g0 += 32 * kU) {
+                uint2 kq[kU];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const uint32_t j = g0 + 32 * q + lane;
+                    kq[q] = j < m ? ld_idl(idx + W->rec[j]) : make_uint2(0u, 0u);
+                }
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const uint32_t g = g0 + 32 * q;
+                    if (g >= m) break;
+                    const uint32_t j = g + lane;
+                    if (g + 32 <= m) {
+                        uint32_t a0, a1, a2, r0, r1;
+                        tri(j, kq[q], a0, a1, a2, r0, r1);
+                        W->st[3 * lane] = a0;
+                        W->st[3 * lane + 1] = a1;
+                        W->st[3 * lane + 2] = a2;
+                        W->sr[3 * lane] = r0;
+                        W->sr[3 * lane + 1] = r1;
+                        W->sr[3 * lane + 2] = p;
+                        __syncwarp();
+                        if (lane < 24) {
+                            __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane,
+                                   reinterpret_cast<const uint4*>(W->st)[lane]);
+                            if (A.rows)
+                                __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
+                                       reinterpret_cast<const uint4*>(W->sr)[lane]);
+                        }
+                        __syncwarp();
+                    } else if (j < m) {
+                        scalar(j, kq[q]);
+                    }
                 }
             }
         }
