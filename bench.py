@@ -187,9 +187,16 @@ def main():
 
     import paper_1809_04424_b200 as vrb
 
-    torch.cuda.set_device(local)
+    # VRB_DIST_BACKEND=gloo: exercise the N > 1 path with several ranks on one
+    # GPU (tests only: gloo stages the exchange through the host); default NCCL
+    backend = os.environ.get("VRB_DIST_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     w = workloads.WORKLOADS[args.workload]
     X = w.points()
     Xd = torch.from_numpy(X).cuda()
@@ -216,7 +223,7 @@ def main():
     counts = None
     launches = 0
     s = torch.cuda.current_stream()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         for _ in range(args.steps):
             flush.fill_(1)
             barrier()
