@@ -1,0 +1,37 @@
+"""Small builds through every entry point, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck): python tools/sanitize_run.py"""
+import math
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1809_04424_b200 as vrb  # noqa: E402
+import workloads  # noqa: E402
+
+torch.cuda.set_device(0)
+for seed, (n, d, kind, r, md) in enumerate([(50, 3, "uniform", math.inf, 2), (120, 3, "lattice", 1.5, 2),
+                                           (200, 4, "gauss", 1.2, 1), (90, 2, "dups", 0.3, 2), (3, 3, "uniform", 1.0, 2)]):
+    X = workloads.random_cloud(seed, n, d, kind)
+    res = vrb.build(X, maxdim=md, radius=r)
+    res.h0()
+    for k in range(1, md + 2):
+        res.simplices(k)
+        res.boundary_colptr(k)
+    del res
+w = workloads.WORKLOADS["C2"]
+res = vrb.build(w.points()[:400], maxdim=2, radius=w.radius)
+res.h0()
+del res
+D = np.abs(np.subtract.outer(np.arange(60.0), np.arange(60.0))) % 7
+vrb.build_dm(D, maxdim=2, radius=3.0)
+vrb.latlon2euc(torch.rand(100, 2, dtype=torch.float64, device="cuda") * 90)
+vrb.sortperm_f64(torch.randn(5000, dtype=torch.float64, device="cuda"))
+cp = torch.tensor([0, 2, 3], dtype=torch.int64, device="cuda")
+rv = torch.tensor([0, 1, 1], dtype=torch.int32, device="cuda")
+vrb.gf2_blockprodsum(2, (cp, rv), (cp, rv), (cp, rv))
+torch.cuda.synchronize()
+print("sanitize run ok")
