@@ -9,7 +9,8 @@ This is a thin ctypes wrapper over ``oracle/liboracle.so`` (plain C, see
 arithmetic of the method: it marshals numpy arrays in and out.
 
 Parity status of each function:
-  length, sortperm, build (edges), simplices, boundary, barcodes: pinned by
+  length, sortperm, build (edges), simplices, boundary, barcodes, the
+  distance-matrix build, latlon2euc and blockprodsum: pinned by
   tests/test_oracle_pins.py.  Nothing here is "parity unpinned".
 """
 from __future__ import annotations

@@ -23,6 +23,11 @@
  *   8 barcodes         Algorithm 1, Algorithm 2 P:229-248,
  *                      Pers/Barcode P:251-260, Fig.4 caption P:286,
  *                      clearing P:302, readings A8,A9,A10,A13 -> or_barcodes
+ * SURVEY 8(f) rows built beyond the path:
+ *   F3 inputs          distance matrix P:351-353 -> or_new_dm; latlon2euc
+ *                      P:383-408 -> or_latlon2euc
+ *   F4 blockprodsum    S = D + C E over GF(2), sec. 4.6 P:986-1022 -> or_blockprodsum
+ *   (F1, dimension-0 bars, is checked against or_barcodes.)
  * plus per-filtration-level helpers used for sampled parity at full size
  * (or_filt_hist, or_simplices_at_filt): the same definitions, evaluated for
  * one filtration level at a time.
