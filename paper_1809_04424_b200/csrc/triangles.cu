@@ -673,6 +673,9 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 // flushes one lane per triangle with (k, pos(x, k)) = idl[off x + r] -- a
 // gather in rank order, so a warp's 32 loads fall in a few sectors.
 // ---------------------------------------------------------------------------
+#ifndef VRB_TRI_COUNT_WARPS
+#define VRB_TRI_COUNT_WARPS 16
+#endif
 #ifndef VRB_TRI_BMFILL
 #define VRB_TRI_BMFILL 1
 #endif
@@ -839,7 +842,7 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
 }
 
 template <bool kFill, bool kPacked, bool kBm>
-__global__ void __launch_bounds__(kFill ? kThreads : kThreads / 2, 1) k_triangles(TriArgs A) {
+__global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2), 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
@@ -1010,7 +1013,9 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     if (bm) {
         per_warp = fill ? (VRB_TRI_BMFILL == 2 ? sizeof(WarpScratch3) : sizeof(WarpScratchB)) : sizeof(WarpScratchC);
         const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(A.n) - 1024;
-        warps = (int)std::min<int64_t>(fill ? kWarps : kWarps / 2, avail / (int64_t)per_warp);
+        // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
+        const int cw = map_bytes(A.n) <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
+        warps = (int)std::min<int64_t>(fill ? kWarps : cw, avail / (int64_t)per_warp);
     }
     if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
