@@ -41,14 +41,16 @@ __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) { GRID_STRIDE(i, n) 
 
 // lightest crossing edge per component root; flags[q] = edge still crosses
 __global__ void k_best(const uint2* __restrict__ ev, const uint32_t* __restrict__ act, int64_t na,
-                       const uint32_t* __restrict__ comp, uint32_t* __restrict__ best) {
+                       const uint32_t* __restrict__ comp, uint32_t* best) {
     GRID_STRIDE(q, na) {
         const uint32_t e = act ? act[q] : (uint32_t)q;
         const uint2 uv = ev[e];
         const uint32_t cu = comp[uv.x], cv = comp[uv.y];
         if (cu != cv) {
-            atomicMin(&best[cu], e);
-            atomicMin(&best[cv], e);
+            // the edges come in position order, so a component usually holds a
+            // smaller candidate already: test before paying for the atomic
+            if (*(volatile const uint32_t*)(best + cu) > e) atomicMin(&best[cu], e);
+            if (*(volatile const uint32_t*)(best + cv) > e) atomicMin(&best[cv], e);
         }
     }
 }
