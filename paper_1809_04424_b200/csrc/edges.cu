@@ -218,6 +218,39 @@ uint32_t* sort_ids(DBuf<uint64_t>& k0, DBuf<uint64_t>& k1, DBuf<uint32_t>& v0, D
 
 }  // namespace
 
+// After a sort on the high digits only (bits >= shift): runs of equal high
+// bits are tiny for continuous data; sort each by the full key in place
+// (insertion sort, stable, so equal keys keep their lex order).  A run longer
+// than 64 whose keys are not all equal sets *fallback (full sort needed).
+__global__ void k_fixup_runs(uint64_t* __restrict__ key, uint32_t* __restrict__ val, int64_t n, int shift,
+                             int* __restrict__ fallback) {
+    GRID_STRIDE(p, n) {
+        const uint64_t hp = key[p] >> shift;
+        if (p > 0 && (key[p - 1] >> shift) == hp) continue;   // not the start of a run
+        int64_t q = p + 1;
+        while (q < n && q - p <= 64 && (key[q] >> shift) == hp) ++q;
+        if (q - p < 2) continue;
+        if (q - p > 64) {
+            const uint64_t k0 = key[p];
+            for (int64_t r = p + 1; r < n && (key[r] >> shift) == hp; ++r)
+                if (key[r] != k0) { atomicOr(fallback, 1); break; }
+            continue;
+        }
+        for (int64_t a = p + 1; a < q; ++a) {
+            const uint64_t k = key[a];
+            const uint32_t v = val[a];
+            int64_t b = a - 1;
+            while (b >= p && key[b] > k) {
+                key[b + 1] = key[b];
+                val[b + 1] = val[b];
+                --b;
+            }
+            key[b + 1] = k;
+            val[b + 1] = v;
+        }
+    }
+}
+
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
     const int64_t E = ke.E;
     if (E == 0) return 0;
@@ -233,9 +266,33 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
     // sort (len bits - min): only the digits of (max - min) vary
     uint64_t kmin = 0;
     const uint64_t vary = key_range(ke.key.get(), E, s, &kmin);
+    // radix passes on the 4 highest varying digits only (~31+ significant
+    // bits); the few runs left with equal high bits are finished in place
+    int hi_digit = -1;
+    for (int dg = 7; dg >= 0; --dg)
+        if ((vary >> (8 * dg)) & 0xFFull) { hi_digit = dg; break; }
+    const int shift = hi_digit >= 4 ? 8 * (hi_digit - 3) : 0;
+    const uint64_t vary_top = shift ? (vary & ~((1ull << shift) - 1ull)) : vary;
     bool biased = false;
-    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary, s, kmin, &biased);
+    bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary_top, s, kmin, &biased);
     const uint64_t bias = biased ? kmin : 0ull;
+    if (shift) {
+        uint64_t* k1 = alt ? key_alt.get() : ke.key.get();
+        uint32_t* v1 = alt ? perm_alt.get() : vals;
+        DBuf<int> fb(1, s);
+        VRB_CUDA(cudaMemsetAsync(fb.get(), 0, sizeof(int), s));
+        k_fixup_runs<<<grid_for(E, 256), 256, 0, s>>>(k1, v1, E, shift, fb.get());
+        VRB_LAUNCH_CHECK();
+        int h = 0;
+        VRB_CUDA(cudaMemcpyAsync(&h, fb.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+        if (h) {   // heavy clustering of the high bits: complete the sort on every digit
+            uint64_t* k2 = alt ? ke.key.get() : key_alt.get();
+            uint32_t* v2 = alt ? vals : perm_alt.get();
+            const bool alt2 = radix_sort_pairs(k1, k2, v1, v2, E, vary, s);
+            if (alt2) alt = !alt;
+        }
+    }
     const uint64_t* skey = alt ? key_alt.get() : ke.key.get();
     const uint32_t* sval = alt ? perm_alt.get() : vals;
     DBuf<uint32_t> head(E, s);

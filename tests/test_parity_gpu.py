@@ -239,6 +239,24 @@ def test_fill_without_apex_bitmaps_high_degree(vrb, monkeypatch):
     compare(vrb, w.points(), w.maxdim, w.radius)
 
 
+def test_edge_sort_high_bit_runs_fallback(vrb):
+    # lengths 1 + k * 1e-12: they agree in the high bits the partial radix
+    # pass sorts on and differ below; runs longer than 64 take the full-sort
+    # fallback, shorter runs the in-place fix-up -- both must give (len, i, j)
+    for m in (40, 150):
+        X = np.zeros((m + 1, 2))
+        theta = np.linspace(0.0, 2.0 * np.pi, m, endpoint=False)
+        rad = 1.0 + np.arange(m)[::-1] * 1e-12              # reversed: the fix-up has to move every key
+        X[1:, 0] = rad * np.cos(theta)
+        X[1:, 1] = rad * np.sin(theta)
+        o = oracle.Oracle(X, math.inf)
+        el = o.edges()[2]
+        near = el[(el > 0.999) & (el < 1.001)]
+        assert len(near) >= m and len(np.unique(near)) >= m   # a run of distinct keys (m = 150: > 64, fallback)
+        compare(vrb, X, 0, math.inf)
+        compare(vrb, X, 1, 1.0 + 1e-9)
+
+
 def test_sortperm_literal_and_random(vrb):
     g = json.load(open(os.path.join(GOLDEN, "sortperm_literal.json")))
     for case in g["cases"]:
