@@ -218,6 +218,12 @@ uint32_t* sort_ids(DBuf<uint64_t>& k0, DBuf<uint64_t>& k1, DBuf<uint32_t>& v0, D
 
 }  // namespace
 
+#ifndef VRB_EDGE_TOP_DIGITS
+#define VRB_EDGE_TOP_DIGITS 4
+#endif
+#ifndef VRB_EDGE_RUN_MAX
+#define VRB_EDGE_RUN_MAX 64
+#endif
 // After a sort on the high digits only (bits >= shift): runs of equal high
 // bits are tiny for continuous data; sort each by the full key in place
 // (insertion sort, stable, so equal keys keep their lex order).  A run longer
@@ -228,9 +234,9 @@ __global__ void k_fixup_runs(uint64_t* __restrict__ key, uint32_t* __restrict__ 
         const uint64_t hp = key[p] >> shift;
         if (p > 0 && (key[p - 1] >> shift) == hp) continue;   // not the start of a run
         int64_t q = p + 1;
-        while (q < n && q - p <= 64 && (key[q] >> shift) == hp) ++q;
+        while (q < n && q - p <= VRB_EDGE_RUN_MAX && (key[q] >> shift) == hp) ++q;
         if (q - p < 2) continue;
-        if (q - p > 64) {
+        if (q - p > VRB_EDGE_RUN_MAX) {
             const uint64_t k0 = key[p];
             for (int64_t r = p + 1; r < n && (key[r] >> shift) == hp; ++r)
                 if (key[r] != k0) { atomicOr(fallback, 1); break; }
@@ -271,7 +277,7 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
     int hi_digit = -1;
     for (int dg = 7; dg >= 0; --dg)
         if ((vary >> (8 * dg)) & 0xFFull) { hi_digit = dg; break; }
-    const int shift = hi_digit >= 4 ? 8 * (hi_digit - 3) : 0;
+    const int shift = hi_digit >= VRB_EDGE_TOP_DIGITS ? 8 * (hi_digit - (VRB_EDGE_TOP_DIGITS - 1)) : 0;
     const uint64_t vary_top = shift ? (vary & ~((1ull << shift) - 1ull)) : vary;
     bool biased = false;
     bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary_top, s, kmin, &biased);
