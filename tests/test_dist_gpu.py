@@ -40,6 +40,8 @@ def _worker(rank, world, port, X, maxdim, radius, q):
             g, off, n = res.count(k)
             v, f = res.simplices(k)
             out[k] = (g, off, n, _u32(v), _u32(f), _u32(res.boundary(k)))
+        pos, death, ness = res.h0()   # every rank holds every edge: the whole H0 result
+        out["h0"] = (_u32(pos), _u32(death), ness)
         q.put(out)
     except Exception as e:   # surface worker errors in the test
         q.put({"rank": rank, "error": repr(e)})
@@ -83,3 +85,6 @@ def test_build_dist_slices_equal_single_gpu(case, world):
         for name, idx, want in (("verts", 3, _u32(rv)), ("filt", 4, _u32(rf)), ("rows", 5, _u32(rr))):
             cat = np.concatenate([o[k][idx] for o in outs])
             assert np.array_equal(cat, want), (k, name)
+    hp, hd, hn = ref.h0()
+    for o in outs:
+        assert np.array_equal(o["h0"][0], _u32(hp)) and np.array_equal(o["h0"][1], _u32(hd)) and o["h0"][2] == hn
