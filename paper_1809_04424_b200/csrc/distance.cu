@@ -30,6 +30,7 @@ namespace {
 constexpr int kT = 64;        // tile edge
 constexpr int kDC = 16;       // coordinates staged per chunk
 constexpr int kThreads = 256;
+constexpr int kFillStageD = 16;   // k_dist_fill stages the tile's points for d <= 16 (16 KB)
 
 __device__ __forceinline__ int64_t tile_index(int64_t ti, int64_t tj, int64_t nt) {
     return ti * nt - ti * (ti - 1) / 2 + (tj - ti);   // packed upper triangle (tj >= ti)
@@ -118,6 +119,26 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
     const unsigned long long* m = masks + tile_index(ti, tj, nt) * kT;
+    // the tile's points, coordinate-major, when they fit (d <= kFillStageD):
+    // the fold then reads shared memory (row point broadcast, column points
+    // conflict-free) instead of strided global loads
+    __shared__ double sA[kFillStageD][kT];
+    __shared__ double sB[kFillStageD][kT];
+    __shared__ int s_any;
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    if (threadIdx.x < kT && m[threadIdx.x]) s_any = 1;
+    __syncthreads();
+    if (!s_any) return;
+    const bool staged = d <= kFillStageD;
+    if (staged) {
+        for (int q = threadIdx.x; q < kT * d; q += kThreads) {
+            const int r = q / d, c = q % d;
+            sA[c][r] = i0 + r < n ? X[(i0 + r) * d + c] : 0.0;
+            sB[c][r] = j0 + r < n ? X[(j0 + r) * d + c] : 0.0;
+        }
+        __syncthreads();
+    }
     for (int r = wid; r < kT; r += kThreads / 32) {
         const int64_t i = i0 + r;
         if (i >= n) break;
@@ -132,9 +153,16 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
             const int64_t j = j0 + c;
             const double* xj = X + j * d;
             double acc = 0.0;
-            for (int q = 0; q < d; ++q) {
-                const double t = __dsub_rn(__ldg(xi + q), __ldg(xj + q));
-                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            if (staged) {
+                for (int q = 0; q < d; ++q) {
+                    const double t = __dsub_rn(sA[q][r], sB[q][c]);
+                    acc = __dadd_rn(acc, __dmul_rn(t, t));
+                }
+            } else {
+                for (int q = 0; q < d; ++q) {
+                    const double t = __dsub_rn(__ldg(xi + q), __ldg(xj + q));
+                    acc = __dadd_rn(acc, __dmul_rn(t, t));
+                }
             }
             const double len = __dsqrt_rn(acc);
             const uint64_t slot = base + __popcll(bits & ((1ull << c) - 1ull));
