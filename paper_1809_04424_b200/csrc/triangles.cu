@@ -131,53 +131,11 @@ __device__ __forceinline__ uint32_t pick(const uint4& q, int e) {
     return e == 0 ? q.x : (e == 1 ? q.y : (e == 2 ? q.z : q.w));
 }
 
-#ifndef VRB_TRI_HINT
-#define VRB_TRI_HINT 0
-#endif
-// Neighbour-list loads: with VRB_TRI_HINT the lines are kept in L2 with the
-// evict_last policy (the lists are re-read by many owner edges while the
-// output stream passes through L2 with evict-first stores).
-__device__ __forceinline__ uint4 ld_list(const uint4* a) {
-#if VRB_TRI_HINT
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    uint4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(a), "l"(pol));
-    return v;
-#else
-    return __ldg(a);
-#endif
-}
-__device__ __forceinline__ uint32_t ld_list(const uint32_t* a) {
-#if VRB_TRI_HINT
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
-    return v;
-#else
-    return __ldg(a);
-#endif
-}
-
-#ifndef VRB_TRI_IDL_HINT
-#define VRB_TRI_IDL_HINT 0
-#endif
-// id-ordered list gathers of the bitmap fill: VRB_TRI_IDL_HINT keeps their
-// lines in L2 with the evict_last policy (the output stream is evict-first)
-__device__ __forceinline__ uint2 ld_idl(const uint2* a) {
-#if VRB_TRI_IDL_HINT
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    uint2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(pol));
-    return v;
-#else
-    return __ldg(a);
-#endif
-}
+// Neighbour-list loads (read-only path).  L2 evict-last cache hints on these
+// loads were measured and did not help.
+__device__ __forceinline__ uint4 ld_list(const uint4* a) { return __ldg(a); }
+__device__ __forceinline__ uint32_t ld_list(const uint32_t* a) { return __ldg(a); }
+__device__ __forceinline__ uint2 ld_idl(const uint2* a) { return __ldg(a); }
 
 __device__ __forceinline__ uint4 no_group() { return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu); }
 
@@ -313,72 +271,6 @@ __device__ __forceinline__ uint32_t rank_bits(WS* __restrict__ W, uint32_t lim) 
     for (int j = 0; j < kWpl; ++j) { W->wpre[kWpl * lane + j] = run; run += c[j]; }
     __syncwarp();
     return __shfl_sync(0xffffffffu, incl, 31);
-}
-
-#ifndef VRB_TRI_VEC
-#define VRB_TRI_VEC 0
-#endif
-// Write the window's m triangles at slots [s0, s0 + m): get(j) -> (k, pos(x, k)),
-// pos(y, k) = map[k].  Slots are taken four at a time per lane where the
-// slot index is a multiple of 4, so every output array gets 16-byte
-// streaming stores (3 for the vertices, 3 for the D_2 rows, 1 for filt);
-// the unaligned head and the tail are written one triangle per lane.
-template <class Get>
-__device__ __forceinline__ void flush_vec(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t m, uint64_t s0,
-                                          uint32_t p, uint32_t y, uint32_t x, uint32_t filt, Get&& get) {
-    const int lane = threadIdx.x & 31;
-    auto one = [&](uint32_t j) {
-        const uint2 kp = get(j);
-        const uint32_t k = kp.x, px = kp.y, py = map[k];
-        uint32_t a0 = y, a1 = x, a2 = k;
-        sort3(a0, a1, a2);
-        uint32_t* tv = A.tv + 3 * (s0 + j);
-        __stcs(tv, a0);
-        __stcs(tv + 1, a1);
-        __stcs(tv + 2, a2);
-        if (A.rows) {
-            uint32_t* rw = A.rows + 3 * (s0 + j);
-            __stcs(rw, min(px, py));
-            __stcs(rw + 1, max(px, py));
-            __stcs(rw + 2, p);
-        }
-        __stcs(A.tf + s0 + j, filt);
-        if (A.apex) A.apex[s0 + j] = (uint16_t)k;
-    };
-    uint32_t h = (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u);
-    if (h > m) h = m;
-    if ((uint32_t)lane < h) one(lane);
-    const uint32_t nq = (m - h) >> 2;
-    for (uint32_t q = lane; q < nq; q += 32) {
-        const uint32_t j = h + 4 * q;
-        uint2 kp[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) kp[e] = get(j + e);
-        uint32_t v[12], r[12];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t k = kp[e].x, px = kp[e].y, py = map[k];
-            uint32_t a0 = y, a1 = x, a2 = k;
-            sort3(a0, a1, a2);
-            v[3 * e] = a0; v[3 * e + 1] = a1; v[3 * e + 2] = a2;
-            r[3 * e] = min(px, py); r[3 * e + 1] = max(px, py); r[3 * e + 2] = p;
-        }
-        uint4* tv = reinterpret_cast<uint4*>(A.tv + 3 * (s0 + j));
-        __stcs(tv, make_uint4(v[0], v[1], v[2], v[3]));
-        __stcs(tv + 1, make_uint4(v[4], v[5], v[6], v[7]));
-        __stcs(tv + 2, make_uint4(v[8], v[9], v[10], v[11]));
-        if (A.rows) {
-            uint4* rw = reinterpret_cast<uint4*>(A.rows + 3 * (s0 + j));
-            __stcs(rw, make_uint4(r[0], r[1], r[2], r[3]));
-            __stcs(rw + 1, make_uint4(r[4], r[5], r[6], r[7]));
-            __stcs(rw + 2, make_uint4(r[8], r[9], r[10], r[11]));
-        }
-        __stcs(reinterpret_cast<uint4*>(A.tf + s0 + j), make_uint4(filt, filt, filt, filt));
-        if (A.apex)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) A.apex[s0 + j + e] = (uint16_t)kp[e].x;
-    }
-    for (uint32_t j = h + 4 * nq + lane; j < m; j += 32) one(j);
 }
 
 // Write the staged window [s0, s0 + m), one lane per triangle, kU position
@@ -541,14 +433,7 @@ __device__ __forceinline__ void warp_fill_impl(const TriArgs& A, const uint32_t*
             }
             __syncwarp();
             if (A.debug != 2) {
-                if constexpr (kPacked && VRB_TRI_VEC) {
-                    flush_vec(A, map, min(win, count - w0), slot + w0, p, y, x, filt, [&](uint32_t j) {
-                        const uint32_t rc = W->rec[j];
-                        return make_uint2(rc & 0xFFFFu, ld_list(npx + (rc >> 16)));
-                    });
-                } else {
-                    flush_window<kPacked>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
-                }
+                flush_window<kPacked>(A, map, W, min(win, count - w0), slot + w0, p, y, x, filt, npx);
             }
             __syncwarp();
         }
@@ -593,7 +478,7 @@ template <bool kOneRound>
 __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* __restrict__ map,
                                              WarpScratch3* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
                                              uint32_t len, uint64_t offx, uint32_t degx, uint64_t slot,
-                                             uint32_t filt, const uint32_t* __restrict__ bmw = nullptr) {
+                                             uint32_t filt) {
     const int lane = threadIdx.x & 31;
     int mis;
     const uint4* gk = aligned_groups(A.nkr + offx, mis);
@@ -601,20 +486,14 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
     const int ngroups = (int)((len + mis + 3) >> 2);
     for (uint32_t R = 0; R < degx; R += kBits) {
         const uint32_t lim = kOneRound ? degx : min((uint32_t)kBits, degx - R);
-        if (bmw) {   // the count pass's apex bitmap replaces the mark
-            const uint32_t nw = (lim + 31) >> 5;
-            for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = __ldcs(bmw + (R >> 5) + w);
-            __syncwarp();
-        } else {
-            clear_bits(W, lim);
-            auto mark = [&](uint32_t w, uint32_t) {
-                const uint32_t r = (w >> 16) - R;
-                if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
-                    atomicOr(&W->bits[r >> 5], 1u << (r & 31));
-            };
-            if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
-            else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
-        }
+        clear_bits(W, lim);
+        auto mark = [&](uint32_t w, uint32_t) {
+            const uint32_t r = (w >> 16) - R;
+            if ((kOneRound || r < (uint32_t)kBits) && map[w & 0xFFFFu] < p)
+                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+        };
+        if (ngroups <= 32) stream_prefix<1>(gk, ngroups, mis, len, mark);
+        else stream_prefix<kRegGroups>(gk, ngroups, mis, len, mark);
         const uint32_t count = rank_bits<kWords>(W, lim);
         if (A.debug == 1) { slot += count; if (kOneRound) break; continue; }
         for (uint32_t w0 = 0; w0 < count; w0 += kWin3) {
@@ -631,9 +510,6 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
             __syncwarp();
             const uint32_t m = min((uint32_t)kWin3, count - w0);
             if (A.debug != 2) {
-#if VRB_TRI_VEC
-                flush_vec(A, map, m, slot + w0, p, y, x, filt, [&](uint32_t j) { return W->rec[j]; });
-#else
                 const uint64_t s0 = slot + w0;
                 for (uint32_t j = lane; j < m; j += 32) {
                     const uint2 rc = W->rec[j];
@@ -654,7 +530,6 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
                     __stcs(A.tf + s0 + j, filt);
                     if (A.apex) A.apex[s0 + j] = (uint16_t)k;
                 }
-#endif
             }
             __syncwarp();
         }
@@ -676,12 +551,6 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 #ifndef VRB_TRI_COUNT_WARPS
 #define VRB_TRI_COUNT_WARPS 16
 #endif
-#ifndef VRB_TRI_BMFILL
-#define VRB_TRI_BMFILL 1
-#endif
-// VRB_TRI_BMFILL: 2 = the bitmap replaces the mark of warp_fill_kp (the emit
-// streams the prefix with its positions); 1 = warp_fill_bm (emit by walking
-// the bitmap, (k, pos) gathered from the id-ordered lists)
 constexpr int kBmWords = (int)(kApexBitmapMaxDeg / 32);
 constexpr int kWinB = 512;
 struct WarpScratchC {              // count
@@ -847,8 +716,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
     uint32_t* map = reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
         kBm,
-        typename std::conditional<kFill, typename std::conditional<VRB_TRI_BMFILL == 2, WarpScratch3, WarpScratchB>::type,
-                                  WarpScratchC>::type,
+        typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
         typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type;
     WS* scratch = reinterpret_cast<WS*>(smem + ((A.n * 4 + 15) / 16) * 16);
     __shared__ int64_t s_lo, s_hi, s_end;
@@ -933,13 +801,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                 }
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kBm && kFill && VRB_TRI_BMFILL == 2) {
-                        const uint32_t* bmw = A.bm + A.bmoff[e0];
-                        if (pl0.w <= (uint32_t)kBits)
-                            warp_fill_kp<true>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0, bmw);
-                        else
-                            warp_fill_kp<false>(A, map, scratch + wid, p, y, x, len, off0, pl0.w, slot0, filt0, bmw);
-                    } else if constexpr (kBm && kFill) {
+                    if constexpr (kBm && kFill) {
                         warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0, filt0);
                     } else if constexpr (kBm) {
                         const uint32_t c = warp_count_bm(A, map, scratch + wid, p, off0, len, pl0.w, e0);
@@ -1011,7 +873,7 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     int warps = fill ? fill_warps(A.n, packed) : kWarps / 2;
     size_t per_warp = fill ? scratch_bytes(packed) : 0;
     if (bm) {
-        per_warp = fill ? (VRB_TRI_BMFILL == 2 ? sizeof(WarpScratch3) : sizeof(WarpScratchB)) : sizeof(WarpScratchC);
+        per_warp = fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC);
         const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(A.n) - 1024;
         // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
         const int cw = map_bytes(A.n) <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
