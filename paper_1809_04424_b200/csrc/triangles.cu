@@ -90,6 +90,8 @@ struct TriArgs {
     uint32_t* tf;
     uint32_t* rows;
     uint16_t* apex;   // K >= 3, n <= 65536: apex id of each triangle (its vertex off the owner edge)
+    uint32_t* gmap;            // global-memory host maps (n u32 per CTA) when n is too large for
+                               // shared memory, else null (the map lives in shared memory)
     uint32_t* bm;              // apex bitmaps (count writes, fill reads), or null
     const uint64_t* bmoff;     // per hosted slot: word offset of its bitmap
     const uint2* idl;          // (k, pos) in neighbour-ID order
@@ -713,12 +715,12 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
 template <bool kFill, bool kPacked, bool kBm>
 __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2), 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t* map = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
         kBm,
         typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
         typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type;
-    WS* scratch = reinterpret_cast<WS*>(smem + ((A.n * 4 + 15) / 16) * 16);
+    WS* scratch = reinterpret_cast<WS*>(smem + (A.gmap ? 0 : ((A.n * 4 + 15) / 16) * 16));
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
     __shared__ unsigned s_next;
@@ -844,22 +846,19 @@ size_t scratch_bytes(bool packed) {
     return packed && VRB_TRI_MODE == 3 ? sizeof(WarpScratch3) : sizeof(WarpScratch);
 }
 
-// warps per CTA of the fill: up to kWarps, fewer when the vertex map leaves
-// too little shared memory
-int fill_warps(int64_t n, bool packed) {
-    const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(n) - 1024;
-    const int64_t w = avail / (int64_t)scratch_bytes(packed);
-    return (int)std::max<int64_t>(0, std::min<int64_t>(kWarps, w));
-}
-
 template <bool kFill, bool kPacked, bool kBm>
-void launch_k(const TriArgs& A, int threads, size_t smem, int64_t nctas_cap, cudaStream_t s) {
+void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap, cudaStream_t s) {
     VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked, kBm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     int per_sm = 0;
     VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked, kBm>, threads, smem));
     if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count() * per_sm, nctas_cap);
+    DBuf<uint32_t> maps;
+    if (gmap) {   // one n-entry host map per CTA in global memory (L2-resident for moderate n)
+        maps.alloc((size_t)grid * (size_t)A.n, s);
+        A.gmap = maps.get();
+    }
     k_triangles<kFill, kPacked, kBm><<<grid, threads, smem, s>>>(A);
     VRB_LAUNCH_CHECK();
 }
@@ -870,18 +869,28 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     const bool bm = A.bm != nullptr;
     // fill: one CTA per SM (the vertex map + per-warp scratch); count:
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
-    int warps = fill ? fill_warps(A.n, packed) : kWarps / 2;
-    size_t per_warp = fill ? scratch_bytes(packed) : 0;
+    // the host map goes to global memory when it would leave shared memory for
+    // fewer than 8 warps of scratch (n above ~40-50k), or when forced (tests)
+    size_t per_warp = bm ? (fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC)) : (fill ? scratch_bytes(packed) : 0);
+    const char* fg = std::getenv("VRB_FORCE_GLOBAL_MAP");   // testing knob
+    const bool gmap = (fg && fg[0] == '1') ||
+                      (int64_t)map_bytes(A.n) + 8 * (int64_t)std::max<size_t>(per_warp, 64) + 1024 >
+                          (int64_t)device_max_smem_optin();
+    const size_t mapb = gmap ? 0 : map_bytes(A.n);
+    const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)mapb - 1024;
+    int warps;
     if (bm) {
-        per_warp = fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC);
-        const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)map_bytes(A.n) - 1024;
         // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
-        const int cw = map_bytes(A.n) <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
+        const int cw = mapb <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
         warps = (int)std::min<int64_t>(fill ? kWarps : cw, avail / (int64_t)per_warp);
+    } else if (fill) {
+        warps = (int)std::min<int64_t>(kWarps, avail / (int64_t)per_warp);
+    } else {
+        warps = kWarps / 2;
     }
     if (warps < 4) fail(VRB_ENOTSUP, "triangle kernel: n = %lld leaves no shared memory", (long long)A.n);
     const int threads = warps * 32;
-    const size_t smem = map_bytes(A.n) + (size_t)warps * per_warp;
+    const size_t smem = mapb + (size_t)warps * per_warp;
     // Task size depends on the work only (identical on every rank, so a
     // partition of the task range is a partition of the owner edges):
     // ~8k tasks, but not below ~64k candidate tests each.
@@ -898,14 +907,14 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     A.task_counter = counter.get();
     const int64_t cap = A.task_hi - A.task_lo;
     if (bm) {
-        if (fill) launch_k<true, true, true>(A, threads, smem, cap, s);
-        else launch_k<false, true, true>(A, threads, smem, cap, s);
+        if (fill) launch_k<true, true, true>(A, threads, smem, cap, gmap, s);
+        else launch_k<false, true, true>(A, threads, smem, cap, gmap, s);
     } else if (fill) {
-        if (packed) launch_k<true, true, false>(A, threads, smem, cap, s);
-        else launch_k<true, false, false>(A, threads, smem, cap, s);
+        if (packed) launch_k<true, true, false>(A, threads, smem, cap, gmap, s);
+        else launch_k<true, false, false>(A, threads, smem, cap, gmap, s);
     } else {
-        if (packed) launch_k<false, true, false>(A, threads, smem, cap, s);
-        else launch_k<false, false, false>(A, threads, smem, cap, s);
+        if (packed) launch_k<false, true, false>(A, threads, smem, cap, gmap, s);
+        else launch_k<false, false, false>(A, threads, smem, cap, gmap, s);
     }
 }
 
@@ -932,10 +941,6 @@ TriArgs graph_args(const Graph& g) {
 
 }  // namespace
 
-int64_t dense_map_limit() {
-    const int64_t smem = (int64_t)device_max_smem_optin();
-    return (smem - 4 * (int64_t)std::max(sizeof(WarpScratch), scratch_bytes(true)) - 1024) / 4;   // >= 4 warps of fill scratch
-}
 
 void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaStream_t s) {
     if (g.E == 0) return;

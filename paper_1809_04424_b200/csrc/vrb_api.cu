@@ -346,9 +346,6 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             h->filt[1] = efilt ? efilt + lo : nullptr;
         }
         if (h->K >= 2) {
-            if (n > dense_map_limit())
-                fail(VRB_ENOTSUP, "n = %lld exceeds the shared-memory vertex map (%lld)", (long long)n,
-                     (long long)dense_map_limit());
             Graph g;
             build_graph(ev, n, E, s, g);
             timer.mark(2);

@@ -105,7 +105,6 @@ void count_tets(const Graph& g, const TriLevels& L, uint32_t* cnt, int part, int
 void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const uint64_t* qoff, int64_t p_lo,
                int64_t p_hi, uint64_t slot0, uint32_t* qv, uint32_t* qf, uint32_t* rows, cudaStream_t s);
 
-int64_t dense_map_limit();   // largest n the shared-memory vertex map supports
 
 // F4 (gf2.cu): S = D + C E over GF(2); writes colptr_out (ncols + 1) and
 // returns nnz(S) with its rows allocated through alloc_rows.

@@ -257,6 +257,70 @@ def test_edge_sort_high_bit_runs_fallback(vrb):
         compare(vrb, X, 1, 1.0 + 1e-9)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_global_host_map_forced(vrb, monkeypatch, seed):
+    # the host map in global memory (used when n is too large for shared
+    # memory), forced on small inputs: bitmap, re-enumerating and wide paths
+    monkeypatch.setenv("VRB_FORCE_GLOBAL_MAP", "1")
+    X = workloads.random_cloud(950 + seed, 300, 3, ["uniform", "lattice"][seed % 2])
+    compare(vrb, X, 1, [0.35, 1.5][seed % 2])
+    monkeypatch.setenv("VRB_NO_APEX_BITMAPS", "1")
+    compare(vrb, X, 1, [0.35, 1.5][seed % 2])
+    monkeypatch.setenv("VRB_FORCE_WIDE_LISTS", "1")
+    compare(vrb, X, 1, [0.35, 1.5][seed % 2])
+
+
+def test_large_n_global_map_wide_lists(vrb):
+    # n = 70000 > 65536 (wide lists) and far beyond the shared-memory host map:
+    # properties against an independent neighbour search (scipy cKDTree) and a
+    # sparse-matrix triangle count (trace(A^3) / 6)
+    spatial = pytest.importorskip("scipy.spatial")
+    sp = pytest.importorskip("scipy.sparse")
+    rng = np.random.default_rng(70000)
+    n = 70000
+    X = rng.uniform(0, 1, (n, 3))
+    r = 0.03                                     # mean degree ~8: ~2.8e5 edges, ~6e5 triangles
+    pairs = spatial.cKDTree(X).query_pairs(r, output_type="ndarray")
+    d = np.sqrt(((X[pairs[:, 0]] - X[pairs[:, 1]]) ** 2).sum(1))
+    assert np.abs(d - r).min() > 1e-9            # no pair at the cap: the reference set is exact
+    vrb.use_torch_allocator(True)
+    try:
+        res = vrb.build(torch.from_numpy(X).cuda(), maxdim=1, radius=r)
+        ev, ef = res.simplices(1)
+        ev, ef = _np(ev).astype(np.int64), _np(ef)
+        assert ev.shape[0] == pairs.shape[0]
+        got = np.sort(ev[:, 0] * n + ev[:, 1])
+        want = np.sort(np.minimum(pairs[:, 0], pairs[:, 1]).astype(np.int64) * n + np.maximum(pairs[:, 0], pairs[:, 1]))
+        np.testing.assert_array_equal(got, want)
+        A = sp.coo_matrix((np.ones(len(pairs)), (pairs[:, 0], pairs[:, 1])), shape=(n, n))
+        A = (A + A.T).tocsr()
+        T = int(round((A @ A).multiply(A).sum() / 6))
+        tv, tf = res.simplices(2)
+        tv, tf = _np(tv).astype(np.int64), _np(tf)
+        assert tv.shape[0] == T and T > 100000
+        rows = _np(res.boundary(2)).astype(np.int64)
+        assert np.all(np.diff(rows, axis=1) > 0)
+        # the rows are the positions of the triangle's three edges
+        ekey = ev[:, 0] * n + ev[:, 1]
+        from_rows = np.sort(ekey[rows], axis=1)
+        from_tri = np.sort(np.stack([tv[:, 0] * n + tv[:, 1], tv[:, 0] * n + tv[:, 2], tv[:, 1] * n + tv[:, 2]], 1),
+                           axis=1)
+        np.testing.assert_array_equal(from_rows, from_tri)
+        # filt = the largest edge filt = the filt of the last (largest-position) row
+        np.testing.assert_array_equal(tf, ef[rows[:, 2]])
+        assert np.all(ef[rows].max(axis=1) == tf)
+        # strict (filt, lex) order: the (filt, v0, v1, v2) sort is the identity, no repeats
+        order = np.lexsort((tv[:, 2], tv[:, 1], tv[:, 0], tf))
+        np.testing.assert_array_equal(order, np.arange(T))
+        dup = (np.diff(tf) == 0) & np.all(np.diff(tv, axis=0) == 0, axis=1)
+        assert not dup.any()
+        del res
+    finally:
+        torch.cuda.synchronize()
+        vrb.use_torch_allocator(False)
+        torch.cuda.empty_cache()
+
+
 def test_sortperm_literal_and_random(vrb):
     g = json.load(open(os.path.join(GOLDEN, "sortperm_literal.json")))
     for case in g["cases"]:
