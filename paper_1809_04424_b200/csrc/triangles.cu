@@ -19,20 +19,26 @@
 // level (ties) get their small ranges re-sorted by lex afterwards (segsort.cu).
 //
 // Kernel shape.  Edges are grouped by a "host" endpoint y; a CTA holds the
-// whole neighbourhood of y as a dense shared-memory map pos_y[k] (n u32) and
-// its warps take the host's owner edges one at a time (longest first, grabbed
-// dynamically).  For edge p = (y, x) a warp streams the older-neighbour PREFIX
-// of x (x's neighbours in position order, cut at p; the endpoint with the
-// shorter prefix is scanned) and tests pos_y[k] < p.
-//   count: per-lane counters, one warp reduction.
-//   fill : the valid apexes' ranks in x's ID-ordered list are flagged, the
-//          flags are folded into a bitmap with per-word prefix popcounts, and
-//          each valid apex computes its own output slot (#valid apexes of
-//          smaller id) -- a counting sort by apex id with no data movement.
-//          The emit pass streams the prefix again together with its edge
-//          positions (coalesced 16-byte groups) and stages (k, pos(x, k)) for
-//          a window of slots in shared memory; the flush writes the window
-//          one lane per triangle with streaming stores and no global gathers.
+// whole neighbourhood of y as a dense map pos_y[k] (n u32; shared memory, or
+// a per-CTA slice of global memory when n is too large) and its warps take
+// the host's owner edges one at a time (longest first, grabbed dynamically).
+// For edge p = (y, x) a warp streams the older-neighbour PREFIX of x (x's
+// neighbours in position order, cut at p; the endpoint with the shorter
+// prefix is scanned) and tests pos_y[k] < p.  Two kernels:
+//   count: per owner edge, the valid apexes' ranks in x's ID-ordered list are
+//          OR-ed into a shared bitmap, which is stored (the "apex bitmap",
+//          ceil(deg x / 32) words) and popcounted -> cnt[p].
+//   fill : (single rank, packed lists, degrees <= 8192: the default) the
+//          bitmap is reloaded in 32-word register chunks; a warp scan of the
+//          popcounts gives each valid apex its slot (#valid apexes of smaller
+//          id) -- a counting sort by apex id with no data movement; the set
+//          bits of a window of slots are walked, (k, pos(x, k)) is gathered
+//          from x's id-ordered list in rank order, pos(y, k) read from the
+//          map, and 32 triangles at a time are staged in shared memory and
+//          written as whole 16-byte chunks.
+//          (Several ranks, or larger degrees: the fill re-enumerates -- mark
+//          as the count does, rank, re-stream the prefix with its positions
+//          staging (k, pos(x, k)) by slot, flush.)
 //          Streams run 4/2/1 groups per lane so short prefixes waste few lanes.
 #include <algorithm>
 #include <cstdlib>
