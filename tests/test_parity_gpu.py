@@ -321,6 +321,19 @@ def test_large_n_global_map_wide_lists(vrb):
         torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("maxdim", [1, 2])
+def test_skip_boundary_same_simplices(vrb, maxdim):
+    # VRB_SKIP_BOUNDARY: no D_k row arrays, identical simplices and levels
+    X = workloads.random_cloud(77, 400, 3, "uniform")
+    o = oracle.Oracle(X, 0.3)
+    res = vrb.build(X, maxdim=maxdim, radius=0.3, skip_boundary=True)
+    for k in range(2, maxdim + 2):
+        v, f, _ = o.simplices(k)
+        gv, gf = res.simplices(k)
+        np.testing.assert_array_equal(_np(gv), v)
+        np.testing.assert_array_equal(_np(gf), f)
+
+
 def test_sortperm_literal_and_random(vrb):
     g = json.load(open(os.path.join(GOLDEN, "sortperm_literal.json")))
     for case in g["cases"]:
