@@ -37,8 +37,9 @@ UNIT = "simplices/s"
 # bytes each triangle's outputs take (vertices 12 + filt 4 + D_2 rows 12):
 # the fill kernel's algorithmic bytes per unit
 TRI_OUT_BYTES = 28
+TET_OUT_BYTES = 36    # 4 vertices + filt + 4 D_3 rows, u32 each
 # SURVEY 8(d) B_alg per unit for the whole path (sort-based accounting)
-SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44}
+SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44, "tet": 52}
 ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400}
 
 
@@ -106,13 +107,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def _ncu_traffic(workload: str):
-    """dram read+write bytes per fill launch from the committed ncu capture."""
+def _ncu_traffic(workload: str, kernel: str):
+    """dram read+write bytes per launch of the roofline kernel, from the
+    committed ncu capture (profiles/fill_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "fill_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        e = d.get(workload, {})
+        return e.get("dram_bytes_per_launch") if e.get("kernel", "k_triangles<fill>") == kernel else None
     except Exception:
         return None
 
@@ -219,7 +222,7 @@ def main():
     torch.cuda.synchronize()
 
     vrb.set_profiling(True)
-    step_ms, fill_ms, stage_acc = [], [], {}
+    step_ms, fill_ms, tet_ms, stage_acc = [], [], [], {}
     counts = None
     launches = 0
     s = torch.cuda.current_stream()
@@ -237,6 +240,7 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
             st = vrb.last_stage_ms()
             fill_ms.append(st["fill"])
+            tet_ms.append(st["tet_fill"])
             for k, v in st.items():
                 stage_acc[k] = stage_acc.get(k, 0.0) + v
             if counts is None:
@@ -265,23 +269,34 @@ def main():
     value = units_global * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
-    # roofline of the dominant kernel: the triangle fill (k_triangles<true>)
+    # roofline of the dominant kernel: the triangle fill (k_triangles<true>),
+    # or the tetrahedron fill when it takes longer (max dim 2)
     peak, peak_kind = _peaks()
     T_local = counts[2][2] if len(counts) > 2 else 0
+    Q_local = counts[3][2] if len(counts) > 3 else 0
     fill_avg = float(np.mean(fill_ms)) if fill_ms else 0.0
+    tet_avg = float(np.mean(tet_ms)) if tet_ms else 0.0
     roofline = None
-    if T_local and fill_avg > 0:
-        bytes_per_launch = TRI_OUT_BYTES * T_local
-        achieved = bytes_per_launch / (fill_avg / 1e3) / 1e9
-        traffic = _ncu_traffic(args.workload)
-        roofline = {"bound": "hbm", "kernel": "k_triangles<fill>", "achieved": achieved, "peak": peak,
+    if Q_local and tet_avg > fill_avg:
+        kname = "k_tets_dense<fill>" if X.shape[0] <= 16384 else "k_tets<fill>"
+        bytes_per_launch, kern_ms = TET_OUT_BYTES * Q_local, tet_avg
+    elif T_local and fill_avg > 0:
+        kname, bytes_per_launch, kern_ms = "k_triangles<fill>", TRI_OUT_BYTES * T_local, fill_avg
+    else:
+        kname = None
+    if kname:
+        achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
+        traffic = _ncu_traffic(args.workload, kname)
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
-                    "fill_ms": fill_avg, "share_of_step": fill_avg / (ms_per_step or 1.0)}
+                    "kernel_ms": kern_ms, "share_of_step": kern_ms / (ms_per_step or 1.0)}
     # whole-path fraction against SURVEY 8(d) B_alg
     E = counts[1][0]
     T = counts[2][0] if len(counts) > 2 else 0
-    balg = E * (SURVEY_BALG["edge_k2"] if w.maxdim >= 1 else SURVEY_BALG["edge_k1"]) + T * SURVEY_BALG["tri"]
+    Q = counts[3][0] if len(counts) > 3 else 0
+    balg = (E * (SURVEY_BALG["edge_k2"] if w.maxdim >= 1 else SURVEY_BALG["edge_k1"]) + T * SURVEY_BALG["tri"]
+            + Q * SURVEY_BALG["tet"])
     path_gbs = balg / (ms_per_step / 1e3) / 1e9
 
     # e2e: through the C-ABI host path: pinned host points -> H2D inside

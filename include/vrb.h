@@ -221,9 +221,15 @@ vrb_status vrb_gf2_free(vrb_gf2_handle h);
  * S3, [2] neighbourhood lists S4, [3] simplex count + offsets + output
  * allocation, [4] simplex fill kernel S5/S6+S8 alone, [5] tie-group sort S7,
  * [6] exchange (vrb_build_dist), [7] total.  Recorded only while profiling
- * is enabled (events add no synchronisation inside the build). */
+ * is enabled (events add no synchronisation inside the build).
+ * vrb_last_stage_ms_n(ms, n) writes the first n of the extended list, which
+ * appends [8] tetrahedron count (levels, count pass, offsets, allocation) and
+ * [9] the tetrahedron fill kernel S6/S8 alone; with maxdim >= 2 slot [4]
+ * holds the triangle fill only and [5] both tie-group sorts.  Entries past
+ * [9] are written as 0.  Errors: VRB_EINVAL for a NULL `ms` or n < 0. */
 vrb_status vrb_set_profiling(int32_t enable);
 vrb_status vrb_last_stage_ms(double* ms8);
+vrb_status vrb_last_stage_ms_n(double* ms, int32_t n);
 
 /* Number of kernels this library has launched in this process (monotonic;
  * the difference across a region is the number of launches inside it). */

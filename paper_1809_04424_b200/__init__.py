@@ -34,10 +34,12 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_launch_count", "vrb_h0", "vrb_build_dm",
+           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
+           "vrb_build_dm",
            "vrb_latlon2euc", "vrb_gf2_blockprodsum", "vrb_gf2_csc", "vrb_gf2_free")
 
-STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total")
+STAGES = ("distance", "edge_rank", "csr", "count", "fill", "tie_sort", "exchange", "total", "tet_count",
+          "tet_fill")
 
 
 class VrbError(RuntimeError):
@@ -103,6 +105,8 @@ def lib() -> ctypes.CDLL:
     L.vrb_set_profiling.argtypes = [i32]
     L.vrb_last_stage_ms.restype = ctypes.c_int
     L.vrb_last_stage_ms.argtypes = [P(ctypes.c_double)]
+    L.vrb_last_stage_ms_n.restype = ctypes.c_int
+    L.vrb_last_stage_ms_n.argtypes = [P(ctypes.c_double), ctypes.c_int32]
     L.vrb_launch_count.restype = ctypes.c_ulonglong
     L.vrb_launch_count.argtypes = []
     L.vrb_build_dm.restype = ctypes.c_int
@@ -173,8 +177,8 @@ def launch_count() -> int:
 
 
 def last_stage_ms() -> dict:
-    arr = (ctypes.c_double * 8)()
-    _check(lib().vrb_last_stage_ms(arr))
+    arr = (ctypes.c_double * len(STAGES))()
+    _check(lib().vrb_last_stage_ms_n(arr, len(STAGES)))
     return {k: float(v) for k, v in zip(STAGES, arr)}
 
 

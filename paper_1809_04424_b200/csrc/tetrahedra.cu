@@ -59,6 +59,7 @@ struct TetArgs {
     const uint64_t* toff;     // E + 1
     const uint64_t* tlo;      // E: start of the triangle range of p's level
     const uint64_t* thi;      // E: end of it
+    const uint2* span;        // E: (toff[p], #triangles of p | 0x80000000 when p shares its level)
     const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
     const ulonglong2* hslots;   // triangle lex code -> position: slot = (code, position), open addressing
     uint64_t hmask;
@@ -201,8 +202,9 @@ __device__ __forceinline__ uint64_t tri_code_sorted(uint32_t a, uint32_t b, uint
 // f (its largest edge position) and apex a (its vertex off f): when f is alone
 // at its filtration level, f's triangles sit at [toff[f], toff[f+1]) in apex
 // order, so its position is toff[f] + #apexes of f below a -- an 8-ary search
-// in the (L2-resident) apex array: 7 independent probes per round, then one
-// 8-entry scan, so ~3 dependent L2 round trips for the usual range of <= 64.
+// in the (L2-resident) apex array: 7 independent probes per round, then two
+// 16-byte reads, so ~3 dependent L2 round trips for the usual range of <= 64
+// (the span -- first triangle and count of f -- is one 8-byte read).
 // A tie level is lex-sorted as a whole: binary search by triple in tv.
 struct FaceQuery {
     uint32_t f, a, a0, a1, a2;
@@ -217,35 +219,45 @@ __device__ __forceinline__ FaceQuery face_query(uint32_t u, uint32_t v, uint32_t
     return q;
 }
 
-// #entries of apex[lo, hi) below a (ascending run)
-__device__ __forceinline__ uint64_t apex_rank(const uint16_t* __restrict__ apex, uint64_t lo, uint64_t hi, uint32_t a) {
+// #entries of apex[lo, hi) below a (ascending run), as a position: 8-ary
+// rounds of 7 independent probes until <= 8 entries are left; those lie in
+// two aligned 16-byte chunks of the apex array (padded by 16 entries), compared
+// 2 entries per SIMD instruction.
+__device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ apex, uint32_t lo, uint32_t hi,
+                                                uint32_t a) {
     while (hi - lo > 8) {
-        const uint64_t step = (hi - lo + 7) >> 3;
+        const uint32_t step = (hi - lo + 7) >> 3;
         uint32_t c = 0;
 #pragma unroll
         for (int i = 1; i < 8; ++i) {
-            const uint64_t q = lo + (uint64_t)i * step;
+            const uint32_t q = lo + (uint32_t)i * step;
             if (q < hi) c += __ldg(apex + q) < a ? 1u : 0u;
         }
-        // all probes before lo + c*step are below a; the answer is in [lo + c*step, lo + (c+1)*step)
-        const uint64_t nlo = lo + (uint64_t)c * step;
+        const uint32_t nlo = lo + c * step;
         hi = min(hi, nlo + step);
         lo = nlo;
     }
-    uint64_t r = lo;
+    const uint32_t base = lo & ~7u;
+    const uint4* pv = reinterpret_cast<const uint4*>(apex + base);
+    const uint4 c0 = __ldg(pv);
+    const uint4 c1 = hi - base > 8 ? __ldg(pv + 1) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    const uint32_t a2 = a * 0x10001u;
+    const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    uint32_t ltm = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (lo + i < hi && __ldg(apex + lo + i) < a) ++r;
-    return r;
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t lt = __vcmpltu2(w[i], a2);   // 0xFFFF per 16-bit lane below a
+        ltm |= ((lt & 1u) | ((lt >> 15) & 2u)) << (2 * i);
+    }
+    const uint32_t valid = ((1u << (hi - base)) - 1u) & ~((1u << (lo - base)) - 1u);
+    return lo + (uint32_t)__popc(ltm & valid);
 }
 
 __device__ __forceinline__ void face_pos2(const TetArgs& A, const FaceQuery& q1, const FaceQuery& q2, uint32_t& r1,
                                           uint32_t& r2) {
-    const uint64_t s1 = A.toff[q1.f], e1 = A.toff[q1.f + 1], s2 = A.toff[q2.f], e2 = A.toff[q2.f + 1];
-    const bool d1 = A.tlo[q1.f] == s1 && A.thi[q1.f] == e1;
-    const bool d2 = A.tlo[q2.f] == s2 && A.thi[q2.f] == e2;
-    r1 = d1 ? (uint32_t)apex_rank(A.apex, s1, e1, q1.a) : tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2);
-    r2 = d2 ? (uint32_t)apex_rank(A.apex, s2, e2, q2.a) : tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2);
+    const uint2 s1 = __ldg(A.span + q1.f), s2 = __ldg(A.span + q2.f);
+    r1 = (s1.y >> 31) ? tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2) : apex_rank_v(A.apex, s1.x, s1.x + s1.y, q1.a);
+    r2 = (s2.y >> 31) ? tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2) : apex_rank_v(A.apex, s2.x, s2.x + s2.y, q2.a);
 }
 
 __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
@@ -466,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                     slot = A.qoff[p] - A.slot0;
                     filt = A.efilt[p];
                     tbase = A.toff[p];
-                    direct = A.tlo[p] == tbase && A.thi[p] == A.toff[p + 1];   // p alone at its level
+                    direct = !(A.span[p].y >> 31);   // p alone at its level
                 }
                 uint32_t total = 0;
                 for (uint32_t ki = 0; ki + 1 < m; ++ki) {
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
                     slot = A.qoff[p] - A.slot0;
                     filt = A.efilt[p];
                     tbase = A.toff[p];
-                    direct = A.tlo[p] == tbase && A.thi[p] == A.toff[p + 1];
+                    direct = !(A.span[p].y >> 31);
                 }
                 const uint32_t npairs = m * (m - 1) / 2;
                 uint32_t total = 0;
@@ -684,14 +696,16 @@ __global__ void k_dense_positions(const uint32_t* __restrict__ ev, int64_t E, in
 }
 
 __global__ void k_level_ranges(const uint32_t* __restrict__ efilt, const uint64_t* __restrict__ toff, int64_t E,
-                               uint64_t* __restrict__ tlo, uint64_t* __restrict__ thi) {
+                               uint64_t* __restrict__ tlo, uint64_t* __restrict__ thi, uint2* __restrict__ span) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
         if (p > 0 && efilt[p - 1] == efilt[p]) continue;   // not a level start
         int64_t q = p + 1;
         while (q < E && efilt[q] == efilt[p]) ++q;
+        const uint32_t shared = q - p > 1 ? 0x80000000u : 0u;
         for (int64_t r = p; r < q; ++r) {
             tlo[r] = toff[p];
             thi[r] = toff[q];
+            span[r] = make_uint2((uint32_t)toff[r], (uint32_t)(toff[r + 1] - toff[r]) | shared);
         }
     }
 }
@@ -808,6 +822,7 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.toff = L.toff;
     A.tlo = L.tlo.get();
     A.thi = L.thi.get();
+    A.span = L.span.get();
     A.tv = L.tv;
     A.hslots = L.hslots.get();
     A.apex = L.apex;
@@ -824,9 +839,10 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
     L.tv = tv;
     L.tlo.alloc(E, s);
     L.thi.alloc(E, s);
+    L.span.alloc(E, s);
     if (E == 0) return;
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
-    k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get());
+    k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get(), L.span.get());
     VRB_LAUNCH_CHECK();
     if (L.apex) {   // face positions by owner-edge search (face_pos2)
         if (L.n <= kDenseMaxN) {   // pair tests through an n x n table of edge positions

@@ -15,7 +15,7 @@ namespace vrb {
 // errors
 // ---------------------------------------------------------------------------
 static thread_local std::string t_last_error;
-static thread_local double t_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+static thread_local double t_stage_ms[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 static bool g_profiling = false;
 
 void fail(vrb_status st, const char* fmt, ...) {
@@ -126,11 +126,12 @@ void StageTimer::mark(int stage) {
 void StageTimer::finish() {
     if (!on || marks.empty()) return;
     VRB_CUDA(cudaEventSynchronize(marks.back().second));
-    for (int q = 0; q < 8; ++q) t_stage_ms[q] = 0.0;
+    for (int q = 0; q < 10; ++q) t_stage_ms[q] = 0.0;
     for (size_t q = 1; q < marks.size(); ++q) {
         float ms = 0.f;
         VRB_CUDA(cudaEventElapsedTime(&ms, marks[q - 1].second, marks[q].second));
-        if (marks[q].first >= 0 && marks[q].first < 7) t_stage_ms[marks[q].first] += ms;
+        const int st = marks[q].first;
+        if (st >= 0 && st < 10 && st != 7) t_stage_ms[st] += ms;
     }
     float tot = 0.f;
     VRB_CUDA(cudaEventElapsedTime(&tot, marks.front().second, marks.back().second));
@@ -391,7 +392,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * Tl, s);
             // apex of every triangle (tetrahedra: face positions by owner-edge search)
             DBuf<uint16_t> tapex;
-            if (h->K >= 3 && n <= 65536) tapex.alloc((size_t)Tl, s);
+            if (h->K >= 3 && n <= 65536) tapex.alloc((size_t)Tl + 16, s);   // padded: 16-byte reads past the end
             timer.mark(3);
             fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s, bm.get(),
                            bmoff.get());
@@ -410,6 +411,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
                 L.n = n;
                 triangle_levels(efilt, toff.get(), E, tv, s, L);
                 DBuf<uint32_t> qc(E, s);
+                timer.mark(3);
                 count_tets(g, L, qc.get(), rank, world, s);
                 if (world > 1) {
                     DBuf<uint32_t> all((size_t)E * world, s);
@@ -433,9 +435,11 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
                 h->verts[3] = h->own<uint32_t>(4 * Ql, s);
                 h->filt[3] = h->own<uint32_t>(Ql, s);
                 if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[3] = h->own<uint32_t>(4 * Ql, s);
+                timer.mark(8);
                 fill_tets(g, L, efilt, qoff.get(), qb[0], qb[1], q0, h->verts[3], h->filt[3], h->rows[3], s);
+                timer.mark(9);
                 sort_tie_groups(3, efilt, qoff.get(), E, qb[0], qb[1], n, h->verts[3], h->rows[3], s);
-                timer.mark(4);
+                timer.mark(5);
                 // triangles: this rank reports its slice of the (replicated) dimension 2
                 if (world > 1) {
                     int64_t tp[2] = {0, E};
@@ -711,6 +715,14 @@ vrb_status vrb_last_stage_ms(double* ms8) {
     return guarded([&] {
         if (!ms8) fail(VRB_EINVAL, "NULL output");
         for (int q = 0; q < 8; ++q) ms8[q] = vrb::t_stage_ms[q];
+    });
+}
+
+vrb_status vrb_last_stage_ms_n(double* ms, int32_t n) {
+    return guarded([&] {
+        if (!ms || n < 0) fail(VRB_EINVAL, "NULL output or negative count");
+        for (int q = 0; q < n && q < 10; ++q) ms[q] = vrb::t_stage_ms[q];
+        for (int q = 10; q < n; ++q) ms[q] = 0.0;
     });
 }
 
