@@ -59,7 +59,7 @@ struct TetArgs {
     const uint64_t* toff;     // E + 1
     const uint64_t* tlo;      // E: start of the triangle range of p's level
     const uint64_t* thi;      // E: end of it
-    const uint2* span;        // E: (toff[p], #triangles of p | 0x80000000 when p shares its level)
+    const uint4* frec;        // 2E: 32-byte face record per owner edge (k_level_ranges)
     const uint32_t* tv;       // 3T (dimension-2 vertices, global order)
     const ulonglong2* hslots;   // triangle lex code -> position: slot = (code, position), open addressing
     uint64_t hmask;
@@ -202,9 +202,11 @@ __device__ __forceinline__ uint64_t tri_code_sorted(uint32_t a, uint32_t b, uint
 // f (its largest edge position) and apex a (its vertex off f): when f is alone
 // at its filtration level, f's triangles sit at [toff[f], toff[f+1]) in apex
 // order, so its position is toff[f] + #apexes of f below a -- an 8-ary search
-// in the (L2-resident) apex array: 7 independent probes per round, then two
-// 16-byte reads, so ~3 dependent L2 round trips for the usual range of <= 64
-// (the span -- first triangle and count of f -- is one 8-byte read).
+// in the (L2-resident) apex array.  One 32-byte record per owner edge (one
+// sector) holds toff[f], the count and 12 separators (every b-th apex,
+// b = ceil(count / 13)); it selects the block of <= b entries that holds a,
+// which two 16-byte reads finish for counts <= 104: two dependent L2 round
+// trips per face.
 // A tie level is lex-sorted as a whole: binary search by triple in tv.
 struct FaceQuery {
     uint32_t f, a, a0, a1, a2;
@@ -221,10 +223,11 @@ __device__ __forceinline__ FaceQuery face_query(uint32_t u, uint32_t v, uint32_t
 
 // #entries of apex[lo, hi) below a (ascending run), as a position: 8-ary
 // rounds of 7 independent probes until <= 8 entries are left; those lie in
-// two aligned 16-byte chunks of the apex array (padded by 16 entries), compared
-// 2 entries per SIMD instruction.
+// two aligned 16-byte chunks of the apex array (padded by 16 entries),
+// compared 2 entries per 32-bit add when ids < 0x7FFF (bit 15 of each half of
+// w + 0x8000 - a is set iff that entry >= a).
 __device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ apex, uint32_t lo, uint32_t hi,
-                                                uint32_t a) {
+                                                uint32_t a, bool small_ids) {
     while (hi - lo > 8) {
         const uint32_t step = (hi - lo + 7) >> 3;
         uint32_t c = 0;
@@ -241,23 +244,53 @@ __device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ ape
     const uint4* pv = reinterpret_cast<const uint4*>(apex + base);
     const uint4 c0 = __ldg(pv);
     const uint4 c1 = hi - base > 8 ? __ldg(pv + 1) : make_uint4(~0u, ~0u, ~0u, ~0u);
-    const uint32_t a2 = a * 0x10001u;
     const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     uint32_t ltm = 0;
+    if (small_ids) {
+        const uint32_t K = 0x80008000u - a * 0x10001u;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t lt = __vcmpltu2(w[i], a2);   // 0xFFFF per 16-bit lane below a
-        ltm |= ((lt & 1u) | ((lt >> 15) & 2u)) << (2 * i);
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t lt = ~(w[i] + K);   // bit 15 / 31: low / high entry < a
+            ltm |= ((lt >> 15) & 1u) << (2 * i) | (lt >> 31) << (2 * i + 1);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t lt = __vcmpltu2(w[i], a * 0x10001u);   // 0xFFFF per 16-bit lane below a
+            ltm |= ((lt & 1u) | ((lt >> 15) & 2u)) << (2 * i);
+        }
     }
     const uint32_t valid = ((1u << (hi - base)) - 1u) & ~((1u << (lo - base)) - 1u);
     return lo + (uint32_t)__popc(ltm & valid);
 }
 
+// position of the triangle with owner edge f and apex a (sorted vertices
+// a0 < a1 < a2, for the tie-level fallback)
+__device__ __forceinline__ uint32_t face_pos(const TetArgs& A, const FaceQuery& q) {
+    const uint4 r0 = __ldg(A.frec + 2 * (uint64_t)q.f), r1 = __ldg(A.frec + 2 * (uint64_t)q.f + 1);
+    if (r0.y >> 31) return tri_pos(A, q.f, q.a0, q.a1, q.a2);
+    const uint32_t start = r0.x, len = r0.y;
+    const uint32_t b = max(1u, (len + 12) / 13);
+    const bool small_ids = A.n < 0x7FFF;
+    const uint32_t sw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t c = 0;
+    if (small_ids) {   // separators past the end are 0x7FFF > a
+        const uint32_t K = 0x80008000u - (q.a + 1) * 0x10001u;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) c += __popc(~(sw[i] + K) & 0x80008000u);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 12; ++i)
+            c += ((uint32_t)(i + 1) * b < len && ((sw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu) <= q.a) ? 1u : 0u;
+    }
+    const uint32_t lo = start + c * b;
+    return apex_rank_v(A.apex, lo, min(lo + b, start + len), q.a, small_ids);
+}
+
 __device__ __forceinline__ void face_pos2(const TetArgs& A, const FaceQuery& q1, const FaceQuery& q2, uint32_t& r1,
                                           uint32_t& r2) {
-    const uint2 s1 = __ldg(A.span + q1.f), s2 = __ldg(A.span + q2.f);
-    r1 = (s1.y >> 31) ? tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2) : apex_rank_v(A.apex, s1.x, s1.x + s1.y, q1.a);
-    r2 = (s2.y >> 31) ? tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2) : apex_rank_v(A.apex, s2.x, s2.x + s2.y, q2.a);
+    r1 = face_pos(A, q1);
+    r2 = face_pos(A, q2);
 }
 
 __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
@@ -478,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                     slot = A.qoff[p] - A.slot0;
                     filt = A.efilt[p];
                     tbase = A.toff[p];
-                    direct = !(A.span[p].y >> 31);   // p alone at its level
+                    direct = !(A.frec[2 * (uint64_t)p].y >> 31);   // p alone at its level
                 }
                 uint32_t total = 0;
                 for (uint32_t ki = 0; ki + 1 < m; ++ki) {
@@ -635,7 +668,7 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
                     slot = A.qoff[p] - A.slot0;
                     filt = A.efilt[p];
                     tbase = A.toff[p];
-                    direct = !(A.span[p].y >> 31);
+                    direct = !(A.frec[2 * (uint64_t)p].y >> 31);
                 }
                 const uint32_t npairs = m * (m - 1) / 2;
                 uint32_t total = 0;
@@ -695,8 +728,11 @@ __global__ void k_dense_positions(const uint32_t* __restrict__ ev, int64_t E, in
     }
 }
 
+// tlo / thi: the triangle range of each edge's filtration level; frec: the
+// face record of each owner edge (see face_pos)
 __global__ void k_level_ranges(const uint32_t* __restrict__ efilt, const uint64_t* __restrict__ toff, int64_t E,
-                               uint64_t* __restrict__ tlo, uint64_t* __restrict__ thi, uint2* __restrict__ span) {
+                               const uint16_t* __restrict__ apex, uint32_t sentinel, uint64_t* __restrict__ tlo,
+                               uint64_t* __restrict__ thi, uint4* __restrict__ frec) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
         if (p > 0 && efilt[p - 1] == efilt[p]) continue;   // not a level start
         int64_t q = p + 1;
@@ -705,7 +741,17 @@ __global__ void k_level_ranges(const uint32_t* __restrict__ efilt, const uint64_
         for (int64_t r = p; r < q; ++r) {
             tlo[r] = toff[p];
             thi[r] = toff[q];
-            span[r] = make_uint2((uint32_t)toff[r], (uint32_t)(toff[r + 1] - toff[r]) | shared);
+            const uint32_t start = (uint32_t)toff[r], len = (uint32_t)(toff[r + 1] - toff[r]);
+            const uint32_t b = max(1u, (len + 12) / 13);
+            uint32_t sep[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i) {
+                const uint32_t o = (uint32_t)(i + 1) * b;
+                sep[i] = (apex && o < len) ? (uint32_t)apex[start + o] : sentinel;
+            }
+            frec[2 * r] = make_uint4(start, len | shared, sep[0] | sep[1] << 16, sep[2] | sep[3] << 16);
+            frec[2 * r + 1] = make_uint4(sep[4] | sep[5] << 16, sep[6] | sep[7] << 16, sep[8] | sep[9] << 16,
+                                         sep[10] | sep[11] << 16);
         }
     }
 }
@@ -822,7 +868,7 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.toff = L.toff;
     A.tlo = L.tlo.get();
     A.thi = L.thi.get();
-    A.span = L.span.get();
+    A.frec = L.frec.get();
     A.tv = L.tv;
     A.hslots = L.hslots.get();
     A.apex = L.apex;
@@ -839,10 +885,11 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
     L.tv = tv;
     L.tlo.alloc(E, s);
     L.thi.alloc(E, s);
-    L.span.alloc(E, s);
+    L.frec.alloc(2 * E, s);
     if (E == 0) return;
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);
-    k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.tlo.get(), L.thi.get(), L.span.get());
+    k_level_ranges<<<g, 256, 0, s>>>(efilt, toff, E, L.apex, L.n < 0x7FFF ? 0x7FFFu : 0xFFFFu, L.tlo.get(),
+                                     L.thi.get(), L.frec.get());
     VRB_LAUNCH_CHECK();
     if (L.apex) {   // face positions by owner-edge search (face_pos2)
         if (L.n <= kDenseMaxN) {   // pair tests through an n x n table of edge positions

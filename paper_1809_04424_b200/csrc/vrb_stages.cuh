@@ -96,7 +96,8 @@ struct TriLevels {
     int64_t n = 0;
     DBuf<uint32_t> dense;             // n x n edge positions (n <= 16384 with apex), NONE32 = no edge
     DBuf<uint64_t> tlo, thi;          // E: triangle range of each edge's filtration level
-    DBuf<uint2> span;                 // E: (first triangle, count | 0x80000000 if the level is shared)
+    DBuf<uint4> frec;                 // 2E: face record per owner edge (first triangle, count | shared flag,
+                                      // 12 apex separators)
     DBuf<ulonglong2> hslots;          // (triangle lex code, position), open addressing
     uint64_t hmask = 0;
 };

@@ -123,6 +123,19 @@ def test_wide_list_layout_tetrahedra(vrb, seed, monkeypatch):
     compare(vrb, X, 2, [0.6, 1.5][seed % 2])
 
 
+def test_long_apex_runs_tetrahedra(vrb):
+    # full filtration of 120 points: owner edges with > 104 triangles, so the
+    # face search goes through its 8-ary rounds after the 12-separator record
+    compare(vrb, workloads.random_cloud(77, 120, 3, "uniform"), 2, math.inf)
+
+
+@pytest.mark.parametrize("n,seed", [(20000, 79), (33000, 78)])
+def test_sparse_tetrahedra_large_n(vrb, n, seed):
+    # n > 16384: the list-based tetrahedron kernel (no dense table); n > 0x7FFF:
+    # vertex ids above 15 bits take the scalar separator / apex comparisons
+    compare(vrb, workloads.random_cloud(seed, n, 3, "uniform"), 2, 0.045 * (33000 / n) ** (1 / 3))
+
+
 @pytest.mark.parametrize("n", [0, 1, 2, 3])
 def test_tiny(vrb, n):
     compare(vrb, workloads.random_cloud(n, n, 2), 1, math.inf)
