@@ -672,12 +672,23 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
                 }
                 const uint32_t npairs = m * (m - 1) / 2;
                 uint32_t total = 0;
+                // the table read of the next warp step is issued before this
+                // step's faces are searched (two L2 round trips overlap)
+                uint32_t i_n = 0, j_n = 0, pkl_n = NONE32;
+                if ((uint32_t)lane < npairs) {
+                    pair_of(lane, m, i_n, j_n);
+                    pkl_n = __ldg(A.dense + (uint64_t)W->Sk[i_n] * n + W->Sk[j_n]);
+                }
                 for (uint32_t q0 = 0; q0 < npairs; q0 += 32) {
-                    const uint32_t q = q0 + lane;
-                    uint32_t i = 0, j = 0, pkl = NONE32;
-                    if (q < npairs) {
-                        pair_of(q, m, i, j);
-                        pkl = __ldg(A.dense + (uint64_t)W->Sk[i] * n + W->Sk[j]);
+                    const uint32_t i = i_n, j = j_n, pkl = pkl_n;
+                    {
+                        const uint32_t qn = q0 + 32 + lane;
+                        pkl_n = NONE32;
+                        if (qn < npairs) {   // advance 32 pairs in row-major order
+                            j_n += 32;
+                            while (j_n >= m) { ++i_n; j_n = j_n - m + i_n + 1; }
+                            pkl_n = __ldg(A.dense + (uint64_t)W->Sk[i_n] * n + W->Sk[j_n]);
+                        }
                     }
                     const bool valid = pkl < p;
                     const uint32_t bal = __ballot_sync(0xffffffffu, valid);
