@@ -308,9 +308,11 @@ __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong
 
 // Warp: S(p) sorted by id into W->Sk / W->Spx, flags S in the vertex bitmap.
 // Returns |S| (may exceed kS: caller checks).
-__device__ uint32_t build_S(const TetArgs& A, const uint32_t* __restrict__ map, TetScratch* __restrict__ W,
+template <int kB, class Scratch>
+__device__ uint32_t build_S(const TetArgs& A, const uint32_t* __restrict__ map, Scratch* __restrict__ W,
                            uint32_t* __restrict__ vbits, uint32_t p, uint32_t x, uint32_t len, uint64_t offx,
                            uint32_t degx) {
+    constexpr int kBits = kB, kWords = kB / 32;
     const int lane = threadIdx.x & 31;
     const uint32_t* lk = A.nkr + offx;
     const uint32_t* lr = A.nr + offx;
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                 if (len < 2) continue;
                 if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
                 const uint64_t offx = A.off[x];
-                const uint32_t m = build_S(A, map, W, vbits, p, x, len, offx, pl.w);
+                const uint32_t m = build_S<kBits>(A, map, W, vbits, p, x, len, offx, pl.w);
                 if (m > (uint32_t)kS) {
                     if (lane == 0) atomicOr(A.overflow, 1u);
                     clear_S(W, vbits, kS);
@@ -582,9 +584,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
 // prefix popcount place each tetrahedron, so emission is in lex order and
 // the stores of a step are contiguous.
 // ---------------------------------------------------------------------------
+constexpr int kBitsD = 1024;   // ranks of x's id list per build_S round (dense path)
 struct TetScratchD {
-    uint32_t bits[kWords];
-    uint32_t wpre[kWords];
+    uint32_t bits[kBitsD / 32];
+    uint32_t wpre[kBitsD / 32];
     uint32_t Sk[kS];          // S sorted by id
     uint32_t Spx[kS];         // pos(x, k)
 };
@@ -610,7 +613,6 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
     const uint32_t lt = (1u << lane) - 1u;
     const int nthreads = blockDim.x;
     TetScratchD* W = reinterpret_cast<TetScratchD*>(smem + map_b) + wid;
-    TetScratch* WS = reinterpret_cast<TetScratch*>(W);   // build_S uses the bits/wpre/Sk/Spx prefix
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
     __shared__ unsigned s_next;
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
                 const uint32_t p = pl.x, x = pl.y, len = pl.z;
                 if (len < 2) continue;
                 if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
-                const uint32_t m = build_S(A, map, WS, nullptr, p, x, len, A.off[x], pl.w);
+                const uint32_t m = build_S<kBitsD>(A, map, W, nullptr, p, x, len, A.off[x], pl.w);
                 if (m > (uint32_t)kS) {
                     if (lane == 0) atomicOr(A.overflow, 1u);
                     continue;
@@ -783,6 +785,9 @@ int tet_warps(int64_t n) {
 #ifndef VRB_TET_CTA_WARPS
 #define VRB_TET_CTA_WARPS 8
 #endif
+#ifndef VRB_TET_DENSE_CTAS
+#define VRB_TET_DENSE_CTAS 3
+#endif
 // dense path: CTAs of up to VRB_TET_CTA_WARPS warps; two per SM when the map
 // is small (shorter per-host barrier tails: hosts own ~E/n edges each)
 int tet_dense_warps(int64_t n) {
@@ -812,11 +817,21 @@ void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cuda
         VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
         A.task_counter = counter.get();
         A.overflow = overflow.get();
+        // fill: at most VRB_TET_DENSE_CTAS CTAs per SM, the rest of the
+        // unified on-chip memory left to L1 (the face searches live on L1
+        // hits; 4 CTAs: 14.4 ms, 3: 11.1 ms on C4); the count takes 4
+        const int cap = fill ? VRB_TET_DENSE_CTAS : 4;
+        const int carve = (int)std::min<int64_t>(
+            100, (int64_t)ceil_div((int64_t)cap * (int64_t)(smem + 1024) * 100, (int64_t)228 * 1024));
         int per_sm = 1;
-        if (fill)
+        if (fill) {
+            VRB_CUDA(cudaFuncSetAttribute(k_tets_dense<true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
             VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tets_dense<true>, warps * 32, smem));
-        else
+        } else {
+            VRB_CUDA(cudaFuncSetAttribute(k_tets_dense<false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
             VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tets_dense<false>, warps * 32, smem));
+        }
+        per_sm = std::min(per_sm, cap);
         const unsigned grid =
             (unsigned)std::min<int64_t>((int64_t)device_sm_count() * std::max(1, per_sm), A.task_hi - A.task_lo);
         if (fill)
