@@ -18,8 +18,13 @@
 // hook along those edges (the larger root of a mutual pair yields), and
 // pointer jumping flattens the forest.  O(log n) rounds, each a streaming
 // pass over the edges that still cross components (compacted every round).
-// The forest's edges, flagged per position, are compacted in position order:
-// they are the D_1 pivot columns (the "clearing" set of P:302), and
+// Filter first: the rounds run on the position prefix [0, P) alone (P = 8n):
+// that is Kruskal's state after P edges.  Then windows [w, 4w) in turn keep
+// only their edges that still join two components, and the rounds continue on
+// those; a spanning tree (n - 1 forest edges) ends the search early.  The
+// union is the same unique forest (positions are distinct weights).
+// The forest's edges, appended as they join and radix-sorted by position,
+// are the D_1 pivot columns (the "clearing" set of P:302), and
 // filt(e) over them is the sorted list of finite H0 deaths.
 #include <algorithm>
 
@@ -43,7 +48,7 @@ __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) { GRID_STRIDE(i, n) 
 __global__ void k_best(const uint2* __restrict__ ev, const uint32_t* __restrict__ act, int64_t na,
                        const uint32_t* __restrict__ comp, uint32_t* best) {
     GRID_STRIDE(q, na) {
-        const uint32_t e = act ? act[q] : (uint32_t)q;
+        const uint32_t e = act ? act[q] : (uint32_t)q;   // act == null: the prefix [0, na)
         const uint2 uv = ev[e];
         const uint32_t cu = comp[uv.x], cv = comp[uv.y];
         if (cu != cv) {
@@ -57,9 +62,11 @@ __global__ void k_best(const uint2* __restrict__ ev, const uint32_t* __restrict_
 
 // root c hooks to the component across its lightest edge; of a mutual pair
 // (both roots chose the same edge) the larger root hooks to the smaller
+// (root c hooks: its edge joins the forest, appended once -- of a mutual
+// pair only the hooking root appends)
 __global__ void k_hook(const uint2* __restrict__ ev, int64_t n, const uint32_t* __restrict__ comp,
-                       const uint32_t* __restrict__ best, uint32_t* __restrict__ hook, uint8_t* __restrict__ in_forest,
-                       int* __restrict__ changed) {
+                       const uint32_t* __restrict__ best, uint32_t* __restrict__ hook, uint32_t* __restrict__ forest,
+                       unsigned long long* __restrict__ nforest, int* __restrict__ changed) {
     GRID_STRIDE(c, n) {
         hook[c] = comp[c];
         if (comp[c] != (uint32_t)c) continue;
@@ -68,10 +75,10 @@ __global__ void k_hook(const uint2* __restrict__ ev, int64_t n, const uint32_t* 
         const uint2 uv = ev[e];
         const uint32_t cu = comp[uv.x], cv = comp[uv.y];
         const uint32_t other = cu == (uint32_t)c ? cv : cu;
-        in_forest[e] = 1;
         *changed = 1;
         if (best[other] == e && other > (uint32_t)c) continue;   // mutual: the smaller root stays
         hook[c] = other;
+        forest[atomicAdd(nforest, 1ull)] = e;
     }
 }
 
@@ -98,19 +105,39 @@ __global__ void k_compact(const uint32_t* __restrict__ act, int64_t na, const ui
     GRID_STRIDE(q, na) if (flag[q]) out[pre[q]] = act ? act[q] : (uint32_t)q;
 }
 
-__global__ void k_forest_flags(const uint8_t* __restrict__ in_forest, int64_t E, uint32_t* __restrict__ flag) {
-    GRID_STRIDE(e, E) flag[e] = in_forest[e];
+// edges of [e0, E) whose endpoints lie in different components: counted
+// (kFill = false) or appended in any order (the rounds do not depend on it)
+template <bool kFill>
+__global__ void k_tail_cross(const uint2* __restrict__ ev, int64_t e0, int64_t E, const uint32_t* __restrict__ comp,
+                             unsigned long long* __restrict__ count, uint32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = e0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q - lane < E; q += stride) {
+        bool x = false;
+        if (q < E) {
+            const uint2 uv = ev[q];
+            x = comp[uv.x] != comp[uv.y];
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, x);
+        if (!b) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (kFill && x) out[base + __popc(b & ((1u << lane) - 1u))] = (uint32_t)q;
+    }
 }
 
-__global__ void k_forest_out(const uint32_t* __restrict__ flag, const uint64_t* __restrict__ pre, int64_t E,
-                             const uint32_t* __restrict__ efilt, uint32_t* __restrict__ pos,
-                             uint32_t* __restrict__ death) {
-    GRID_STRIDE(e, E) {
-        if (flag[e]) {
-            pos[pre[e]] = (uint32_t)e;
-            death[pre[e]] = efilt[e];
-        }
+__global__ void k_forest_out(const uint64_t* __restrict__ sorted, int64_t nf, const uint32_t* __restrict__ efilt,
+                             uint32_t* __restrict__ pos, uint32_t* __restrict__ death) {
+    GRID_STRIDE(i, nf) {
+        const uint32_t e = (uint32_t)sorted[i];
+        pos[i] = e;
+        death[i] = efilt[e];
     }
+}
+
+__global__ void k_widen(const uint32_t* __restrict__ a, int64_t n, uint64_t* __restrict__ b) {
+    GRID_STRIDE(i, n) b[i] = a[i];
 }
 
 }  // namespace
@@ -120,21 +147,51 @@ int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t 
     *pos_out = *death_out = nullptr;
     if (n == 0 || E == 0) return 0;
     const uint2* ev2 = reinterpret_cast<const uint2*>(ev);
-    DBuf<uint32_t> comp(n, s), hook(n, s), best(n, s);
-    DBuf<uint8_t> in_forest(E, s);
+    DBuf<uint32_t> comp(n, s), hook(n, s), best(n, s), forest(n, s);
+    DBuf<unsigned long long> nforest(1, s);
     DBuf<int> changed(1, s);
     k_iota<<<grid_for(n), 256, 0, s>>>(comp.get(), n);
     VRB_LAUNCH_CHECK();
-    VRB_CUDA(cudaMemsetAsync(in_forest.get(), 0, in_forest.bytes(), s));
-    DBuf<uint32_t> act, act_next, flag(E, s);
-    DBuf<uint64_t> pre(E + 1, s);
-    int64_t na = E;   // active (crossing) edges; the first round takes all positions
-    for (int round = 0; round < 64 && na > 0; ++round) {
+    VRB_CUDA(cudaMemsetAsync(nforest.get(), 0, sizeof(unsigned long long), s));
+    const int64_t P = std::min<int64_t>(E, 8 * n);   // the prefix the first rounds run on
+    DBuf<uint32_t> act, act_next, flag(P, s);
+    DBuf<uint64_t> pre(P + 1, s);
+    int64_t na = P;   // active (crossing) edges; the first rounds take the prefix positions
+    int64_t w1 = P;   // end of the windows processed so far
+    for (int round = 0; round < 4096; ++round) {
+        while (na == 0) {
+            // the windows so far have converged: a spanning tree ends the search;
+            // else the next window [w1, 4 w1) keeps its edges that still cross
+            unsigned long long nf = 0;
+            VRB_CUDA(cudaMemcpyAsync(&nf, nforest.get(), sizeof(nf), cudaMemcpyDeviceToHost, s));
+            VRB_CUDA(cudaStreamSynchronize(s));
+            if ((int64_t)nf == n - 1 || w1 == E) break;
+            const int64_t w0 = w1;
+            w1 = std::min<int64_t>(E, 4 * w1);
+            DBuf<unsigned long long> cnt(1, s);
+            VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+            k_tail_cross<false><<<grid_for(w1 - w0), 256, 0, s>>>(ev2, w0, w1, comp.get(), cnt.get(), nullptr);
+            VRB_LAUNCH_CHECK();
+            unsigned long long nt = 0;
+            VRB_CUDA(cudaMemcpyAsync(&nt, cnt.get(), sizeof(nt), cudaMemcpyDeviceToHost, s));
+            VRB_CUDA(cudaStreamSynchronize(s));
+            if (nt == 0) continue;
+            act.alloc((int64_t)nt, s);
+            VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+            k_tail_cross<true><<<grid_for(w1 - w0), 256, 0, s>>>(ev2, w0, w1, comp.get(), cnt.get(), act.get());
+            VRB_LAUNCH_CHECK();
+            na = (int64_t)nt;
+            if ((size_t)na > flag.size()) {
+                flag.alloc(na, s);
+                pre.alloc(na + 1, s);
+            }
+        }
+        if (na == 0) break;
         VRB_CUDA(cudaMemsetAsync(best.get(), 0xFF, best.bytes(), s));
         VRB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int), s));
         k_best<<<grid_for(na), 256, 0, s>>>(ev2, act.get(), na, comp.get(), best.get());
         VRB_LAUNCH_CHECK();
-        k_hook<<<grid_for(n), 256, 0, s>>>(ev2, n, comp.get(), best.get(), hook.get(), in_forest.get(),
+        k_hook<<<grid_for(n), 256, 0, s>>>(ev2, n, comp.get(), best.get(), hook.get(), forest.get(), nforest.get(),
                                            changed.get());
         VRB_LAUNCH_CHECK();
         k_jump<<<grid_for(n), 256, 0, s>>>(hook.get(), n, comp.get());
@@ -148,7 +205,7 @@ int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t 
         uint64_t nn = 0;
         VRB_CUDA(cudaMemcpyAsync(&nn, pre.get() + na, sizeof(nn), cudaMemcpyDeviceToHost, s));
         VRB_CUDA(cudaStreamSynchronize(s));
-        if (!h) break;
+        if (!h) nn = 0;   // no component has an outgoing edge left in this set
         if ((int64_t)nn > 0) {
             act_next.alloc(nn, s);
             k_compact<<<grid_for(na), 256, 0, s>>>(act.get(), na, flag.get(), pre.get(), act_next.get());
@@ -157,17 +214,23 @@ int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t 
         act = std::move(act_next);
         na = (int64_t)nn;
     }
-    // forest edges in position order
-    k_forest_flags<<<grid_for(E), 256, 0, s>>>(in_forest.get(), E, flag.get());
-    VRB_LAUNCH_CHECK();
-    exclusive_scan(flag.get(), pre.get(), E, s);
-    uint64_t nf = 0;
-    VRB_CUDA(cudaMemcpyAsync(&nf, pre.get() + E, sizeof(nf), cudaMemcpyDeviceToHost, s));
+    // forest edges in position order (<= n - 1 of them)
+    unsigned long long nf = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nf, nforest.get(), sizeof(nf), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     if (nf) {
+        DBuf<uint64_t> k0(nf, s), k1(nf, s);
+        DBuf<uint32_t> v0(nf, s), v1(nf, s);
+        k_widen<<<grid_for((int64_t)nf), 256, 0, s>>>(forest.get(), (int64_t)nf, k0.get());
+        VRB_LAUNCH_CHECK();
+        uint64_t vary = 0;
+        for (int64_t b = 1; b <= E; b <<= 1) vary |= (uint64_t)b;   // positions < 2^ceil(log2(E + 1))
+        iota_u32(v0.get(), (int64_t)nf, s);
+        const bool alt = radix_sort_pairs(k0.get(), k1.get(), v0.get(), v1.get(), (int64_t)nf, vary, s);
         *pos_out = alloc_out((int64_t)nf, ctx);
         *death_out = alloc_out((int64_t)nf, ctx);
-        k_forest_out<<<grid_for(E), 256, 0, s>>>(flag.get(), pre.get(), E, efilt, *pos_out, *death_out);
+        k_forest_out<<<grid_for((int64_t)nf), 256, 0, s>>>(alt ? k1.get() : k0.get(), (int64_t)nf, efilt, *pos_out,
+                                                           *death_out);
         VRB_LAUNCH_CHECK();
     }
     return (int64_t)nf;
