@@ -28,6 +28,10 @@ constexpr int kWarps = kThreads / 32;
 #ifndef VRB_SORT_MINB
 #define VRB_SORT_MINB 4
 #endif
+#ifndef VRB_SORT_LOOK
+#define VRB_SORT_LOOK 4
+#endif
+constexpr int kLook = VRB_SORT_LOOK;         // tiles read per look-back step
 constexpr int kItems = VRB_SORT_ITEMS;       // per thread
 constexpr int kTile = kThreads * kItems;     // 3072 items per tile
 constexpr int kWarpItems = 32 * kItems;      // contiguous items per warp
@@ -141,12 +145,24 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
         atomicExch(st, kFlagPre | cnt);
     } else {
         atomicExch(st, kFlagAgg | cnt);
-        for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
-            const volatile unsigned long long* sp = status + j * kBins + d;
-            unsigned long long s;
-            do { s = *sp; } while ((s & (kFlagAgg | kFlagPre)) == 0);
-            excl += s & kValMask;
-            if (s & kFlagPre) break;
+        // look back kLook tiles per step: their status words are read
+        // together, so a walk over aggregate-only tiles is not a chain of
+        // single dependent L2 reads
+        bool done = false;
+        for (int64_t j = (int64_t)tile - 1; !done; j -= kLook) {
+            unsigned long long sv[kLook];
+#pragma unroll
+            for (int u = 0; u < kLook; ++u)
+                sv[u] = j - u >= 0 ? *(const volatile unsigned long long*)(status + (j - u) * kBins + d) : kFlagPre;
+#pragma unroll
+            for (int u = 0; u < kLook; ++u) {
+                if (done) break;
+                unsigned long long s = sv[u];
+                while ((s & (kFlagAgg | kFlagPre)) == 0)
+                    s = *(const volatile unsigned long long*)(status + (j - u) * kBins + d);
+                excl += s & kValMask;
+                if (s & kFlagPre) done = true;
+            }
         }
         atomicExch(st, kFlagPre | (excl + cnt));
     }
