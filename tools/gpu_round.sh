@@ -23,4 +23,7 @@ python tools/launches.py gpurun_out/${TAG}_launches_c5b.csv 4 2>/dev/null | head
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_triangles -s 2 -c 2 -o gpurun_out/${TAG}_fill python tools/one_build.py C5B 2 > gpurun_out/${TAG}_fill_ncu.log 2>&1
 echo "ncu full rc=$?"
 { python tools/ncu_summary.py gpurun_out/${TAG}_fill.ncu-rep "" 8; python tools/ncu_lines.py gpurun_out/${TAG}_fill.ncu-rep "k_triangles<(bool)1" 40; } > gpurun_out/${TAG}_ncu_fill_c5b.txt 2>&1
+# the C4 tetrahedron fill (its bench line names it)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tets_dense -s 1 -c 1 -o gpurun_out/${TAG}_tets python tools/one_build.py C4 1 > gpurun_out/${TAG}_tets_ncu.log 2>&1
+{ python tools/ncu_summary.py gpurun_out/${TAG}_tets.ncu-rep "" 8; python tools/ncu_lines.py gpurun_out/${TAG}_tets.ncu-rep "k_tets_dense" 30; } > gpurun_out/${TAG}_ncu_tets_c4.txt 2>&1
 head -5 gpurun_out/${TAG}_ncu_fill_c5b.txt
