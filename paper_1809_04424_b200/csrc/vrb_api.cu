@@ -392,7 +392,10 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
             if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * Tl, s);
             // apex of every triangle (tetrahedra: face positions by owner-edge search)
             DBuf<uint16_t> tapex;
-            if (h->K >= 3 && n <= 65536) tapex.alloc((size_t)Tl + 16, s);   // padded: 16-byte reads past the end
+            if (h->K >= 3 && n <= 65536) {   // padded: the face search reads 16-byte chunks past the end
+                tapex.alloc((size_t)Tl + 16, s);
+                VRB_CUDA(cudaMemsetAsync(tapex.get() + Tl, 0xFF, 16 * sizeof(uint16_t), s));
+            }
             timer.mark(3);
             fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s, bm.get(),
                            bmoff.get());

@@ -14,7 +14,8 @@ import workloads  # noqa: E402
 
 torch.cuda.set_device(0)
 for seed, (n, d, kind, r, md) in enumerate([(50, 3, "uniform", math.inf, 2), (120, 3, "lattice", 1.5, 2),
-                                           (200, 4, "gauss", 1.2, 1), (90, 2, "dups", 0.3, 2), (3, 3, "uniform", 1.0, 2)]):
+                                           (200, 4, "gauss", 1.2, 1), (90, 2, "dups", 0.3, 2), (3, 3, "uniform", 1.0, 2),
+                                           (120, 3, "uniform", math.inf, 2)]):   # apex runs > 104
     X = workloads.random_cloud(seed, n, d, kind)
     res = vrb.build(X, maxdim=md, radius=r)
     res.h0()
