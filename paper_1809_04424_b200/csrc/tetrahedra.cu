@@ -221,13 +221,10 @@ __device__ __forceinline__ FaceQuery face_query(uint32_t u, uint32_t v, uint32_t
     return q;
 }
 
-// #entries of apex[lo, hi) below a (ascending run), as a position: 8-ary
-// rounds of 7 independent probes until <= 8 entries are left; those lie in
-// two aligned 16-byte chunks of the apex array (padded by 16 entries),
-// compared 2 entries per 32-bit add when ids < 0x7FFF (bit 15 of each half of
-// w + 0x8000 - a is set iff that entry >= a).
-__device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ apex, uint32_t lo, uint32_t hi,
-                                                uint32_t a, bool small_ids) {
+// 8-ary rounds of 7 independent probes over apex[lo, hi) (ascending) until
+// <= 8 entries are left that hold the first entry >= a.
+__device__ __forceinline__ void apex_narrow(const uint16_t* __restrict__ apex, uint32_t& lo, uint32_t& hi,
+                                            uint32_t a) {
     while (hi - lo > 8) {
         const uint32_t step = (hi - lo + 7) >> 3;
         uint32_t c = 0;
@@ -240,10 +237,24 @@ __device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ ape
         hi = min(hi, nlo + step);
         lo = nlo;
     }
+}
+
+// The <= 8 entries [lo, hi) lie in two aligned 16-byte chunks of the apex
+// array (padded by 16 entries): load them ...
+__device__ __forceinline__ void apex_chunks(const uint16_t* __restrict__ apex, uint32_t lo, uint32_t hi, uint4& c0,
+                                            uint4& c1) {
     const uint32_t base = lo & ~7u;
     const uint4* pv = reinterpret_cast<const uint4*>(apex + base);
-    const uint4 c0 = __ldg(pv);
-    const uint4 c1 = hi - base > 8 ? __ldg(pv + 1) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    c0 = __ldg(pv);
+    c1 = hi - base > 8 ? __ldg(pv + 1) : make_uint4(~0u, ~0u, ~0u, ~0u);
+}
+
+// ... and return lo + #entries of [lo, hi) below a, compared 2 entries per
+// 32-bit add when ids < 0x7FFF (bit 15 of each half of w + 0x8000 - a is set
+// iff that entry >= a).
+__device__ __forceinline__ uint32_t apex_count(const uint4& c0, const uint4& c1, uint32_t lo, uint32_t hi, uint32_t a,
+                                               bool small_ids) {
+    const uint32_t base = lo & ~7u;
     const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     uint32_t ltm = 0;
     if (small_ids) {
@@ -264,33 +275,46 @@ __device__ __forceinline__ uint32_t apex_rank_v(const uint16_t* __restrict__ ape
     return lo + (uint32_t)__popc(ltm & valid);
 }
 
-// position of the triangle with owner edge f and apex a (sorted vertices
-// a0 < a1 < a2, for the tie-level fallback)
-__device__ __forceinline__ uint32_t face_pos(const TetArgs& A, const FaceQuery& q) {
-    const uint4 r0 = __ldg(A.frec + 2 * (uint64_t)q.f), r1 = __ldg(A.frec + 2 * (uint64_t)q.f + 1);
-    if (r0.y >> 31) return tri_pos(A, q.f, q.a0, q.a1, q.a2);
+// Block of the triangle with owner edge f and apex a from f's face record:
+// returns false when f shares its filtration level (tie: search by triple).
+__device__ __forceinline__ bool face_block(const uint4& r0, const uint4& r1, uint32_t a, bool small_ids, uint32_t& lo,
+                                           uint32_t& hi) {
+    if (r0.y >> 31) return false;
     const uint32_t start = r0.x, len = r0.y;
     const uint32_t b = max(1u, (len + 12) / 13);
-    const bool small_ids = A.n < 0x7FFF;
     const uint32_t sw[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
     uint32_t c = 0;
     if (small_ids) {   // separators past the end are 0x7FFF > a
-        const uint32_t K = 0x80008000u - (q.a + 1) * 0x10001u;
+        const uint32_t K = 0x80008000u - (a + 1) * 0x10001u;
 #pragma unroll
         for (int i = 0; i < 6; ++i) c += __popc(~(sw[i] + K) & 0x80008000u);
     } else {
 #pragma unroll
         for (int i = 0; i < 12; ++i)
-            c += ((uint32_t)(i + 1) * b < len && ((sw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu) <= q.a) ? 1u : 0u;
+            c += ((uint32_t)(i + 1) * b < len && ((sw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu) <= a) ? 1u : 0u;
     }
-    const uint32_t lo = start + c * b;
-    return apex_rank_v(A.apex, lo, min(lo + b, start + len), q.a, small_ids);
+    lo = start + c * b;
+    hi = min(lo + b, start + len);
+    return true;
 }
 
+// Positions of the two faces: both records read together, both blocks
+// narrowed (no-op for counts <= 104), all four 16-byte chunks read together.
 __device__ __forceinline__ void face_pos2(const TetArgs& A, const FaceQuery& q1, const FaceQuery& q2, uint32_t& r1,
                                           uint32_t& r2) {
-    r1 = face_pos(A, q1);
-    r2 = face_pos(A, q2);
+    const bool small_ids = A.n < 0x7FFF;
+    const uint4 a0 = __ldg(A.frec + 2 * (uint64_t)q1.f), a1 = __ldg(A.frec + 2 * (uint64_t)q1.f + 1);
+    const uint4 b0 = __ldg(A.frec + 2 * (uint64_t)q2.f), b1 = __ldg(A.frec + 2 * (uint64_t)q2.f + 1);
+    uint32_t lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0;
+    const bool d1 = face_block(a0, a1, q1.a, small_ids, lo1, hi1);
+    const bool d2 = face_block(b0, b1, q2.a, small_ids, lo2, hi2);
+    if (d1) apex_narrow(A.apex, lo1, hi1, q1.a);
+    if (d2) apex_narrow(A.apex, lo2, hi2, q2.a);
+    uint4 c10, c11, c20, c21;
+    if (d1) apex_chunks(A.apex, lo1, hi1, c10, c11);
+    if (d2) apex_chunks(A.apex, lo2, hi2, c20, c21);
+    r1 = d1 ? apex_count(c10, c11, lo1, hi1, q1.a, small_ids) : tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2);
+    r2 = d2 ? apex_count(c20, c21, lo2, hi2, q2.a, small_ids) : tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2);
 }
 
 __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
