@@ -807,13 +807,14 @@ int tet_warps(int64_t n) {
 }
 
 #ifndef VRB_TET_CTA_WARPS
-#define VRB_TET_CTA_WARPS 8
+#define VRB_TET_CTA_WARPS 10
 #endif
 #ifndef VRB_TET_DENSE_CTAS
 #define VRB_TET_DENSE_CTAS 3
 #endif
-// dense path: CTAs of up to VRB_TET_CTA_WARPS warps; two per SM when the map
-// is small (shorter per-host barrier tails: hosts own ~E/n edges each)
+// dense path: CTAs of up to VRB_TET_CTA_WARPS warps, 3 per SM when the map
+// is small (C4 fill: 8 warps 10.7 ms, 10 warps 10.0 ms; 16-warp CTAs two per
+// SM are slower: longer per-host barrier tails, hosts own ~E/n edges each)
 int tet_dense_warps(int64_t n) {
     const int64_t avail = (int64_t)device_max_smem_optin() - 1024 - (int64_t)((n * 4 + 15) / 16) * 16;
     return (int)std::min<int64_t>(VRB_TET_CTA_WARPS, avail / (int64_t)sizeof(TetScratchD));
