@@ -45,6 +45,9 @@ for a, b, nm in dev[1:]:
         hc = [h[2] for h in host if h[0] < a and h[1] > prev_end and "cuda" in h[2].lower()]
         gaps.append((a - prev_end, prev_name[:40], nm[:40], sorted(set(hc))[:4]))
     prev_end, prev_name = max(prev_end, b), nm
+if os.environ.get("TL_ALL"):
+    for a, b, nm in dev:
+        print(f"{(a - t0) / 1e3:9.3f} ms {(b - a):9.1f} us  {nm[:90]}")
 for g, p, q, hc in gaps:
     print(f"gap {g:8.1f} us after {p:40s} before {q:40s} {hc}")
 print(f"gaps > {min_gap} us: {len(gaps)}, total {sum(g[0] for g in gaps) / 1e3:.3f} ms")
