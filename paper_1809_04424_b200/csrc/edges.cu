@@ -60,10 +60,6 @@ __global__ void k_edge_outputs_packed(const uint64_t* __restrict__ key, const ui
     }
 }
 
-__global__ void k_degree(const uint32_t* __restrict__ ev, int64_t n2, uint32_t* __restrict__ deg) {
-    GRID_STRIDE(q, n2) atomicAdd(&deg[ev[q]], 1u);
-}
-
 __global__ void k_keys_vertex(const uint32_t* __restrict__ ev, int64_t n2, uint64_t* __restrict__ key) {
     GRID_STRIDE(q, n2) key[q] = ev[q];
 }
@@ -72,13 +68,27 @@ __global__ void k_keys_vertex_nbr(const uint32_t* __restrict__ ev, int64_t n2, u
     GRID_STRIDE(q, n2) key[q] = ((uint64_t)ev[q] << 21) | ev[q ^ 1];
 }
 
-// position-ordered lists: slot s holds entry q = sorted[s]
-__global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
-                            const uint64_t* __restrict__ off, int64_t n2, uint32_t* __restrict__ nkr,
-                            uint32_t* __restrict__ np, uint32_t* __restrict__ listidx) {
+// list offsets from the vertex-sorted entries: off[u] = first slot with
+// key >= u (binary search per vertex; off[n] = 2E)
+__global__ void k_offsets_from_sorted(const uint64_t* __restrict__ skey, int64_t n2, int64_t n,
+                                      uint64_t* __restrict__ off) {
+    GRID_STRIDE(u, n + 1) {
+        int64_t lo = 0, hi = n2;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (skey[mid] < (uint64_t)u) lo = mid + 1; else hi = mid;
+        }
+        off[u] = (uint64_t)lo;
+    }
+}
+
+// position-ordered lists: slot s holds entry q = sorted[s] of vertex skey[s]
+__global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ skey,
+                            const uint32_t* __restrict__ ev, const uint64_t* __restrict__ off, int64_t n2,
+                            uint32_t* __restrict__ nkr, uint32_t* __restrict__ np, uint32_t* __restrict__ listidx) {
     GRID_STRIDE(s, n2) {
         const uint32_t q = sorted[s];
-        const uint32_t v = ev[q];
+        const uint32_t v = (uint32_t)skey[s];
         nkr[s] = ev[q ^ 1];
         np[s] = q >> 1;
         listidx[q] = (uint32_t)(s - (int64_t)off[v]);
@@ -197,9 +207,9 @@ __global__ void k_id_lists(const uint64_t* __restrict__ off, int64_t n, const ui
     }
 }
 
-__global__ void k_max_deg(const uint32_t* __restrict__ deg, int64_t n, unsigned* __restrict__ out) {
+__global__ void k_max_deg(const uint64_t* __restrict__ off, int64_t n, unsigned* __restrict__ out) {
     unsigned m = 0;
-    GRID_STRIDE(v, n) m = max(m, deg[v]);
+    GRID_STRIDE(v, n) m = max(m, (unsigned)(off[v + 1] - off[v]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
@@ -323,15 +333,31 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     g.E = E;
     const int64_t n2 = 2 * E;
     g.off.alloc(n + 1, s);
-    {
-        DBuf<uint32_t> deg(n, s);
-        VRB_CUDA(cudaMemsetAsync(deg.get(), 0, deg.bytes(), s));
-        if (n2) k_degree<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, deg.get());
+    // (a) lists in edge-position order: stable sort of the 2E entries by
+    // vertex; the list offsets are the run starts of the sorted keys
+    DBuf<uint64_t> lk0, lk1;
+    DBuf<uint32_t> lv0, lv1;
+    const uint32_t* lsorted = nullptr;
+    const uint64_t* lskeys = nullptr;
+    if (n2) {
+        lk0.alloc(n2, s);
+        lk1.alloc(n2, s);
+        lv0.alloc(n2, s);
+        lv1.alloc(n2, s);
+        k_keys_vertex<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, lk0.get());
         VRB_LAUNCH_CHECK();
-        exclusive_scan(deg.get(), g.off.get(), n, s);
+        uint64_t* sk = nullptr;
+        lsorted = sort_ids(lk0, lk1, lv0, lv1, n2, s, &sk);
+        lskeys = sk;
+        k_offsets_from_sorted<<<grid_for(n + 1, 256), 256, 0, s>>>(lskeys, n2, n, g.off.get());
+        VRB_LAUNCH_CHECK();
+    } else {
+        VRB_CUDA(cudaMemsetAsync(g.off.get(), 0, g.off.bytes(), s));
+    }
+    {
         DBuf<unsigned> mx(1, s);
         VRB_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned), s));
-        if (n) k_max_deg<<<grid_for(n, 256), 256, 0, s>>>(deg.get(), n, mx.get());
+        if (n) k_max_deg<<<grid_for(n, 256), 256, 0, s>>>(g.off.get(), n, mx.get());
         VRB_LAUNCH_CHECK();
         unsigned h = 0;
         VRB_CUDA(cudaMemcpyAsync(&h, mx.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -358,15 +384,14 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         return;
     }
     {
-        DBuf<uint64_t> k0(n2, s), k1(n2, s);
-        DBuf<uint32_t> v0(n2, s), v1(n2, s);
-        // (a) lists in edge-position order: stable sort of entries by vertex
-        k_keys_vertex<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
-        VRB_LAUNCH_CHECK();
-        const uint32_t* sorted = sort_ids(k0, k1, v0, v1, n2, s);
-        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(sorted, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
+        DBuf<uint64_t>& k0 = lk0;
+        DBuf<uint64_t>& k1 = lk1;
+        DBuf<uint32_t>& v0 = lv0;
+        DBuf<uint32_t>& v1 = lv1;
+        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(lsorted, lskeys, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
                                                        g.listidx.get());
         VRB_LAUNCH_CHECK();
+        const uint32_t* sorted = nullptr;
         // (b) ranks in neighbour-id order
         const char* force_sort = std::getenv("VRB_FORCE_SORT_RANKS");   // testing knob
         if (n <= kRankBitmapMax && !(force_sort && force_sort[0] == '1')) {
