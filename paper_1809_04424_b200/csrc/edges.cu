@@ -118,7 +118,8 @@ __global__ void k_id_ranks(const uint32_t* __restrict__ sorted, const uint32_t* 
 constexpr int64_t kRankBitmapMax = 262144;
 
 __global__ void __launch_bounds__(256) k_ranks_bitmap(const uint64_t* __restrict__ off, int64_t n, int packed,
-                                                      uint32_t* __restrict__ nkr, uint32_t* __restrict__ nr) {
+                                                      uint32_t* __restrict__ nkr, uint32_t* __restrict__ nr,
+                                                      const uint32_t* __restrict__ np, uint2* __restrict__ idl) {
     extern __shared__ uint32_t sm[];
     const int64_t nw = (n + 31) >> 5;
     uint32_t* bm = sm;
@@ -155,10 +156,12 @@ __global__ void __launch_bounds__(256) k_ranks_bitmap(const uint64_t* __restrict
         for (uint64_t t = o0 + threadIdx.x; t < o1; t += blockDim.x) {
             const uint32_t k = nkr[t];
             const uint32_t r = wp[k >> 5] + __popc(bm[k >> 5] & ((1u << (k & 31)) - 1u));
-            if (packed)
+            if (packed) {
                 nkr[t] = k | (r << 16);
-            else
+                if (idl) idl[o0 + r] = make_uint2(k, np[t]);   // the id-ordered list, fused
+            } else {
                 nr[t] = r;
+            }
         }
         __syncthreads();
     }
@@ -398,7 +401,9 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
             const size_t smem = (size_t)2 * ((n + 31) >> 5) * sizeof(uint32_t);
             VRB_CUDA(cudaFuncSetAttribute(k_ranks_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)device_sm_count() * 8);
-            k_ranks_bitmap<<<grid, 256, smem, s>>>(g.off.get(), n, g.packed ? 1 : 0, g.nkr.get(), g.nr.get());
+            if (g.packed) g.idl.alloc(n2, s);
+            k_ranks_bitmap<<<grid, 256, smem, s>>>(g.off.get(), n, g.packed ? 1 : 0, g.nkr.get(), g.nr.get(),
+                                                   g.np.get(), g.packed ? g.idl.get() : nullptr);
             VRB_LAUNCH_CHECK();
         } else {
             // large n: sort entries by (vertex, neighbour)
@@ -410,7 +415,7 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
             VRB_LAUNCH_CHECK();
         }
     }
-    if (g.packed) {
+    if (g.packed && !g.idl.get()) {   // (the bitmap rank path wrote it already)
         g.idl.alloc(n2, s);
         const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)device_sm_count() * 16);
         k_id_lists<<<gw, 256, 0, s>>>(g.off.get(), n, g.nkr.get(), g.np.get(), g.idl.get());
