@@ -292,7 +292,7 @@ def main():
         kname = None
     if kname:
         achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
-        traffic = _ncu_traffic(args.workload, kname)
+        traffic = _ncu_traffic(args.workload, kname) if world == 1 else None   # capture is of the 1-GPU launch
         roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
