@@ -18,6 +18,8 @@
 //   scan        : per (row, tile) counts -> lex slot bases
 //   k_dist_fill : kept pairs only: recompute the fold, sqrt, write
 //                 (len bits, i, j) at its lex slot          (write bound)
+// Full filtration (r = inf, inclusive): every pair is kept, so the mask pass
+// and the scan are skipped and k_dist_fill derives bits and slots in closed form.
 // Output: the kept edges in lexicographic (i, j) order.
 #include <cmath>
 
@@ -106,6 +108,16 @@ __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict
     }
 }
 
+// Full filtration (masks == null): every pair j > i is kept, so the row
+// bits and the lex slot are closed-form and the mask pass is skipped.
+__device__ __forceinline__ unsigned long long full_row_bits(int64_t i, int64_t j0, int64_t n) {
+    const int64_t a = i + 1 - j0, b = n - j0;
+    const int64_t lo = a > 0 ? a : 0, hi = b < kT ? b : kT;   // columns [lo, hi)
+    if (lo >= hi) return 0ull;
+    const unsigned long long upto = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+    return upto & ~((1ull << lo) - 1ull);
+}
+
 __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict__ X, int64_t n, int d,
                                                         int64_t nt,
                                                         const unsigned long long* __restrict__ masks,
@@ -118,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
     if (tj < ti) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
-    const unsigned long long* m = masks + tile_index(ti, tj, nt) * kT;
+    const unsigned long long* m = masks ? masks + tile_index(ti, tj, nt) * kT : nullptr;
     // the tile's points, coordinate-major, when they fit (d <= kFillStageD):
     // the fold then reads shared memory (row point broadcast, column points
     // conflict-free) instead of strided global loads
@@ -127,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
     __shared__ int s_any;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
-    if (threadIdx.x < kT && m[threadIdx.x]) s_any = 1;
+    if (threadIdx.x < kT && (m ? m[threadIdx.x] : full_row_bits(i0 + threadIdx.x, j0, n))) s_any = 1;
     __syncthreads();
     if (!s_any) return;
     const bool staged = d <= kFillStageD;
@@ -142,9 +154,12 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
     for (int r = wid; r < kT; r += kThreads / 32) {
         const int64_t i = i0 + r;
         if (i >= n) break;
-        const unsigned long long bits = m[r];
+        const unsigned long long bits = m ? m[r] : full_row_bits(i, j0, n);
         if (!bits) continue;
-        const uint64_t base = slot_base[i * nt + tj];
+        // full filtration: row i starts at lex slot i n - i (i + 1) / 2; its
+        // columns j0 + c (c >= lo) follow from j = max(i + 1, j0)
+        const uint64_t base = m ? slot_base[i * nt + tj]
+                                : (uint64_t)(i * n - i * (i + 1) / 2 + (j0 - i - 1 > 0 ? j0 - i - 1 : 0));
         const double* xi = X + i * d;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -390,11 +405,28 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     const double thr = cap_threshold(radius, strict);
     const int all = (!strict && std::isinf(radius)) ? 1 : 0;
     if (thr < 0.0) return;
+    dim3 grid((unsigned)nt, (unsigned)nt);
+    if (all) {   // full filtration: no mask pass, closed-form slots
+        const uint64_t E = (uint64_t)n * (uint64_t)(n - 1) / 2;
+        if (E >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu kept edges exceed u32 positions", (unsigned long long)E);
+        out.E = (int64_t)E;
+        out.key.alloc(E, s);
+        out.packed = n <= 65536;
+        if (out.packed) {
+            out.pij.alloc(E, s);
+        } else {
+            out.ei.alloc(E, s);
+            out.ej.alloc(E, s);
+        }
+        k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, nullptr, nullptr, out.key.get(), out.ei.get(),
+                                              out.ej.get(), out.pij.get());
+        VRB_LAUNCH_CHECK();
+        return;
+    }
     const int64_t ntiles = nt * (nt + 1) / 2;
     DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
     DBuf<uint32_t> cnt((size_t)(n * nt), s);
     VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    dim3 grid((unsigned)nt, (unsigned)nt);
     k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get());
     VRB_LAUNCH_CHECK();
     DBuf<uint64_t> base((size_t)(n * nt + 1), s);
