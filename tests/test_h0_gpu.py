@@ -122,3 +122,27 @@ def test_h0_full_size_vs_scipy_mst(vrb, config):
         torch.cuda.synchronize()
         vrb.use_torch_allocator(False)
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("radius", [math.inf, 30.0])
+def test_h0_late_crossing_edges_vs_scipy(vrb, radius):
+    # three far-apart blobs: the edges joining them come after ~3e6 intra-blob
+    # edges, so the forest is finished in the last filter windows (radius inf:
+    # a spanning tree ends the search; radius 30: two blobs never join)
+    sp = pytest.importorskip("scipy.sparse")
+    csgraph = pytest.importorskip("scipy.sparse.csgraph")
+    rng = np.random.default_rng(11)
+    X = np.concatenate([rng.normal(0.0, 1.0, (1400, 3)), rng.normal(0.0, 1.0, (1100, 3)) + [100.0, 0, 0],
+                        rng.normal(0.0, 1.0, (500, 3)) + [0, 25.0, 0]])
+    res = vrb.build(X, maxdim=0, radius=radius)
+    ev, ef = res.simplices(1)
+    ev, ef = _u32(ev).astype(np.int64), _u32(ef)
+    pos, death, ness = res.h0()
+    pos, death = _u32(pos), _u32(death)
+    E, n = ev.shape[0], X.shape[0]
+    G = sp.coo_matrix((np.arange(1, E + 1, dtype=np.float64), (ev[:, 0], ev[:, 1])), shape=(n, n)).tocsr()
+    ref = np.sort(csgraph.minimum_spanning_tree(G).tocoo().data.astype(np.int64) - 1)
+    np.testing.assert_array_equal(pos.astype(np.int64), ref)
+    np.testing.assert_array_equal(death, ef[pos])
+    ncomp, _ = csgraph.connected_components(G, directed=False)
+    assert ness == ncomp == (1 if math.isinf(radius) else 2)
