@@ -286,34 +286,43 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(int(s.cuda_stream))
 
 
-def _prepare_points(points, device):
-    """Returns (pointer, n, d, flags, keepalive)."""
+def _prepare_points(points, device, rowsare: str = "points"):
+    """Returns (pointer, n, d, flags, keepalive).  rowsare="points": the array
+    is (n, d), one point per row; rowsare="dimensions" (Eirene's keyword,
+    P:385-386): it is (d, n), one point per column, passed to the
+    library as is with VRB_DIM_MAJOR (the transpose runs on the device)."""
     import torch
 
+    if rowsare not in ("points", "dimensions"):
+        raise ValueError('rowsare must be "points" or "dimensions"')
+    dm = rowsare == "dimensions"
+    flags = VRB_DIM_MAJOR if dm else 0
     if isinstance(points, torch.Tensor):
         t = points.detach()
         if t.dtype != torch.float64:
             raise TypeError("points must be float64")
         if t.ndim != 2:
-            raise ValueError("points must be (n, d)")
-        if t.is_cuda:
-            t = t.contiguous()
-            return t.data_ptr(), t.shape[0], t.shape[1], VRB_POINTS_ON_DEVICE, t
+            raise ValueError("points must be 2-D")
         t = t.contiguous()
-        return t.data_ptr(), t.shape[0], t.shape[1], 0, t
+        n, d = (t.shape[1], t.shape[0]) if dm else (t.shape[0], t.shape[1])
+        if t.is_cuda:
+            flags |= VRB_POINTS_ON_DEVICE
+        return t.data_ptr(), n, d, flags, t
     a = np.ascontiguousarray(points, dtype=np.float64)
     if a.ndim != 2:
-        raise ValueError("points must be (n, d)")
-    return a.ctypes.data, a.shape[0], a.shape[1], 0, a
+        raise ValueError("points must be 2-D")
+    n, d = (a.shape[1], a.shape[0]) if dm else (a.shape[0], a.shape[1])
+    return a.ctypes.data, n, d, flags, a
 
 
 def build(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
-          skip_boundary: bool = False, stream=None) -> VRResult:
-    """vrb_build: points (n, d) float64 (numpy / CPU tensor -> copied H2D inside
-    the call; CUDA tensor -> used in place on its device)."""
+          skip_boundary: bool = False, stream=None, rowsare: str = "points") -> VRResult:
+    """vrb_build: points (n, d) float64, or (d, n) with rowsare="dimensions"
+    (numpy / CPU tensor -> copied H2D inside the call; CUDA tensor -> used in
+    place on its device)."""
     import torch
 
-    ptr, n, d, flags, keep = _prepare_points(points, None)
+    ptr, n, d, flags, keep = _prepare_points(points, None, rowsare)
     if flags & VRB_POINTS_ON_DEVICE:
         device = keep.device
     else:

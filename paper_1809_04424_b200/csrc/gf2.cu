@@ -50,7 +50,7 @@ __global__ void k_cand_count(int64_t nc, const uint64_t* __restrict__ dcp, const
         uint64_t c = 0;
         for (uint64_t q = ecp[j] + lane; q < ecp[j + 1]; q += 32) {
             const uint32_t i = erv[q];
-            c += ccp[i + 1] - ccp[i];
+            c += ccp[(uint64_t)i + 1] - ccp[i];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
@@ -74,7 +74,7 @@ __global__ void k_cand_fill(int64_t nc, int rowbits, const uint64_t* __restrict_
         o += d1 - d0;
         for (uint64_t q = ecp[j]; q < ecp[j + 1]; ++q) {
             const uint32_t i = erv[q];
-            const uint64_t c0 = ccp[i], c1 = ccp[i + 1];
+            const uint64_t c0 = ccp[i], c1 = ccp[(uint64_t)i + 1];
             for (uint64_t t = c0 + lane; t < c1; t += 32) keys[o + (t - c0)] = hi | crv[t];
             o += c1 - c0;
         }
@@ -106,9 +106,11 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, int64_t M, int rowbits
     }
 }
 
-__global__ void k_max_u32(const uint32_t* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
-    unsigned m = 0;
-    GRID_STRIDE(i, n) m = max(m, a[i] + 1u);   // + 1: 0 means empty
+// 1 + the largest index, accumulated in 64 bits (an index of 0xFFFFFFFF, an
+// int32 -1, gives 2^32 and fails the range check instead of wrapping to 0)
+__global__ void k_max_u32(const uint32_t* __restrict__ a, int64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long m = 0;
+    GRID_STRIDE(i, n) m = max(m, (unsigned long long)a[i] + 1ull);   // + 1: 0 means empty
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
@@ -117,14 +119,33 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, int64_t n, unsigned* _
 // 1 + the largest index in a[0, n) (0 when n == 0)
 uint64_t max_plus_one(const uint32_t* a, int64_t n, cudaStream_t s) {
     if (n <= 0) return 0;
-    DBuf<unsigned> m(1, s);
-    VRB_CUDA(cudaMemsetAsync(m.get(), 0, sizeof(unsigned), s));
+    DBuf<unsigned long long> m(1, s);
+    VRB_CUDA(cudaMemsetAsync(m.get(), 0, sizeof(unsigned long long), s));
     k_max_u32<<<grid_for(n), 256, 0, s>>>(a, n, m.get());
     VRB_LAUNCH_CHECK();
-    unsigned h = 0;
+    unsigned long long h = 0;
     VRB_CUDA(cudaMemcpyAsync(&h, m.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     return h;
+}
+
+// colptr must start at 0 and be non-decreasing (else the ranges it names are
+// not columns of one array)
+__global__ void k_colptr_ok(const uint64_t* __restrict__ cp, int64_t n, int* __restrict__ bad) {
+    GRID_STRIDE(j, n) if ((j == 0 && cp[0] != 0) || cp[j] > cp[j + 1]) atomicOr(bad, 1);
+}
+
+bool colptr_ok(const uint64_t* cp, int64_t n, cudaStream_t s) {
+    DBuf<int> bad(1, s);
+    VRB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    if (n > 0) {
+        k_colptr_ok<<<grid_for(n), 256, 0, s>>>(cp, n, bad.get());
+        VRB_LAUNCH_CHECK();
+    }
+    int h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    return h == 0;
 }
 
 uint64_t last_of(const uint64_t* colptr, int64_t n, cudaStream_t s) {
@@ -142,6 +163,8 @@ int64_t gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t kdim, const uint6
                          uint32_t** rowval_out) {
     *rowval_out = nullptr;
     if (ncols == 0) return 0;
+    if (!colptr_ok(dcp, ncols, s) || !colptr_ok(ccp, kdim, s) || !colptr_ok(ecp, ncols, s))
+        fail(VRB_EINVAL, "blockprodsum: a colptr does not start at 0 or decreases");
     // index ranges (out-of-range rows would gather outside C): VRB_EINVAL
     if (max_plus_one(drv, (int64_t)last_of(dcp, ncols, s), s) > (uint64_t)nrows ||
         max_plus_one(crv, (int64_t)last_of(ccp, kdim, s), s) > (uint64_t)nrows ||

@@ -27,6 +27,7 @@
 //           p's level is a single edge); faces (y,k,l), (x,k,l) are found by
 //           binary search in the triangle range of their owner edge.
 #include <algorithm>
+#include <cstdlib>
 
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
@@ -38,7 +39,7 @@ constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kBits = 4096;     // ranks of x's id list per round
 constexpr int kWords = kBits / 32;
-constexpr int kS = 512;         // max |S(p)| handled (else VRB_ENOTSUP)
+constexpr int kS = 512;         // max |S(p)| in warp scratch (larger: k_tets_big)
 constexpr int64_t kDenseMaxN = 16384;   // n x n u32 edge-position table (<= 1 GiB)
 
 struct TetArgs {
@@ -54,7 +55,12 @@ struct TetArgs {
     uint64_t chunk;
     int64_t ntasks, task_lo, task_hi;
     unsigned long long* task_counter;
-    unsigned* overflow;       // set when |S(p)| > kS
+    unsigned* ovf_n;          // owner edges with |S(p)| > kS: their hosted slots are
+    uint32_t* ovf_list;       // listed here and handled by k_tets_big
+    const uint2* idl;         // (k, pos) in neighbour-id order (packed lists), for k_tets_big
+    uint32_t* big;            // k_tets_big scratch, big_stride u32 per CTA
+    uint64_t big_stride;
+    uint32_t max_deg;
     // triangles (dimension 2, global arrays)
     const uint64_t* toff;     // E + 1
     const uint64_t* tlo;      // E: start of the triangle range of p's level
@@ -503,8 +509,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tets(TetArgs A) {
                 if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
                 const uint64_t offx = A.off[x];
                 const uint32_t m = build_S<kBits>(A, map, W, vbits, p, x, len, offx, pl.w);
-                if (m > (uint32_t)kS) {
-                    if (lane == 0) atomicOr(A.overflow, 1u);
+                if (m > (uint32_t)kS) {   // too large for warp scratch: k_tets_big
+                    if (lane == 0) A.ovf_list[atomicAdd(A.ovf_n, 1u)] = (uint32_t)e;
                     clear_S(W, vbits, kS);
                     continue;
                 }
@@ -683,8 +689,8 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
                 if (len < 2) continue;
                 if (kFill && ((int64_t)p < A.p_lo || (int64_t)p >= A.p_hi)) continue;
                 const uint32_t m = build_S<kBitsD>(A, map, W, nullptr, p, x, len, A.off[x], pl.w);
-                if (m > (uint32_t)kS) {
-                    if (lane == 0) atomicOr(A.overflow, 1u);
+                if (m > (uint32_t)kS) {   // too large for warp scratch: k_tets_big
+                    if (lane == 0) A.ovf_list[atomicAdd(A.ovf_n, 1u)] = (uint32_t)e;
                     continue;
                 }
                 uint64_t slot = 0, tbase = 0;
@@ -757,6 +763,181 @@ __global__ void __launch_bounds__(1024, 1) k_tets_dense(TetArgs A) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Owner edges whose apex set S(p) exceeds the warp scratch (|S| > kS = 512):
+// one CTA per such edge, S and the per-row counts in global scratch.  The
+// definition is the same: S(p) = the common neighbours k of the
+// owner's endpoints with both edges older than p, sorted by id (an
+// intersection of x's and y's id-ordered lists); the tetrahedra of p are the
+// pairs k < l of S adjacent through an edge older than p (k's id-ordered list
+// merged with S), emitted row by row in (k, l) order -- the lex order of the
+// sorted 4-tuples -- at slots from an exclusive scan of the row counts.
+// ---------------------------------------------------------------------------
+constexpr int kBigThreads = 512;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t& total) {
+    // sh: >= 32 words of shared scratch
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) sh[wid] = incl;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+        const uint32_t c = sh[w];
+        if (w < wid) before += c;
+        tot += c;
+    }
+    __syncthreads();
+    total = tot;
+    return before + incl - v;
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(kBigThreads) k_tets_big(TetArgs A) {
+    __shared__ uint32_t sh[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t* Sk = A.big + (uint64_t)blockIdx.x * A.big_stride;
+    uint32_t* Spx = Sk + A.max_deg;
+    uint32_t* Spy = Spx + A.max_deg;
+    uint32_t* crow = Spy + A.max_deg;   // row counts, then row offsets
+    const unsigned nbig = *A.ovf_n;
+    for (unsigned q = blockIdx.x; q < nbig; q += gridDim.x) {
+        const uint32_t e = A.ovf_list[q];
+        const uint4 pl = A.plan[e];
+        const uint32_t p = pl.x, x = pl.y, y = A.hosted_v[e];
+        const uint64_t ox = A.off[x], oy = A.off[y];
+        const uint32_t dx = (uint32_t)(A.off[x + 1] - ox), dy = (uint32_t)(A.off[y + 1] - oy);
+        // ---- S(p), sorted by id, with pos(x, k) and pos(y, k)
+        uint32_t m = 0;
+        for (uint32_t b0 = 0; b0 < dx; b0 += blockDim.x) {
+            const uint32_t t = b0 + threadIdx.x;
+            bool v = false;
+            uint32_t k = 0, px = 0, py = 0;
+            if (t < dx) {
+                const uint2 ek = __ldg(A.idl + ox + t);
+                k = ek.x;
+                px = ek.y;
+                if (px < p) {
+                    uint32_t lo = 0, hi = dy;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (__ldg(&A.idl[oy + mid].x) < k) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo < dy) {
+                        const uint2 fy = __ldg(A.idl + oy + lo);
+                        if (fy.x == k && fy.y < p) { v = true; py = fy.y; }
+                    }
+                }
+            }
+            uint32_t tot = 0;
+            const uint32_t at = m + block_excl_scan(v ? 1u : 0u, sh, tot);
+            if (v) { Sk[at] = k; Spx[at] = px; Spy[at] = py; }
+            m += tot;
+        }
+        __syncthreads();
+        // ---- row i (k = Sk[i]): the l in S, l > k, with pos(k, l) < p
+        auto row_pass = [&](uint32_t i, bool emit, uint32_t base, uint64_t slot, uint32_t filt, bool direct,
+                            uint64_t tbase) -> uint32_t {
+            const uint32_t k = Sk[i];
+            const uint64_t ok = A.off[k];
+            const uint32_t dk = (uint32_t)(A.off[k + 1] - ok);
+            // first entry of k's id list above k
+            uint32_t lo = 0, hi = dk;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(&A.idl[ok + mid].x) <= k) lo = mid + 1; else hi = mid;
+            }
+            uint32_t c = 0;
+            for (uint32_t t0 = lo; t0 < dk; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                bool v = false;
+                uint32_t j = 0, pkl = 0, l = 0;
+                if (t < dk) {
+                    const uint2 el = __ldg(A.idl + ok + t);
+                    l = el.x;
+                    pkl = el.y;
+                    if (pkl < p) {
+                        uint32_t a = i + 1, b = m;
+                        while (a < b) {
+                            const uint32_t mid = (a + b) >> 1;
+                            if (Sk[mid] < l) a = mid + 1; else b = mid;
+                        }
+                        if (a < m && Sk[a] == l) { v = true; j = a; }
+                    }
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, v);
+                if (emit && v) {
+                    const uint64_t s = slot + base + c + __popc(bal & lt);
+                    uint32_t vv[4] = {y, x, k, l};
+                    sort4v(vv);
+                    __stcs(reinterpret_cast<uint4*>(A.qv + 4 * s), make_uint4(vv[0], vv[1], vv[2], vv[3]));
+                    __stcs(A.qf + s, filt);
+                    if (A.rows) {
+                        uint32_t r[4];
+                        if (direct) {
+                            r[0] = (uint32_t)(tbase + i);
+                            r[1] = (uint32_t)(tbase + j);
+                        } else {
+                            uint32_t a0 = y, a1 = x, a2 = k;
+                            sort3v(a0, a1, a2);
+                            r[0] = tri_pos(A, p, a0, a1, a2);
+                            a0 = y; a1 = x; a2 = l;
+                            sort3v(a0, a1, a2);
+                            r[1] = tri_pos(A, p, a0, a1, a2);
+                        }
+                        if (A.apex)
+                            face_pos2(A, face_query(y, k, l, Spy[i], Spy[j], pkl),
+                                      face_query(x, k, l, Spx[i], Spx[j], pkl), r[2], r[3]);
+                        else
+                            tri_lookup2(A, tri_code_sorted(y, k, l), tri_code_sorted(x, k, l), r[2], r[3]);
+                        sort4v(r);
+                        __stcs(reinterpret_cast<uint4*>(A.rows + 4 * s), make_uint4(r[0], r[1], r[2], r[3]));
+                    }
+                }
+                c += __popc(bal);
+            }
+            return c;
+        };
+        for (uint32_t i = wid; i < m; i += nwarps) {
+            const uint32_t c = row_pass(i, false, 0, 0, 0, false, 0);
+            if (lane == 0) crow[i] = c;
+        }
+        __syncthreads();
+        if (!kFill) {
+            uint32_t part = 0;
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) part += crow[i];
+            uint32_t tot = 0;
+            block_excl_scan(part, sh, tot);
+            if (threadIdx.x == 0) A.cnt[p] = tot;
+        } else {
+            // exclusive offsets of the rows, in chunks of blockDim
+            uint32_t run = 0;
+            for (uint32_t b0 = 0; b0 < m; b0 += blockDim.x) {
+                const uint32_t i = b0 + threadIdx.x;
+                const uint32_t c = i < m ? crow[i] : 0u;
+                uint32_t tot = 0;
+                const uint32_t ex = block_excl_scan(c, sh, tot);
+                if (i < m) crow[i] = run + ex;
+                run += tot;
+            }
+            __syncthreads();
+            const uint64_t slot = A.qoff[p] - A.slot0;
+            const uint32_t filt = A.efilt[p];
+            const uint64_t tbase = A.toff[p];
+            const bool direct = !(A.frec[2 * (uint64_t)p].y >> 31);
+            for (uint32_t i = wid; i < m; i += nwarps) row_pass(i, true, crow[i], slot, filt, direct, tbase);
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_dense_positions(const uint32_t* __restrict__ ev, int64_t E, int64_t n, uint32_t* __restrict__ tab) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t a = ev[2 * p], b = ev[2 * p + 1];
@@ -820,6 +1001,24 @@ int tet_dense_warps(int64_t n) {
     return (int)std::min<int64_t>(VRB_TET_CTA_WARPS, avail / (int64_t)sizeof(TetScratchD));
 }
 
+// The owner edges the main kernel listed (|S(p)| > kS): one CTA each.
+void launch_big(TetArgs A, bool fill, cudaStream_t s) {
+    unsigned h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, A.ovf_n, sizeof(h), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (h == 0) return;
+    if (!A.idl) fail(VRB_ENOTSUP, "an edge owns more than %d triangles and the lists are not packed", kS);
+    const unsigned grid = std::min<unsigned>(h, (unsigned)device_sm_count() * 2);
+    A.big_stride = 4 * (uint64_t)A.max_deg + 4;
+    DBuf<uint32_t> scratch((size_t)grid * A.big_stride, s);
+    A.big = scratch.get();
+    if (fill)
+        k_tets_big<true><<<grid, kBigThreads, 0, s>>>(A);
+    else
+        k_tets_big<false><<<grid, kBigThreads, 0, s>>>(A);
+    VRB_LAUNCH_CHECK();
+}
+
 void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     if (A.dense && tet_dense_warps(A.n) >= 8) {
         const int warps = tet_dense_warps(A.n);
@@ -837,11 +1036,13 @@ void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cuda
         A.task_hi = A.ntasks * (part + 1) / nparts;
         if (A.task_lo >= A.task_hi) return;
         DBuf<unsigned long long> counter(1, s);
-        DBuf<unsigned> overflow(1, s);
+        DBuf<unsigned> ovf_n(1, s);
+        DBuf<uint32_t> ovf_list(A.E, s);
         VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
-        VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
+        VRB_CUDA(cudaMemsetAsync(ovf_n.get(), 0, sizeof(unsigned), s));
         A.task_counter = counter.get();
-        A.overflow = overflow.get();
+        A.ovf_n = ovf_n.get();
+        A.ovf_list = ovf_list.get();
         // fill: at most VRB_TET_DENSE_CTAS CTAs per SM, the rest of the
         // unified on-chip memory left to L1 (the face searches live on L1
         // hits; 4 CTAs: 14.4 ms, 3: 11.1 ms on C4); the count takes 4
@@ -864,10 +1065,7 @@ void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cuda
         else
             k_tets_dense<false><<<grid, warps * 32, smem, s>>>(A);
         VRB_LAUNCH_CHECK();
-        unsigned h = 0;
-        VRB_CUDA(cudaMemcpyAsync(&h, overflow.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-        VRB_CUDA(cudaStreamSynchronize(s));
-        if (h) fail(VRB_ENOTSUP, "an edge owns more than %d triangles; tetrahedra not supported for this input", kS);
+        launch_big(A, fill, s);
         return;
     }
     const int warps = tet_warps(A.n);
@@ -887,22 +1085,38 @@ void launch_tets(TetArgs A, bool fill, uint64_t work, int part, int nparts, cuda
     A.task_hi = A.ntasks * (part + 1) / nparts;
     if (A.task_lo >= A.task_hi) return;
     DBuf<unsigned long long> counter(1, s);
-    DBuf<unsigned> overflow(1, s);
+    DBuf<unsigned> ovf_n(1, s);
+    DBuf<uint32_t> ovf_list(A.E, s);
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
-    VRB_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(unsigned), s));
+    VRB_CUDA(cudaMemsetAsync(ovf_n.get(), 0, sizeof(unsigned), s));
     A.task_counter = counter.get();
-    A.overflow = overflow.get();
+    A.ovf_n = ovf_n.get();
+    A.ovf_list = ovf_list.get();
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count(), A.task_hi - A.task_lo);
     if (fill)
         k_tets<true><<<grid, threads, smem, s>>>(A);
     else
         k_tets<false><<<grid, threads, smem, s>>>(A);
     VRB_LAUNCH_CHECK();
-    unsigned h = 0;
-    VRB_CUDA(cudaMemcpyAsync(&h, overflow.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
-    VRB_CUDA(cudaStreamSynchronize(s));
-    if (h) fail(VRB_ENOTSUP, "an edge owns more than %d triangles; tetrahedra not supported for this input", kS);
+    launch_big(A, fill, s);
 }
+
+}  // namespace
+
+// Largest vertex count the tetrahedron stage supports on this device: the
+// tie-group sort packs lex codes in 16-bit ids (n <= 65536), and the sparse
+// kernel keeps an n-entry host map plus per-warp vertex bitmaps in shared
+// memory (>= 4 warps; ~38k vertices with 227 KB of shared memory).
+int64_t tets_max_n() {
+    int64_t lo = 0, hi = 65536;
+    while (lo < hi) {   // largest n with tet_warps(n) >= 4
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (tet_warps(mid) >= 4) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+namespace {
 
 TetArgs tet_args(const Graph& g, const TriLevels& L) {
     TetArgs A{};
@@ -916,6 +1130,8 @@ TetArgs tet_args(const Graph& g, const TriLevels& L) {
     A.plan = g.plan.get();
     A.hosted_v = g.hosted_v.get();
     A.work_pre = g.work_pre.get();
+    A.idl = g.idl.get();
+    A.max_deg = g.max_deg;
     A.toff = L.toff;
     A.tlo = L.tlo.get();
     A.thi = L.thi.get();
@@ -943,7 +1159,8 @@ void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, con
                                      L.thi.get(), L.frec.get());
     VRB_LAUNCH_CHECK();
     if (L.apex) {   // face positions by owner-edge search (face_pos2)
-        if (L.n <= kDenseMaxN) {   // pair tests through an n x n table of edge positions
+        const char* fs = std::getenv("VRB_FORCE_SPARSE_TETS");   // testing knob: the k_tets path
+        if (L.n <= kDenseMaxN && !(fs && fs[0] == '1')) {   // pair tests through an n x n table of edge positions
             L.dense.alloc((size_t)(L.n * L.n), s);
             VRB_CUDA(cudaMemsetAsync(L.dense.get(), 0xFF, L.dense.bytes(), s));
             const unsigned gd = (unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16);

@@ -101,7 +101,7 @@ struct TriArgs {
     uint32_t* bm;              // apex bitmaps (count writes, fill reads), or null
     const uint64_t* bmoff;     // per hosted slot: word offset of its bitmap
     const uint2* idl;          // (k, pos) in neighbour-ID order
-    int debug;   // ablation knob (VRB_DEBUG_FILL): 1 = stop after mark, 2 = skip the flush
+    int debug;   // ablation (experiment builds with -DVRB_ABLATION only): 1 = stop after mark, 2 = skip the flush
 };
 
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t v) {
@@ -1005,8 +1005,14 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.apex = g.n <= 65536 ? apex : nullptr;
     A.bm = const_cast<uint32_t*>(bm);
     A.bmoff = bmoff;
-    const char* dbg = std::getenv("VRB_DEBUG_FILL");   // ablation timing only; breaks outputs
-    A.debug = dbg ? std::atoi(dbg) : 0;
+#ifdef VRB_ABLATION
+    // ablation timing of experiment builds only (tools/variants.py
+    // -DVRB_ABLATION=<mode>); it breaks the outputs, so the shipped library
+    // (built without the macro) has no such knob
+    A.debug = VRB_ABLATION;
+#else
+    A.debug = 0;
+#endif
     launch(A, true, g.work, 0, 1, s);
 }
 

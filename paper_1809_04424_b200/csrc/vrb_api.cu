@@ -300,6 +300,10 @@ void read_offsets(const uint64_t* off, int64_t E, const int64_t* b, cudaStream_t
 void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
                 cudaStream_t s, vrb_handle* out, bool matrix = false) {
     check_opts(X, n, d, opts, out);
+    // limits of the layout, checked before any work
+    if (opts->maxdim >= 2 && n > tets_max_n())
+        fail(VRB_ENOTSUP, "tetrahedra (maxdim 2) need n <= %lld on this device (n = %lld)",
+             (long long)tets_max_n(), (long long)n);
     const int rank = comm ? comm->rank : 0;
     const int world = comm ? comm->world : 1;
     if (comm && (world < 1 || rank < 0 || rank >= world || !comm->allgather))

@@ -103,6 +103,8 @@ struct TriLevels {
 };
 void triangle_levels(const uint32_t* efilt, const uint64_t* toff, int64_t E, const uint32_t* tv, cudaStream_t s,
                      TriLevels& L);
+// largest n for which K = 3 (tetrahedra) is supported (VRB_ENOTSUP above)
+int64_t tets_max_n();
 void count_tets(const Graph& g, const TriLevels& L, uint32_t* cnt, int part, int nparts, cudaStream_t s);
 void fill_tets(const Graph& g, const TriLevels& L, const uint32_t* efilt, const uint64_t* qoff, int64_t p_lo,
                int64_t p_hi, uint64_t slot0, uint32_t* qv, uint32_t* qf, uint32_t* rows, cudaStream_t s);

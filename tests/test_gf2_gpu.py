@@ -122,3 +122,33 @@ def test_blockprodsum_edge_cases(vrb):
     assert cp.tolist() == [0, 0] and rv.size == 0
     with pytest.raises(vrb.VrbError):
         run(vrb, 2, D, C, E)          # row 3 >= nrows = 2
+
+
+@pytest.mark.parametrize("which", ["D", "C", "E"])
+def test_blockprodsum_index_minus_one_rejected(vrb, which):
+    # an int32 -1 is the u32 index 0xFFFFFFFF: out of range in every operand
+    # (the range check once wrapped it to 0 and passed)
+    ok = {"D": (np.array([0, 1], dtype=np.int64), np.array([1], dtype=np.uint32)),
+          "C": (np.array([0, 2], dtype=np.int64), np.array([0, 2], dtype=np.uint32)),
+          "E": (np.array([0, 1], dtype=np.int64), np.array([0], dtype=np.uint32))}
+    cp, rv = ok[which]
+    bad = rv.copy()
+    bad[-1] = 0xFFFFFFFF
+    ops = dict(ok)
+    ops[which] = (cp, bad)
+    with pytest.raises(vrb.VrbError) as ei:
+        run(vrb, 4, ops["D"], ops["C"], ops["E"])
+    assert ei.value.status == vrb.VRB_EINVAL
+    run(vrb, 4, ok["D"], ok["C"], ok["E"])   # the unmodified operands are accepted
+
+
+def test_blockprodsum_bad_colptr_rejected(vrb):
+    C = (np.array([0, 2], dtype=np.int64), np.array([1, 3], dtype=np.uint32))
+    E = (np.array([0, 1], dtype=np.int64), np.array([0], dtype=np.uint32))
+    for cp in ([1, 2], [0, 3, 2]):   # not starting at 0; decreasing
+        nc = len(cp) - 1
+        D = (np.array(cp, dtype=np.int64), np.array([0, 1, 2], dtype=np.uint32)[:max(cp)])
+        Ek = (np.arange(nc + 1, dtype=np.int64), np.zeros(nc, dtype=np.uint32))
+        with pytest.raises(vrb.VrbError) as ei:
+            run(vrb, 4, D, C, Ek)
+        assert ei.value.status == vrb.VRB_EINVAL
