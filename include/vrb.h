@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define VRB_ABI_VERSION 1
+#define VRB_ABI_VERSION 2
 
 typedef enum {
     VRB_OK = 0,
@@ -96,29 +96,62 @@ vrb_status vrb_set_allocator(vrb_alloc_fn alloc, vrb_free_fn free_fn, void* ctx)
 vrb_status vrb_build(const double* X, int64_t n, int32_t d, const vrb_opts* opts,
                      void* stream, vrb_handle* out);
 
-/* Collective callback for vrb_build_dist: gather `bytes` bytes from every
- * rank into recv (world * bytes, rank order).  send/recv are DEVICE pointers
- * on the build's stream; return 0 on success.  (The Python binding implements
- * it with torch.distributed all_gather_into_tensor over NCCL.) */
+/* Collective callbacks for vrb_build_dist.  All buffers are DEVICE pointers
+ * and every call is ordered on `stream` (the build's stream): the callee
+ * must enqueue its collective after the work already on that stream and the
+ * library's later work must see its result (e.g. torch.distributed NCCL
+ * collectives issued with `stream` as the current stream).  Return 0 on
+ * success; anything else makes the build fail with VRB_ECOMM.
+ *   allgather: recv (world * bytes) <- every rank's `bytes` bytes of send,
+ *              in rank order;
+ *   broadcast: buf (bytes) on every rank <- buf of rank `root`. */
 typedef int (*vrb_allgather_fn)(const void* send, void* recv, size_t bytes, void* stream, void* ctx);
+typedef int (*vrb_bcast_fn)(void* buf, size_t bytes, int root, void* stream, void* ctx);
 
 typedef struct {
     int32_t rank;
-    int32_t world;
+    int32_t world;            /* >= 1 */
     vrb_allgather_fn allgather;
-    void* ctx;
+    vrb_bcast_fn broadcast;
+    void* ctx;                /* passed to the callbacks */
 } vrb_comm;
 
-/* Multi-GPU build, one process per GPU; every rank calls it with the same
- * X (valid on every rank), n, d and opts.  Triangles/tetrahedra are
- * partitioned by ranges of their owner edge in the global edge order, so each
- * rank produces a contiguous slice of the global (filt, lex) order; the
- * slices concatenated in rank order are byte-identical to vrb_build (SURVEY
- * 8(e), pin P13).  The edge level is computed redundantly on every rank; the
- * one exchange is an all-gather of per-edge simplex counts.  Errors as
- * vrb_build plus VRB_ECOMM. */
+/* Multi-GPU build, one process per GPU (the paper's column
+ * partition with its colptr fix-up "one after the other", is
+ * here an exclusive scan of per-rank totals).  Every rank calls it with the
+ * same n, d and opts; X is read on rank 0 only (other ranks may pass NULL).
+ *   S1   rank 0 places and checks the points and broadcasts them;
+ *   S2   each rank computes the distances of one row block of the pair
+ *        matrix (tile-aligned, balanced by pair count);
+ *   S3   each rank sorts its kept edges; the sorted runs are all-gathered
+ *        (16 bytes per edge) and merged, so every rank holds the global edge
+ *        order, the dense ranks and value_of_rank;
+ *   S4   the neighbour lists are rebuilt on every rank (the one replicated
+ *        stage);
+ *   S5-8 each rank counts, fills and tie-sorts the triangles of one range of
+ *        owner edges (level-aligned, balanced by enumeration work); its slice
+ *        starts at the exclusive prefix of the per-rank totals (world x 8
+ *        bytes all-gathered);
+ *   S6   with maxdim 2, the per-edge triangle counts and the triangle
+ *        vertices are all-gathered, then tetrahedra are partitioned the same
+ *        way.
+ * The slices of dimensions 2 and 3, concatenated in rank order, are
+ * byte-identical to vrb_build's arrays (pin P13).  Edges (dimension 1) are
+ * held whole by every rank; vrb_count reports the slice
+ * [E rank / world, E (rank + 1) / world).  Errors as vrb_build (raised on
+ * every rank alike, e.g. a non-finite coordinate found on rank 0) plus
+ * VRB_ECOMM. */
 vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts,
                           const vrb_comm* comm, void* stream, vrb_handle* out);
+
+/* The owner-edge partition rule of vrb_build_dist, on HOST arrays (for
+ * tests and planning): prefix = E + 1 exclusive work prefix over the edge
+ * positions, efilt = E edge levels; bounds (world + 1) receives the first
+ * owner edge of each rank: the first p whose prefix reaches g / world of
+ * the total, moved back to the start of its level.  VRB_EINVAL on NULL
+ * pointers, E < 0 or world < 1. */
+vrb_status vrb_partition_bounds(const uint64_t* prefix, const uint32_t* efilt, int64_t E, int32_t world,
+                                int64_t* bounds);
 
 /* Counts of dimension dim (0..K): global_n = size of the whole dimension;
  * local_off/local_n = this handle's slice (the whole for vrb_build).  Any

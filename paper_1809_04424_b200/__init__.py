@@ -34,7 +34,7 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
+           "vrb_free", "vrb_sortperm_f64", "vrb_partition_bounds", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
            "vrb_build_dm",
            "vrb_latlon2euc", "vrb_gf2_blockprodsum", "vrb_gf2_csc", "vrb_gf2_free")
 
@@ -54,6 +54,8 @@ class vrb_opts(ctypes.Structure):
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                 ctypes.c_void_p, ctypes.c_void_p)
+BCAST_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                            ctypes.c_void_p)
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
                            ctypes.c_void_p)
@@ -61,7 +63,7 @@ FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
 
 class vrb_comm(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("allgather", ALLGATHER_FN),
-                ("ctx", ctypes.c_void_p)]
+                ("broadcast", BCAST_FN), ("ctx", ctypes.c_void_p)]
 
 
 _lib = None
@@ -119,6 +121,8 @@ def lib() -> ctypes.CDLL:
     L.vrb_gf2_csc.argtypes = [p, P(i64), P(p), P(p)]
     L.vrb_gf2_free.restype = ctypes.c_int
     L.vrb_gf2_free.argtypes = [p]
+    L.vrb_partition_bounds.restype = ctypes.c_int
+    L.vrb_partition_bounds.argtypes = [p, p, i64, i32, p]
     L.vrb_h0.restype = ctypes.c_int
     L.vrb_h0.argtypes = [p, p, P(p), P(p), P(i64), P(i64)]
     _lib = L
@@ -425,8 +429,8 @@ def gf2_blockprodsum(nrows: int, D, C, E, stream=None) -> Gf2Matrix:
 
 def allgather_bytes(src, dst, group=None):
     """dst (world * nbytes, uint8) <- all-gather of src (nbytes, uint8) over the
-    process group: NCCL on device tensors directly, other backends (gloo)
-    through host memory.  Used by the collective callback of build_dist."""
+    process group, on the current stream: NCCL on the device tensors directly,
+    other backends (gloo) through host memory."""
     import torch
     import torch.distributed as dist
 
@@ -439,34 +443,76 @@ def allgather_bytes(src, dst, group=None):
     dst.copy_(hd)
 
 
-def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
-               skip_boundary: bool = False, group=None, stream=None) -> VRResult:
-    """vrb_build_dist: one process per GPU; every rank passes the same points.
-    The all-gather the library asks for runs over torch.distributed."""
-    import torch
+def broadcast_bytes(buf, root: int, group=None):
+    """buf (nbytes, uint8) <- rank root's buf, on the current stream (NCCL on
+    device, other backends through host memory)."""
     import torch.distributed as dist
 
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    ptr, n, d, flags, keep = _prepare_points(points, None)
-    device = keep.device if (flags & VRB_POINTS_ON_DEVICE) else torch.device("cuda", torch.cuda.current_device())
-    if strict:
-        flags |= VRB_STRICT_RADIUS
-    if skip_boundary:
-        flags |= VRB_SKIP_BOUNDARY
+    src = dist.get_global_rank(group, root) if group is not None else root
+    if dist.get_backend(group) == "nccl" or buf.device.type == "cpu":
+        dist.broadcast(buf, src, group=group)
+        return
+    h = buf.cpu()
+    dist.broadcast(h, src, group=group)
+    buf.copy_(h)
+
+
+def _comm_callbacks(device, world, group):
+    """The vrb_comm callbacks over torch.distributed.  Each one runs its
+    collective with the library's build stream as torch's current stream, so
+    it is ordered after the work the library enqueued and the library's later
+    work is ordered after it (NCCL: no host synchronisation)."""
+    import torch
 
     def _allgather(send, recv, nbytes, stream_, ctx):
         try:
-            src = torch.as_tensor(_CAI(send, (nbytes,), "|u1", None), device=device)
-            dst = torch.as_tensor(_CAI(recv, (nbytes * world,), "|u1", None), device=device)
-            allgather_bytes(src, dst, group)
-            torch.cuda.current_stream(device).synchronize()
+            with torch.cuda.stream(torch.cuda.ExternalStream(int(stream_ or 0), device=device)):
+                src = torch.as_tensor(_CAI(send, (nbytes,), "|u1", None), device=device)
+                dst = torch.as_tensor(_CAI(recv, (nbytes * world,), "|u1", None), device=device)
+                allgather_bytes(src, dst, group)
             return 0
         except Exception as e:   # reported as VRB_ECOMM
             print("vrb allgather failed:", e)
             return 1
 
-    cb = ALLGATHER_FN(_allgather)
-    comm = vrb_comm(rank, world, cb, None)
+    def _broadcast(buf, nbytes, root, stream_, ctx):
+        try:
+            with torch.cuda.stream(torch.cuda.ExternalStream(int(stream_ or 0), device=device)):
+                t = torch.as_tensor(_CAI(buf, (nbytes,), "|u1", None), device=device)
+                broadcast_bytes(t, root, group)
+            return 0
+        except Exception as e:   # reported as VRB_ECOMM
+            print("vrb broadcast failed:", e)
+            return 1
+
+    return ALLGATHER_FN(_allgather), BCAST_FN(_broadcast)
+
+
+def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool = False,
+               skip_boundary: bool = False, group=None, stream=None, rowsare: str = "points", n: int = None,
+               d: int = None) -> VRResult:
+    """vrb_build_dist: one process per GPU.  Rank 0 passes the points (as
+    build()); the other ranks may pass None with n and d (the library
+    broadcasts rank 0's points).  The collectives the library asks for run
+    over torch.distributed on the build stream."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if points is None:
+        if n is None or d is None:
+            raise ValueError("ranks without points must pass n and d")
+        ptr, flags, keep = 0, 0, None
+        device = torch.device("cuda", torch.cuda.current_device())
+    else:
+        ptr, n, d, flags, keep = _prepare_points(points, None, rowsare)
+        device = keep.device if (flags & VRB_POINTS_ON_DEVICE) else torch.device("cuda", torch.cuda.current_device())
+    if strict:
+        flags |= VRB_STRICT_RADIUS
+    if skip_boundary:
+        flags |= VRB_SKIP_BOUNDARY
+    ag, bc = _comm_callbacks(device, world, group)
+    comm = vrb_comm(rank, world, ag, bc, None)
     opts = vrb_opts(int(maxdim), float(radius), flags)
     h = ctypes.c_void_p()
     with torch.cuda.device(device):
@@ -474,6 +520,20 @@ def build_dist(points, maxdim: int = 1, radius: float = math.inf, strict: bool =
                                     _stream_ptr(stream), ctypes.byref(h)))
     del keep
     return VRResult(h.value, device)
+
+
+def partition_bounds(prefix, efilt, world: int):
+    """vrb_partition_bounds on host arrays (the owner-edge split rule of
+    build_dist): prefix (E + 1,) uint64 work prefix, efilt (E,) uint32 levels
+    -> (world + 1,) int64 first owner edge of each rank."""
+    pre = np.ascontiguousarray(prefix, dtype=np.uint64)
+    ef = np.ascontiguousarray(efilt, dtype=np.uint32)
+    if pre.shape[0] != ef.shape[0] + 1:
+        raise ValueError("prefix must have E + 1 entries")
+    out = np.zeros(world + 1, dtype=np.int64)
+    _check(lib().vrb_partition_bounds(pre.ctypes.data, ef.ctypes.data if ef.size else None, ef.shape[0], int(world),
+                                      out.ctypes.data))
+    return out
 
 
 def sortperm_f64(keys):

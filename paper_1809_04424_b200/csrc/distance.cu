@@ -38,11 +38,15 @@ __device__ __forceinline__ int64_t tile_index(int64_t ti, int64_t tj, int64_t nt
     return ti * nt - ti * (ti - 1) / 2 + (tj - ti);   // packed upper triangle (tj >= ti)
 }
 
+// Tile rows [ti_lo, ti_lo + gridDim.y) (a rank's row block);
+// masks are indexed from the block's first tile (mask_base) and the per
+// (row, tile) counts from its first row.
 __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict__ X, int64_t n, int d,
                                                         int64_t nt, double thr, int all,
                                                         unsigned long long* __restrict__ masks,
-                                                        uint32_t* __restrict__ rowtile_cnt) {
-    const int64_t tj = blockIdx.x, ti = blockIdx.y;
+                                                        uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo,
+                                                        int64_t mask_base) {
+    const int64_t tj = blockIdx.x, ti = blockIdx.y + ti_lo;
     if (tj < ti) return;
     __shared__ double sA[kDC][kT];
     __shared__ double sB[kDC][kT];
@@ -103,8 +107,8 @@ __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict
     if (threadIdx.x < kT) {
         const int r = threadIdx.x;
         const unsigned long long m = mrow[r];
-        masks[tile_index(ti, tj, nt) * kT + r] = m;
-        if (i0 + r < n) rowtile_cnt[(i0 + r) * nt + tj] = (uint32_t)__popcll(m);
+        masks[(tile_index(ti, tj, nt) - mask_base) * kT + r] = m;
+        if (i0 + r < n) rowtile_cnt[(i0 + r - ti_lo * kT) * nt + tj] = (uint32_t)__popcll(m);
     }
 }
 
@@ -125,12 +129,14 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
                                                         uint64_t* __restrict__ key,
                                                         uint32_t* __restrict__ ei,
                                                         uint32_t* __restrict__ ej,
-                                                        uint32_t* __restrict__ pij) {
-    const int64_t tj = blockIdx.x, ti = blockIdx.y;
+                                                        uint32_t* __restrict__ pij, int64_t ti_lo,
+                                                        int64_t mask_base) {
+    const int64_t tj = blockIdx.x, ti = blockIdx.y + ti_lo;
     if (tj < ti) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
-    const unsigned long long* m = masks ? masks + tile_index(ti, tj, nt) * kT : nullptr;
+    const int64_t row_lo = ti_lo * kT;
+    const unsigned long long* m = masks ? masks + (tile_index(ti, tj, nt) - mask_base) * kT : nullptr;
     // the tile's points, coordinate-major, when they fit (d <= kFillStageD):
     // the fold then reads shared memory (row point broadcast, column points
     // conflict-free) instead of strided global loads
@@ -158,8 +164,9 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
         if (!bits) continue;
         // full filtration: row i starts at lex slot i n - i (i + 1) / 2; its
         // columns j0 + c (c >= lo) follow from j = max(i + 1, j0)
-        const uint64_t base = m ? slot_base[i * nt + tj]
-                                : (uint64_t)(i * n - i * (i + 1) / 2 + (j0 - i - 1 > 0 ? j0 - i - 1 : 0));
+        const uint64_t base = m ? slot_base[(i - row_lo) * nt + tj]
+                                : (uint64_t)(i * n - i * (i + 1) / 2 + (j0 - i - 1 > 0 ? j0 - i - 1 : 0) -
+                                             (row_lo * n - row_lo * (row_lo + 1) / 2));
         const double* xi = X + i * d;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -361,10 +368,10 @@ double cap_threshold(double r, bool strict) {
     return x;
 }
 
-void place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out) {
+bool place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out, bool soft) {
     const int64_t total = n * d;
-    out.alloc((size_t)total, s);
-    if (total == 0) return;
+    if (out.size() != (size_t)total) out.alloc((size_t)total, s);
+    if (total == 0) return true;
     DBuf<double> staged;
     const double* src = X;
     if (!(flags & VRB_POINTS_ON_DEVICE)) {
@@ -394,20 +401,29 @@ void place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_
     int h = 0;
     VRB_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
-    if (h) fail(VRB_EINVAL, "non-finite coordinate in the point cloud");
+    if (h && !soft) fail(VRB_EINVAL, "non-finite coordinate in the point cloud");
+    return h == 0;
 }
 
+int64_t edge_tile() { return kT; }
+
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
-                      KeptEdges& out) {
+                      KeptEdges& out, int64_t row_lo, int64_t row_hi) {
     out.E = 0;
-    if (n < 2) return;
+    if (row_hi < 0 || row_hi > n) row_hi = n;
+    if (n < 2 || row_lo >= row_hi) return;
+    if (row_lo % kT) fail(VRB_EINVAL, "row block must start at a multiple of %d", kT);
     const int64_t nt = ceil_div(n, kT);
+    const int64_t ti_lo = row_lo / kT, ti_hi = ceil_div(row_hi, kT);
+    if (row_hi != n && row_hi % kT) fail(VRB_EINVAL, "row block must end at a multiple of %d", kT);
+    const int64_t nrows = std::min(row_hi, n) - row_lo;
     const double thr = cap_threshold(radius, strict);
     const int all = (!strict && std::isinf(radius)) ? 1 : 0;
     if (thr < 0.0) return;
-    dim3 grid((unsigned)nt, (unsigned)nt);
+    dim3 grid((unsigned)nt, (unsigned)(ti_hi - ti_lo));
     if (all) {   // full filtration: no mask pass, closed-form slots
-        const uint64_t E = (uint64_t)n * (uint64_t)(n - 1) / 2;
+        auto start = [&](int64_t i) { return (uint64_t)(i * n - i * (i + 1) / 2); };   // lex slot of row i
+        const uint64_t E = start(std::min(row_hi, n)) - start(row_lo);
         if (E >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu kept edges exceed u32 positions", (unsigned long long)E);
         out.E = (int64_t)E;
         out.key.alloc(E, s);
@@ -418,21 +434,24 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
             out.ei.alloc(E, s);
             out.ej.alloc(E, s);
         }
+        if (E == 0) return;
         k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, nullptr, nullptr, out.key.get(), out.ei.get(),
-                                              out.ej.get(), out.pij.get());
+                                              out.ej.get(), out.pij.get(), ti_lo, 0);
         VRB_LAUNCH_CHECK();
         return;
     }
-    const int64_t ntiles = nt * (nt + 1) / 2;
+    auto tidx = [&](int64_t ti) { return ti * nt - ti * (ti - 1) / 2; };   // first packed tile of tile row ti
+    const int64_t mask_base = tidx(ti_lo);
+    const int64_t ntiles = tidx(ti_hi) - mask_base;
     DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
-    DBuf<uint32_t> cnt((size_t)(n * nt), s);
+    DBuf<uint32_t> cnt((size_t)(nrows * nt), s);
     VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get());
+    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, mask_base);
     VRB_LAUNCH_CHECK();
-    DBuf<uint64_t> base((size_t)(n * nt + 1), s);
-    exclusive_scan(cnt.get(), base.get(), n * nt, s);
+    DBuf<uint64_t> base((size_t)(nrows * nt + 1), s);
+    exclusive_scan(cnt.get(), base.get(), nrows * nt, s);
     uint64_t E = 0;
-    VRB_CUDA(cudaMemcpyAsync(&E, base.get() + n * nt, sizeof(E), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(&E, base.get() + nrows * nt, sizeof(E), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     if (E >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu kept edges exceed u32 positions", (unsigned long long)E);
     out.E = (int64_t)E;
@@ -446,7 +465,7 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
         out.ej.alloc(E, s);
     }
     k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, masks.get(), base.get(), out.key.get(),
-                                          out.ei.get(), out.ej.get(), out.pij.get());
+                                          out.ei.get(), out.ej.get(), out.pij.get(), ti_lo, mask_base);
     VRB_LAUNCH_CHECK();
 }
 

@@ -168,25 +168,34 @@ __global__ void __launch_bounds__(256) k_ranks_bitmap(const uint64_t* __restrict
 }
 
 __global__ void k_assign(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ listidx, int64_t E,
-                         uint32_t* __restrict__ scan_v, uint32_t* __restrict__ scan_len,
-                         uint64_t* __restrict__ host_key) {
+                         uint32_t* __restrict__ scan_v, uint32_t* __restrict__ scan_len) {
     GRID_STRIDE(p, E) {
         const uint32_t la = listidx[2 * p], lb = listidx[2 * p + 1];
         const uint32_t a = ev[2 * p], b = ev[2 * p + 1];
         const bool scan_a = la <= lb;
         scan_v[p] = scan_a ? a : b;
         scan_len[p] = scan_a ? la : lb;
-        // sort key: host, then longest prefix first (LPT order inside a host)
-        host_key[p] = ((uint64_t)(scan_a ? b : a) << 32) | (uint32_t)~(scan_a ? la : lb);
+    }
+}
+
+// plan sort key of the owner edges p_lo + [0, m): host, then longest prefix
+// first (LPT order inside a host)
+__global__ void k_host_keys(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ scan_v,
+                            const uint32_t* __restrict__ scan_len, int64_t p_lo, int64_t m,
+                            uint64_t* __restrict__ host_key) {
+    GRID_STRIDE(q, m) {
+        const int64_t p = p_lo + q;
+        const uint32_t a = ev[2 * p], b = ev[2 * p + 1], x = scan_v[p];
+        host_key[q] = ((uint64_t)(x == a ? b : a) << 32) | (uint32_t)~scan_len[p];
     }
 }
 
 __global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_t* __restrict__ host_key,
                               const uint32_t* __restrict__ scan_v, const uint32_t* __restrict__ scan_len,
-                              const uint64_t* __restrict__ off, int64_t E, uint32_t* __restrict__ hosted_v,
-                              uint4* __restrict__ plan, uint32_t* __restrict__ work) {
+                              const uint64_t* __restrict__ off, int64_t E, int64_t p_lo,
+                              uint32_t* __restrict__ hosted_v, uint4* __restrict__ plan, uint32_t* __restrict__ work) {
     GRID_STRIDE(i, E) {
-        const uint32_t p = hosted[i];
+        const uint32_t p = (uint32_t)(p_lo + hosted[i]);
         const uint32_t x = scan_v[p], len = scan_len[p];
         hosted_v[i] = (uint32_t)(host_key[i] >> 32);
         plan[i] = make_uint4(p, x, len, (uint32_t)(off[x + 1] - off[x]));
@@ -270,12 +279,20 @@ __global__ void k_fixup_runs(uint64_t* __restrict__ key, uint32_t* __restrict__ 
     }
 }
 
-int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
+// Sort the kept edges by (len, i, j): a stable radix sort of the length bits
+// (the input is in lex order).  Results: so.key[q] + so.bias = length bits of
+// the q-th edge, so.val[q] = its packed (i, j) (ke.packed) or lex index.
+void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so) {
     const int64_t E = ke.E;
-    if (E == 0) return 0;
-    DBuf<uint64_t> key_alt(E, s);
+    so.E = E;
+    so.packed = ke.packed;
+    if (E == 0) return;
+    DBuf<uint64_t>& key_alt = so.key_alt;
+    key_alt.alloc(E, s);
     // values: the packed (i, j) ids, or the lex index (permutation) for large n
-    DBuf<uint32_t> perm, perm_alt(E, s);
+    DBuf<uint32_t>& perm = so.perm;
+    DBuf<uint32_t>& perm_alt = so.perm_alt;
+    perm_alt.alloc(E, s);
     uint32_t* vals = ke.pij.get();
     if (!ke.packed) {
         perm.alloc(E, s);
@@ -312,8 +329,19 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
             if (alt2) alt = !alt;
         }
     }
-    const uint64_t* skey = alt ? key_alt.get() : ke.key.get();
-    const uint32_t* sval = alt ? perm_alt.get() : vals;
+    so.key = alt ? key_alt.get() : ke.key.get();
+    so.val = alt ? perm_alt.get() : vals;
+    so.bias = bias;
+}
+
+int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
+    const int64_t E = ke.E;
+    if (E == 0) return 0;
+    SortedEdges so;
+    sort_edges(ke, s, so);
+    const uint64_t* skey = so.key;
+    const uint32_t* sval = so.val;
+    const uint64_t bias = so.bias;
     DBuf<uint32_t> head(E, s);
     k_rank_heads<<<grid_for(E, 256), 256, 0, s>>>(skey, E, head.get());
     VRB_LAUNCH_CHECK();
@@ -332,6 +360,11 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
 }
 
 void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g) {
+    build_lists(ev, n, E, s, g);
+    build_plan(ev, 0, E, s, g);
+}
+
+void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g) {
     g.n = n;
     g.E = E;
     const int64_t n2 = 2 * E;
@@ -378,14 +411,7 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     g.listidx.alloc(n2, s);
     g.scan_v.alloc(E, s);
     g.scan_len.alloc(E, s);
-    g.plan.alloc(E, s);
-    g.hosted_v.alloc(E, s);
-    g.work_pre.alloc(E + 1, s);
-    if (E == 0) {
-        VRB_CUDA(cudaMemsetAsync(g.work_pre.get(), 0, sizeof(uint64_t), s));
-        g.work = 0;
-        return;
-    }
+    if (E == 0) return;
     {
         DBuf<uint64_t>& k0 = lk0;
         DBuf<uint64_t>& k1 = lk1;
@@ -421,23 +447,38 @@ void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         k_id_lists<<<gw, 256, 0, s>>>(g.off.get(), n, g.nkr.get(), g.np.get(), g.idl.get());
         VRB_LAUNCH_CHECK();
     }
-    {
-        // (c) owner-edge plan: scanned endpoint, prefix length, host; edges by host
-        DBuf<uint64_t> k0(E, s), k1(E, s);
-        DBuf<uint32_t> v0(E, s), v1(E, s);
-        k_assign<<<grid_for(E, 256), 256, 0, s>>>(ev, g.listidx.get(), E, g.scan_v.get(), g.scan_len.get(),
-                                                  k0.get());
-        VRB_LAUNCH_CHECK();
-        uint64_t* skeys = nullptr;
-        const uint32_t* sorted = sort_ids(k0, k1, v0, v1, E, s, &skeys);
-        DBuf<uint32_t> work(E, s);
-        k_hosted_work<<<grid_for(E, 256), 256, 0, s>>>(sorted, skeys, g.scan_v.get(), g.scan_len.get(), g.off.get(),
-                                                       E, g.hosted_v.get(), g.plan.get(), work.get());
-        VRB_LAUNCH_CHECK();
-        exclusive_scan(work.get(), g.work_pre.get(), E, s);
-        VRB_CUDA(cudaMemcpyAsync(&g.work, g.work_pre.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        VRB_CUDA(cudaStreamSynchronize(s));
+    // (c) scanned endpoint of every edge: the one with the shorter prefix of
+    // neighbours older than the edge
+    k_assign<<<grid_for(E, 256), 256, 0, s>>>(ev, g.listidx.get(), E, g.scan_v.get(), g.scan_len.get());
+    VRB_LAUNCH_CHECK();
+}
+
+void build_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, Graph& g) {
+    // owner-edge plan of the owner edges [p_lo, p_hi): scanned endpoint,
+    // prefix length, host; hosted slots grouped by host
+    const int64_t m = p_hi > p_lo ? p_hi - p_lo : 0;
+    g.nplan = m;
+    g.plan.alloc(m, s);
+    g.hosted_v.alloc(m, s);
+    g.work_pre.alloc(m + 1, s);
+    if (m == 0) {
+        VRB_CUDA(cudaMemsetAsync(g.work_pre.get(), 0, sizeof(uint64_t), s));
+        g.work = 0;
+        return;
     }
+    DBuf<uint64_t> k0(m, s), k1(m, s);
+    DBuf<uint32_t> v0(m, s), v1(m, s);
+    k_host_keys<<<grid_for(m, 256), 256, 0, s>>>(ev, g.scan_v.get(), g.scan_len.get(), p_lo, m, k0.get());
+    VRB_LAUNCH_CHECK();
+    uint64_t* skeys = nullptr;
+    const uint32_t* sorted = sort_ids(k0, k1, v0, v1, m, s, &skeys);
+    DBuf<uint32_t> work(m, s);
+    k_hosted_work<<<grid_for(m, 256), 256, 0, s>>>(sorted, skeys, g.scan_v.get(), g.scan_len.get(), g.off.get(), m,
+                                                   p_lo, g.hosted_v.get(), g.plan.get(), work.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(work.get(), g.work_pre.get(), m, s);
+    VRB_CUDA(cudaMemcpyAsync(&g.work, g.work_pre.get() + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace vrb

@@ -1121,7 +1121,7 @@ namespace {
 TetArgs tet_args(const Graph& g, const TriLevels& L) {
     TetArgs A{};
     A.n = g.n;
-    A.E = g.E;
+    A.E = g.nplan;   // hosted slots of the plan (A.E bounds the plan and work_pre)
     A.off = g.off.get();
     A.nkr = g.nkr.get();
     A.nr = g.nr.get();

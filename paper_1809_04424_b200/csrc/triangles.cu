@@ -932,7 +932,7 @@ __global__ void k_bm_words(const uint4* __restrict__ plan, int64_t E, uint32_t* 
 TriArgs graph_args(const Graph& g) {
     TriArgs A{};
     A.n = g.n;
-    A.E = g.E;
+    A.E = g.nplan;   // hosted slots of the plan (A.E bounds the plan and work_pre)
     A.off = g.off.get();
     A.nkr = g.nkr.get();
     A.nr = g.nr.get();
@@ -963,18 +963,19 @@ bool apex_bitmaps_apply(const Graph& g) {
 }
 
 void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words, cudaStream_t s) {
-    bmoff.alloc(g.E + 1, s);
+    const int64_t m = g.nplan;
+    bmoff.alloc(m + 1, s);
     words = 0;
-    if (g.E == 0) {
+    if (m == 0) {
         VRB_CUDA(cudaMemsetAsync(bmoff.get(), 0, sizeof(uint64_t), s));
         return;
     }
-    DBuf<uint32_t> w(g.E, s);
-    k_bm_words<<<(unsigned)std::min<int64_t>(ceil_div(g.E, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
-        g.plan.get(), g.E, w.get());
+    DBuf<uint32_t> w(m, s);
+    k_bm_words<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
+        g.plan.get(), m, w.get());
     VRB_LAUNCH_CHECK();
-    exclusive_scan(w.get(), bmoff.get(), g.E, s);
-    VRB_CUDA(cudaMemcpyAsync(&words, bmoff.get() + g.E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    exclusive_scan(w.get(), bmoff.get(), m, s);
+    VRB_CUDA(cudaMemcpyAsync(&words, bmoff.get() + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
 }
 

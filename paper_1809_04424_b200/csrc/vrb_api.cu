@@ -168,6 +168,29 @@ struct vrb_result {
     uint32_t* h0_death = nullptr;
     std::vector<vrb::Alloc> owned;
 
+    void init(int64_t n_, int32_t d_, const vrb_opts* opts) {
+        device = 0;
+        VRB_CUDA(cudaGetDevice(&device));
+        n = n_;
+        d = d_;
+        maxdim = opts->maxdim;
+        K = opts->maxdim + 1;
+        flags = opts->flags;
+        count[0] = n;
+        local_off[0] = 0;
+        local_n[0] = n;
+    }
+    // edges are held whole; the handle reports the slice of rank / world
+    void set_edges(uint32_t* ev, uint32_t* efilt, int rank, int world) {
+        ev_all = ev;
+        efilt_all = efilt;
+        const int64_t E = count[1], lo = E * rank / world, hi = E * (rank + 1) / world;
+        local_off[1] = lo;
+        local_n[1] = hi - lo;
+        verts[1] = ev ? ev + 2 * lo : nullptr;
+        filt[1] = efilt ? efilt + lo : nullptr;
+    }
+
     template <class T>
     T* own(size_t n_elems, cudaStream_t s) {
         if (n_elems == 0) return nullptr;
@@ -203,16 +226,20 @@ vrb_status guarded(F&& f) {
     }
 }
 
-void check_opts(const double* X, int64_t n, int32_t d, const vrb_opts* opts, vrb_handle* out) {
+void check_opts(const double* X, int64_t n, int32_t d, const vrb_opts* opts, vrb_handle* out, bool x_required) {
     if (!out) fail(VRB_EINVAL, "out handle pointer is NULL");
     *out = nullptr;
     if (!opts) fail(VRB_EINVAL, "opts is NULL");
     if (n < 0) fail(VRB_EINVAL, "n = %lld < 0", (long long)n);
     if (d < 1) fail(VRB_EINVAL, "d = %d < 1", d);
-    if (n > 0 && !X) fail(VRB_EINVAL, "X is NULL");
+    if (x_required && n > 0 && !X) fail(VRB_EINVAL, "X is NULL");
     if (opts->maxdim < 0 || opts->maxdim > 2) fail(VRB_EINVAL, "maxdim = %d not in 0..2", opts->maxdim);
     if (std::isnan(opts->radius) || opts->radius < 0.0) fail(VRB_EINVAL, "radius must be >= 0 (got %g)", opts->radius);
     if (n >= kMaxN) fail(VRB_EOVERFLOW, "n = %lld exceeds the 21-bit vertex id limit", (long long)n);
+    // limits of the layout, checked before any work (DESIGN.md "Limits")
+    if (opts->maxdim >= 2 && n > tets_max_n())
+        fail(VRB_ENOTSUP, "tetrahedra (maxdim 2) need n <= %lld on this device (n = %lld)",
+             (long long)tets_max_n(), (long long)n);
 }
 
 __global__ void k_colptr(uint64_t* colptr, int64_t ncols, uint64_t k1, uint64_t off) {
@@ -244,81 +271,26 @@ __global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, uint32_t* _
         head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
 }
 
-__global__ void k_sum_slices(const uint32_t* __restrict__ all, int64_t E, int world, uint32_t* __restrict__ out) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t s = 0;
-        for (int r = 0; r < world; ++r) s += all[(int64_t)r * E + p];
-        out[p] = s;
-    }
-}
-
-// boundaries[g] = first edge p with toff[p] >= T*g/G, moved back to the start
-// of its filtration level (a level is never split across ranks).
-__global__ void k_partition(const uint64_t* __restrict__ toff, const uint32_t* __restrict__ efilt, int64_t E,
-                            int world, int64_t* __restrict__ bounds) {
-    const int g = threadIdx.x;
-    if (g > world) return;
-    if (g == 0) { bounds[0] = 0; return; }
-    if (g == world) { bounds[world] = E; return; }
-    const uint64_t T = toff[E];
-    const uint64_t target = (uint64_t)(((__uint128_t)T * (uint64_t)g) / (uint64_t)world);
-    int64_t lo = 0, hi = E;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (toff[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    while (lo > 0 && lo < E && efilt[lo - 1] == efilt[lo]) --lo;
-    bounds[g] = lo;
-}
-
 unsigned grid_of(int64_t n) {
     int64_t g = ceil_div(n, 256);
     return (unsigned)(g < 1 ? 1 : (g > 4096 ? 4096 : g));
 }
 
-// Owner-edge range [b[0], b[1]) of `rank`: level-aligned split of the
-// simplex offsets off (E + 1 entries) into `world` equal parts.
-void partition_range(const uint64_t* off, const uint32_t* efilt, int64_t E, int world, int rank, cudaStream_t s,
-                     int64_t* b) {
-    DBuf<int64_t> bd(world + 1, s);
-    k_partition<<<1, 64, 0, s>>>(off, efilt, E, world, bd.get());
-    VRB_LAUNCH_CHECK();
-    VRB_CUDA(cudaMemcpyAsync(b, bd.get() + rank, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    VRB_CUDA(cudaStreamSynchronize(s));
-}
-
-// total = off[E], lo = off[b[0]], hi = off[b[1]]
-void read_offsets(const uint64_t* off, int64_t E, const int64_t* b, cudaStream_t s, uint64_t& total, uint64_t& lo,
-                  uint64_t& hi) {
+// total = off[E]
+uint64_t read_total(const uint64_t* off, int64_t E, cudaStream_t s) {
+    uint64_t total = 0;
     VRB_CUDA(cudaMemcpyAsync(&total, off + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    VRB_CUDA(cudaMemcpyAsync(&lo, off + b[0], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    VRB_CUDA(cudaMemcpyAsync(&hi, off + b[1], sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
+    return total;
 }
 
-// The shared body of vrb_build / vrb_build_dist.
-void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
-                cudaStream_t s, vrb_handle* out, bool matrix = false) {
-    check_opts(X, n, d, opts, out);
-    // limits of the layout, checked before any work (DESIGN.md "Limits")
-    if (opts->maxdim >= 2 && n > tets_max_n())
-        fail(VRB_ENOTSUP, "tetrahedra (maxdim 2) need n <= %lld on this device (n = %lld)",
-             (long long)tets_max_n(), (long long)n);
-    const int rank = comm ? comm->rank : 0;
-    const int world = comm ? comm->world : 1;
-    if (comm && (world < 1 || rank < 0 || rank >= world || !comm->allgather))
-        fail(VRB_EINVAL, "bad communicator (rank %d, world %d)", rank, world);
+// vrb_build / vrb_build_dm (one GPU).
+void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cudaStream_t s, vrb_handle* out,
+                bool matrix = false) {
+    check_opts(X, n, d, opts, out, true);
     vrb_result* h = new vrb_result();
     try {
-        h->device = current_device();
-        h->n = n;
-        h->d = d;
-        h->maxdim = opts->maxdim;
-        h->K = opts->maxdim + 1;
-        h->flags = opts->flags;
-        h->count[0] = n;
-        h->local_off[0] = 0;
-        h->local_n[0] = n;
+        h->init(n, d, opts);
         StageTimer timer;
         timer.start(s);
 
@@ -339,79 +311,54 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
         uint32_t* efilt = h->own<uint32_t>(E, s);
         h->vor = h->own<double>(E, s);
         h->nvals = rank_edges(ke, ev, efilt, h->vor, s);
-        h->ev_all = ev;
-        h->efilt_all = efilt;
+        h->set_edges(ev, efilt, 0, 1);
         ke = KeptEdges();
         timer.mark(1);
-        {
-            const int64_t lo = E * rank / world, hi = E * (rank + 1) / world;
-            h->local_off[1] = lo;
-            h->local_n[1] = hi - lo;
-            h->verts[1] = ev ? ev + 2 * lo : nullptr;
-            h->filt[1] = efilt ? efilt + lo : nullptr;
-        }
         if (h->K >= 2) {
             Graph g;
             build_graph(ev, n, E, s, g);
             timer.mark(2);
-            // ---- triangles: count per owner edge (work split over the ranks), offsets
+            // ---- triangles: count per owner edge, offsets
             DBuf<uint32_t> cnt(E, s);
-            // single rank: the count pass keeps the apex bitmaps the fill emits from
+            // the count pass keeps the apex bitmaps the fill emits from
             DBuf<uint64_t> bmoff;
             DBuf<uint32_t> bm;
-            if (world == 1 && apex_bitmaps_apply(g)) {
+            if (apex_bitmaps_apply(g)) {
                 uint64_t words = 0;
                 apex_bitmap_offsets(g, bmoff, words, s);
                 bm.alloc(words ? words : 1, s);
                 count_triangles_bm(g, cnt.get(), bm.get(), bmoff.get(), s);
             } else {
-                count_triangles(g, cnt.get(), rank, world, s);
-            }
-            if (world > 1) {
-                // the exchange: every rank counted a disjoint, work-balanced part
-                // of the owner edges; gather and add the parts
-                DBuf<uint32_t> all((size_t)E * world, s);
-                if (comm->allgather(cnt.get(), all.get(), E * sizeof(uint32_t), (void*)s, comm->ctx) != 0)
-                    fail(VRB_ECOMM, "allgather of triangle counts failed");
-                k_sum_slices<<<grid_of(E), 256, 0, s>>>(all.get(), E, world, cnt.get());
-                VRB_LAUNCH_CHECK();
-                timer.mark(6);
+                count_triangles(g, cnt.get(), 0, 1, s);
             }
             DBuf<uint64_t> toff(E + 1, s);
             exclusive_scan(cnt.get(), toff.get(), E, s);
-            // owner-edge range of this rank (whole levels); with tetrahedra every
-            // rank needs all triangles (face positions of D_3)
-            int64_t tb_[2] = {0, E};
-            if (world > 1 && h->K == 2) partition_range(toff.get(), efilt, E, world, rank, s, tb_);
-            uint64_t T = 0, t0 = 0, t1 = 0;
-            read_offsets(toff.get(), E, tb_, s, T, t0, t1);
+            const uint64_t T = read_total(toff.get(), E, s);
             if (T >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu triangles exceed u32 positions", (unsigned long long)T);
             h->count[2] = (int64_t)T;
-            h->local_off[2] = (int64_t)t0;
-            h->local_n[2] = (int64_t)(t1 - t0);
-            const int64_t Tl = h->local_n[2];
-            uint32_t* tv = h->own<uint32_t>(3 * Tl, s);
-            uint32_t* tf = h->own<uint32_t>(Tl, s);
+            h->local_off[2] = 0;
+            h->local_n[2] = (int64_t)T;
+            uint32_t* tv = h->own<uint32_t>(3 * T, s);
+            uint32_t* tf = h->own<uint32_t>(T, s);
             uint32_t* trows = nullptr;
-            if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * Tl, s);
+            if (!(opts->flags & VRB_SKIP_BOUNDARY)) trows = h->own<uint32_t>(3 * T, s);
             // apex of every triangle (tetrahedra: face positions by owner-edge search)
             DBuf<uint16_t> tapex;
             if (h->K >= 3 && n <= 65536) {   // padded: the face search reads 16-byte chunks past the end
-                tapex.alloc((size_t)Tl + 16, s);
-                VRB_CUDA(cudaMemsetAsync(tapex.get() + Tl, 0xFF, 16 * sizeof(uint16_t), s));
+                tapex.alloc((size_t)T + 16, s);
+                VRB_CUDA(cudaMemsetAsync(tapex.get() + T, 0xFF, 16 * sizeof(uint16_t), s));
             }
             timer.mark(3);
-            fill_triangles(g, efilt, toff.get(), tb_[0], tb_[1], t0, tv, tf, trows, tapex.get(), s, bm.get(),
-                           bmoff.get());
+            fill_triangles(g, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s, bm.get(), bmoff.get());
             bm.reset();
             timer.mark(4);
-            sort_tie_groups(2, efilt, toff.get(), E, tb_[0], tb_[1], n, tv, trows, s);
+            sort_tie_groups(2, efilt, toff.get(), E, 0, E, n, tv, trows, s);
             timer.mark(5);
             h->verts[2] = tv;
             h->filt[2] = tf;
             h->rows[2] = trows;
             if (h->K >= 3) {
-                // ---- tetrahedra (all triangles are on this rank)
+                // ---- tetrahedra
                 TriLevels L;
                 L.apex = tapex.get();
                 L.ev = ev;
@@ -419,47 +366,74 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, con
                 triangle_levels(efilt, toff.get(), E, tv, s, L);
                 DBuf<uint32_t> qc(E, s);
                 timer.mark(3);
-                count_tets(g, L, qc.get(), rank, world, s);
-                if (world > 1) {
-                    DBuf<uint32_t> all((size_t)E * world, s);
-                    if (comm->allgather(qc.get(), all.get(), E * sizeof(uint32_t), (void*)s, comm->ctx) != 0)
-                        fail(VRB_ECOMM, "allgather of tetrahedron counts failed");
-                    k_sum_slices<<<grid_of(E), 256, 0, s>>>(all.get(), E, world, qc.get());
-                    VRB_LAUNCH_CHECK();
-                }
+                count_tets(g, L, qc.get(), 0, 1, s);
                 DBuf<uint64_t> qoff(E + 1, s);
                 exclusive_scan(qc.get(), qoff.get(), E, s);
-                int64_t qb[2] = {0, E};
-                if (world > 1) partition_range(qoff.get(), efilt, E, world, rank, s, qb);
-                uint64_t Q = 0, q0 = 0, q1 = 0;
-                read_offsets(qoff.get(), E, qb, s, Q, q0, q1);
+                const uint64_t Q = read_total(qoff.get(), E, s);
                 if (Q >= 0xFFFFFFFFull)
                     fail(VRB_EOVERFLOW, "%llu tetrahedra exceed u32 positions", (unsigned long long)Q);
                 h->count[3] = (int64_t)Q;
-                h->local_off[3] = (int64_t)q0;
-                h->local_n[3] = (int64_t)(q1 - q0);
-                const int64_t Ql = h->local_n[3];
-                h->verts[3] = h->own<uint32_t>(4 * Ql, s);
-                h->filt[3] = h->own<uint32_t>(Ql, s);
-                if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[3] = h->own<uint32_t>(4 * Ql, s);
+                h->local_off[3] = 0;
+                h->local_n[3] = (int64_t)Q;
+                h->verts[3] = h->own<uint32_t>(4 * Q, s);
+                h->filt[3] = h->own<uint32_t>(Q, s);
+                if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[3] = h->own<uint32_t>(4 * Q, s);
                 timer.mark(8);
-                fill_tets(g, L, efilt, qoff.get(), qb[0], qb[1], q0, h->verts[3], h->filt[3], h->rows[3], s);
+                fill_tets(g, L, efilt, qoff.get(), 0, E, 0, h->verts[3], h->filt[3], h->rows[3], s);
                 timer.mark(9);
-                sort_tie_groups(3, efilt, qoff.get(), E, qb[0], qb[1], n, h->verts[3], h->rows[3], s);
+                sort_tie_groups(3, efilt, qoff.get(), E, 0, E, n, h->verts[3], h->rows[3], s);
                 timer.mark(5);
-                // triangles: this rank reports its slice of the (replicated) dimension 2
-                if (world > 1) {
-                    int64_t tp[2] = {0, E};
-                    partition_range(toff.get(), efilt, E, world, rank, s, tp);
-                    uint64_t Tt, a0, a1;
-                    read_offsets(toff.get(), E, tp, s, Tt, a0, a1);
-                    h->local_off[2] = (int64_t)a0;
-                    h->local_n[2] = (int64_t)(a1 - a0);
-                    h->verts[2] = tv + 3 * a0;
-                    h->filt[2] = tf + a0;
-                    h->rows[2] = trows ? trows + 3 * a0 : nullptr;
-                }
             }
+        }
+        VRB_CUDA(cudaStreamSynchronize(s));
+        VRB_CUDA(cudaGetLastError());
+        timer.finish();
+        *out = h;
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaGetLastError();
+        h->release_all();
+        delete h;
+        throw;
+    }
+}
+
+// vrb_build_dist: this rank's slices (dist.cu) wrapped in a handle.
+void build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm, cudaStream_t s,
+                vrb_handle* out) {
+    if (!comm) fail(VRB_EINVAL, "comm is NULL");
+    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world || !comm->allgather || !comm->broadcast)
+        fail(VRB_EINVAL, "bad communicator (rank %d, world %d)", comm->rank, comm->world);
+    check_opts(X, n, d, opts, out, comm->rank == 0);
+    vrb_result* h = new vrb_result();
+    try {
+        h->init(n, d, opts);
+        StageTimer timer;
+        timer.start(s);
+        DistOut o;
+        o.timer = &timer;
+        o.alloc_u32 = [&](size_t m) { return h->own<uint32_t>(m, s); };
+        o.alloc_f64 = [&](size_t m) { return h->own<double>(m, s); };
+        build_dist_impl(X, n, d, opts, comm, s, o);
+        h->count[1] = o.E;
+        h->vor = o.vor;
+        h->nvals = o.nvals;
+        h->set_edges(o.ev, o.efilt, comm->rank, comm->world);
+        if (h->K >= 2) {
+            h->count[2] = (int64_t)o.T;
+            h->local_off[2] = (int64_t)o.t0;
+            h->local_n[2] = (int64_t)o.Tl;
+            h->verts[2] = o.tv;
+            h->filt[2] = o.tf;
+            h->rows[2] = o.trows;
+        }
+        if (h->K >= 3) {
+            h->count[3] = (int64_t)o.Q;
+            h->local_off[3] = (int64_t)o.q0;
+            h->local_n[3] = (int64_t)o.Ql;
+            h->verts[3] = o.qv;
+            h->filt[3] = o.qf;
+            h->rows[3] = o.qrows;
         }
         VRB_CUDA(cudaStreamSynchronize(s));
         VRB_CUDA(cudaGetLastError());
@@ -492,13 +466,13 @@ vrb_status vrb_set_allocator(vrb_alloc_fn alloc, vrb_free_fn free_fn, void* ctx)
 }
 
 vrb_status vrb_build(const double* X, int64_t n, int32_t d, const vrb_opts* opts, void* stream, vrb_handle* out) {
-    return guarded([&] { build_impl(X, n, d, opts, nullptr, (cudaStream_t)stream, out); });
+    return guarded([&] { build_impl(X, n, d, opts, (cudaStream_t)stream, out); });
 }
 
 vrb_status vrb_build_dm(const double* D, int64_t n, const vrb_opts* opts, void* stream, vrb_handle* out) {
     return guarded([&] {
         if (opts && (opts->flags & VRB_DIM_MAJOR)) fail(VRB_EINVAL, "VRB_DIM_MAJOR does not apply to a distance matrix");
-        build_impl(D, n, 1, opts, nullptr, (cudaStream_t)stream, out, true);
+        build_impl(D, n, 1, opts, (cudaStream_t)stream, out, true);
     });
 }
 
@@ -513,9 +487,15 @@ vrb_status vrb_latlon2euc(const double* latlon_dev, int64_t n, double* xyz_dev, 
 
 vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
                           void* stream, vrb_handle* out) {
+    return guarded([&] { build_dist(X, n, d, opts, comm, (cudaStream_t)stream, out); });
+}
+
+vrb_status vrb_partition_bounds(const uint64_t* prefix, const uint32_t* efilt, int64_t E, int32_t world,
+                                int64_t* bounds) {
     return guarded([&] {
-        if (!comm) fail(VRB_EINVAL, "comm is NULL");
-        build_impl(X, n, d, opts, comm, (cudaStream_t)stream, out);
+        if (!prefix || !bounds || (E > 0 && !efilt)) fail(VRB_EINVAL, "NULL pointer");
+        if (E < 0 || world < 1) fail(VRB_EINVAL, "E < 0 or world < 1");
+        vrb::partition_bounds_host(prefix, efilt, E, world, bounds);
     });
 }
 

@@ -2,12 +2,16 @@
 // launchers over device buffers.  Product path only.
 #pragma once
 
+#include <functional>
+
 #include "vrb_internal.cuh"
 
 namespace vrb {
 
-// S1: device copy of the points, row-major n x d, finite-checked.
-void place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out);
+// S1: device copy of the points, row-major n x d, finite-checked (a
+// non-finite coordinate: VRB_EINVAL, or with soft a false return).
+bool place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_t s, DBuf<double>& out,
+                  bool soft = false);
 
 // d2 threshold equivalent to the cap on sqrt_rn(d2) (reading A1); < 0: none kept.
 double cap_threshold(double r, bool strict);
@@ -19,8 +23,11 @@ struct KeptEdges {
     bool packed = false;  // n <= 65536: (i << 16 | j) in pij, else i, j in ei, ej
     DBuf<uint32_t> ei, ej, pij;
 };
+// Rows [row_lo, row_hi) only (a rank's row block; row_lo and row_hi < n
+// multiples of edge_tile(); row_hi = -1: to n): their pairs j > i.
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
-                      KeptEdges& out);
+                      KeptEdges& out, int64_t row_lo = 0, int64_t row_hi = -1);
+int64_t edge_tile();
 
 // F3: distance-matrix input.  place_matrix copies (if host) and checks D
 // (n x n, off-diagonal finite, >= 0, symmetric; VRB_EINVAL otherwise);
@@ -35,6 +42,19 @@ void latlon2euc(const double* latlon, int64_t n, double* xyz, cudaStream_t s);
 //   efilt : E u32 dense rank, 1-based                    (caller-allocated)
 //   vor   : >= nvals f64, vor[f-1] = length of level f  (caller-allocated, E entries)
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s);
+// The sort of rank_edges alone: key[q] + bias = length bits of the q-th edge
+// in (len, i, j) order; val[q] = packed (i << 16 | j) when packed, else the
+// lex index into ke.ei / ke.ej.  Buffers owned here or by ke (keep both alive).
+struct SortedEdges {
+    int64_t E = 0;
+    bool packed = false;
+    const uint64_t* key = nullptr;
+    const uint32_t* val = nullptr;
+    uint64_t bias = 0;
+    DBuf<uint64_t> key_alt;
+    DBuf<uint32_t> perm, perm_alt;
+};
+void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so);
 
 // S4: neighbourhoods of the edge graph, used by the simplex enumeration.
 struct Graph {
@@ -55,11 +75,17 @@ struct Graph {
     DBuf<uint4> plan;          // E: per hosted slot (edge position p, scanned x, prefix length, deg x),
                                //    slots sorted by (host endpoint, longest prefix first)
     DBuf<uint32_t> hosted_v;   // E: host endpoint of each hosted slot
-    DBuf<uint64_t> work_pre;   // E + 1: exclusive prefix of scan_len over hosted order
+    DBuf<uint64_t> work_pre;   // nplan + 1: exclusive prefix of scan_len over hosted order
+    int64_t nplan = 0;         // hosted slots in the plan (owner edges of [p_lo, p_hi))
     uint64_t work = 0;
     uint32_t max_deg = 0;
 };
+// build_graph = build_lists + build_plan over every owner edge
 void build_graph(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g);
+// the neighbour lists and the scanned endpoint of every edge (scan_v, scan_len)
+void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph& g);
+// the owner-edge plan of the edges [p_lo, p_hi) only (plan, hosted_v, work_pre, nplan, work)
+void build_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, Graph& g);
 
 // S5 + S7 + S8 for triangles (owner-edge enumeration, see triangles.cu).
 // Count per owner edge: cnt[p] (E entries, zero-initialised here).  The
@@ -122,5 +148,26 @@ int64_t gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t kdim, const uint6
 // and their filt.
 int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t E, cudaStream_t s,
                   uint32_t* (*alloc_out)(int64_t, void*), void* ctx, uint32_t** pos_out, uint32_t** death_out);   // largest n the shared-memory vertex map supports
+
+// Multi-GPU build (dist.cu).  Outputs are allocated through the callbacks
+// (handle-owned); this rank's slices of dimensions 2 and 3.
+struct DistOut {
+    StageTimer* timer = nullptr;
+    std::function<uint32_t*(size_t)> alloc_u32;
+    std::function<double*(size_t)> alloc_f64;
+    int64_t E = 0, nvals = 0;
+    uint32_t* ev = nullptr;
+    uint32_t* efilt = nullptr;
+    double* vor = nullptr;
+    uint64_t T = 0, t0 = 0, Tl = 0;
+    uint32_t *tv = nullptr, *tf = nullptr, *trows = nullptr;
+    uint64_t Q = 0, q0 = 0, Ql = 0;
+    uint32_t *qv = nullptr, *qf = nullptr, *qrows = nullptr;
+};
+void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, const vrb_comm* comm,
+                     cudaStream_t s, DistOut& o);
+// The owner-edge partition rule (host copy of the device one, for tests):
+// bounds[g], g = 0..G, over the work prefix (E + 1 entries).
+void partition_bounds_host(const uint64_t* prefix, const uint32_t* efilt, int64_t E, int G, int64_t* bounds);
 
 }  // namespace vrb

@@ -58,25 +58,15 @@ def test_gloo_allgather_count_exchange():
 
 
 # ---------------------------------------------------------------------------
-# virtual-rank simulation of the level-aligned owner-edge partition
+# virtual-rank simulation of the level-aligned owner-edge partition, driven
+# by the library's own rule (any per-edge work vector; world up to 100)
 # ---------------------------------------------------------------------------
 
-def partition_bounds(off, efilt, world):
-    """Re-implementation of the library's split (vrb_api.cu k_partition):
-    bound g = first owner edge p with off[p] >= floor(T g / G), moved back to
-    the start of its filtration level."""
-    E = len(efilt)
-    T = int(off[E])
-    b = [0]
-    for g in range(1, world):
-        target = (T * g) // world
-        p = int(np.searchsorted(off[: E + 1], target, side="left"))
-        p = min(p, E)
-        while 0 < p < E and efilt[p - 1] == efilt[p]:
-            p -= 1
-        b.append(p)
-    b.append(E)
-    return b
+def partition_bounds(work_prefix, efilt, world):
+    """The library's owner-edge split (vrb_partition_bounds: the same
+    __host__ __device__ function the multi-GPU build runs on the device)."""
+    import paper_1809_04424_b200 as vrb
+    return [int(x) for x in vrb.partition_bounds(np.asarray(work_prefix, dtype=np.uint64), efilt, world)]
 
 
 def _owner(o, simplex):
@@ -101,8 +91,11 @@ def test_partition_slices_concatenate_to_global_order(case):
         owners = np.array([_owner(o, s) for s in v], dtype=np.int64)
         cnt = np.bincount(owners, minlength=o.E) if len(owners) else np.zeros(o.E, np.int64)
         off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
-        for world in (1, 2, 3, 4, 8):
-            b = partition_bounds(off, ef, world)
+        rng = np.random.default_rng(case)
+        works = {"counts": off, "random": np.concatenate([[0], np.cumsum(rng.integers(0, 50, o.E))])}
+        for (wname, wpre), world in [(w, g) for w in works.items() for g in (1, 2, 3, 4, 8, 64, 100)]:
+            b = partition_bounds(wpre, ef, world)
+            assert len(b) == world + 1
             assert b[0] == 0 and b[-1] == o.E and all(x <= y for x, y in zip(b, b[1:]))
             pieces = []
             for g in range(world):
@@ -125,3 +118,48 @@ def test_partition_edge_slices():
         cuts = [E * g // world for g in range(world + 1)]
         assert cuts[0] == 0 and cuts[-1] == E
         assert sum(cuts[g + 1] - cuts[g] for g in range(world)) == E
+
+
+def test_partition_bounds_balance_and_errors():
+    import paper_1809_04424_b200 as vrb
+    # distinct levels: the split lands at the first edge reaching g / G of the work
+    E = 1000
+    ef = np.arange(1, E + 1, dtype=np.uint32)
+    pre = np.arange(E + 1, dtype=np.uint64) * 3
+    b = vrb.partition_bounds(pre, ef, 4)
+    assert b.tolist() == [0, 250, 500, 750, 1000]
+    # one level for everything: a level is never split -> all on the last rank
+    b = vrb.partition_bounds(pre, np.ones(E, dtype=np.uint32), 4)
+    assert b.tolist() == [0, 0, 0, 0, 1000]
+    # empty input
+    assert vrb.partition_bounds(np.zeros(1, np.uint64), np.zeros(0, np.uint32), 3).tolist() == [0, 0, 0, 0]
+    with pytest.raises(vrb.VrbError):
+        vrb.partition_bounds(pre, ef, 0)
+
+
+def _bcast_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1809_04424_b200 as vrb
+        X = np.random.default_rng(1).standard_normal((50, 3))
+        buf = torch.from_numpy(X.copy().view(np.uint8).reshape(-1)) if rank == 0 else torch.zeros(X.nbytes, dtype=torch.uint8)
+        vrb.broadcast_bytes(buf, 0)
+        out_q.put((rank, bool(np.array_equal(buf.numpy().view(np.float64).reshape(50, 3), X))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_broadcast_points():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(0, True), (1, True)]

@@ -39,8 +39,11 @@ def _np(t):
     return t.cpu().numpy().view(np.uint32) if t.dtype == torch.int32 else t.cpu().numpy()
 
 
-def compare(vrb, X, maxdim, radius, strict=False, via_torch_alloc=False):
-    res = vrb.build(X, maxdim=maxdim, radius=radius, strict=strict)
+def compare(vrb, X, maxdim, radius, strict=False, via_torch_alloc=False, res=None):
+    """Element-by-element parity of a build of X (or of `res`, a build of the
+    same points passed in another layout) against the oracle on X."""
+    if res is None:
+        res = vrb.build(X, maxdim=maxdim, radius=radius, strict=strict)
     o = oracle.Oracle(X, radius, strict)
     ev, ef, el, vor = o.edges()
     assert res.count(0)[0] == X.shape[0]
@@ -178,12 +181,47 @@ def test_lattice_heavy_ties_large_segments(vrb):
     compare(vrb, X, 1, 2.0)
 
 
-def test_dim_major_and_device_points(vrb):
+def test_device_points(vrb):
     X = workloads.random_cloud(5, 120, 3, "gauss")
     res, o = compare(vrb, X, 1, 1.3)
     Xd = torch.from_numpy(X).cuda()
-    r2 = vrb.build(Xd, maxdim=1, radius=1.3)
-    np.testing.assert_array_equal(_np(r2.simplices(2)[0]), _np(res.simplices(2)[0]))
+    compare(vrb, X, 1, 1.3, res=vrb.build(Xd, maxdim=1, radius=1.3))
+
+
+# rowsare="dimensions": a d x n array whose COLUMNS are the
+# points, passed as is with VRB_DIM_MAJOR; the library transposes on the
+# device.  Host and device inputs, several tiles plus a ragged tail, d = 1,
+# ties (lattice), tetrahedra, strict caps.
+@pytest.mark.parametrize("on_device", [False, True])
+@pytest.mark.parametrize("case", range(5))
+def test_rowsare_dimensions(vrb, on_device, case):
+    n, d, kind, maxdim, radius, strict = [
+        (300, 3, "gauss", 2, 0.9, False),
+        (257, 7, "uniform", 1, math.inf, False),
+        (130, 1, "uniform", 1, 0.05, True),
+        (0, 3, "uniform", 1, 1.0, False),
+        (None, 3, "lattice", 2, 1.5, False)][case]
+    X = workloads.integer_lattice(4, 3) if n is None else workloads.random_cloud(77 + case, n, d, kind)
+    Xt = np.ascontiguousarray(X.T)                       # d x n
+    arg = torch.from_numpy(Xt).cuda() if on_device else Xt
+    res = vrb.build(arg, maxdim=maxdim, radius=radius, strict=strict, rowsare="dimensions")
+    assert res.count(0)[0] == X.shape[0]
+    compare(vrb, X, maxdim, radius, strict=strict, res=res)
+
+
+def test_rowsare_dimensions_worldmap_pipeline(vrb):
+    # the paper's WorldMap call sequence: latlon (n x 2 degrees)
+    # -> latlon2euc -> a 3 x n matrix -> eirene(c, rowsare="dimensions",
+    # upperlim=0.15); 2000 synthetic cities uniform on the sphere
+    rng = np.random.default_rng(1809)
+    n = 2000
+    ll = np.stack([np.degrees(np.arcsin(rng.uniform(-1, 1, n))), rng.uniform(-180, 180, n)], 1)
+    xyz = vrb.latlon2euc(torch.from_numpy(ll).cuda())     # n x 3, device
+    c = xyz.T.contiguous()                                # 3 x n, as the paper's latlon2euc returns
+    res = vrb.build(c, maxdim=1, radius=0.15, rowsare="dimensions")
+    compare(vrb, xyz.cpu().numpy(), 1, 0.15, res=res)
+    with pytest.raises(ValueError):
+        vrb.build(c, rowsare="columns")
 
 
 def test_high_degree_over_apex_bitmap_limit(vrb):
