@@ -266,6 +266,22 @@ def main():
             del r
         h0 = {"ms": float(np.median(h0_ms)), "ms_all": h0_ms, "essential_bars": int(ness),
               "finite_bars": int(counts[0][0] - ness) if counts else None}
+        # F1 "clear and compress": D_2 without the H0 forest's rows,
+        # on a build whose H0 is already computed (device-timed, not part of the step)
+        if w.maxdim >= 1:
+            r = one_build(Xd)
+            r.h0()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            cp, rv, rm = r.compress_d2()
+            e1.record(s)
+            torch.cuda.synchronize()
+            T_ = counts[2][0]
+            h0["clear_compress"] = {"ms": e0.elapsed_time(e1), "d2_rows": int(counts[1][0]), "rows_kept": int(rm.numel()),
+                                    "d2_nnz": int(3 * T_), "nnz_kept": int(rv.numel()),
+                                    "nnz_removed_frac": (1.0 - rv.numel() / (3 * T_)) if T_ else 0.0}
+            del r, cp, rv, rm
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)

@@ -222,6 +222,26 @@ vrb_status vrb_latlon2euc(const double* latlon_dev, int64_t n, double* xyz_dev, 
 vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const uint32_t** death_filt,
                   int64_t* n_finite, int64_t* n_essential);
 
+/* "Clear and compress" of D_2 ("a preprocessing step
+ * motivated by homological algebra, which reduces the size of the boundary
+ * operator before it is passed to either Pers or LU", after Bauer, Kerber
+ * and Reininghaus).  The pivots of a reduced D_2 lie in the rows of edges
+ * whose own D_1 column reduces to zero; the other edges -- the D_1 pivot
+ * columns, i.e. the H0 forest of vrb_h0 -- are removed from D_2's rows,
+ * which leaves every pivot pair (every dimension-1 bar) unchanged.
+ * Output (device, handle-owned, computed on the first call on `stream` and
+ * cached; vrb_h0 runs first if it has not):
+ *   nrows  : E - (forest size): the edges kept as rows
+ *   nnz    : entries of the compressed matrix
+ *   colptr : this handle's D_2 columns + 1 u64 offsets (column j of the
+ *            slice = rows rowval[colptr[j] .. colptr[j+1]), ascending)
+ *   rowval : u32 compressed row indices
+ *   rowmap : nrows u32, compressed row -> edge position (ascending)
+ * A column keeps 1 to 3 rows (a forest holds no triangle's three edges).
+ * VRB_EINVAL without dimension 2 or with VRB_SKIP_BOUNDARY. */
+vrb_status vrb_compress_d2(vrb_handle h, void* stream, int64_t* nrows, int64_t* nnz, const uint64_t** colptr,
+                           const uint32_t** rowval, const uint32_t** rowmap);
+
 /* sortperm (Fig. GPU_sortperm) on device: perm_dev gets
  * the 0-based stable ascending permutation of keys_dev (n doubles; -0.0 ==
  * +0.0; NaN -> VRB_EINVAL), dense_rank_dev (nullable) gets 1-based dense ranks

@@ -34,7 +34,7 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_partition_bounds", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
+           "vrb_free", "vrb_sortperm_f64", "vrb_partition_bounds", "vrb_compress_d2", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
            "vrb_build_dm",
            "vrb_latlon2euc", "vrb_gf2_blockprodsum", "vrb_gf2_csc", "vrb_gf2_free")
 
@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
     L.vrb_gf2_free.argtypes = [p]
     L.vrb_partition_bounds.restype = ctypes.c_int
     L.vrb_partition_bounds.argtypes = [p, p, i64, i32, p]
+    L.vrb_compress_d2.restype = ctypes.c_int
+    L.vrb_compress_d2.argtypes = [p, p, P(i64), P(i64), P(p), P(p), P(p)]
     L.vrb_h0.restype = ctypes.c_int
     L.vrb_h0.argtypes = [p, p, P(p), P(p), P(i64), P(i64)]
     _lib = L
@@ -255,6 +257,20 @@ class VRResult:
                             ctypes.byref(nf), ctypes.byref(ne)))
         return (_view(pos.value, (nf.value,), "<i4", self, self.device),
                 _view(dth.value, (nf.value,), "<i4", self, self.device), ne.value)
+
+    def compress_d2(self, stream=None):
+        """vrb_compress_d2 ("clear and compress"): D_2
+        without the rows of the H0 forest edges (the D_1 pivot columns).
+        Returns (colptr (ncols+1,) int64, rowval (nnz,) int32[u32] compressed
+        rows, rowmap (nrows,) int32[u32] compressed row -> edge position)."""
+        nr, nz = ctypes.c_int64(), ctypes.c_int64()
+        cp, rv, rm = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().vrb_compress_d2(self._h, _stream_ptr(stream), ctypes.byref(nr), ctypes.byref(nz),
+                                     ctypes.byref(cp), ctypes.byref(rv), ctypes.byref(rm)))
+        nc = self.count(2)[2]
+        return (_view(cp.value, (nc + 1,), "<i8", self, self.device),
+                _view(rv.value, (nz.value,), "<i4", self, self.device),
+                _view(rm.value, (nr.value,), "<i4", self, self.device))
 
     def rank_values(self):
         p, nv = ctypes.c_void_p(), ctypes.c_int64()
@@ -457,6 +473,15 @@ def broadcast_bytes(buf, root: int, group=None):
     buf.copy_(h)
 
 
+def _torch_stream(ptr, device):
+    """torch view of the library's stream.  0 is the legacy default stream:
+    torch.cuda.ExternalStream(0) would hand out a fresh pool stream instead,
+    so stream 0 maps to torch's default stream (the legacy one)."""
+    import torch
+
+    return torch.cuda.ExternalStream(int(ptr), device=device) if ptr else torch.cuda.default_stream(device)
+
+
 def _comm_callbacks(device, world, group):
     """The vrb_comm callbacks over torch.distributed.  Each one runs its
     collective with the library's build stream as torch's current stream, so
@@ -466,7 +491,7 @@ def _comm_callbacks(device, world, group):
 
     def _allgather(send, recv, nbytes, stream_, ctx):
         try:
-            with torch.cuda.stream(torch.cuda.ExternalStream(int(stream_ or 0), device=device)):
+            with torch.cuda.stream(_torch_stream(stream_, device)):
                 src = torch.as_tensor(_CAI(send, (nbytes,), "|u1", None), device=device)
                 dst = torch.as_tensor(_CAI(recv, (nbytes * world,), "|u1", None), device=device)
                 allgather_bytes(src, dst, group)
@@ -477,7 +502,7 @@ def _comm_callbacks(device, world, group):
 
     def _broadcast(buf, nbytes, root, stream_, ctx):
         try:
-            with torch.cuda.stream(torch.cuda.ExternalStream(int(stream_ or 0), device=device)):
+            with torch.cuda.stream(_torch_stream(stream_, device)):
                 t = torch.as_tensor(_CAI(buf, (nbytes,), "|u1", None), device=device)
                 broadcast_bytes(t, root, group)
             return 0

@@ -236,4 +236,85 @@ int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t 
     return (int64_t)nf;
 }
 
+// ---------------------------------------------------------------------------
+// "Clear and compress" (Bauer-Kerber-Reininghaus, cited there): the
+// pivots of a reduced D_k lie in rows of POSITIVE (k-1)-simplices -- those
+// whose own column of D_{k-1} reduces to zero -- so deleting the rows of the
+// negative ones leaves every pivot pair of D_k unchanged.  For k = 2 the
+// negative edges are exactly the D_1 pivot columns, i.e. the H0 forest, so
+// D_2 is compressed by dropping the forest's rows.  Rows are renumbered
+// densely in position order (rowmap: new row -> edge position); a column
+// keeps 1..3 entries (a forest has no cycle, so never 0), ascending.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_keep_flags(const uint32_t* __restrict__ forest, int64_t nf, uint32_t* __restrict__ keep) {
+    GRID_STRIDE(q, nf) keep[forest[q]] = 0u;
+}
+
+__global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __restrict__ newidx, int64_t E,
+                         uint32_t* __restrict__ rowmap) {
+    GRID_STRIDE(e, E) if (keep[e]) rowmap[newidx[e]] = (uint32_t)e;
+}
+
+__global__ void k_col_counts(const uint32_t* __restrict__ rows, int64_t ncols, const uint32_t* __restrict__ keep,
+                             uint32_t* __restrict__ cnt) {
+    GRID_STRIDE(j, ncols) cnt[j] = keep[rows[3 * j]] + keep[rows[3 * j + 1]] + keep[rows[3 * j + 2]];
+}
+
+__global__ void k_col_fill(const uint32_t* __restrict__ rows, int64_t ncols, const uint32_t* __restrict__ keep,
+                           const uint64_t* __restrict__ newidx, const uint64_t* __restrict__ colptr,
+                           uint32_t* __restrict__ out) {
+    GRID_STRIDE(j, ncols) {
+        uint64_t o = colptr[j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t r = rows[3 * j + c];
+            if (keep[r]) out[o++] = (uint32_t)newidx[r];
+        }
+    }
+}
+
+}  // namespace
+
+int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_t* rows, int64_t ncols,
+                    cudaStream_t s, uint64_t* colptr, uint32_t* (*alloc_out)(int64_t, void*), void* ctx,
+                    uint32_t** rowval_out, uint32_t** rowmap_out, int64_t* nrows_out) {
+    *rowval_out = nullptr;
+    *rowmap_out = nullptr;
+    DBuf<uint32_t> keep(std::max<int64_t>(E, 1), s);
+    fill_u32(keep.get(), 1u, E, s);
+    if (nf) {
+        k_keep_flags<<<grid_for(nf), 256, 0, s>>>(forest, nf, keep.get());
+        VRB_LAUNCH_CHECK();
+    }
+    DBuf<uint64_t> newidx(E + 1, s);
+    exclusive_scan(keep.get(), newidx.get(), E, s);
+    uint64_t nr = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nr, newidx.get() + E, sizeof(nr), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    *nrows_out = (int64_t)nr;
+    *rowmap_out = alloc_out((int64_t)nr, ctx);
+    if (nr) {
+        k_rowmap<<<grid_for(E), 256, 0, s>>>(keep.get(), newidx.get(), E, *rowmap_out);
+        VRB_LAUNCH_CHECK();
+    }
+    DBuf<uint32_t> cnt(std::max<int64_t>(ncols, 1), s);
+    if (ncols) {
+        k_col_counts<<<grid_for(ncols), 256, 0, s>>>(rows, ncols, keep.get(), cnt.get());
+        VRB_LAUNCH_CHECK();
+    }
+    exclusive_scan(cnt.get(), colptr, ncols, s);
+    uint64_t nnz = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nnz, colptr + ncols, sizeof(nnz), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    *rowval_out = alloc_out((int64_t)nnz, ctx);
+    if (nnz) {
+        k_col_fill<<<grid_for(ncols), 256, 0, s>>>(rows, ncols, keep.get(), newidx.get(), colptr, *rowval_out);
+        VRB_LAUNCH_CHECK();
+    }
+    VRB_CUDA(cudaStreamSynchronize(s));
+    return (int64_t)nnz;
+}
+
 }  // namespace vrb

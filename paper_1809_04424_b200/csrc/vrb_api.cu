@@ -166,6 +166,11 @@ struct vrb_result {
     int64_t h0_nf = 0;
     uint32_t* h0_pos = nullptr;
     uint32_t* h0_death = nullptr;
+    bool c2_done = false;            // vrb_compress_d2 cache
+    int64_t c2_nrows = 0, c2_nnz = 0;
+    uint64_t* c2_colptr = nullptr;
+    uint32_t* c2_rowval = nullptr;
+    uint32_t* c2_rowmap = nullptr;
     std::vector<vrb::Alloc> owned;
 
     void init(int64_t n_, int32_t d_, const vrb_opts* opts) {
@@ -583,6 +588,35 @@ vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const
         if (death_filt) *death_filt = h->h0_death;
         if (n_finite) *n_finite = h->h0_nf;
         if (n_essential) *n_essential = h->n - h->h0_nf;
+    });
+}
+
+vrb_status vrb_compress_d2(vrb_handle h, void* stream, int64_t* nrows, int64_t* nnz, const uint64_t** colptr,
+                           const uint32_t** rowval, const uint32_t** rowmap) {
+    return guarded([&] {
+        if (!h) fail(VRB_EINVAL, "NULL handle");
+        if (h->K < 2) fail(VRB_EINVAL, "the build has no dimension 2 (maxdim 0)");
+        if (h->flags & VRB_SKIP_BOUNDARY) fail(VRB_EINVAL, "D_2 was not materialised (VRB_SKIP_BOUNDARY)");
+        const cudaStream_t s = (cudaStream_t)stream;
+        if (!h->h0_done) {
+            H0Alloc ctx{h, s};
+            h->h0_nf = vrb::h0_forest(h->ev_all, h->efilt_all, h->n, h->count[1], s, h0_alloc, &ctx, &h->h0_pos,
+                                      &h->h0_death);
+            h->h0_done = true;
+        }
+        if (!h->c2_done) {
+            const int64_t nc = h->local_n[2];
+            h->c2_colptr = h->own<uint64_t>((size_t)nc + 1, s);
+            H0Alloc ctx{h, s};
+            h->c2_nnz = vrb::compress_d2(h->h0_pos, h->h0_nf, h->count[1], h->rows[2], nc, s, h->c2_colptr, h0_alloc,
+                                         &ctx, &h->c2_rowval, &h->c2_rowmap, &h->c2_nrows);
+            h->c2_done = true;
+        }
+        if (nrows) *nrows = h->c2_nrows;
+        if (nnz) *nnz = h->c2_nnz;
+        if (colptr) *colptr = h->c2_colptr;
+        if (rowval) *rowval = h->c2_rowval;
+        if (rowmap) *rowmap = h->c2_rowmap;
     });
 }
 

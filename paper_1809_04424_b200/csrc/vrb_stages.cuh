@@ -149,6 +149,13 @@ int64_t gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t kdim, const uint6
 int64_t h0_forest(const uint32_t* ev, const uint32_t* efilt, int64_t n, int64_t E, cudaStream_t s,
                   uint32_t* (*alloc_out)(int64_t, void*), void* ctx, uint32_t** pos_out, uint32_t** death_out);   // largest n the shared-memory vertex map supports
 
+// F1 "clear and compress" (h0.cu): D_2 (ncols columns of 3 rows) without
+// the rows of the forest edges; colptr (ncols + 1, caller), rows renumbered
+// densely, rowmap (new row -> edge position); returns nnz.
+int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_t* rows, int64_t ncols,
+                    cudaStream_t s, uint64_t* colptr, uint32_t* (*alloc_out)(int64_t, void*), void* ctx,
+                    uint32_t** rowval_out, uint32_t** rowmap_out, int64_t* nrows_out);
+
 // Multi-GPU build (dist.cu).  Outputs are allocated through the callbacks
 // (handle-owned); this rank's slices of dimensions 2 and 3.
 struct DistOut {

@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_symbol():
     L = vrb.lib()
     for name in _declared_symbols():
         assert hasattr(L, name), name
-    assert vrb.abi_version() == 1
+    assert vrb.abi_version() == 2
 
 
 def test_binding_has_no_oracle_or_cpu_path():

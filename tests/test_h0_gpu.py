@@ -6,6 +6,7 @@ independent library routine: with unique weights the Kruskal forest is what
 pHcol pairs with vertex rows).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -146,3 +147,59 @@ def test_h0_late_crossing_edges_vs_scipy(vrb, radius):
     np.testing.assert_array_equal(death, ef[pos])
     ncomp, _ = csgraph.connected_components(G, directed=False)
     assert ness == ncomp == (1 if math.isinf(radius) else 2)
+
+
+# ---------------------------------------------------------------------------
+# "Clear and compress": D_2 without the rows of the
+# H0 forest (the D_1 pivot columns).  Checked two ways against the oracle:
+# (1) the compressed matrix equals the oracle's D_2 with the rows of the
+#     edges whose D_1 column the oracle's textbook reduction leaves nonzero
+#     removed and the rest renumbered; (2) the oracle's reduction of the
+#     compressed matrix pairs exactly the (edge, triangle) pivots its
+#     reduction of the full D_2 pairs -- the compression lemma (every
+#     dimension-1 bar is unchanged).
+# ---------------------------------------------------------------------------
+def _compress_cases():
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ties_five_points.json")))
+    return {
+        "c1": (workloads.WORKLOADS["C1"].points(), math.inf),
+        "c2": (workloads.WORKLOADS["C2"].points(), 0.45),
+        "lattice": (workloads.integer_lattice(4, 3), 1.5),
+        "five": (np.array(g["points"], dtype=np.float64), 5.0),
+        "gauss": (workloads.random_cloud(12, 120, 4, "gauss"), 1.6),
+        "two_blobs": (np.concatenate([workloads.random_cloud(13, 40, 3, "uniform"),
+                                      workloads.random_cloud(14, 40, 3, "uniform") + 10.0]), 0.5),
+    }
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "lattice", "five", "gauss", "two_blobs"])
+def test_compress_d2_vs_oracle(vrb, case):
+    X, radius = _compress_cases()[case]
+    res = vrb.build(X, maxdim=1, radius=radius)
+    cp, rv, rm = res.compress_d2()
+    cp, rv, rm = cp.cpu().numpy(), _u32(rv), _u32(rm)
+    o = oracle.Oracle(X, radius)
+    ev, ef, _, _ = o.edges()
+    E = o.E
+    _, _, rows = o.simplices(2)
+    # the oracle's D_1 reduction: edge columns that stay nonzero are the pivots
+    _, zero1 = oracle.reduce(X.shape[0], [list(map(int, e)) for e in ev], "col")
+    negative = ~zero1
+    keep = np.flatnonzero(~negative)
+    newidx = np.full(E, -1, dtype=np.int64)
+    newidx[keep] = np.arange(keep.size)
+    want_cols = [[int(newidx[r]) for r in col if newidx[r] >= 0] for col in rows]
+    assert np.array_equal(rm, keep.astype(np.uint32))
+    assert cp[0] == 0 and cp.shape[0] == rows.shape[0] + 1
+    got_cols = [rv[cp[j]:cp[j + 1]].astype(np.int64).tolist() for j in range(rows.shape[0])]
+    assert got_cols == want_cols
+    assert all(1 <= len(c) <= 3 for c in got_cols)
+    # compression lemma: identical pivot pairs
+    piv_full, _ = oracle.reduce(E, [list(map(int, c)) for c in rows], "col")
+    piv_c, _ = oracle.reduce(keep.size, got_cols, "col")
+    full_pairs = {(int(r), int(c)) for r, c in enumerate(piv_full) if c >= 0}
+    comp_pairs = {(int(rm[r]), int(c)) for r, c in enumerate(piv_c) if c >= 0}
+    assert comp_pairs == full_pairs
+    # the forest edges are never pivots of D_2
+    assert not any(negative[r] for r, _ in full_pairs)
