@@ -40,7 +40,7 @@ TRI_OUT_BYTES = 28
 TET_OUT_BYTES = 36    # 4 vertices + filt + 4 D_3 rows, u32 each
 # SURVEY 8(d) B_alg per unit for the whole path (sort-based accounting)
 SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44, "tet": 52}
-ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400}
+ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400, "HIV": 700}
 
 
 def _peaks():
@@ -127,8 +127,10 @@ def oracle_sample(workload: workloads.Workload, m: int):
     import oracle
 
     X = workload.points()[:m]
+    if workload.kind == "matrix":
+        X = np.ascontiguousarray(X[:, :m])
     t0 = time.perf_counter()
-    o = oracle.Oracle(X, workload.radius)
+    o = oracle.Oracle(None, workload.radius, D=X) if workload.kind == "matrix" else oracle.Oracle(X, workload.radius)
     units = o.E
     if workload.maxdim >= 1:
         units += o.simplices(2)[0].shape[0]
@@ -207,6 +209,10 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # 512 MB > 126 MB L2
 
     def one_build(points):
+        if w.kind == "matrix":   # F3: a distance matrix (HIV), one GPU
+            if world > 1:
+                raise SystemExit("distance-matrix workloads run on one GPU")
+            return vrb.build_dm(points, maxdim=w.maxdim, radius=w.radius)
         if world > 1:
             return vrb.build_dist(points, maxdim=w.maxdim, radius=w.radius)
         return vrb.build(points, maxdim=w.maxdim, radius=w.radius)

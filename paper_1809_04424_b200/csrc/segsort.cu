@@ -7,10 +7,18 @@
 // lengths share a level; reading A4: ties broken lexicographically
 // "does not determine a total ordering") the level's range must be sorted by
 // the lex code of its vertex tuple.  Levels are contiguous output ranges
-// [off[g0], off[g1]), so this is a segmented sort over the (few, usually tiny)
-// tie ranges: one CTA bitonic sort per segment up to kSmall entries, the
-// global radix sort beyond.  Lex codes pack the sorted vertex tuple into 64
-// bits: 3 x 21 bits for triangles, 4 x 16 bits for tetrahedra.
+// [off[g0], off[g1]), so this is a segmented sort over the tie ranges:
+//   levels : head flags over the owner edges + a scan list every level start
+//            (no thread walks a level);
+//   small  : one CTA bitonic sort per segment of <= kSmall entries;
+//   large  : ALL larger segments in ONE radix sort of (segment, lex code)
+//            keys -- packed into 64 bits when they fit (n <= 2^16 for
+//            triangles with up to 2^16 segments, ...), else two stable LSD
+//            sorts (code, then segment) -- and one scatter back, so a tie-heavy
+//            input (HIV's Hamming distances) costs a few device-wide
+//            passes, not a host loop of per-level sorts.
+// Lex codes pack the sorted vertex tuple: 3 x 21 bits for triangles, 4 x 16
+// bits for tetrahedra.
 #include <algorithm>
 #include <vector>
 
@@ -29,21 +37,31 @@ struct Seg {
     uint64_t len;
 };
 
-// One thread per level start; appends (start, len) segments of tie levels.
-__global__ void k_find_ties(const uint32_t* __restrict__ efilt, const uint64_t* __restrict__ off, int64_t E,
-                            int64_t p_lo, int64_t p_hi, uint64_t slot0, Seg* __restrict__ segs,
-                            unsigned long long* __restrict__ nseg) {
+// level heads over the owner edges [p_lo, p_hi)
+__global__ void k_level_heads(const uint32_t* __restrict__ efilt, int64_t p_lo, int64_t p_hi,
+                              uint32_t* __restrict__ head) {
     for (int64_t p = p_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p_hi;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t f = efilt[p];
-        if (p > 0 && efilt[p - 1] == f) continue;          // not a level start
-        if (p + 1 >= E || efilt[p + 1] != f) continue;     // single-edge level: already lex
-        int64_t q = p + 1;
-        while (q < E && efilt[q] == f) ++q;
-        const uint64_t len = off[q] - off[p];
+         p += (int64_t)gridDim.x * blockDim.x)
+        head[p - p_lo] = (p == p_lo || efilt[p - 1] != efilt[p]) ? 1u : 0u;
+}
+
+// level starts, compacted in order (starts[nlev] = p_hi)
+__global__ void k_level_starts(const uint32_t* __restrict__ head, const uint64_t* __restrict__ pos, int64_t p_lo,
+                               int64_t span, uint32_t* __restrict__ starts) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < span; q += (int64_t)gridDim.x * blockDim.x)
+        if (head[q]) starts[pos[q]] = (uint32_t)(p_lo + q);
+}
+
+// one thread per level: levels of >= 2 edges and >= 2 simplices are tie segments
+__global__ void k_tie_segs(const uint32_t* __restrict__ starts, int64_t nlev, int64_t p_hi,
+                           const uint64_t* __restrict__ off, uint64_t slot0, Seg* __restrict__ segs,
+                           unsigned long long* __restrict__ nseg) {
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < nlev; l += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = starts[l], b = l + 1 < nlev ? (int64_t)starts[l + 1] : p_hi;
+        if (b - a < 2) continue;
+        const uint64_t len = off[b] - off[a];
         if (len < 2) continue;
-        const unsigned long long at = atomicAdd(nseg, 1ull);
-        segs[at] = Seg{off[p] - slot0, len};
+        segs[atomicAdd(nseg, 1ull)] = Seg{off[a] - slot0, len};
     }
 }
 
@@ -117,71 +135,185 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_small(const Seg* __restri
     }
 }
 
+// Keys of the large segments: element q (0..M) of the concatenated segments
+// (segment g at [segoff[g], segoff[g+1])) -> (g << cbits | code) when packed,
+// else the code alone; vals = the element's slot.
 template <int K>
-__global__ void k_seg_keys(const uint32_t* __restrict__ verts, uint64_t start, int64_t len, uint64_t* __restrict__ key) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x)
-        key[q] = Code<K>::pack(verts + (K + 1) * (start + q));
-}
-
-template <int K>
-__global__ void k_seg_apply(const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
-                            const uint32_t* __restrict__ rows_copy, uint64_t start, int64_t len,
-                            uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t v[K + 1];
-        Code<K>::unpack(key[q], v);
-        uint32_t* o = verts + (K + 1) * (start + q);
-        for (int c = 0; c <= K; ++c) o[c] = v[c];
-        if (rows) {
-            const uint32_t src = perm[q];
-            for (int c = 0; c <= K; ++c) rows[(K + 1) * (start + q) + c] = rows_copy[(K + 1) * (int64_t)src + c];
+__global__ void k_big_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
+                           const uint32_t* __restrict__ verts, int cbits, int packed, uint64_t* __restrict__ key,
+                           uint32_t* __restrict__ val) {
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const Seg S = segs[g];
+        const uint64_t o = segoff[g];
+        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
+            const uint64_t slot = S.start + q;
+            const uint64_t code = Code<K>::pack(verts + (K + 1) * slot);
+            key[o + q] = packed ? (((uint64_t)g << cbits) | code) : code;
+            val[o + q] = (uint32_t)slot;
         }
     }
 }
 
+// segment index of each sorted element's slot (two-pass path): binary search
+// in the segment starts (segments sorted by start)
+__global__ void k_seg_of(const uint32_t* __restrict__ val, int64_t M, const Seg* __restrict__ segs, int64_t nseg,
+                         uint64_t* __restrict__ key) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < M; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t slot = val[q];
+        int64_t lo = 0, hi = nseg;   // last segment with start <= slot
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (segs[mid].start <= slot) lo = mid; else hi = mid;
+        }
+        key[q] = (uint64_t)lo;
+    }
+}
+
+// gather the rows of the sorted elements (before any is overwritten)
 template <int K>
-void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi, uint32_t* verts,
-               uint32_t* rows, cudaStream_t s) {
+__global__ void k_big_rows(const uint32_t* __restrict__ val, int64_t M, const uint32_t* __restrict__ rows,
+                           uint32_t* __restrict__ rcopy) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < M; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t src = val[q];
+#pragma unroll
+        for (int c = 0; c <= K; ++c) rcopy[(K + 1) * q + c] = rows[(K + 1) * src + c];
+    }
+}
+
+// scatter: the q-th sorted element goes to slot segs[g].start + (q - segoff[g])
+// of its segment g; its vertices are re-read from the source slot's code
+template <int K>
+__global__ void k_big_apply(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
+                            const uint32_t* __restrict__ val, const uint64_t* __restrict__ codes,
+                            const uint32_t* __restrict__ rcopy, uint32_t* __restrict__ verts,
+                            uint32_t* __restrict__ rows) {
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const Seg S = segs[g];
+        const uint64_t o = segoff[g];
+        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
+            uint32_t v[K + 1];
+            Code<K>::unpack(codes[o + q], v);
+            uint32_t* out = verts + (K + 1) * (S.start + q);
+            for (int c = 0; c <= K; ++c) out[c] = v[c];
+            if (rows)
+                for (int c = 0; c <= K; ++c) rows[(K + 1) * (S.start + q) + c] = rcopy[(K + 1) * (o + q) + c];
+        }
+    }
+}
+
+__global__ void k_codes_of(const uint32_t* __restrict__ val, int64_t M, const uint32_t* __restrict__ verts, int k,
+                           uint64_t* __restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < M; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t* v = verts + (uint64_t)(k + 1) * val[q];
+        uint64_t c = 0;
+        const int bits = k == 2 ? 21 : 16;
+        for (int i = 0; i <= k; ++i) c = (c << bits) | v[i];
+        out[q] = c;
+    }
+}
+
+int bits_for(uint64_t v) {   // bits to hold 0..v
+    int b = 1;
+    while (b < 64 && (v >> b)) ++b;
+    return b;
+}
+
+template <int K>
+void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi, int64_t n,
+               uint32_t* verts, uint32_t* rows, cudaStream_t s) {
+    (void)E;
     uint64_t slot0 = 0;
     VRB_CUDA(cudaMemcpyAsync(&slot0, off + p_lo, sizeof(slot0), cudaMemcpyDeviceToHost, s));
     const int64_t span = p_hi - p_lo;
-    DBuf<Seg> segs((size_t)span, s);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(span, 256), (int64_t)device_sm_count() * 16);
+    // ---- levels (heads + scan), then tie segments
+    DBuf<uint32_t> head(span, s), starts(span, s);
+    DBuf<uint64_t> hpos(span + 1, s);
+    k_level_heads<<<g, 256, 0, s>>>(efilt, p_lo, p_hi, head.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(head.get(), hpos.get(), span, s);
+    uint64_t nlev = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nlev, hpos.get() + span, sizeof(nlev), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (nlev == (uint64_t)span) return;   // every level holds one edge: nothing to re-sort
+    k_level_starts<<<g, 256, 0, s>>>(head.get(), hpos.get(), p_lo, span, starts.get());
+    VRB_LAUNCH_CHECK();
+    DBuf<Seg> segs((size_t)nlev, s);
     DBuf<unsigned long long> nseg(1, s);
     VRB_CUDA(cudaMemsetAsync(nseg.get(), 0, sizeof(unsigned long long), s));
-    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(span, 256), (int64_t)device_sm_count() * 16);
-    k_find_ties<<<g, 256, 0, s>>>(efilt, off, E, p_lo, p_hi, slot0, segs.get(), nseg.get());
+    const unsigned gl = (unsigned)std::min<int64_t>(ceil_div((int64_t)nlev, 256), (int64_t)device_sm_count() * 16);
+    k_tie_segs<<<gl, 256, 0, s>>>(starts.get(), (int64_t)nlev, p_hi, off, slot0, segs.get(), nseg.get());
     VRB_LAUNCH_CHECK();
     unsigned long long h = 0;
     VRB_CUDA(cudaMemcpyAsync(&h, nseg.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
+    head.reset();
+    starts.reset();
+    hpos.reset();
     if (h == 0) return;
+    // ---- small segments: one CTA each
     const unsigned gs = (unsigned)std::min<unsigned long long>(h, (unsigned long long)device_sm_count() * 4);
     k_sort_small<K><<<gs, kSortThreads, 0, s>>>(segs.get(), (int64_t)h, verts, rows);
     VRB_LAUNCH_CHECK();
+    // ---- large segments: one batched sort
     std::vector<Seg> hs(h);
     VRB_CUDA(cudaMemcpyAsync(hs.data(), segs.get(), h * sizeof(Seg), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
-    for (const Seg& S : hs) {
-        if (S.len <= (uint64_t)small_cap<K>()) continue;
-        const int64_t len = (int64_t)S.len;
-        DBuf<uint64_t> k0(len, s), k1(len, s);
-        DBuf<uint32_t> v0(len, s), v1(len, s);
-        const unsigned gg = (unsigned)std::min<int64_t>(ceil_div(len, 256), 4096);
-        k_seg_keys<K><<<gg, 256, 0, s>>>(verts, S.start, len, k0.get());
+    std::vector<Seg> big;
+    for (const Seg& S : hs)
+        if (S.len > (uint64_t)small_cap<K>()) big.push_back(S);
+    if (big.empty()) return;
+    std::sort(big.begin(), big.end(), [](const Seg& a, const Seg& b) { return a.start < b.start; });
+    const int64_t nb = (int64_t)big.size();
+    std::vector<uint64_t> hoff(nb + 1, 0);
+    for (int64_t q = 0; q < nb; ++q) hoff[q + 1] = hoff[q] + big[q].len;
+    const int64_t M = (int64_t)hoff[nb];
+    DBuf<Seg> dseg(nb, s);
+    DBuf<uint64_t> dsegoff(nb + 1, s);
+    VRB_CUDA(cudaMemcpyAsync(dseg.get(), big.data(), nb * sizeof(Seg), cudaMemcpyHostToDevice, s));
+    VRB_CUDA(cudaMemcpyAsync(dsegoff.get(), hoff.data(), (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    const int cbits = (K + 1) * Code<K>::kBitsPer;   // as packed by Code<K>
+    const int vbits = bits_for((uint64_t)std::max<int64_t>(n - 1, 1));
+    // the code's top (K + 1) * kBitsPer bits hold K + 1 ids of vbits each:
+    // only its low (K + 1 - 1) * kBitsPer + vbits bits can be nonzero
+    const int code_bits = K * Code<K>::kBitsPer + vbits;
+    const bool packed = code_bits + bits_for((uint64_t)std::max<int64_t>(nb - 1, 1)) <= 64;
+    (void)cbits;
+    DBuf<uint64_t> k0(M, s), k1(M, s);
+    DBuf<uint32_t> v0(M, s), v1(M, s);
+    const unsigned gb = (unsigned)std::min<int64_t>(nb, (int64_t)device_sm_count() * 8);
+    k_big_keys<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, verts, code_bits, packed ? 1 : 0, k0.get(),
+                                    v0.get());
+    VRB_LAUNCH_CHECK();
+    const uint64_t vary = varying_bits(k0.get(), M, s);
+    bool alt = radix_sort_pairs(k0.get(), k1.get(), v0.get(), v1.get(), M, vary, s);
+    uint64_t* sk = alt ? k1.get() : k0.get();
+    uint32_t* sv = alt ? v1.get() : v0.get();
+    const unsigned gm = (unsigned)std::min<int64_t>(ceil_div(M, 256), (int64_t)device_sm_count() * 16);
+    if (!packed) {
+        // stable second pass on the segment index (LSD: code, then segment)
+        uint64_t* ok = alt ? k0.get() : k1.get();
+        uint32_t* ov = alt ? v0.get() : v1.get();
+        k_seg_of<<<gm, 256, 0, s>>>(sv, M, dseg.get(), nb, sk);
         VRB_LAUNCH_CHECK();
-        iota_u32(v0.get(), len, s);
-        const uint64_t vary = varying_bits(k0.get(), len, s);
-        const bool alt = radix_sort_pairs(k0.get(), k1.get(), v0.get(), v1.get(), len, vary, s);
-        DBuf<uint32_t> rcopy;
-        if (rows) {
-            rcopy.alloc((size_t)((K + 1) * len), s);
-            VRB_CUDA(cudaMemcpyAsync(rcopy.get(), rows + (K + 1) * S.start, (K + 1) * len * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToDevice, s));
-        }
-        k_seg_apply<K><<<gg, 256, 0, s>>>(alt ? k1.get() : k0.get(), alt ? v1.get() : v0.get(), rcopy.get(),
-                                          S.start, len, verts, rows);
+        const uint64_t vary2 = varying_bits(sk, M, s);
+        const bool alt2 = radix_sort_pairs(sk, ok, sv, ov, M, vary2, s);
+        if (alt2) { sk = ok; sv = ov; }
+        k_codes_of<<<gm, 256, 0, s>>>(sv, M, verts, K, sk);   // the sorted elements' codes
+        VRB_LAUNCH_CHECK();
+    } else {
+        // strip the segment bits: keys are then the codes
+        k_codes_of<<<gm, 256, 0, s>>>(sv, M, verts, K, sk);
         VRB_LAUNCH_CHECK();
     }
+    DBuf<uint32_t> rcopy;
+    if (rows) {
+        rcopy.alloc((size_t)(K + 1) * M, s);
+        k_big_rows<K><<<gm, 256, 0, s>>>(sv, M, rows, rcopy.get());
+        VRB_LAUNCH_CHECK();
+    }
+    k_big_apply<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, sv, sk, rcopy.get(), verts, rows);
+    VRB_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -190,10 +322,10 @@ void sort_tie_groups(int k, const uint32_t* efilt, const uint64_t* off, int64_t 
                      int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s) {
     if (p_lo >= p_hi) return;
     if (k == 2) {
-        sort_ties<2>(efilt, off, E, p_lo, p_hi, verts, rows, s);
+        sort_ties<2>(efilt, off, E, p_lo, p_hi, n, verts, rows, s);
     } else {
         if (n > 65536) fail(VRB_ENOTSUP, "tetrahedra tie sort needs n <= 65536 (16-bit lex codes)");
-        sort_ties<3>(efilt, off, E, p_lo, p_hi, verts, rows, s);
+        sort_ties<3>(efilt, off, E, p_lo, p_hi, n, verts, rows, s);
     }
 }
 

@@ -488,6 +488,30 @@ def test_full_size_config(vrb, config):
         torch.cuda.empty_cache()
 
 
+def test_hiv_tie_heavy_full(vrb):
+    # the paper's tie-heavy benchmark at full size (HIV: 1088 sequences,
+    # Hamming distances): 159 distinct lengths for 591,328 edges,
+    # so EVERY level is a tie group and all 214,060,736 triangles go through
+    # the batched tie-group sort (segsort.cu).  Per-level histogram against the
+    # oracle's golden digest, strict (filt, lex) order, rows = edges, and
+    # sampled tie levels element by element.
+    golden = json.load(open(os.path.join(GOLDEN, "hiv_levels.json")))
+    w = workloads.WORKLOADS["HIV"]
+    D = w.points()
+    assert hashlib.sha256(np.ascontiguousarray(D).tobytes()).hexdigest() == golden["points_sha256"]
+    vrb.use_torch_allocator(True)
+    try:
+        res = vrb.build_dm(torch.from_numpy(D).cuda(), maxdim=1, radius=w.radius)
+        o = oracle.Oracle(None, w.radius, D=D)
+        assert o.E == golden["E"] and o.nvals == golden["nvals"]
+        _check_triangles_full(vrb, res, o, golden, n_levels_sampled=10)
+        del res
+    finally:
+        torch.cuda.synchronize()
+        vrb.use_torch_allocator(False)
+        torch.cuda.empty_cache()
+
+
 def test_c5a_edges_full(vrb):
     # C5A: 199,990,000 edges, all pairs (r = inf).  Full edge parity on a
     # sample of positions plus global properties (the oracle's full sort of

@@ -6,7 +6,7 @@ per-level simplex histogram of C3/C5B takes minutes on one core, so it is
 stored as a SHA-256 digest plus coarse bucket sums instead of being recomputed
 on every GPU test run.
 
-    python tools/make_golden.py C3 C5B
+    python tools/make_golden.py C3 C5B C4 HIV
 """
 import hashlib
 import json
@@ -29,7 +29,7 @@ def digest(config: str, k: int = 2) -> dict:
     w = workloads.WORKLOADS[config]
     X = w.points()
     t0 = time.time()
-    o = oracle.Oracle(X, w.radius)
+    o = oracle.Oracle(None, w.radius, D=X) if w.kind == "matrix" else oracle.Oracle(X, w.radius)
     ev, ef, el, vor = o.edges()
     t1 = time.time()
     hist = o.filt_hist(k)

@@ -24,6 +24,7 @@ class Workload:
     maxdim: int        # homology dimension; simplices are built up to K = maxdim + 1
     radius: float      # inclusive cap on edge length (math.inf = full filtration)
     seed: int
+    kind: str = "points"   # "points": n x d cloud; "matrix": n x n distance matrix
 
     def points(self) -> np.ndarray:
         return _GENERATORS[self.name](self.seed)
@@ -83,7 +84,46 @@ def _c5(seed: int) -> np.ndarray:
     return np.random.default_rng(seed).standard_normal((20000, 10))
 
 
-_GENERATORS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5A": _c5, "C5B": _c5}
+def hamming_sequences(seed: int, n: int = 1088, length: int = 1000, clades: int = 16, p_clade: float = 0.08,
+                      p_leaf: float = 0.03) -> np.ndarray:
+    """n synthetic genomic sequences over a 4-letter alphabet (uint8, n x
+    length): a random root, `clades` ancestors each with a fraction p_clade of
+    its sites mutated, and every sequence its clade ancestor (i mod clades)
+    with a fraction p_leaf of its sites mutated (a mutation replaces the
+    letter by one of the 3 others).  A two-level star phylogeny: the shape of
+    the HIV benchmark's input (1088 genomic sequences of the HIV virus,
+    P:520-521), whose Hamming distances tie heavily."""
+    rng = np.random.default_rng(seed)
+    root = rng.integers(0, 4, length)
+
+    def mutate(a, p):
+        a = a.copy()
+        m = rng.random(length) < p
+        a[m] = (a[m] + rng.integers(1, 4, int(m.sum()))) % 4
+        return a
+
+    anc = [mutate(root, p_clade) for _ in range(clades)]
+    return np.stack([mutate(anc[i % clades], p_leaf) for i in range(n)]).astype(np.uint8)
+
+
+def hamming_matrix(seqs: np.ndarray) -> np.ndarray:
+    """D[i][j] = number of sites where sequences i and j differ (float64; the
+    input of the distance-matrix build, not a step of it).  Counted as
+    length - (one-hot agreements), exact in float64 for lengths < 2^53."""
+    n, length = seqs.shape
+    onehot = np.zeros((n, length * 4), dtype=np.float64)
+    onehot[np.repeat(np.arange(n), length), (np.arange(length) * 4)[None, :].repeat(n, 0).ravel() + seqs.ravel()] = 1.0
+    same = onehot @ onehot.T
+    D = length - same
+    np.fill_diagonal(D, 0.0)
+    return np.ascontiguousarray(D)
+
+
+def _hiv(seed: int) -> np.ndarray:
+    return hamming_matrix(hamming_sequences(seed))
+
+
+_GENERATORS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5A": _c5, "C5B": _c5, "HIV": _hiv}
 
 WORKLOADS = {
     "C1": Workload("C1", "50 uniform random points in R^3, max dim 1 (edges + triangles), full filtration",
@@ -98,6 +138,12 @@ WORKLOADS = {
                     0, math.inf, 5),
     "C5B": Workload("C5B", "20,000 Gaussian points in R^10, max dim 1, distance + edge ranking + triangle build at 1/2/4/8 GPUs",
                     1, 2.8, 5),
+    # the paper's tie-heavy benchmark (not a BASELINE.json config): HIV's 1088
+    # genomic sequences as a Hamming distance matrix (Table tab1
+    # P:1054-1069), the distance-matrix input of F3, max dim 1 (Eirene's
+    # default), full filtration
+    "HIV": Workload("HIV", "HIV analog: Hamming distance matrix of 1088 synthetic genomic sequences, max dim 1, "
+                           "full filtration (P:520-521)", 1, math.inf, 6, "matrix"),
 }
 
 
