@@ -40,7 +40,7 @@ TRI_OUT_BYTES = 28
 TET_OUT_BYTES = 36    # 4 vertices + filt + 4 D_3 rows, u32 each
 # SURVEY 8(d) B_alg per unit for the whole path (sort-based accounting)
 SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44, "tet": 52}
-ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400, "HIV": 700}
+ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400, "HIV": 500}
 
 
 def _peaks():
