@@ -157,6 +157,58 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
         }
         __syncthreads();
     }
+    if (m && staged) {
+        // capped build: the tile's kept pairs are sparse (C5B: ~5% of 4096),
+        // so compact them first (row starts by a warp scan of the row
+        // popcounts, then each row's set bits) and give every thread whole
+        // pairs: no lane idles on a dropped pair
+        __shared__ uint32_t rstart[kT + 1];
+        __shared__ uint16_t plist[kT * kT];
+        if (wid == 0) {
+            uint32_t c0 = __popcll(m[lane]), c1 = __popcll(m[lane + 32]);
+            uint32_t x0 = c0, x1 = c1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+                if (lane >= o) { x0 += y0; x1 += y1; }
+            }
+            const uint32_t t0 = __shfl_sync(0xffffffffu, x0, 31);
+            rstart[lane] = x0 - c0;
+            rstart[lane + 32] = t0 + x1 - c1;
+            if (lane == 31) rstart[kT] = t0 + x1;
+        }
+        __syncthreads();
+        for (int r = wid; r < kT; r += kThreads / 32) {
+            const unsigned long long bits = m[r];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = lane + 32 * h;
+                if ((bits >> c) & 1ull)
+                    plist[rstart[r] + __popcll(bits & ((1ull << c) - 1ull))] = (uint16_t)(r << 6 | c);
+            }
+        }
+        __syncthreads();
+        const uint32_t total = rstart[kT];
+        for (uint32_t q = threadIdx.x; q < total; q += kThreads) {
+            const int rc = plist[q], r = rc >> 6, c = rc & 63;
+            const int64_t i = i0 + r, j = j0 + c;
+            double acc = 0.0;
+            for (int u = 0; u < d; ++u) {
+                const double t = __dsub_rn(sA[u][r], sB[u][c]);
+                acc = __dadd_rn(acc, __dmul_rn(t, t));
+            }
+            const double len = __dsqrt_rn(acc);
+            const uint64_t slot = slot_base[(i - row_lo) * nt + tj] + (q - rstart[r]);
+            key[slot] = (uint64_t)__double_as_longlong(len);
+            if (pij) {
+                pij[slot] = ((uint32_t)i << 16) | (uint32_t)j;
+            } else {
+                ei[slot] = (uint32_t)i;
+                ej[slot] = (uint32_t)j;
+            }
+        }
+        return;
+    }
     for (int r = wid; r < kT; r += kThreads / 32) {
         const int64_t i = i0 + r;
         if (i >= n) break;

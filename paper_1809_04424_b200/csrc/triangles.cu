@@ -99,6 +99,7 @@ struct TriArgs {
     uint32_t* gmap;            // global-memory host maps (n u32 per CTA) when n is too large for
                                // shared memory, else null (the map lives in shared memory)
     uint32_t* bm;              // apex bitmaps (count writes, fill reads), or null
+    int bm_mode;               // 1: by id rank in x's list (deg x bits); 2: by prefix entry (len bits)
     const uint64_t* bmoff;     // per hosted slot: word offset of its bitmap
     const uint2* idl;          // (k, pos) in neighbour-ID order
     int debug;   // ablation (experiment builds with -DVRB_ABLATION only): 1 = stop after mark, 2 = skip the flush
@@ -718,14 +719,202 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
     }
 }
 
-template <bool kFill, bool kPacked, bool kBm>
+// ---------------------------------------------------------------------------
+// Position-bitmap path (the default for single-rank-range builds with packed
+// lists and degrees <= kApexBitmapMaxDeg).  The count stores, per owner edge,
+// one bit per entry t of the scanned prefix (bit t of word t / 32: entry t is
+// a valid apex), built by ballots -- 32 candidates per map lookup + vote, no
+// shared-memory atomics.  The fill then reads those words, marks the valid
+// entries' id ranks (krank, in the packed list word) in a shared bitmap,
+// prefix-popcounts it -- the slot of an apex is the number of valid apexes of
+// smaller id -- and places (k, pos(x, k)) read from the prefix itself (nkr,
+// np: contiguous, coalesced) into a window of slots, flushed as 16-byte
+// chunks.  No per-apex gathers from another list.
+// ---------------------------------------------------------------------------
+constexpr int kWinT = 512;
+struct WarpScratchT {              // fill (position bitmaps)
+    uint32_t bits[kBmWords];       // valid apexes by id rank in x's list
+    uint32_t wpre[kBmWords];       // exclusive prefix popcounts
+    uint16_t reck[kWinT];          // staged window: apex ids ...
+    uint32_t recp[kWinT];          // ... and pos(x, k)
+    alignas(16) uint32_t st[96];
+    alignas(16) uint32_t sr[96];
+};
+struct WarpScratchNone {
+    uint32_t unused;
+};
+
+__device__ __forceinline__ uint32_t warp_count_tbm(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t p,
+                                                   uint64_t offx, uint32_t len, int64_t e) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t* __restrict__ lst = A.nkr + offx;
+    uint32_t* __restrict__ out = A.bm + A.bmoff[e];
+    const uint32_t nch = (len + 31) >> 5;
+    uint32_t c = 0;
+    constexpr int U = 8;
+    for (uint32_t c0 = 0; c0 < nch; c0 += U) {
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = 32 * (c0 + u) + lane;
+            w[u] = t < len ? ld_list(lst + t) : 0u;
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = 32 * (c0 + u) + lane;
+            const bool v = t < len && map[w[u] & 0xFFFFu] < p;
+            const uint32_t b = __ballot_sync(0xffffffffu, v);
+            if (lane == u) mine = b;
+            c += __popc(b);
+        }
+        if (lane < U && c0 + lane < nch) __stcg(out + c0 + lane, mine);
+    }
+    return c;
+}
+
+// Store slots [0, m) of a window at output slot s0: kp_of(j) = (k, pos(x, k))
+// of slot j; pos(y, k) = map[k].  Groups of 32 triangles are staged in shared
+// memory and stored as 16-byte chunks (every L2 sector written whole).
+template <int kU, class KP>
+__device__ __forceinline__ void store_window(const TriArgs& A, const uint32_t* __restrict__ map,
+                                             uint32_t* __restrict__ st, uint32_t* __restrict__ sr, uint64_t s0,
+                                             uint32_t m, uint32_t p, uint32_t y, uint32_t x, uint32_t filt,
+                                             KP&& kp_of) {
+    const int lane = threadIdx.x & 31;
+    auto tri = [&](uint32_t j, uint2 kp, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0, uint32_t& r1) {
+        const uint32_t k = kp.x, px = kp.y, py = map[k];
+        a0 = y; a1 = x; a2 = k;
+        sort3(a0, a1, a2);
+        r0 = min(px, py);
+        r1 = max(px, py);
+        __stcs(A.tf + s0 + j, filt);
+        if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+    };
+    auto scalar = [&](uint32_t j, uint2 kp) {
+        uint32_t a0, a1, a2, r0, r1;
+        tri(j, kp, a0, a1, a2, r0, r1);
+        uint32_t* tv = A.tv + 3 * (s0 + j);
+        __stcs(tv, a0);
+        __stcs(tv + 1, a1);
+        __stcs(tv + 2, a2);
+        if (A.rows) {
+            uint32_t* rw = A.rows + 3 * (s0 + j);
+            __stcs(rw, r0);
+            __stcs(rw + 1, r1);
+            __stcs(rw + 2, p);
+        }
+    };
+    const uint32_t h = min(m, (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u));
+    if ((uint32_t)lane < h) scalar(lane, kp_of(lane));
+    for (uint32_t g0 = h; g0 < m; g0 += 32 * kU) {
+        uint2 kq[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t j = g0 + 32 * q + lane;
+            kq[q] = j < m ? kp_of(j) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t g = g0 + 32 * q;
+            if (g >= m) break;
+            const uint32_t j = g + lane;
+            if (g + 32 <= m) {
+                uint32_t a0, a1, a2, r0, r1;
+                tri(j, kq[q], a0, a1, a2, r0, r1);
+                st[3 * lane] = a0;
+                st[3 * lane + 1] = a1;
+                st[3 * lane + 2] = a2;
+                sr[3 * lane] = r0;
+                sr[3 * lane + 1] = r1;
+                sr[3 * lane + 2] = p;
+                __syncwarp();
+                if (lane < 24) {
+                    __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane, reinterpret_cast<const uint4*>(st)[lane]);
+                    if (A.rows)
+                        __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
+                               reinterpret_cast<const uint4*>(sr)[lane]);
+                }
+                __syncwarp();
+            } else if (j < m) {
+                scalar(j, kq[q]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_fill_tbm(const TriArgs& A, const uint32_t* __restrict__ map,
+                                              WarpScratchT* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                              uint32_t len, uint64_t offx, uint32_t degx, uint64_t tbo, uint64_t slot,
+                                              uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t* __restrict__ lk = A.nkr + offx;
+    const uint32_t* __restrict__ lp = A.np + offx;
+    const uint32_t* __restrict__ tb = A.bm + tbo;
+    const uint32_t nch = (len + 31) >> 5;
+    const uint32_t nw = (degx + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
+    __syncwarp();
+    constexpr int U = 8;
+    // ---- mark the id ranks of the valid entries
+    for (uint32_t c0 = 0; c0 < nch; c0 += U) {
+        const uint32_t wl = (lane < U && c0 + lane < nch) ? __ldg(tb + c0 + lane) : 0u;
+        uint32_t ent[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
+            ent[u] = ((word >> lane) & 1u) ? ld_list(lk + 32 * (c0 + u) + lane) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (ent[u] != 0xFFFFFFFFu) {
+                const uint32_t r = ent[u] >> 16;
+                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+            }
+    }
+    const uint32_t count = rank_bits<kBmWords>(W, degx);
+    // ---- windows of kWinT slots: place (k, pos(x, k)) by slot, then store
+    for (uint32_t w0 = 0; w0 < count; w0 += kWinT) {
+        for (uint32_t c0 = 0; c0 < nch; c0 += U) {
+            const uint32_t wl = (lane < U && c0 + lane < nch) ? __ldg(tb + c0 + lane) : 0u;
+            uint32_t ent[U], pos[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
+                const bool v = (word >> lane) & 1u;
+                const uint32_t t = 32 * (c0 + u) + lane;
+                ent[u] = v ? ld_list(lk + t) : 0xFFFFFFFFu;
+                pos[u] = v ? ld_list(lp + t) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (ent[u] != 0xFFFFFFFFu) {
+                    const uint32_t r = ent[u] >> 16;
+                    const uint32_t wd = W->bits[r >> 5];
+                    const uint32_t sl = W->wpre[r >> 5] + __popc(wd & ((2u << (r & 31)) - 1u)) - 1u - w0;
+                    if (sl < (uint32_t)kWinT) {
+                        W->reck[sl] = (uint16_t)(ent[u] & 0xFFFFu);
+                        W->recp[sl] = pos[u];
+                    }
+                }
+        }
+        __syncwarp();
+        const uint32_t m = min((uint32_t)kWinT, count - w0);
+        store_window<4>(A, map, W->st, W->sr, slot + w0, m, p, y, x, filt,
+                        [&](uint32_t j) { return make_uint2(W->reck[j], W->recp[j]); });
+        __syncwarp();
+    }
+}
+
+template <bool kFill, bool kPacked, int kBm>
 __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2), 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
-        kBm,
-        typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
-        typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type;
+        kBm == 2, typename std::conditional<kFill, WarpScratchT, WarpScratchNone>::type,
+        typename std::conditional<
+            kBm == 1, typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
+            typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type>::type;
     WS* scratch = reinterpret_cast<WS*>(smem + (A.gmap ? 0 : ((A.n * 4 + 15) / 16) * 16));
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
@@ -803,13 +992,19 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                 if (kBm && kFill && pl1.z) {
                     // pull the next edge's bitmap into L2 while this edge runs
                     const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.bm + bmo1) & ~(uintptr_t)127;
-                    const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.bm + bmo1 + ((pl1.w + 31) >> 5));
+                    const uintptr_t a1 =
+                        reinterpret_cast<uintptr_t>(A.bm + bmo1 + (((kBm == 2 ? pl1.z : pl1.w) + 31) >> 5));
                     for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a < a1; a += 128 * 32)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
                 }
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kBm && kFill) {
+                    if constexpr (kBm == 2 && kFill) {
+                        warp_fill_tbm(A, map, scratch + wid, p, y, x, len, off0, pl0.w, bmo0, slot0, filt0);
+                    } else if constexpr (kBm == 2) {
+                        const uint32_t c = warp_count_tbm(A, map, p, off0, len, e0);
+                        if (lane == 0) A.cnt[p] = c;
+                    } else if constexpr (kBm && kFill) {
                         warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0, filt0);
                     } else if constexpr (kBm) {
                         const uint32_t c = warp_count_bm(A, map, scratch + wid, p, off0, len, pl0.w, e0);
@@ -852,7 +1047,7 @@ size_t scratch_bytes(bool packed) {
     return packed && VRB_TRI_MODE == 3 ? sizeof(WarpScratch3) : sizeof(WarpScratch);
 }
 
-template <bool kFill, bool kPacked, bool kBm>
+template <bool kFill, bool kPacked, int kBm>
 void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap, cudaStream_t s) {
     VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked, kBm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
@@ -873,11 +1068,13 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     TriArgs A = base;
     const bool packed = A.packed != 0;
     const bool bm = A.bm != nullptr;
+    const bool tbm = bm && A.bm_mode == 2;
     // fill: one CTA per SM (the vertex map + per-warp scratch); count:
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
     // the host map goes to global memory when it would leave shared memory for
     // fewer than 8 warps of scratch (n above ~40-50k), or when forced (tests)
-    size_t per_warp = bm ? (fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC)) : (fill ? scratch_bytes(packed) : 0);
+    size_t per_warp = tbm ? (fill ? sizeof(WarpScratchT) : sizeof(WarpScratchNone))
+                          : bm ? (fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC)) : (fill ? scratch_bytes(packed) : 0);
     const char* fg = std::getenv("VRB_FORCE_GLOBAL_MAP");   // testing knob
     const bool gmap = (fg && fg[0] == '1') ||
                       (int64_t)map_bytes(A.n) + 8 * (int64_t)std::max<size_t>(per_warp, 64) + 1024 >
@@ -912,21 +1109,32 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     A.task_counter = counter.get();
     const int64_t cap = A.task_hi - A.task_lo;
-    if (bm) {
-        if (fill) launch_k<true, true, true>(A, threads, smem, cap, gmap, s);
-        else launch_k<false, true, true>(A, threads, smem, cap, gmap, s);
+    if (tbm) {
+        if (fill) launch_k<true, true, 2>(A, threads, smem, cap, gmap, s);
+        else launch_k<false, true, 2>(A, threads, smem, cap, gmap, s);
+    } else if (bm) {
+        if (fill) launch_k<true, true, 1>(A, threads, smem, cap, gmap, s);
+        else launch_k<false, true, 1>(A, threads, smem, cap, gmap, s);
     } else if (fill) {
-        if (packed) launch_k<true, true, false>(A, threads, smem, cap, gmap, s);
-        else launch_k<true, false, false>(A, threads, smem, cap, gmap, s);
+        if (packed) launch_k<true, true, 0>(A, threads, smem, cap, gmap, s);
+        else launch_k<true, false, 0>(A, threads, smem, cap, gmap, s);
     } else {
-        if (packed) launch_k<false, true, false>(A, threads, smem, cap, gmap, s);
-        else launch_k<false, false, false>(A, threads, smem, cap, gmap, s);
+        if (packed) launch_k<false, true, 0>(A, threads, smem, cap, gmap, s);
+        else launch_k<false, false, 0>(A, threads, smem, cap, gmap, s);
     }
 }
 
-__global__ void k_bm_words(const uint4* __restrict__ plan, int64_t E, uint32_t* __restrict__ words) {
+__global__ void k_bm_words(const uint4* __restrict__ plan, int64_t E, int mode, uint32_t* __restrict__ words) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
-        words[e] = (plan[e].w + 31u) >> 5;
+        words[e] = ((mode == 2 ? plan[e].z : plan[e].w) + 31u) >> 5;
+}
+
+// 1 = id-rank bitmaps (default), 2 = position bitmaps (VRB_TRI_BITMAPS=pos:
+// an experiment, measured slower on C5B -- count 8.4 ms instead of 9.3, fill
+// 34.0 ms instead of 22.6 -- DESIGN.md section 10)
+int bitmap_mode() {
+    const char* m = std::getenv("VRB_TRI_BITMAPS");
+    return (m && m[0] == 'p') ? 2 : 1;
 }
 
 TriArgs graph_args(const Graph& g) {
@@ -972,7 +1180,7 @@ void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words,
     }
     DBuf<uint32_t> w(m, s);
     k_bm_words<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
-        g.plan.get(), m, w.get());
+        g.plan.get(), m, bitmap_mode(), w.get());
     VRB_LAUNCH_CHECK();
     exclusive_scan(w.get(), bmoff.get(), m, s);
     VRB_CUDA(cudaMemcpyAsync(&words, bmoff.get() + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -986,6 +1194,7 @@ void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint6
     TriArgs A = graph_args(g);
     A.cnt = cnt;
     A.bm = bm;
+    A.bm_mode = bitmap_mode();
     A.bmoff = bmoff;
     launch(A, false, g.work, 0, 1, s);
 }
@@ -1005,6 +1214,7 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.rows = rows;
     A.apex = g.n <= 65536 ? apex : nullptr;
     A.bm = const_cast<uint32_t*>(bm);
+    A.bm_mode = bm ? bitmap_mode() : 0;
     A.bmoff = bmoff;
 #ifdef VRB_ABLATION
     // ablation timing of experiment builds only (tools/variants.py

@@ -80,6 +80,24 @@ void dfree(void* p, size_t bytes, cudaStream_t s) {
     cudaFreeAsync(p, s);   // never throws (called from destructors)
 }
 
+Alloc dalloc_owned(size_t bytes, cudaStream_t s) {
+    Alloc a;
+    a.p = dalloc(bytes, s);
+    a.bytes = bytes;
+    a.fn = g_free;
+    a.ctx = g_ctx;
+    return a;
+}
+
+void dfree_owned(const Alloc& a) {
+    if (!a.p) return;
+    if (a.fn) {
+        a.fn(a.p, a.bytes, current_device(), nullptr, a.ctx);
+        return;
+    }
+    cudaFreeAsync(a.p, 0);
+}
+
 int device_sm_count() {
     static int cached[64] = {0};
     const int dev = current_device();
@@ -199,12 +217,12 @@ struct vrb_result {
     template <class T>
     T* own(size_t n_elems, cudaStream_t s) {
         if (n_elems == 0) return nullptr;
-        T* p = static_cast<T*>(vrb::dalloc(n_elems * sizeof(T), s));
-        owned.push_back({p, n_elems * sizeof(T)});
-        return p;
+        const vrb::Alloc a = vrb::dalloc_owned(n_elems * sizeof(T), s);
+        owned.push_back(a);
+        return static_cast<T*>(a.p);
     }
     void release_all() {
-        for (auto& a : owned) vrb::dfree(a.p, a.bytes, 0);
+        for (auto& a : owned) vrb::dfree_owned(a);
         owned.clear();
     }
 };
@@ -216,6 +234,8 @@ using namespace vrb;
 template <class F>
 vrb_status guarded(F&& f) {
     try {
+        cudaGetLastError();   // an error left by a call outside the library is not this call's
+
         f();
         t_last_error.clear();
         return VRB_OK;
@@ -626,7 +646,7 @@ struct vrb_gf2 {
     uint32_t* rowval = nullptr;
     std::vector<vrb::Alloc> owned;
     void release_all() {
-        for (auto& a : owned) vrb::dfree(a.p, a.bytes, 0);
+        for (auto& a : owned) vrb::dfree_owned(a);
         owned.clear();
     }
 };
@@ -638,9 +658,9 @@ struct Gf2Alloc {
 };
 uint32_t* gf2_alloc_rows(int64_t n, void* ctx) {
     auto* a = static_cast<Gf2Alloc*>(ctx);
-    auto* p = static_cast<uint32_t*>(vrb::dalloc((size_t)n * sizeof(uint32_t), a->s));
-    a->g->owned.push_back({p, (size_t)n * sizeof(uint32_t)});
-    return p;
+    const vrb::Alloc al = vrb::dalloc_owned((size_t)n * sizeof(uint32_t), a->s);
+    a->g->owned.push_back(al);
+    return static_cast<uint32_t*>(al.p);
 }
 }  // namespace
 
@@ -658,8 +678,9 @@ vrb_status vrb_gf2_blockprodsum(int64_t nrows, int64_t ncols, int64_t k, const u
         vrb_gf2* g = new vrb_gf2();
         try {
             g->ncols = ncols;
-            g->colptr = static_cast<uint64_t*>(vrb::dalloc((size_t)(ncols + 1) * sizeof(uint64_t), s));
-            g->owned.push_back({g->colptr, (size_t)(ncols + 1) * sizeof(uint64_t)});
+            const vrb::Alloc al = vrb::dalloc_owned((size_t)(ncols + 1) * sizeof(uint64_t), s);
+            g->colptr = static_cast<uint64_t*>(al.p);
+            g->owned.push_back(al);
             VRB_CUDA(cudaMemsetAsync(g->colptr, 0, (size_t)(ncols + 1) * sizeof(uint64_t), s));
             Gf2Alloc ctx{g, s};
             g->nnz = vrb::gf2_blockprodsum(nrows, ncols, k, d_colptr, d_rowval, c_colptr, c_rowval, e_colptr,

@@ -85,11 +85,16 @@ class DBuf {
     cudaStream_t s_ = 0;
 };
 
-// Owned output allocation recorded in the result handle.
+// Owned output allocation recorded in a result handle, with the free hook in
+// force when it was made (the hook may be changed before the handle is freed).
 struct Alloc {
     void* p;
     size_t bytes;
+    vrb_free_fn fn = nullptr;   // nullptr: cudaFreeAsync
+    void* ctx = nullptr;
 };
+Alloc dalloc_owned(size_t bytes, cudaStream_t s);
+void dfree_owned(const Alloc& a);
 
 // ---------------------------------------------------------------------------
 // Constants

@@ -406,6 +406,21 @@ def test_sortperm_nan_rejected(vrb):
         vrb.sortperm_f64(torch.tensor([1.0, float("nan")], dtype=torch.float64, device="cuda"))
 
 
+def test_handle_outlives_allocator_switch(vrb):
+    # a handle built through torch's caching allocator and freed after the hook
+    # is switched back releases its memory through the hook that allocated it
+    # (freeing torch memory with cudaFreeAsync would fail and leave an error
+    # pending for the next call)
+    X = workloads.random_cloud(9, 150, 3, "uniform")
+    vrb.use_torch_allocator(True)
+    try:
+        res = vrb.build(X, maxdim=1, radius=0.4)
+    finally:
+        vrb.use_torch_allocator(False)
+    res.free()
+    compare(vrb, X, 1, 0.4)
+
+
 def test_torch_allocator_hook(vrb):
     vrb.use_torch_allocator(True)
     try:
@@ -431,7 +446,7 @@ def _check_triangles_full(vrb, res, o, golden, n_levels_sampled=40):
     T = tv.shape[0]
     assert T == golden["count"]
     # (a) per-level histogram == oracle's
-    hist = torch.bincount(tf.to(torch.int64), minlength=E + 1).cpu().numpy().astype(np.uint64)
+    hist = torch.bincount(tf.to(torch.int64), minlength=o.nvals + 1).cpu().numpy().astype(np.uint64)
     assert hashlib.sha256(hist.tobytes()).hexdigest() == golden["hist_sha256"]
     # (b) strict (filt, lex) order, (c) rows are the three edges, filt = max edge filt
     evd = torch.from_numpy(ev.astype(np.int64)).to(dev)
