@@ -20,7 +20,10 @@
 namespace vrb {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef VRB_SORT_THREADS
+#define VRB_SORT_THREADS 256
+#endif
+constexpr int kThreads = VRB_SORT_THREADS;   // >= 256, a multiple of 32
 constexpr int kWarps = kThreads / 32;
 #ifndef VRB_SORT_ITEMS
 #define VRB_SORT_ITEMS 12
@@ -129,58 +132,64 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
         __syncwarp();
     }
     __syncthreads();
-    // ---- digit d (thread d): warps in order -> per-warp starts; tile count
-    const int d = threadIdx.x;   // kThreads == kBins
+    // ---- digit d (thread d < 256): warps in order -> per-warp starts; tile count
+    const int d = threadIdx.x;
+    const bool has_digit = d < kBins;
     uint32_t cnt = 0;
+    if (has_digit) {
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = S.woff[w][d];
-        S.woff[w][d] = cnt;
-        cnt += c;
-    }
-    // publish the tile aggregate early, then look back over earlier tiles
-    unsigned long long* st = status + (int64_t)tile * kBins + d;
-    unsigned long long excl = 0;
-    if (tile == 0) {
-        atomicExch(st, kFlagPre | cnt);
-    } else {
-        atomicExch(st, kFlagAgg | cnt);
-        // look back kLook tiles per step: their status words are read
-        // together, so a walk over aggregate-only tiles is not a chain of
-        // single dependent L2 reads
-        bool done = false;
-        for (int64_t j = (int64_t)tile - 1; !done; j -= kLook) {
-            unsigned long long sv[kLook];
-#pragma unroll
-            for (int u = 0; u < kLook; ++u)
-                sv[u] = j - u >= 0 ? *(const volatile unsigned long long*)(status + (j - u) * kBins + d) : kFlagPre;
-#pragma unroll
-            for (int u = 0; u < kLook; ++u) {
-                if (done) break;
-                unsigned long long s = sv[u];
-                while ((s & (kFlagAgg | kFlagPre)) == 0)
-                    s = *(const volatile unsigned long long*)(status + (j - u) * kBins + d);
-                excl += s & kValMask;
-                if (s & kFlagPre) done = true;
-            }
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = S.woff[w][d];
+            S.woff[w][d] = cnt;
+            cnt += c;
         }
-        atomicExch(st, kFlagPre | (excl + cnt));
+        // publish the tile aggregate early, then look back over earlier tiles
+        unsigned long long* st = status + (int64_t)tile * kBins + d;
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            atomicExch(st, kFlagPre | cnt);
+        } else {
+            atomicExch(st, kFlagAgg | cnt);
+            // look back kLook tiles per step: their status words are read
+            // together, so a walk over aggregate-only tiles is not a chain of
+            // single dependent L2 reads
+            bool done = false;
+            for (int64_t j = (int64_t)tile - 1; !done; j -= kLook) {
+                unsigned long long sv[kLook];
+#pragma unroll
+                for (int u = 0; u < kLook; ++u)
+                    sv[u] = j - u >= 0 ? *(const volatile unsigned long long*)(status + (j - u) * kBins + d)
+                                       : kFlagPre;
+#pragma unroll
+                for (int u = 0; u < kLook; ++u) {
+                    if (done) break;
+                    unsigned long long s = sv[u];
+                    while ((s & (kFlagAgg | kFlagPre)) == 0)
+                        s = *(const volatile unsigned long long*)(status + (j - u) * kBins + d);
+                    excl += s & kValMask;
+                    if (s & kFlagPre) done = true;
+                }
+            }
+            atomicExch(st, kFlagPre | (excl + cnt));
+        }
+        S.gstart[d] = pass_base[d] + excl;
     }
-    S.gstart[d] = pass_base[d] + excl;
-    // tile-local starts: exclusive scan of cnt over the 256 digits
+    // tile-local starts: exclusive scan of cnt over the 256 digits (warps 0..7)
     uint32_t x = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) S.wsum[wid] = x;
+    if (lane == 31 && wid < kBins / 32) S.wsum[wid] = x;
     __syncthreads();
-    uint32_t wpre = 0;
+    if (has_digit) {
+        uint32_t wpre = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w)
-        if (w < wid) wpre += S.wsum[w];
-    S.tstart[d] = wpre + x - cnt;
+        for (int w = 0; w < kBins / 32; ++w)
+            if (w < wid) wpre += S.wsum[w];
+        S.tstart[d] = wpre + x - cnt;
+    }
     __syncthreads();
     // ---- exchange through shared memory in tile order
 #pragma unroll
