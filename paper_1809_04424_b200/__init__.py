@@ -144,6 +144,8 @@ def abi_version() -> int:
 # allocator hook -> PyTorch caching allocator
 # ---------------------------------------------------------------------------
 _hooks = None
+_hooks_ever = []   # every hook pair ever installed: a handle frees through the hook
+                   # that allocated it, so its C callback must outlive the switch
 
 
 def use_torch_allocator(enable: bool = True):
@@ -171,6 +173,7 @@ def use_torch_allocator(enable: bool = True):
     hooks = (ALLOC_FN(_alloc), FREE_FN(_free))
     _check(lib().vrb_set_allocator(hooks[0], hooks[1], None))
     _hooks = hooks
+    _hooks_ever.append(hooks)
 
 
 def set_profiling(enable: bool):

@@ -383,7 +383,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
                    bmoff.get());
     bm.reset();
     timer.mark(4);
-    sort_tie_groups(2, o.efilt, toff.get(), E, tb[0], tb[1], n, o.tv, o.trows, s);
+    sort_tie_groups(2, o.efilt, toff.get(), E, tb[0], tb[1], n, o.tv, o.trows, s, o.ev);
     timer.mark(5);
     if (K < 3) return;
 

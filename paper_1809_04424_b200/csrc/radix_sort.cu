@@ -81,9 +81,10 @@ __global__ void k_scan_bins(unsigned long long* __restrict__ hist) {
     }
 }
 
+template <bool kVals>
 struct SweepSmem {
     uint64_t key[kTile];
-    uint32_t val[kTile];
+    uint32_t val[kVals ? kTile : 1];
     uint32_t woff[kWarps][kBins];   // per-warp digit counts -> tile-local start per warp
     uint32_t tstart[kBins];         // tile-local start of each digit
     unsigned long long gstart[kBins];   // global position of the tile's run of each digit
@@ -91,6 +92,8 @@ struct SweepSmem {
     uint32_t tile_id;
 };
 
+// kVals = false: keys only (vals_in / vals_out unused)
+template <bool kVals>
 __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint64_t* __restrict__ keys_in,
                                                        const uint32_t* __restrict__ vals_in,
                                                        uint64_t* __restrict__ keys_out,
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
                                                        unsigned long long* __restrict__ status,
                                                        unsigned* __restrict__ tile_counter, uint64_t bias) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SweepSmem& S = *reinterpret_cast<SweepSmem*>(smem_raw);
+    SweepSmem<kVals>& S = *reinterpret_cast<SweepSmem<kVals>*>(smem_raw);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) S.tile_id = atomicAdd(tile_counter, 1u);
     for (int q = threadIdx.x; q < kWarps * kBins; q += kThreads) (&S.woff[0][0])[q] = 0;
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
     for (int r = 0; r < kItems; ++r) {
         const int64_t i = base + r * 32 + lane;
         k[r] = i < n ? keys_in[i] - bias : 0ull;
-        v[r] = i < n ? vals_in[i] : 0u;
+        v[r] = (kVals && i < n) ? vals_in[i] : 0u;
     }
     // ---- stable warp-local ranks (rounds in order, lanes in order)
     const uint32_t lt = (1u << lane) - 1u;
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
             const uint32_t dg = (uint32_t)((k[r] >> shift) & 0xFF);
             const uint32_t pos = S.tstart[dg] + S.woff[wid][dg] + rk[r];
             S.key[pos] = k[r];
-            S.val[pos] = v[r];
+            if (kVals) S.val[pos] = v[r];
         }
     }
     __syncthreads();
@@ -208,14 +211,15 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
         const uint32_t dg = (uint32_t)((kk >> shift) & 0xFF);
         const unsigned long long dst = S.gstart[dg] + (uint32_t)(q - S.tstart[dg]);
         keys_out[dst] = kk;
-        vals_out[dst] = S.val[q];
+        if (kVals) vals_out[dst] = S.val[q];
     }
 }
 
 }  // namespace
 
-bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
-                      int64_t n, uint64_t varying, cudaStream_t s, uint64_t bias, bool* biased) {
+template <bool kVals>
+bool radix_sort_impl(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt, int64_t n,
+                     uint64_t varying, cudaStream_t s, uint64_t bias, bool* biased) {
     if (biased) *biased = false;
     if (n <= 1 || varying == 0) return false;
     if (biased) *biased = true;
@@ -235,8 +239,8 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
     DBuf<unsigned> counters(npass, s);
     VRB_CUDA(cudaMemsetAsync(status.get(), 0, status.bytes(), s));
     VRB_CUDA(cudaMemsetAsync(counters.get(), 0, counters.bytes(), s));
-    const size_t smem = sizeof(SweepSmem);
-    VRB_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = sizeof(SweepSmem<kVals>);
+    VRB_CUDA(cudaFuncSetAttribute(k_onesweep<kVals>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool alt = false;
     int pass = 0;
     for (int d = 0; d < 8; ++d) {
@@ -245,7 +249,7 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
         uint64_t* kout = alt ? keys : keys_alt;
         uint32_t* vin = alt ? vals_alt : vals;
         uint32_t* vout = alt ? vals : vals_alt;
-        k_onesweep<<<(unsigned)ntiles, kThreads, smem, s>>>(kin, vin, kout, vout, n, 8 * d, hist.get() + d * kBins,
+        k_onesweep<kVals><<<(unsigned)ntiles, kThreads, smem, s>>>(kin, vin, kout, vout, n, 8 * d, hist.get() + d * kBins,
                                                             status.get() + (size_t)pass * ntiles * kBins,
                                                             counters.get() + pass, pass == 0 ? bias : 0ull);
         VRB_LAUNCH_CHECK();
@@ -253,6 +257,15 @@ bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32
         ++pass;
     }
     return alt;
+}
+
+bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt, int64_t n,
+                      uint64_t varying, cudaStream_t s, uint64_t bias, bool* biased) {
+    return radix_sort_impl<true>(keys, keys_alt, vals, vals_alt, n, varying, s, bias, biased);
+}
+
+bool radix_sort_keys(uint64_t* keys, uint64_t* keys_alt, int64_t n, uint64_t varying, cudaStream_t s) {
+    return radix_sort_impl<false>(keys, keys_alt, nullptr, nullptr, n, varying, s, 0, nullptr);
 }
 
 }  // namespace vrb

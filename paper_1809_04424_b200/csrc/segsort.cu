@@ -212,6 +212,63 @@ __global__ void k_codes_of(const uint32_t* __restrict__ val, int64_t M, const ui
     }
 }
 
+// ---- keys-only path (triangles, n <= kTableMaxN): the key packs (segment,
+// v0, v1, v2) with vbits per vertex; after the sort the vertices are decoded
+// from the key and the D_2 rows recomputed from an n x n table of edge
+// positions (L2-resident for the tie-heavy inputs: HIV's 1088 vertices take
+// 4.7 MB), so no row or value moves through the sort.
+constexpr int64_t kTableMaxN = 8192;
+
+__global__ void k_tab_positions(const uint32_t* __restrict__ ev, int64_t E, int64_t n, uint32_t* __restrict__ tab) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = ev[2 * p], b = ev[2 * p + 1];
+        tab[a * (uint64_t)n + b] = (uint32_t)p;
+        tab[b * (uint64_t)n + a] = (uint32_t)p;
+    }
+}
+
+__global__ void k_tri_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
+                           const uint32_t* __restrict__ verts, int vb, uint64_t* __restrict__ key) {
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const Seg S = segs[g];
+        const uint64_t o = segoff[g];
+        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
+            const uint32_t* v = verts + 3 * (S.start + q);
+            key[o + q] = ((uint64_t)g << (3 * vb)) | ((uint64_t)v[0] << (2 * vb)) | ((uint64_t)v[1] << vb) | v[2];
+        }
+    }
+}
+
+__global__ void k_tri_apply(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
+                            const uint64_t* __restrict__ key, int vb, const uint32_t* __restrict__ tab, int64_t n,
+                            uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
+    const uint64_t m = (1ull << vb) - 1ull;
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const Seg S = segs[g];
+        const uint64_t o = segoff[g];
+        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
+            const uint64_t kk = key[o + q];
+            const uint32_t a = (uint32_t)((kk >> (2 * vb)) & m), b = (uint32_t)((kk >> vb) & m), c = (uint32_t)(kk & m);
+            uint32_t* out = verts + 3 * (S.start + q);
+            out[0] = a;
+            out[1] = b;
+            out[2] = c;
+            if (rows) {
+                uint32_t r0 = __ldg(tab + (uint64_t)a * n + b), r1 = __ldg(tab + (uint64_t)a * n + c),
+                         r2 = __ldg(tab + (uint64_t)b * n + c);
+                uint32_t t;
+                if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
+                if (r1 > r2) { t = r1; r1 = r2; r2 = t; }
+                if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
+                uint32_t* rw = rows + 3 * (S.start + q);
+                rw[0] = r0;
+                rw[1] = r1;
+                rw[2] = r2;
+            }
+        }
+    }
+}
+
 int bits_for(uint64_t v) {   // bits to hold 0..v
     int b = 1;
     while (b < 64 && (v >> b)) ++b;
@@ -220,8 +277,7 @@ int bits_for(uint64_t v) {   // bits to hold 0..v
 
 template <int K>
 void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi, int64_t n,
-               uint32_t* verts, uint32_t* rows, cudaStream_t s) {
-    (void)E;
+               uint32_t* verts, uint32_t* rows, const uint32_t* ev, cudaStream_t s) {
     uint64_t slot0 = 0;
     VRB_CUDA(cudaMemcpyAsync(&slot0, off + p_lo, sizeof(slot0), cudaMemcpyDeviceToHost, s));
     const int64_t span = p_hi - p_lo;
@@ -272,8 +328,28 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
     DBuf<uint64_t> dsegoff(nb + 1, s);
     VRB_CUDA(cudaMemcpyAsync(dseg.get(), big.data(), nb * sizeof(Seg), cudaMemcpyHostToDevice, s));
     VRB_CUDA(cudaMemcpyAsync(dsegoff.get(), hoff.data(), (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    const int cbits = (K + 1) * Code<K>::kBitsPer;   // as packed by Code<K>
     const int vbits = bits_for((uint64_t)std::max<int64_t>(n - 1, 1));
+    const unsigned gb = (unsigned)std::min<int64_t>(nb, (int64_t)device_sm_count() * 8);
+    if (K == 2 && (!rows || (ev && n <= kTableMaxN)) && 3 * vbits + bits_for((uint64_t)std::max<int64_t>(nb - 1, 1)) <= 64) {
+        DBuf<uint32_t> tab;
+        if (rows) {
+            tab.alloc((size_t)(n * n), s);
+            VRB_CUDA(cudaMemsetAsync(tab.get(), 0xFF, tab.bytes(), s));
+            k_tab_positions<<<(unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16), 256, 0,
+                              s>>>(ev, E, n, tab.get());
+            VRB_LAUNCH_CHECK();
+        }
+        DBuf<uint64_t> k0(M, s), k1(M, s);
+        k_tri_keys<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, verts, vbits, k0.get());
+        VRB_LAUNCH_CHECK();
+        const uint64_t vary = varying_bits(k0.get(), M, s);
+        const bool alt = radix_sort_keys(k0.get(), k1.get(), M, vary, s);
+        k_tri_apply<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, alt ? k1.get() : k0.get(), vbits, tab.get(), n,
+                                       verts, rows);
+        VRB_LAUNCH_CHECK();
+        return;
+    }
+    const int cbits = (K + 1) * Code<K>::kBitsPer;   // as packed by Code<K>
     // the code's top (K + 1) * kBitsPer bits hold K + 1 ids of vbits each:
     // only its low (K + 1 - 1) * kBitsPer + vbits bits can be nonzero
     const int code_bits = K * Code<K>::kBitsPer + vbits;
@@ -281,7 +357,6 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
     (void)cbits;
     DBuf<uint64_t> k0(M, s), k1(M, s);
     DBuf<uint32_t> v0(M, s), v1(M, s);
-    const unsigned gb = (unsigned)std::min<int64_t>(nb, (int64_t)device_sm_count() * 8);
     k_big_keys<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, verts, code_bits, packed ? 1 : 0, k0.get(),
                                     v0.get());
     VRB_LAUNCH_CHECK();
@@ -319,13 +394,13 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
 }  // namespace
 
 void sort_tie_groups(int k, const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi,
-                     int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s) {
+                     int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s, const uint32_t* ev) {
     if (p_lo >= p_hi) return;
     if (k == 2) {
-        sort_ties<2>(efilt, off, E, p_lo, p_hi, n, verts, rows, s);
+        sort_ties<2>(efilt, off, E, p_lo, p_hi, n, verts, rows, ev, s);
     } else {
         if (n > 65536) fail(VRB_ENOTSUP, "tetrahedra tie sort needs n <= 65536 (16-bit lex codes)");
-        sort_ties<3>(efilt, off, E, p_lo, p_hi, n, verts, rows, s);
+        sort_ties<3>(efilt, off, E, p_lo, p_hi, n, verts, rows, ev, s);
     }
 }
 

@@ -377,7 +377,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
             fill_triangles(g, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s, bm.get(), bmoff.get());
             bm.reset();
             timer.mark(4);
-            sort_tie_groups(2, efilt, toff.get(), E, 0, E, n, tv, trows, s);
+            sort_tie_groups(2, efilt, toff.get(), E, 0, E, n, tv, trows, s, ev);
             timer.mark(5);
             h->verts[2] = tv;
             h->filt[2] = tf;

@@ -133,6 +133,9 @@ uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* km
 bool radix_sort_pairs(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_t* vals_alt,
                       int64_t n, uint64_t varying, cudaStream_t s, uint64_t bias = 0, bool* biased = nullptr);
 
+// The same sort on keys alone (8 bytes per item per pass instead of 12).
+bool radix_sort_keys(uint64_t* keys, uint64_t* keys_alt, int64_t n, uint64_t varying, cudaStream_t s);
+
 // Fill helpers
 void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s);
 void iota_u32(uint32_t* p, int64_t n, cudaStream_t s);

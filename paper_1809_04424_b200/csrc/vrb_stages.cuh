@@ -109,8 +109,10 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
 // Reorder the k-simplices (k = 2, 3) of every tie group (>= 2 edges sharing a
 // level) into lex order (readings A3, A4); only owner edges in [p_lo, p_hi).
 // off = per-owner-edge simplex offsets (E + 1); verts/rows: (k+1) u32 each.
+// ev (2E edge endpoints, nullable): lets the triangle path recompute D_2 rows
+// from an edge-position table instead of carrying them through the sort.
 void sort_tie_groups(int k, const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_lo, int64_t p_hi,
-                     int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s);
+                     int64_t n, uint32_t* verts, uint32_t* rows, cudaStream_t s, const uint32_t* ev = nullptr);
 
 // S6 + S7 + S8 for tetrahedra (tetrahedra.cu).  Needs the complete triangle
 // arrays of dimension 2 (face positions for D_3).
