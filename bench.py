@@ -43,6 +43,20 @@ SURVEY_BALG = {"edge_k1": 44, "edge_k2": 56, "tri": 44, "tet": 52}
 ORACLE_SAMPLE = {"C1": 50, "C2": 1000, "C3": 900, "C4": 2200, "C5A": 6000, "C5B": 4400, "HIV": 500}
 
 
+def _host_cpu():
+    """(logical cores of the host, CPU model) -- context for the oracle baseline."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -162,7 +176,8 @@ def run_reference(args, rank, world):
         "data": "synthetic", "config": {"workload": args.workload, "desc": w.config, "maxdim": w.maxdim,
                                         "radius": w.radius if math.isfinite(w.radius) else "inf",
                                         "sample_points": m},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_cores": _host_cpu()[0], "host_cpu": _host_cpu()[1]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -358,7 +373,11 @@ def main():
             em = float(t.item())
         e2e = {"value": units_global * len(e2e_ms) / (em / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": em / len(e2e_ms)}
+               "ms_per_step": em / len(e2e_ms),
+               "d2h": "per-dimension counts + value_of_rank; the simplex, filt and boundary arrays "
+                      "stay device-resident for the persistence reduction (%.1f GB for this workload)"
+                      % (4e-9 * (2 * counts[1][0] + sum((k + 2) * counts[k][0] + (k + 1) * counts[k][0]
+                                                       for k in range(2, len(counts)))))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -366,7 +385,8 @@ def main():
         u, sec = oracle_sample(w, m)
         cpu = {"value": u / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"first {m} of {X.shape[0]} points of {args.workload} ({u} simplices, "
-                         f"{sec:.1f} s), oracle steps 1-7 single-threaded"}
+                         f"{sec:.1f} s), oracle steps 1-7 single-threaded",
+               "host_cores": _host_cpu()[0], "host_cpu": _host_cpu()[1]}
 
     if rank == 0:
         line = {

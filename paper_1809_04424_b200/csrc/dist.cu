@@ -230,6 +230,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     const int K = opts->maxdim + 1;
     const bool strict = (opts->flags & VRB_STRICT_RADIUS) != 0;
     StageTimer& timer = *o.timer;
+    timer.begin(6);
 
     // ---- S1: rank 0 places the points, everyone receives them
     DBuf<double> Xd((size_t)(n * d), s);
@@ -247,12 +248,14 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
         if (n * d) C.bcast(Xd.get(), (size_t)(n * d) * sizeof(double), 0);
     }
     timer.mark(6);
+    timer.begin(0);
     // ---- S2: this rank's row block
     KeptEdges ke;
     const std::vector<int64_t> rows = row_blocks(n, G);
     build_kept_edges(Xd.get(), n, d, opts->radius, strict, s, ke, rows[rk], rows[rk + 1] == n ? -1 : rows[rk + 1]);
     Xd.reset();
     timer.mark(0);
+    timer.begin(1);
     // ---- S3: local sort, all-gather of the runs, merge
     DBuf<uint64_t> rkey, rij;   // this rank's run, padded to the longest
     const std::vector<uint64_t> Es = C.allgather_u64((uint64_t)ke.E);
@@ -271,6 +274,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     }
     ke = KeptEdges();
     timer.mark(1);
+    timer.begin(6);
     DBuf<uint64_t> ak((size_t)G * std::max<uint64_t>(maxE, 1), s), ai((size_t)G * std::max<uint64_t>(maxE, 1), s);
     if (maxE) {
         C.allgather(rkey.get(), ak.get(), maxE * sizeof(uint64_t));
@@ -279,6 +283,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     rkey.reset();
     rij.reset();
     timer.mark(6);
+    timer.begin(1);
     // merge rounds: adjacent runs merged pairwise into the other buffer
     // (the first round also compacts the maxE-strided runs), log2 G rounds
     DBuf<uint64_t> bk(std::max<int64_t>(E, 1), s), bi(std::max<int64_t>(E, 1), s);
@@ -328,12 +333,14 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     }
     ak.reset(); ai.reset(); bk.reset(); bi.reset();
     timer.mark(1);
+    timer.begin(2);
     if (K < 2) return;
 
     // ---- S4: neighbour lists (every rank), S5: this rank's owner edges
     Graph g;
     build_lists(o.ev, n, E, s, g);
     timer.mark(2);
+    timer.begin(3);
     int64_t tb[2] = {0, 0};
     if (E) {
         DBuf<uint64_t> w(E, s);
@@ -361,6 +368,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     else VRB_CUDA(cudaMemsetAsync(toff.get(), 0, sizeof(uint64_t), s));
     const uint64_t Tl = E ? read_u64(toff.get() + E, s) : 0;
     timer.mark(3);
+    timer.begin(6);
     const std::vector<uint64_t> Ts = C.allgather_u64(Tl);
     uint64_t T = 0, t0 = 0, maxT = 0;
     for (int q = 0; q < G; ++q) {
@@ -369,6 +377,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
         maxT = std::max(maxT, Ts[q]);
     }
     timer.mark(6);
+    timer.begin(3);
     if (T >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu triangles exceed u32 positions", (unsigned long long)T);
     o.T = T;
     o.t0 = t0;
@@ -379,12 +388,15 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     DBuf<uint16_t> tapex;
     if (K >= 3 && n <= 65536) tapex.alloc((size_t)std::max<uint64_t>(Tl, 1), s);
     timer.mark(3);
+    timer.begin(4);
     fill_triangles(g, o.efilt, toff.get(), tb[0], tb[1], 0, o.tv, o.tf, o.trows, tapex.get(), s, bm.get(),
                    bmoff.get());
     bm.reset();
     timer.mark(4);
+    timer.begin(5);
     sort_tie_groups(2, o.efilt, toff.get(), E, tb[0], tb[1], n, o.tv, o.trows, s, o.ev);
     timer.mark(5);
+    timer.begin(6);
     if (K < 3) return;
 
     // ---- S6: tetrahedra.  Exchange the per-edge triangle counts and the
@@ -432,6 +444,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     }
     tapex.reset();
     timer.mark(6);
+    timer.begin(8);
     TriLevels L;
     L.apex = apex_all.get();
     L.ev = o.ev;
@@ -452,6 +465,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     else VRB_CUDA(cudaMemsetAsync(qoff.get(), 0, sizeof(uint64_t), s));
     const uint64_t Ql = E ? read_u64(qoff.get() + E, s) : 0;
     timer.mark(8);
+    timer.begin(6);
     const std::vector<uint64_t> Qs = C.allgather_u64(Ql);
     uint64_t Q = 0, q0 = 0;
     for (int q = 0; q < G; ++q) {
@@ -459,6 +473,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
         Q += Qs[q];
     }
     timer.mark(6);
+    timer.begin(8);
     if (Q >= 0xFFFFFFFFull) fail(VRB_EOVERFLOW, "%llu tetrahedra exceed u32 positions", (unsigned long long)Q);
     o.Q = Q;
     o.q0 = q0;
@@ -467,8 +482,10 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     o.qf = o.alloc_u32(Ql);
     o.qrows = (opts->flags & VRB_SKIP_BOUNDARY) ? nullptr : o.alloc_u32(4 * Ql);
     timer.mark(8);
+    timer.begin(9);
     fill_tets(g, L, o.efilt, qoff.get(), qb[0], qb[1], 0, o.qv, o.qf, o.qrows, s);
     timer.mark(9);
+    timer.begin(5);
     sort_tie_groups(3, o.efilt, qoff.get(), E, qb[0], qb[1], n, o.qv, o.qrows, s);
     timer.mark(5);
 }

@@ -6,6 +6,8 @@
 #include <mutex>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
 
@@ -133,7 +135,34 @@ void StageTimer::start(cudaStream_t st) {
     marks.push_back({-1, e});
 }
 
+// NVTX ranges per stage ("vrb/S2 distance", ...; visible to nsys / ncu
+// --nvtx): begin(stage) opens one, the next mark() closes it.
+static const char* stage_name(int st) {
+    switch (st) {
+        case 0: return "vrb/S1-S2 points+distance";
+        case 1: return "vrb/S3 edge rank";
+        case 2: return "vrb/S4 neighbour lists";
+        case 3: return "vrb/S5 count+offsets";
+        case 4: return "vrb/S5-S8 triangle fill";
+        case 5: return "vrb/S7 tie-group sort";
+        case 6: return "vrb/exchange";
+        case 8: return "vrb/S6 tetrahedron count";
+        case 9: return "vrb/S6-S8 tetrahedron fill";
+        default: return "vrb/stage";
+    }
+}
+
+void StageTimer::begin(int stage) {
+    if (nvtx_open) nvtxRangePop();
+    nvtxRangePushA(stage_name(stage));
+    nvtx_open = true;
+}
+
 void StageTimer::mark(int stage) {
+    if (nvtx_open) {
+        nvtxRangePop();
+        nvtx_open = false;
+    }
     if (!on) return;
     cudaEvent_t e;
     VRB_CUDA(cudaEventCreate(&e));
@@ -157,6 +186,7 @@ void StageTimer::finish() {
 }
 
 StageTimer::~StageTimer() {
+    if (nvtx_open) nvtxRangePop();
     for (auto& m : marks) cudaEventDestroy(m.second);
 }
 
@@ -318,6 +348,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
         h->init(n, d, opts);
         StageTimer timer;
         timer.start(s);
+        timer.begin(0);
 
         DBuf<double> Xd;
         KeptEdges ke;
@@ -330,6 +361,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
         }
         Xd.reset();
         timer.mark(0);
+        timer.begin(1);
         const int64_t E = ke.E;
         h->count[1] = E;
         uint32_t* ev = h->own<uint32_t>(2 * E, s);
@@ -339,10 +371,12 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
         h->set_edges(ev, efilt, 0, 1);
         ke = KeptEdges();
         timer.mark(1);
+        timer.begin(2);
         if (h->K >= 2) {
             Graph g;
             build_graph(ev, n, E, s, g);
             timer.mark(2);
+            timer.begin(3);
             // ---- triangles: count per owner edge, offsets
             DBuf<uint32_t> cnt(E, s);
             // the count pass keeps the apex bitmaps the fill emits from
@@ -374,11 +408,14 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
                 VRB_CUDA(cudaMemsetAsync(tapex.get() + T, 0xFF, 16 * sizeof(uint16_t), s));
             }
             timer.mark(3);
+            timer.begin(4);
             fill_triangles(g, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s, bm.get(), bmoff.get());
             bm.reset();
             timer.mark(4);
+            timer.begin(5);
             sort_tie_groups(2, efilt, toff.get(), E, 0, E, n, tv, trows, s, ev);
             timer.mark(5);
+            timer.begin(3);
             h->verts[2] = tv;
             h->filt[2] = tf;
             h->rows[2] = trows;
@@ -391,6 +428,7 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
                 triangle_levels(efilt, toff.get(), E, tv, s, L);
                 DBuf<uint32_t> qc(E, s);
                 timer.mark(3);
+                timer.begin(8);
                 count_tets(g, L, qc.get(), 0, 1, s);
                 DBuf<uint64_t> qoff(E + 1, s);
                 exclusive_scan(qc.get(), qoff.get(), E, s);
@@ -404,8 +442,10 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
                 h->filt[3] = h->own<uint32_t>(Q, s);
                 if (!(opts->flags & VRB_SKIP_BOUNDARY)) h->rows[3] = h->own<uint32_t>(4 * Q, s);
                 timer.mark(8);
+                timer.begin(9);
                 fill_tets(g, L, efilt, qoff.get(), 0, E, 0, h->verts[3], h->filt[3], h->rows[3], s);
                 timer.mark(9);
+                timer.begin(5);
                 sort_tie_groups(3, efilt, qoff.get(), E, 0, E, n, h->verts[3], h->rows[3], s);
                 timer.mark(5);
             }

@@ -145,7 +145,9 @@ struct StageTimer {
     bool on = false;
     cudaStream_t s = 0;
     std::vector<std::pair<int, cudaEvent_t>> marks;
+    bool nvtx_open = false;
     void start(cudaStream_t st);
+    void begin(int stage);  // start of `stage` (NVTX range)
     void mark(int stage);   // end of `stage`
     void finish();          // synchronises and stores into the thread-local slot
     ~StageTimer();

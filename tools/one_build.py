@@ -12,10 +12,16 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "C5B"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 w = workloads.WORKLOADS[cfg]
 npts = int(sys.argv[3]) if len(sys.argv) > 3 else None   # optional: first npts points only
-X = torch.from_numpy(w.points()[:npts]).cuda()
+P = w.points()
+if w.kind == "matrix":
+    P = P[:npts, :npts] if npts else P
+else:
+    P = P[:npts]
+X = torch.from_numpy(P.copy()).cuda()
 vrb.use_torch_allocator(True)
 for _ in range(reps):
-    r = vrb.build(X, maxdim=w.maxdim, radius=w.radius)
+    r = (vrb.build_dm(X, maxdim=w.maxdim, radius=w.radius) if w.kind == "matrix"
+         else vrb.build(X, maxdim=w.maxdim, radius=w.radius))
     torch.cuda.synchronize()
     del r
 print("done", cfg, reps)
