@@ -312,7 +312,7 @@ void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so) {
     bool biased = false;
     bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary_top, s, kmin, &biased);
     const uint64_t bias = biased ? kmin : 0ull;
-    if (shift) {
+    if (shift && (vary & ((1ull << shift) - 1ull))) {   // varying bits below the sorted digits
         uint64_t* k1 = alt ? key_alt.get() : ke.key.get();
         uint32_t* v1 = alt ? perm_alt.get() : vals;
         DBuf<int> fb(1, s);

@@ -113,22 +113,25 @@ __global__ void k_varying(const uint64_t* __restrict__ k, int64_t n, unsigned lo
 }
 
 __global__ void k_minmax(const uint64_t* __restrict__ k, int64_t n, unsigned long long* out) {
-    uint64_t mn = ~0ull, mx = 0;
+    uint64_t mn = ~0ull, mx = 0, any = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t v = k[i];
         mn = v < mn ? v : mn;
         mx = v > mx ? v : mx;
+        any |= v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const uint64_t a = __shfl_down_sync(0xffffffffu, mn, o), b = __shfl_down_sync(0xffffffffu, mx, o);
         mn = a < mn ? a : mn;
         mx = b > mx ? b : mx;
+        any |= __shfl_down_sync(0xffffffffu, any, o);
     }
     if ((threadIdx.x & 31) == 0) {
         atomicMin(&out[0], (unsigned long long)mn);
         atomicMax(&out[1], (unsigned long long)mx);
+        atomicOr(&out[2], (unsigned long long)any);
     }
 }
 
@@ -177,17 +180,24 @@ uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s) {
 uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin) {
     *kmin = 0;
     if (n <= 0) return 0;
-    DBuf<unsigned long long> acc(2, s);
-    const unsigned long long init[2] = {~0ull, 0ull};
+    DBuf<unsigned long long> acc(3, s);
+    const unsigned long long init[3] = {~0ull, 0ull, 0ull};
     VRB_CUDA(cudaMemcpyAsync(acc.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
     k_minmax<<<grid_for(n, 256), 256, 0, s>>>(keys, n, acc.get());
     VRB_LAUNCH_CHECK();
-    unsigned long long h[2] = {0, 0};
+    unsigned long long h[3] = {0, 0, 0};
     VRB_CUDA(cudaMemcpyAsync(h, acc.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *kmin = h[0];
     uint64_t d = h[1] - h[0], mask = 0;
     while (d) { mask = (mask << 1) | 1ull; d >>= 1; }
+    // bits below the lowest set bit of any key are zero in every key, and so
+    // in every (key - min): those digits never vary (e.g. integer-valued
+    // lengths, HIV's Hamming distances)
+    if (h[2]) {
+        const int tz = __builtin_ctzll(h[2]);
+        mask &= tz >= 64 ? 0ull : ~((1ull << tz) - 1ull);
+    }
     return mask;
 }
 

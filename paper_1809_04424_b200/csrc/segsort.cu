@@ -135,22 +135,34 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_small(const Seg* __restri
     }
 }
 
+// segment of element q of the concatenated large segments (segoff: nseg + 1
+// ascending offsets): binary search, element-parallel kernels below
+__device__ __forceinline__ int64_t seg_of(const uint64_t* __restrict__ segoff, int64_t nseg, uint64_t q) {
+    int64_t lo = 0, hi = nseg;   // last g with segoff[g] <= q
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(segoff + mid) <= q) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+#define ELEM_STRIDE(q, M) \
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (uint64_t)(M); \
+         q += (uint64_t)gridDim.x * blockDim.x)
+
 // Keys of the large segments: element q (0..M) of the concatenated segments
 // (segment g at [segoff[g], segoff[g+1])) -> (g << cbits | code) when packed,
 // else the code alone; vals = the element's slot.
 template <int K>
 __global__ void k_big_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
-                           const uint32_t* __restrict__ verts, int cbits, int packed, uint64_t* __restrict__ key,
-                           uint32_t* __restrict__ val) {
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-        const Seg S = segs[g];
-        const uint64_t o = segoff[g];
-        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
-            const uint64_t slot = S.start + q;
-            const uint64_t code = Code<K>::pack(verts + (K + 1) * slot);
-            key[o + q] = packed ? (((uint64_t)g << cbits) | code) : code;
-            val[o + q] = (uint32_t)slot;
-        }
+                           int64_t M, const uint32_t* __restrict__ verts, int cbits, int packed,
+                           uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+    ELEM_STRIDE(q, M) {
+        const int64_t g = seg_of(segoff, nseg, q);
+        const uint64_t slot = segs[g].start + (q - segoff[g]);
+        const uint64_t code = Code<K>::pack(verts + (K + 1) * slot);
+        key[q] = packed ? (((uint64_t)g << cbits) | code) : code;
+        val[q] = (uint32_t)slot;
     }
 }
 
@@ -181,23 +193,20 @@ __global__ void k_big_rows(const uint32_t* __restrict__ val, int64_t M, const ui
 }
 
 // scatter: the q-th sorted element goes to slot segs[g].start + (q - segoff[g])
-// of its segment g; its vertices are re-read from the source slot's code
+// of its segment g; its vertices are decoded from its code
 template <int K>
 __global__ void k_big_apply(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
-                            const uint32_t* __restrict__ val, const uint64_t* __restrict__ codes,
-                            const uint32_t* __restrict__ rcopy, uint32_t* __restrict__ verts,
-                            uint32_t* __restrict__ rows) {
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-        const Seg S = segs[g];
-        const uint64_t o = segoff[g];
-        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
-            uint32_t v[K + 1];
-            Code<K>::unpack(codes[o + q], v);
-            uint32_t* out = verts + (K + 1) * (S.start + q);
-            for (int c = 0; c <= K; ++c) out[c] = v[c];
-            if (rows)
-                for (int c = 0; c <= K; ++c) rows[(K + 1) * (S.start + q) + c] = rcopy[(K + 1) * (o + q) + c];
-        }
+                            int64_t M, const uint64_t* __restrict__ codes, const uint32_t* __restrict__ rcopy,
+                            uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
+    ELEM_STRIDE(q, M) {
+        const int64_t g = seg_of(segoff, nseg, q);
+        const uint64_t slot = segs[g].start + (q - segoff[g]);
+        uint32_t v[K + 1];
+        Code<K>::unpack(codes[q], v);
+        uint32_t* out = verts + (K + 1) * slot;
+        for (int c = 0; c <= K; ++c) out[c] = v[c];
+        if (rows)
+            for (int c = 0; c <= K; ++c) rows[(K + 1) * slot + c] = rcopy[(K + 1) * q + c];
     }
 }
 
@@ -228,43 +237,38 @@ __global__ void k_tab_positions(const uint32_t* __restrict__ ev, int64_t E, int6
 }
 
 __global__ void k_tri_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
-                           const uint32_t* __restrict__ verts, int vb, uint64_t* __restrict__ key) {
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-        const Seg S = segs[g];
-        const uint64_t o = segoff[g];
-        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
-            const uint32_t* v = verts + 3 * (S.start + q);
-            key[o + q] = ((uint64_t)g << (3 * vb)) | ((uint64_t)v[0] << (2 * vb)) | ((uint64_t)v[1] << vb) | v[2];
-        }
+                           int64_t M, const uint32_t* __restrict__ verts, int vb, uint64_t* __restrict__ key) {
+    ELEM_STRIDE(q, M) {
+        const int64_t g = seg_of(segoff, nseg, q);
+        const uint32_t* v = verts + 3 * (segs[g].start + (q - segoff[g]));
+        key[q] = ((uint64_t)g << (3 * vb)) | ((uint64_t)v[0] << (2 * vb)) | ((uint64_t)v[1] << vb) | v[2];
     }
 }
 
 __global__ void k_tri_apply(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
-                            const uint64_t* __restrict__ key, int vb, const uint32_t* __restrict__ tab, int64_t n,
-                            uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
+                            int64_t M, const uint64_t* __restrict__ key, int vb, const uint32_t* __restrict__ tab,
+                            int64_t n, uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
     const uint64_t m = (1ull << vb) - 1ull;
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-        const Seg S = segs[g];
-        const uint64_t o = segoff[g];
-        for (uint64_t q = threadIdx.x; q < S.len; q += blockDim.x) {
-            const uint64_t kk = key[o + q];
-            const uint32_t a = (uint32_t)((kk >> (2 * vb)) & m), b = (uint32_t)((kk >> vb) & m), c = (uint32_t)(kk & m);
-            uint32_t* out = verts + 3 * (S.start + q);
-            out[0] = a;
-            out[1] = b;
-            out[2] = c;
-            if (rows) {
-                uint32_t r0 = __ldg(tab + (uint64_t)a * n + b), r1 = __ldg(tab + (uint64_t)a * n + c),
-                         r2 = __ldg(tab + (uint64_t)b * n + c);
-                uint32_t t;
-                if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
-                if (r1 > r2) { t = r1; r1 = r2; r2 = t; }
-                if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
-                uint32_t* rw = rows + 3 * (S.start + q);
-                rw[0] = r0;
-                rw[1] = r1;
-                rw[2] = r2;
-            }
+    ELEM_STRIDE(q, M) {
+        const int64_t g = seg_of(segoff, nseg, q);
+        const uint64_t slot = segs[g].start + (q - segoff[g]);
+        const uint64_t kk = key[q];
+        const uint32_t a = (uint32_t)((kk >> (2 * vb)) & m), b = (uint32_t)((kk >> vb) & m), c = (uint32_t)(kk & m);
+        uint32_t* out = verts + 3 * slot;
+        out[0] = a;
+        out[1] = b;
+        out[2] = c;
+        if (rows) {
+            uint32_t r0 = __ldg(tab + (uint64_t)a * n + b), r1 = __ldg(tab + (uint64_t)a * n + c),
+                     r2 = __ldg(tab + (uint64_t)b * n + c);
+            uint32_t t;
+            if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
+            if (r1 > r2) { t = r1; r1 = r2; r2 = t; }
+            if (r0 > r1) { t = r0; r0 = r1; r1 = t; }
+            uint32_t* rw = rows + 3 * slot;
+            rw[0] = r0;
+            rw[1] = r1;
+            rw[2] = r2;
         }
     }
 }
@@ -329,7 +333,7 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
     VRB_CUDA(cudaMemcpyAsync(dseg.get(), big.data(), nb * sizeof(Seg), cudaMemcpyHostToDevice, s));
     VRB_CUDA(cudaMemcpyAsync(dsegoff.get(), hoff.data(), (nb + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     const int vbits = bits_for((uint64_t)std::max<int64_t>(n - 1, 1));
-    const unsigned gb = (unsigned)std::min<int64_t>(nb, (int64_t)device_sm_count() * 8);
+    const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(M, 256), (int64_t)device_sm_count() * 16);
     if (K == 2 && (!rows || (ev && n <= kTableMaxN)) && 3 * vbits + bits_for((uint64_t)std::max<int64_t>(nb - 1, 1)) <= 64) {
         DBuf<uint32_t> tab;
         if (rows) {
@@ -340,11 +344,11 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
             VRB_LAUNCH_CHECK();
         }
         DBuf<uint64_t> k0(M, s), k1(M, s);
-        k_tri_keys<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, verts, vbits, k0.get());
+        k_tri_keys<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, M, verts, vbits, k0.get());
         VRB_LAUNCH_CHECK();
         const uint64_t vary = varying_bits(k0.get(), M, s);
         const bool alt = radix_sort_keys(k0.get(), k1.get(), M, vary, s);
-        k_tri_apply<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, alt ? k1.get() : k0.get(), vbits, tab.get(), n,
+        k_tri_apply<<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, M, alt ? k1.get() : k0.get(), vbits, tab.get(), n,
                                        verts, rows);
         VRB_LAUNCH_CHECK();
         return;
@@ -357,7 +361,7 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
     (void)cbits;
     DBuf<uint64_t> k0(M, s), k1(M, s);
     DBuf<uint32_t> v0(M, s), v1(M, s);
-    k_big_keys<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, verts, code_bits, packed ? 1 : 0, k0.get(),
+    k_big_keys<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, M, verts, code_bits, packed ? 1 : 0, k0.get(),
                                     v0.get());
     VRB_LAUNCH_CHECK();
     const uint64_t vary = varying_bits(k0.get(), M, s);
@@ -387,7 +391,7 @@ void sort_ties(const uint32_t* efilt, const uint64_t* off, int64_t E, int64_t p_
         k_big_rows<K><<<gm, 256, 0, s>>>(sv, M, rows, rcopy.get());
         VRB_LAUNCH_CHECK();
     }
-    k_big_apply<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, sv, sk, rcopy.get(), verts, rows);
+    k_big_apply<K><<<gb, 256, 0, s>>>(dseg.get(), dsegoff.get(), nb, M, sk, rcopy.get(), verts, rows);
     VRB_LAUNCH_CHECK();
 }
 

@@ -29,6 +29,23 @@ res.h0()
 del res
 D = np.abs(np.subtract.outer(np.arange(60.0), np.arange(60.0))) % 7
 vrb.build_dm(D, maxdim=2, radius=3.0)
+# round 2 paths: rowsare="dimensions", clear-and-compress, an owner edge with
+# > 512 triangles (k_tets_big, dense and sparse), the HIV-like tie sort (keys
+# only, rows from the position table)
+X = workloads.random_cloud(7, 150, 3, "gauss")
+r2 = vrb.build(np.ascontiguousarray(X.T), maxdim=2, radius=1.0, rowsare="dimensions")
+r2.compress_d2()
+del r2
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from test_limits_gpu import big_apex_matrix  # noqa: E402
+for sparse in ("0", "1"):
+    os.environ["VRB_FORCE_SPARSE_TETS"] = sparse
+    for tie in (False, True):
+        vrb.build_dm(big_apex_matrix(m_apex=600, clique=10, tie=tie), maxdim=2, radius=1.0)
+os.environ.pop("VRB_FORCE_SPARSE_TETS")
+H = workloads.hamming_matrix(workloads.hamming_sequences(3, n=140, length=120, clades=4))
+vrb.build_dm(H, maxdim=1, radius=math.inf)
+vrb.build_dm(H, maxdim=2, radius=60.0)
 vrb.latlon2euc(torch.rand(100, 2, dtype=torch.float64, device="cuda") * 90)
 vrb.sortperm_f64(torch.randn(5000, dtype=torch.float64, device="cuda"))
 cp = torch.tensor([0, 2, 3], dtype=torch.int64, device="cuda")
