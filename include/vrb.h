@@ -50,7 +50,10 @@ typedef enum {
                            stores u32 positions (E, T, Q >= 2^32), or n >= 2^21 */
     VRB_ECUDA = 4,      /* CUDA runtime error; text in vrb_last_error() */
     VRB_ECOMM = 5,      /* the collective callback of vrb_build_dist failed */
-    VRB_ENOTSUP = 6     /* configuration outside what this build implements */
+    VRB_ENOTSUP = 6     /* configuration outside what this build implements:
+                           maxdim 2 with n above the tetrahedron kernels'
+                           shared-memory map (38 784 on a B200; checked before
+                           any work) -- DESIGN.md section 10 "Limits" */
 } vrb_status;
 
 /* vrb_opts.flags */

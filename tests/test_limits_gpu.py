@@ -80,3 +80,17 @@ def test_owner_edge_with_more_than_512_triangles(vrb, monkeypatch, tie, sparse):
     top = ef.max()
     assert ((tv[:, 0] == 0) & (tv[:, 1] == 1) & (tf == top)).sum() == 600
     assert o.simplices(3)[0].shape[0] >= 14 * 13 // 2
+
+
+def test_tetrahedra_vertex_limit_is_rejected_before_work(vrb):
+    # K = 3 needs n <= tets_max_n() (38 784 on a B200: the sparse kernel's
+    # shared-memory host map) -- rejected up front, not after the triangles
+    import time
+    X = np.random.default_rng(0).uniform(0, 1, (40000, 3))
+    t0 = time.time()
+    with pytest.raises(vrb.VrbError) as ei:
+        vrb.build(X, maxdim=2, radius=0.01)
+    assert ei.value.status == vrb.VRB_ENOTSUP
+    assert time.time() - t0 < 5.0
+    res = vrb.build(X, maxdim=1, radius=0.01)   # triangles have no such limit
+    assert res.count(2)[0] >= 0
