@@ -576,26 +576,35 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
                                                   uint32_t len, uint32_t degx, int64_t e) {
     const int lane = threadIdx.x & 31;
     const uint32_t nw = (degx + 31) >> 5;
-    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
-    __syncwarp();
+    // the bitmap words start at zero (cleared at kernel start, and re-zeroed
+    // as they are stored below); the output offset is loaded before the
+    // stream so its latency hides behind it
+    uint32_t* out = A.bm + __ldg(A.bmoff + e);
     int mis;
     const uint4* g = aligned_groups(A.nkr + offx, mis);
     const int ngroups = (int)((len + mis + 3) >> 2);
     auto mark = [&](uint32_t w, uint32_t) {
+#ifndef VRB_ABL_NOATOM
         if (map[w & 0xFFFFu] < p) {
             const uint32_t r = w >> 16;
             atomicOr(&W->bits[r >> 5], 1u << (r & 31));
         }
+#else
+        if (map[w & 0xFFFFu] < p) W->bits[0] += 1u;
+#endif
     };
     stream_prefix<kRegGroups>(g, ngroups, mis, len, mark);
     __syncwarp();
-    uint32_t* out = A.bm + A.bmoff[e];
     uint32_t c = 0;
     for (uint32_t w = lane; w < nw; w += 32) {
         const uint32_t b = W->bits[w];
+        W->bits[w] = 0u;
+#ifndef VRB_ABL_NOSTORE
         __stcg(out + w, b);
+#endif
         c += __popc(b);
     }
+    __syncwarp();
     return __reduce_add_sync(0xffffffffu, c);
 }
 
@@ -922,7 +931,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nthreads = blockDim.x;
     for (int64_t q = threadIdx.x; q < A.n; q += nthreads) map[q] = NONE32;
-    if (kFill && !kBm)   // the flags are cleared after every use, so they must start at 0
+    if ((kFill && !kBm) || (!kFill && kBm == 1))   // cleared after every use, so they must start at 0
         for (int q = threadIdx.x; q < (int)((nthreads / 32) * sizeof(WS) / 4); q += nthreads)
             reinterpret_cast<uint32_t*>(scratch)[q] = 0u;
     __syncthreads();
