@@ -71,7 +71,10 @@ typedef struct {
 
 typedef struct vrb_result* vrb_handle;   /* opaque; owns all device outputs */
 
-/* Allocator hook (e.g. PyTorch's caching allocator).  Both calls are made on
+/* Allocator hook (e.g. PyTorch's caching allocator; SURVEY 8(b) "library-
+ * owned device outputs ... allocated through the hook").  The paper's own
+ * native calls take caller-allocated buffers; here the sizes are
+ * only known after the count passes, so the library allocates.  Both calls are made on
  * the build's stream and device.  alloc returns NULL on failure.  The default
  * (hook unset or set to NULL) is cudaMallocAsync / cudaFreeAsync.  Process-
  * wide; set it before any build, never while a build runs. */
@@ -156,20 +159,26 @@ vrb_status vrb_build_dist(const double* X, int64_t n, int32_t d, const vrb_opts*
 vrb_status vrb_partition_bounds(const uint64_t* prefix, const uint32_t* efilt, int64_t E, int32_t world,
                                 int64_t* bounds);
 
-/* Counts of dimension dim (0..K): global_n = size of the whole dimension;
+/* Counts of dimension dim (0..K) -- the "size of complex" per dimension the
+ * paper tabulates (Table OSCmach; C(n, k+1) at full filtration,
+ * pin P5): global_n = size of the whole dimension;
  * local_off/local_n = this handle's slice (the whole for vrb_build).  Any
  * output pointer may be NULL.  dim out of range -> VRB_EINVAL. */
 vrb_status vrb_count(vrb_handle h, int32_t dim, int64_t* global_n, int64_t* local_off,
                      int64_t* local_n);
 
-/* Simplices of dimension dim in 1..K (this handle's slice): verts = (dim+1)
+/* Simplices of dimension dim in 1..K in filtration order ("ordered
+ * according to t"; ties by lex order, reading A4) -- this handle's
+ * slice: verts = (dim+1)
  * u32 per simplex, ascending vertex ids, filtration order; filt = u32 level
  * per simplex (vertices, dim 0, are implicit: id order, filt 0).  Device
  * pointers owned by the handle. */
 vrb_status vrb_simplices(vrb_handle h, int32_t dim, const uint32_t** verts_dev,
                          const uint32_t** filt_dev);
 
-/* value_of_rank: nvals float64 lengths, value_of_rank[f-1] = length of level f
+/* value_of_rank (the paper's ranking of the distance entries into integer
+ * filtration levels, with Eirene's "filtration" values P:439-442):
+ * nvals float64 lengths, value_of_rank[f-1] = length of level f
  * (strictly increasing; level 0 = vertices = 0.0).  Device, owned. */
 vrb_status vrb_rank_values(vrb_handle h, const double** value_of_rank_dev, int64_t* nvals);
 
@@ -186,6 +195,8 @@ vrb_status vrb_boundary(vrb_handle h, int32_t k, int64_t* nrows, int64_t* ncols,
  * into caller device memory on `stream`. */
 vrb_status vrb_boundary_colptr(vrb_handle h, int32_t k, uint64_t* colptr_dev, void* stream);
 
+/* Release every device output of the handle (through the allocator hook
+ * that allocated it).  NULL is a no-op. */
 vrb_status vrb_free(vrb_handle h);
 
 /* Build from a distance matrix ("x is either a
