@@ -1094,7 +1094,10 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     if (bm) {
         // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
         const int cw = mapb <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
-        warps = (int)std::min<int64_t>(fill ? kWarps : cw, avail / (int64_t)per_warp);
+        // fill: VRB_TRI_FILL_WARPS (experiment knob) warps per CTA, default 32
+        const char* fw = std::getenv("VRB_TRI_FILL_WARPS");
+        const int fill_warps = fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : kWarps;
+        warps = (int)std::min<int64_t>(fill ? fill_warps : cw, avail / (int64_t)per_warp);
     } else if (fill) {
         warps = (int)std::min<int64_t>(kWarps, avail / (int64_t)per_warp);
     } else {
