@@ -34,8 +34,23 @@ constexpr int kDC = 16;       // coordinates staged per chunk
 constexpr int kThreads = 256;
 constexpr int kFillStageD = 16;   // k_dist_fill stages the tile's points for d <= 16 (16 KB)
 
-__device__ __forceinline__ int64_t tile_index(int64_t ti, int64_t tj, int64_t nt) {
+__device__ __host__ __forceinline__ int64_t tile_index(int64_t ti, int64_t tj, int64_t nt) {
     return ti * nt - ti * (ti - 1) / 2 + (tj - ti);   // packed upper triangle (tj >= ti)
+}
+
+// The grid is 1-D over the upper-triangular tiles of tile rows [ti_lo, ti_hi)
+// only (no block of the lower triangle is launched): block b is packed tile
+// mask_base + b, whose row is found by a binary search of the row starts.
+__device__ __forceinline__ void tile_of_block(int64_t b, int64_t nt, int64_t ti_lo, int64_t ti_hi, int64_t mask_base,
+                                              int64_t& ti, int64_t& tj) {
+    const int64_t q = mask_base + b;
+    int64_t lo = ti_lo, hi = ti_hi;   // last row with tile_index(row, row) <= q
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (tile_index(mid, mid, nt) <= q) lo = mid; else hi = mid;
+    }
+    ti = lo;
+    tj = ti + (q - tile_index(ti, ti, nt));
 }
 
 // Tile rows [ti_lo, ti_lo + gridDim.y) (a rank's row block);
@@ -45,9 +60,9 @@ __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict
                                                         int64_t nt, double thr, int all,
                                                         unsigned long long* __restrict__ masks,
                                                         uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo,
-                                                        int64_t mask_base) {
-    const int64_t tj = blockIdx.x, ti = blockIdx.y + ti_lo;
-    if (tj < ti) return;
+                                                        int64_t ti_hi, int64_t mask_base) {
+    int64_t ti, tj;
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
     __shared__ double sA[kDC][kT];
     __shared__ double sB[kDC][kT];
     __shared__ unsigned long long mrow[kT];
@@ -130,9 +145,9 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
                                                         uint32_t* __restrict__ ei,
                                                         uint32_t* __restrict__ ej,
                                                         uint32_t* __restrict__ pij, int64_t ti_lo,
-                                                        int64_t mask_base) {
-    const int64_t tj = blockIdx.x, ti = blockIdx.y + ti_lo;
-    if (tj < ti) return;
+                                                        int64_t ti_hi, int64_t mask_base) {
+    int64_t ti, tj;
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
     const int64_t row_lo = ti_lo * kT;
@@ -472,7 +487,10 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     const double thr = cap_threshold(radius, strict);
     const int all = (!strict && std::isinf(radius)) ? 1 : 0;
     if (thr < 0.0) return;
-    dim3 grid((unsigned)nt, (unsigned)(ti_hi - ti_lo));
+    auto tidx = [&](int64_t ti) { return ti * nt - ti * (ti - 1) / 2; };   // first packed tile of tile row ti
+    const int64_t mask_base = tidx(ti_lo);
+    const int64_t ntiles = tidx(ti_hi) - mask_base;
+    const unsigned grid = (unsigned)ntiles;
     if (all) {   // full filtration: no mask pass, closed-form slots
         auto start = [&](int64_t i) { return (uint64_t)(i * n - i * (i + 1) / 2); };   // lex slot of row i
         const uint64_t E = start(std::min(row_hi, n)) - start(row_lo);
@@ -488,17 +506,14 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
         }
         if (E == 0) return;
         k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, nullptr, nullptr, out.key.get(), out.ei.get(),
-                                              out.ej.get(), out.pij.get(), ti_lo, 0);
+                                              out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base);
         VRB_LAUNCH_CHECK();
         return;
     }
-    auto tidx = [&](int64_t ti) { return ti * nt - ti * (ti - 1) / 2; };   // first packed tile of tile row ti
-    const int64_t mask_base = tidx(ti_lo);
-    const int64_t ntiles = tidx(ti_hi) - mask_base;
     DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
     DBuf<uint32_t> cnt((size_t)(nrows * nt), s);
     VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, mask_base);
+    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, ti_hi, mask_base);
     VRB_LAUNCH_CHECK();
     DBuf<uint64_t> base((size_t)(nrows * nt + 1), s);
     exclusive_scan(cnt.get(), base.get(), nrows * nt, s);
@@ -517,7 +532,7 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
         out.ej.alloc(E, s);
     }
     k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, masks.get(), base.get(), out.key.get(),
-                                          out.ei.get(), out.ej.get(), out.pij.get(), ti_lo, mask_base);
+                                          out.ei.get(), out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base);
     VRB_LAUNCH_CHECK();
 }
 

@@ -1094,9 +1094,11 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     if (bm) {
         // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
         const int cw = mapb <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
-        // fill: VRB_TRI_FILL_WARPS (experiment knob) warps per CTA, default 32
+        // fill: 32-warp CTAs (one per SM) when the host map is large (C5B:
+        // 16 / 8 warps 27.4 / 28.2 ms against 22.5), 8-warp CTAs when it is
+        // small (C3, 8 KB map: 8.9 ms against 9.9); VRB_TRI_FILL_WARPS overrides
         const char* fw = std::getenv("VRB_TRI_FILL_WARPS");
-        const int fill_warps = fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : kWarps;
+        const int fill_warps = fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : (mapb <= 32768 ? 8 : kWarps);
         warps = (int)std::min<int64_t>(fill ? fill_warps : cw, avail / (int64_t)per_warp);
     } else if (fill) {
         warps = (int)std::min<int64_t>(kWarps, avail / (int64_t)per_warp);
