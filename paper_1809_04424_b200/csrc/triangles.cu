@@ -1098,7 +1098,7 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
         // 16 / 8 warps 27.4 / 28.2 ms against 22.5), 8-warp CTAs when it is
         // small (C3, 8 KB map: 8.9 ms against 9.9); VRB_TRI_FILL_WARPS overrides
         const char* fw = std::getenv("VRB_TRI_FILL_WARPS");
-        const int fill_warps = fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : (mapb <= 32768 ? 8 : kWarps);
+        const int fill_warps = fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : ((!gmap && mapb <= 32768) ? 8 : kWarps);
         warps = (int)std::min<int64_t>(fill ? fill_warps : cw, avail / (int64_t)per_warp);
     } else if (fill) {
         warps = (int)std::min<int64_t>(kWarps, avail / (int64_t)per_warp);
