@@ -133,3 +133,42 @@ def test_build_dist_on_side_stream():
     X, maxdim, radius = CASES["c2_tets"]()
     outs = run_dist(X, maxdim, radius, 3, side_stream=True)
     check_vs_oracle(outs, X, maxdim, radius)
+
+
+def _nccl_worker(port, X, maxdim, radius, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_1809_04424_b200 as vrb
+
+        res = vrb.build_dist(torch.from_numpy(X).cuda(), maxdim=maxdim, radius=radius)
+        out = {"rank": 0}
+        for k in range(1, maxdim + 2):
+            g, off, n = res.count(k)
+            v, f = res.simplices(k)
+            out[k] = (g, off, n, _u32(v), _u32(f), _u32(res.boundary(k)))
+        out["vor"] = res.rank_values().cpu().numpy()
+        q.put(out)
+    except Exception as e:
+        q.put({"rank": 0, "error": repr(e)})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_build_dist_over_nccl_one_rank():
+    # the NCCL code path of the collective callbacks (device tensors, the
+    # library's stream as torch's current stream, no host synchronisation):
+    # one rank per GPU, so one rank here
+    X, maxdim, radius = CASES["c2_tets"]()
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), X, maxdim, radius, q))
+    p.start()
+    out = q.get(timeout=600)
+    p.join(timeout=120)
+    assert "error" not in out, out
+    check_vs_oracle([out], X, maxdim, radius)
