@@ -352,8 +352,20 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     DBuf<uint32_t> cnt(std::max<int64_t>(E, 1), s);
     DBuf<uint64_t> bmoff;
     DBuf<uint32_t> bm;
-    const bool use_bm = apex_bitmaps_apply(g);
-    if (E) {
+    TriRecords R;
+    bool xmajor = E && records_apply(g);
+    if (xmajor) {
+        try {
+            count_triangles_rec(g, o.ev, tb[0], tb[1], cnt.get(), R, s);
+        } catch (const Error& e) {
+            if (e.status != VRB_ENOMEM) throw;
+            cudaGetLastError();
+            R = TriRecords();
+            xmajor = false;
+        }
+    }
+    const bool use_bm = !xmajor && apex_bitmaps_apply(g);
+    if (E && !xmajor) {
         if (use_bm) {
             uint64_t words = 0;
             apex_bitmap_offsets(g, bmoff, words, s);
@@ -389,9 +401,13 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     if (K >= 3 && n <= 65536) tapex.alloc((size_t)std::max<uint64_t>(Tl, 1), s);
     timer.mark(3);
     timer.begin(4);
-    fill_triangles(g, o.efilt, toff.get(), tb[0], tb[1], 0, o.tv, o.tf, o.trows, tapex.get(), s, bm.get(),
-                   bmoff.get());
+    if (xmajor)
+        fill_triangles_x(g, R, o.efilt, toff.get(), tb[0], tb[1], 0, o.tv, o.tf, o.trows, tapex.get(), s);
+    else
+        fill_triangles(g, o.efilt, toff.get(), tb[0], tb[1], 0, o.tv, o.tf, o.trows, tapex.get(), s, bm.get(),
+                       bmoff.get());
     bm.reset();
+    R = TriRecords();
     timer.mark(4);
     timer.begin(5);
     sort_tie_groups(2, o.efilt, toff.get(), E, tb[0], tb[1], n, o.tv, o.trows, s, o.ev);

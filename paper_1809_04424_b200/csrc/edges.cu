@@ -453,6 +453,58 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     VRB_LAUNCH_CHECK();
 }
 
+// fill plan of the x-major triangle fill: owner edges [p_lo, p_hi) grouped
+// by their SCANNED endpoint x, longest prefix first: (p, host y, prefix
+// length, deg x); work = prefix length
+__global__ void k_scan_keys(const uint32_t* __restrict__ scan_v, const uint32_t* __restrict__ scan_len, int64_t p_lo,
+                            int64_t m, uint64_t* __restrict__ key) {
+    GRID_STRIDE(q, m) {
+        const int64_t p = p_lo + q;
+        key[q] = ((uint64_t)scan_v[p] << 32) | (uint32_t)~scan_len[p];
+    }
+}
+
+__global__ void k_fill_plan(const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ ev,
+                            const uint32_t* __restrict__ scan_v, const uint32_t* __restrict__ scan_len,
+                            const uint64_t* __restrict__ off, int64_t m, int64_t p_lo, uint32_t* __restrict__ group_v,
+                            uint4* __restrict__ plan, uint32_t* __restrict__ work) {
+    GRID_STRIDE(i, m) {
+        const uint32_t p = (uint32_t)(p_lo + sorted[i]);
+        const uint32_t x = scan_v[p], a = ev[2 * (uint64_t)p], b = ev[2 * (uint64_t)p + 1];
+        const uint32_t len = scan_len[p];
+        group_v[i] = x;
+        plan[i] = make_uint4(p, x == a ? b : a, len, (uint32_t)(off[x + 1] - off[x]));
+        work[i] = len + 32;   // + a per-edge constant: the edge's fixed costs
+    }
+}
+
+void build_fill_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, const Graph& g,
+                     DBuf<uint4>& plan, DBuf<uint32_t>& group_v, DBuf<uint64_t>& work_pre, int64_t& m_out,
+                     uint64_t& work) {
+    const int64_t m = p_hi > p_lo ? p_hi - p_lo : 0;
+    m_out = m;
+    plan.alloc(m, s);
+    group_v.alloc(m, s);
+    work_pre.alloc(m + 1, s);
+    work = 0;
+    if (m == 0) {
+        VRB_CUDA(cudaMemsetAsync(work_pre.get(), 0, sizeof(uint64_t), s));
+        return;
+    }
+    DBuf<uint64_t> k0(m, s), k1(m, s);
+    DBuf<uint32_t> v0(m, s), v1(m, s);
+    k_scan_keys<<<grid_for(m, 256), 256, 0, s>>>(g.scan_v.get(), g.scan_len.get(), p_lo, m, k0.get());
+    VRB_LAUNCH_CHECK();
+    const uint32_t* sorted = sort_ids(k0, k1, v0, v1, m, s);
+    DBuf<uint32_t> w(m, s);
+    k_fill_plan<<<grid_for(m, 256), 256, 0, s>>>(sorted, ev, g.scan_v.get(), g.scan_len.get(), g.off.get(), m, p_lo,
+                                                 group_v.get(), plan.get(), w.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(w.get(), work_pre.get(), m, s);
+    VRB_CUDA(cudaMemcpyAsync(&work, work_pre.get() + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+}
+
 void build_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, Graph& g) {
     // owner-edge plan of the owner edges [p_lo, p_hi): scanned endpoint,
     // prefix length, host; hosted slots grouped by host

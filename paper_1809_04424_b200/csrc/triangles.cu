@@ -103,6 +103,16 @@ struct TriArgs {
     const uint64_t* bmoff;     // per hosted slot: word offset of its bitmap
     const uint2* idl;          // (k, pos) in neighbour-ID order
     int debug;   // ablation (experiment builds with -DVRB_ABLATION only): 1 = stop after mark, 2 = skip the flush
+    // x-major path (records): per owner edge p (by position), its scanned
+    // prefix's validity bits (tb + tb_off[p], ceil(len/32) words) and the host
+    // positions pos(y, k) of its valid apexes in prefix order (rec + rec_off[p])
+    uint32_t* rec;
+    const uint64_t* rec_off;
+    uint32_t* tb;
+    const uint64_t* tb_off;
+    const uint4* fplan;        // fill plan: slots grouped by scanned vertex x: (p, host y, len, deg x)
+    const uint32_t* fgroup_v;  // x of each fill-plan slot
+    int lists_cap;             // shared-memory list capacity (entries) of the x-major fill
 };
 
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t v) {
@@ -915,12 +925,253 @@ __device__ __forceinline__ void warp_fill_tbm(const TriArgs& A, const uint32_t* 
     }
 }
 
+// ---------------------------------------------------------------------------
+// x-major path ("records"; the default for single-range builds with packed
+// lists and degrees <= kApexBitmapMaxDeg).
+//   count (hosted by y, as before): per owner edge p, ballots over the
+//          scanned prefix of x give one bit per candidate t (valid apex:
+//          pos(y, k) < p) -- 32 candidates per map lookup + vote, no shared
+//          atomics -- and the valid candidates' host positions pos(y, k) are
+//          appended in prefix order (a coalesced 4-byte store per valid lane).
+//   fill  (x-major): a CTA holds the scanned vertex x's whole position-
+//          ordered list (k | krank, pos(x, k)) in shared memory and its warps
+//          take x's owner edges; per edge the validity words say which prefix
+//          entries are apexes, their id ranks (in the list word) give the
+//          slots (a shared bitmap + prefix popcounts: the lex order), k and
+//          pos(x, k) come from shared memory and pos(y, k) from the appended
+//          records (contiguous).  No neighbourhood is re-read from DRAM per
+//          owner edge: the fill reads 4 B per triangle and a bit per candidate
+//          besides writing its 28 B per triangle.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t warp_count_rec(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t p,
+                                                   uint64_t offx, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t* __restrict__ lst = A.nkr + offx;
+    uint32_t* __restrict__ rec = A.rec + __ldg(A.rec_off + p);
+    uint32_t* __restrict__ tb = A.tb + __ldg(A.tb_off + p);
+    const uint32_t nch = (len + 31) >> 5;
+    uint32_t c = 0;
+    constexpr int U = 8;
+    for (uint32_t c0 = 0; c0 < nch; c0 += U) {
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = 32 * (c0 + u) + lane;
+            w[u] = t < len ? ld_list(lst + t) : 0u;
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = 32 * (c0 + u) + lane;
+            const uint32_t py = t < len ? map[w[u] & 0xFFFFu] : NONE32;
+            const bool v = py < p;
+            const uint32_t b = __ballot_sync(0xffffffffu, v);
+            if (v) __stcg(rec + c + __popc(b & lt), py);
+            if (lane == u) mine = b;
+            c += __popc(b);
+        }
+        if (lane < U && c0 + lane < nch) __stcg(tb + c0 + lane, mine);
+    }
+    return c;
+}
+
+constexpr int kWinX = 256;
+struct WarpScratchX {
+    uint32_t bits[kBmWords];   // valid apexes by id rank in x's list
+    uint32_t wpre[kBmWords];
+    uint16_t rk[kWinX];        // staged window: apex ...
+    uint32_t rpx[kWinX];       // ... pos(x, k) ...
+    uint32_t rpy[kWinX];       // ... pos(y, k)
+    alignas(16) uint32_t st[96];
+    alignas(16) uint32_t sr[96];
+};
+
+// store_window with pos(y, k) from the staging too: kpq(j) = (k, pos(x,k), pos(y,k))
+template <int kU, class KPQ>
+__device__ __forceinline__ void store_window3(const TriArgs& A, uint32_t* __restrict__ st, uint32_t* __restrict__ sr,
+                                              uint64_t s0, uint32_t m, uint32_t p, uint32_t y, uint32_t x,
+                                              uint32_t filt, KPQ&& kpq) {
+    const int lane = threadIdx.x & 31;
+    auto tri = [&](uint32_t j, uint3 q, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0, uint32_t& r1) {
+        a0 = y; a1 = x; a2 = q.x;
+        sort3(a0, a1, a2);
+        r0 = min(q.y, q.z);
+        r1 = max(q.y, q.z);
+        __stcs(A.tf + s0 + j, filt);
+        if (A.apex) A.apex[s0 + j] = (uint16_t)q.x;
+    };
+    auto scalar = [&](uint32_t j, uint3 q) {
+        uint32_t a0, a1, a2, r0, r1;
+        tri(j, q, a0, a1, a2, r0, r1);
+        uint32_t* tv = A.tv + 3 * (s0 + j);
+        __stcs(tv, a0);
+        __stcs(tv + 1, a1);
+        __stcs(tv + 2, a2);
+        if (A.rows) {
+            uint32_t* rw = A.rows + 3 * (s0 + j);
+            __stcs(rw, r0);
+            __stcs(rw + 1, r1);
+            __stcs(rw + 2, p);
+        }
+    };
+    const uint32_t h = min(m, (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u));
+    if ((uint32_t)lane < h) scalar(lane, kpq(lane));
+    for (uint32_t g0 = h; g0 < m; g0 += 32 * kU) {
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t g = g0 + 32 * q;
+            if (g >= m) break;
+            const uint32_t j = g + lane;
+            if (g + 32 <= m) {
+                uint32_t a0, a1, a2, r0, r1;
+                tri(j, kpq(j), a0, a1, a2, r0, r1);
+                st[3 * lane] = a0;
+                st[3 * lane + 1] = a1;
+                st[3 * lane + 2] = a2;
+                sr[3 * lane] = r0;
+                sr[3 * lane + 1] = r1;
+                sr[3 * lane + 2] = p;
+                __syncwarp();
+                if (lane < 24) {
+                    __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane, reinterpret_cast<const uint4*>(st)[lane]);
+                    if (A.rows)
+                        __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
+                               reinterpret_cast<const uint4*>(sr)[lane]);
+                }
+                __syncwarp();
+            } else if (j < m) {
+                scalar(j, kpq(j));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_fill_x(const TriArgs& A, const uint32_t* __restrict__ lk,
+                                            const uint32_t* __restrict__ lp, WarpScratchX* __restrict__ W, uint32_t p,
+                                            uint32_t y, uint32_t x, uint32_t len, uint32_t degx, uint64_t slot,
+                                            uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t* __restrict__ tb = A.tb + __ldg(A.tb_off + p);
+    const uint32_t* __restrict__ rec = A.rec + __ldg(A.rec_off + p);
+    const uint32_t nch = (len + 31) >> 5;
+    const uint32_t nw = (degx + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
+    __syncwarp();
+    // ---- mark the id ranks of the valid entries (lane j holds word c0 + j)
+    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+        const uint32_t wl = c0 + lane < nch ? __ldg(tb + c0 + lane) : 0u;
+        const uint32_t nu = min(32u, nch - c0);
+        for (uint32_t u = 0; u < nu; ++u) {
+            const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
+            if ((word >> lane) & 1u) {
+                const uint32_t r = lk[32 * (c0 + u) + lane] >> 16;
+                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+            }
+        }
+    }
+    const uint32_t count = rank_bits<kBmWords>(W, degx);
+    // ---- windows of kWinX slots: stage (k, pos(x,k), pos(y,k)) by slot, store
+    for (uint32_t w0 = 0; w0 < count; w0 += kWinX) {
+        uint32_t run = 0;   // records before this chunk (prefix order)
+        for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+            const uint32_t wl = c0 + lane < nch ? __ldg(tb + c0 + lane) : 0u;
+            const uint32_t nu = min(32u, nch - c0);
+            for (uint32_t u = 0; u < nu; ++u) {
+                const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
+                if ((word >> lane) & 1u) {
+                    const uint32_t t = 32 * (c0 + u) + lane;
+                    const uint32_t e = lk[t];
+                    const uint32_t r = e >> 16;
+                    const uint32_t wd = W->bits[r >> 5];
+                    const uint32_t sl = W->wpre[r >> 5] + __popc(wd & ((2u << (r & 31)) - 1u)) - 1u - w0;
+                    if (sl < (uint32_t)kWinX) {
+                        W->rk[sl] = (uint16_t)(e & 0xFFFFu);
+                        W->rpx[sl] = lp[t];
+                        W->rpy[sl] = __ldg(rec + run + __popc(word & lt));
+                    }
+                }
+                run += __popc(word);
+            }
+        }
+        __syncwarp();
+        const uint32_t m = min((uint32_t)kWinX, count - w0);
+        store_window3<4>(A, W->st, W->sr, slot + w0, m, p, y, x, filt,
+                         [&](uint32_t j) { return make_uint3(W->rk[j], W->rpx[j], W->rpy[j]); });
+        __syncwarp();
+    }
+}
+
+// The x-major fill: CTAs take tasks (work-balanced ranges of fill-plan slots),
+// each slot range grouped by scanned vertex x; per x the CTA loads x's list
+// into shared memory once and its warps take x's owner edges.
+__global__ void __launch_bounds__(kThreads, 1) k_tri_fill_x(TriArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* lk = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* lp = lk + A.lists_cap;
+    WarpScratchX* scratch = reinterpret_cast<WarpScratchX*>(smem + (size_t)8 * A.lists_cap);
+    __shared__ int64_t s_lo, s_hi, s_end;
+    __shared__ uint32_t s_x;
+    __shared__ unsigned s_next;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nthreads = blockDim.x;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
+            if (task >= A.task_hi) {
+                s_lo = s_hi = -1;
+            } else {
+                s_lo = lower_bound_u64(A.work_pre, 0, A.E + 1, (uint64_t)task * A.chunk);
+                s_hi = task == A.ntasks - 1 ? A.E
+                                            : lower_bound_u64(A.work_pre, 0, A.E + 1, (uint64_t)(task + 1) * A.chunk);
+                if (s_lo > A.E) s_lo = A.E;
+                if (s_hi > A.E) s_hi = A.E;
+            }
+        }
+        __syncthreads();
+        const int64_t lo = s_lo, hi = s_hi;
+        __syncthreads();
+        if (lo < 0) break;
+        for (int64_t seg = lo; seg < hi;) {
+            if (threadIdx.x == 0) {
+                const uint32_t x = A.fgroup_v[seg];
+                s_x = x;
+                s_end = upper_bound_u32(A.fgroup_v, seg, hi, x);
+                s_next = 0;
+            }
+            __syncthreads();
+            const uint32_t x = s_x;
+            const int64_t end = s_end;
+            const uint64_t ox = A.off[x];
+            const uint32_t degx = (uint32_t)(A.off[x + 1] - ox);
+            for (uint32_t t = threadIdx.x; t < degx; t += nthreads) {
+                lk[t] = A.nkr[ox + t];
+                lp[t] = A.np[ox + t];
+            }
+            __syncthreads();
+            for (;;) {
+                unsigned my = 0;
+                if (lane == 0) my = atomicAdd(&s_next, 1u);
+                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+                if (e >= end) break;
+                const uint4 pl = A.fplan[e];
+                const uint32_t p = pl.x, y = pl.y, len = pl.z;
+                if (len == 0 || (int64_t)p < A.p_lo || (int64_t)p >= A.p_hi) continue;
+                warp_fill_x(A, lk, lp, scratch + wid, p, y, x, len, degx, A.toff[p] - A.slot0, A.efilt[p]);
+            }
+            __syncthreads();
+            seg = end;
+        }
+    }
+}
+
 template <bool kFill, bool kPacked, int kBm>
 __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2), 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
-        kBm == 2, typename std::conditional<kFill, WarpScratchT, WarpScratchNone>::type,
+        kBm >= 2, typename std::conditional<kFill, WarpScratchT, WarpScratchNone>::type,
         typename std::conditional<
             kBm == 1, typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
             typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type>::type;
@@ -1008,7 +1259,10 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                 }
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kBm == 2 && kFill) {
+                    if constexpr (kBm == 3 && !kFill) {
+                        const uint32_t c = warp_count_rec(A, map, p, off0, len);
+                        if (lane == 0) A.cnt[p] = c;
+                    } else if constexpr (kBm == 2 && kFill) {
                         warp_fill_tbm(A, map, scratch + wid, p, y, x, len, off0, pl0.w, bmo0, slot0, filt0);
                     } else if constexpr (kBm == 2) {
                         const uint32_t c = warp_count_tbm(A, map, p, off0, len, e0);
@@ -1076,8 +1330,9 @@ void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap,
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
     const bool packed = A.packed != 0;
-    const bool bm = A.bm != nullptr;
-    const bool tbm = bm && A.bm_mode == 2;
+    const bool recm = A.rec != nullptr;   // x-major path: the count stores records
+    const bool bm = A.bm != nullptr || recm;
+    const bool tbm = (A.bm != nullptr && A.bm_mode == 2) || recm;
     // fill: one CTA per SM (the vertex map + per-warp scratch); count:
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
     // the host map goes to global memory when it would leave shared memory for
@@ -1123,7 +1378,9 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     A.task_counter = counter.get();
     const int64_t cap = A.task_hi - A.task_lo;
-    if (tbm) {
+    if (recm) {
+        launch_k<false, true, 3>(A, threads, smem, cap, gmap, s);
+    } else if (tbm) {
         if (fill) launch_k<true, true, 2>(A, threads, smem, cap, gmap, s);
         else launch_k<false, true, 2>(A, threads, smem, cap, gmap, s);
     } else if (bm) {
@@ -1211,6 +1468,104 @@ void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint6
     A.bm_mode = bitmap_mode();
     A.bmoff = bmoff;
     launch(A, false, g.work, 0, 1, s);
+}
+
+namespace {
+__global__ void k_rec_words(const uint32_t* __restrict__ scan_len, int64_t E, int64_t p_lo, int64_t p_hi,
+                            uint32_t* __restrict__ nrec, uint32_t* __restrict__ nwords) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t len = (p >= p_lo && p < p_hi) ? scan_len[p] : 0u;
+        nrec[p] = len;
+        nwords[p] = (len + 31u) >> 5;
+    }
+}
+}  // namespace
+
+bool records_apply(const Graph& g) {
+    const char* m = std::getenv("VRB_TRI_PATH");   // "bitmap": the round-1 apex-bitmap path
+    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && !(m && m[0] == 'b');
+}
+
+void count_triangles_rec(const Graph& g, const uint32_t* ev, int64_t p_lo, int64_t p_hi, uint32_t* cnt,
+                         TriRecords& R, cudaStream_t s) {
+    const int64_t E = g.E;
+    if (E == 0) return;
+    VRB_CUDA(cudaMemsetAsync(cnt, 0, E * sizeof(uint32_t), s));
+    R.rec_off.alloc(E + 1, s);
+    R.tb_off.alloc(E + 1, s);
+    {
+        DBuf<uint32_t> a(E, s), b(E, s);
+        k_rec_words<<<(unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
+            g.scan_len.get(), E, p_lo, p_hi, a.get(), b.get());
+        VRB_LAUNCH_CHECK();
+        exclusive_scan(a.get(), R.rec_off.get(), E, s);
+        exclusive_scan(b.get(), R.tb_off.get(), E, s);
+    }
+    uint64_t nrec = 0, nw = 0;
+    VRB_CUDA(cudaMemcpyAsync(&nrec, R.rec_off.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(&nw, R.tb_off.get() + E, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    R.rec.alloc(std::max<uint64_t>(nrec, 1), s);   // a slot per candidate (only the valid ones are written)
+    R.tb.alloc(std::max<uint64_t>(nw, 1), s);
+    build_fill_plan(ev, p_lo, p_hi, s, g, R.fplan, R.fgroup_v, R.fwork_pre, R.nfplan, R.fwork);
+    if (g.work == 0) return;
+    TriArgs A = graph_args(g);
+    A.cnt = cnt;
+    A.rec = R.rec.get();
+    A.rec_off = R.rec_off.get();
+    A.tb = R.tb.get();
+    A.tb_off = R.tb_off.get();
+    launch(A, false, g.work, 0, 1, s);
+}
+
+void fill_triangles_x(const Graph& g, const TriRecords& R, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo,
+                      int64_t p_hi, uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex,
+                      cudaStream_t s) {
+    if (g.E == 0 || R.nfplan == 0 || R.fwork == 0 || p_lo >= p_hi) return;
+    TriArgs A = graph_args(g);
+    A.E = R.nfplan;
+    A.work_pre = R.fwork_pre.get();
+    A.fplan = R.fplan.get();
+    A.fgroup_v = R.fgroup_v.get();
+    A.rec = const_cast<uint32_t*>(R.rec.get());
+    A.rec_off = R.rec_off.get();
+    A.tb = const_cast<uint32_t*>(R.tb.get());
+    A.tb_off = R.tb_off.get();
+    A.efilt = efilt;
+    A.toff = toff;
+    A.p_lo = p_lo;
+    A.p_hi = p_hi;
+    A.slot0 = slot0;
+    A.tv = tv;
+    A.tf = tf;
+    A.rows = rows;
+    A.apex = g.n <= 65536 ? apex : nullptr;
+    A.lists_cap = (int)((g.max_deg + 3) & ~3u);
+    const size_t lists = (size_t)8 * A.lists_cap;
+    const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)lists - 1024;
+    const char* fw = std::getenv("VRB_TRI_FILL_WARPS");
+    int warps = (int)std::min<int64_t>(fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : kWarps,
+                                       avail / (int64_t)sizeof(WarpScratchX));
+    if (warps < 4) fail(VRB_ENOTSUP, "x-major triangle fill: degree %u leaves no shared memory", g.max_deg);
+    const int threads = warps * 32;
+    const size_t smem = lists + (size_t)warps * sizeof(WarpScratchX);
+    VRB_CUDA(cudaFuncSetAttribute(k_tri_fill_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_fill_x, threads, smem));
+    if (per_sm < 1) fail(VRB_ENOTSUP, "x-major triangle fill does not fit");
+    uint64_t chunk = R.fwork / 8192 + 1;
+    if (chunk < 65536) chunk = 65536;
+    A.chunk = chunk;
+    A.ntasks = (int64_t)((R.fwork + chunk - 1) / chunk);
+    if (A.ntasks < 1) A.ntasks = 1;
+    A.task_lo = 0;
+    A.task_hi = A.ntasks;
+    DBuf<unsigned long long> counter(1, s);
+    VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
+    A.task_counter = counter.get();
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count() * per_sm, A.ntasks);
+    k_tri_fill_x<<<grid, threads, smem, s>>>(A);
+    VRB_LAUNCH_CHECK();
 }
 
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,

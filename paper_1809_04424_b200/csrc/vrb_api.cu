@@ -379,10 +379,24 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
             timer.begin(3);
             // ---- triangles: count per owner edge, offsets
             DBuf<uint32_t> cnt(E, s);
-            // the count pass keeps the apex bitmaps the fill emits from
+            // the count pass keeps what the fill needs: validity bits and host
+            // positions (x-major path) or the apex bitmaps (round-1 path)
+            TriRecords R;
+            bool xmajor = records_apply(g);
+            if (xmajor) {
+                try {
+                    count_triangles_rec(g, ev, 0, E, cnt.get(), R, s);
+                } catch (const Error& e) {
+                    if (e.status != VRB_ENOMEM) throw;
+                    cudaGetLastError();
+                    R = TriRecords();   // not enough memory for the records: the bitmap path
+                    xmajor = false;
+                }
+            }
             DBuf<uint64_t> bmoff;
             DBuf<uint32_t> bm;
-            if (apex_bitmaps_apply(g)) {
+            if (xmajor) {
+            } else if (apex_bitmaps_apply(g)) {
                 uint64_t words = 0;
                 apex_bitmap_offsets(g, bmoff, words, s);
                 bm.alloc(words ? words : 1, s);
@@ -409,8 +423,12 @@ void build_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts, cud
             }
             timer.mark(3);
             timer.begin(4);
-            fill_triangles(g, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s, bm.get(), bmoff.get());
+            if (xmajor)
+                fill_triangles_x(g, R, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s);
+            else
+                fill_triangles(g, efilt, toff.get(), 0, E, 0, tv, tf, trows, tapex.get(), s, bm.get(), bmoff.get());
             bm.reset();
+            R = TriRecords();
             timer.mark(4);
             timer.begin(5);
             sort_tie_groups(2, efilt, toff.get(), E, 0, E, n, tv, trows, s, ev);

@@ -106,6 +106,28 @@ void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint6
 void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo, int64_t p_hi,
                     uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex, cudaStream_t s,
                     const uint32_t* bm = nullptr, const uint64_t* bmoff = nullptr);
+// x-major triangle path (triangles.cu, "records"; packed lists, degrees <=
+// kApexBitmapMaxDeg): the count (hosted by y) stores per owner edge the
+// validity bits of its scanned prefix and the host positions of its valid
+// apexes; the fill runs per scanned vertex x with x's list in shared memory.
+struct TriRecords {
+    DBuf<uint64_t> rec_off, tb_off;   // E + 1 each: per owner edge (0 outside [p_lo, p_hi))
+    DBuf<uint32_t> rec, tb;
+    DBuf<uint4> fplan;                // fill plan (p, host y, len, deg x), grouped by scanned x
+    DBuf<uint32_t> fgroup_v;
+    DBuf<uint64_t> fwork_pre;
+    int64_t nfplan = 0;
+    uint64_t fwork = 0;
+};
+bool records_apply(const Graph& g);
+void count_triangles_rec(const Graph& g, const uint32_t* ev, int64_t p_lo, int64_t p_hi, uint32_t* cnt,
+                         TriRecords& R, cudaStream_t s);
+void fill_triangles_x(const Graph& g, const TriRecords& R, const uint32_t* efilt, const uint64_t* toff, int64_t p_lo,
+                      int64_t p_hi, uint64_t slot0, uint32_t* tv, uint32_t* tf, uint32_t* rows, uint16_t* apex,
+                      cudaStream_t s);
+void build_fill_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, const Graph& g,
+                     DBuf<uint4>& plan, DBuf<uint32_t>& group_v, DBuf<uint64_t>& work_pre, int64_t& m_out,
+                     uint64_t& work);
 // Reorder the k-simplices (k = 2, 3) of every tie group (>= 2 edges sharing a
 // level) into lex order (readings A3, A4); only owner edges in [p_lo, p_hi).
 // off = per-owner-edge simplex offsets (E + 1); verts/rows: (k+1) u32 each.
