@@ -926,7 +926,7 @@ __device__ __forceinline__ void warp_fill_tbm(const TriArgs& A, const uint32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// x-major path ("records"; the default for single-range builds with packed
+// x-major path ("records"; an experiment behind VRB_TRI_PATH=xmajor, packed
 // lists and degrees <= kApexBitmapMaxDeg).
 //   count (hosted by y, as before): per owner edge p, ballots over the
 //          scanned prefix of x give one bit per candidate t (valid apex:
@@ -1481,9 +1481,13 @@ __global__ void k_rec_words(const uint32_t* __restrict__ scan_len, int64_t E, in
 }
 }  // namespace
 
+// The x-major path is an experiment (VRB_TRI_PATH=xmajor): correct, but
+// measured slower than the apex-bitmap path on C5B (count 16.7 ms against
+// 9.0, fill 45.4 against 22.5) -- the fill touches
+// every candidate twice instead of only the valid apexes.
 bool records_apply(const Graph& g) {
-    const char* m = std::getenv("VRB_TRI_PATH");   // "bitmap": the round-1 apex-bitmap path
-    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && !(m && m[0] == 'b');
+    const char* m = std::getenv("VRB_TRI_PATH");
+    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && m && m[0] == 'x';
 }
 
 void count_triangles_rec(const Graph& g, const uint32_t* ev, int64_t p_lo, int64_t p_hi, uint32_t* cnt,

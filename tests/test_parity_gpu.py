@@ -624,3 +624,15 @@ def test_full_size_c4_tetrahedra(vrb):
         torch.cuda.synchronize()
         vrb.use_torch_allocator(False)
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_xmajor_triangle_path(vrb, case, monkeypatch):
+    # the experimental x-major triangle path (VRB_TRI_PATH=xmajor) must be as
+    # exact as the default one
+    monkeypatch.setenv("VRB_TRI_PATH", "xmajor")
+    X, maxdim, radius = [(workloads.random_cloud(21, 300, 4, "gauss"), 1, 1.8),
+                         (workloads.integer_lattice(4, 3), 2, 1.5),
+                         (workloads.WORKLOADS["C2"].points(), 2, 0.45),
+                         (workloads.random_cloud(22, 200, 3, "dups"), 1, 0.35)][case]
+    compare(vrb, X, maxdim, radius)
