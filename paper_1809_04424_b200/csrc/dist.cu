@@ -113,10 +113,6 @@ __global__ void k_merge(const uint64_t* __restrict__ ak, const uint64_t* __restr
     }
 }
 
-__global__ void k_heads64(const uint64_t* __restrict__ key, int64_t E, uint32_t* __restrict__ head) {
-    GRID_STRIDE(p, E) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
-}
-
 __global__ void k_edge_out(const uint64_t* __restrict__ key, const uint64_t* __restrict__ ij,
                            const uint32_t* __restrict__ efilt, int64_t E, uint32_t* __restrict__ ev,
                            double* __restrict__ vor) {
@@ -320,10 +316,7 @@ void build_dist_impl(const double* X, int64_t n, int32_t d, const vrb_opts* opts
     o.vor = o.alloc_f64(E);
     o.nvals = 0;
     if (E) {
-        DBuf<uint32_t> head(E, s);
-        k_heads64<<<grid_of(E), 256, 0, s>>>(gk, E, head.get());
-        VRB_LAUNCH_CHECK();
-        inclusive_scan_u32(head.get(), o.efilt, E, s);
+        dense_ranks(gk, o.efilt, E, s);
         k_edge_out<<<grid_of(E), 256, 0, s>>>(gk, gi, o.efilt, E, o.ev, o.vor);
         VRB_LAUNCH_CHECK();
         uint32_t nv = 0;

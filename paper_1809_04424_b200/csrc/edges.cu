@@ -32,10 +32,6 @@ unsigned grid_for(int64_t n, int threads) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n);       \
          i += (int64_t)gridDim.x * blockDim.x)
 
-__global__ void k_rank_heads(const uint64_t* __restrict__ key, int64_t E, uint32_t* __restrict__ head) {
-    GRID_STRIDE(p, E) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
-}
-
 __global__ void k_edge_outputs(const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
                                const uint32_t* __restrict__ ei, const uint32_t* __restrict__ ej,
                                const uint32_t* __restrict__ efilt, int64_t E, uint32_t* __restrict__ ev,
@@ -342,10 +338,7 @@ int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cu
     const uint64_t* skey = so.key;
     const uint32_t* sval = so.val;
     const uint64_t bias = so.bias;
-    DBuf<uint32_t> head(E, s);
-    k_rank_heads<<<grid_for(E, 256), 256, 0, s>>>(skey, E, head.get());
-    VRB_LAUNCH_CHECK();
-    inclusive_scan_u32(head.get(), efilt, E, s);
+    dense_ranks(skey, efilt, E, s);   // heads + inclusive scan in one pass over the keys
     if (ke.packed)
         k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, efilt, E, reinterpret_cast<uint2*>(ev),
                                                                vor, bias);

@@ -38,9 +38,9 @@ __device__ __forceinline__ T block_inclusive(T v, T* smem_warp, T& total) {
     return inc + prefix;
 }
 
-template <class Tin, class Tacc>
-__global__ void __launch_bounds__(kScanThreads) k_tile_sums(const Tin* __restrict__ in, int64_t n,
-                                                            Tacc* __restrict__ sums) {
+// In: a pointer, or an index view such as HeadFlags
+template <class In, class Tacc>
+__global__ void __launch_bounds__(kScanThreads) k_tile_sums(In in, int64_t n, Tacc* __restrict__ sums) {
     __shared__ Tacc red[kScanThreads / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     Tacc acc = 0;
@@ -61,9 +61,8 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sums(const Tin* __restric
 }
 
 // Scan one tile with a per-tile offset.  Exclusive: out has n + 1 entries.
-template <class Tin, class Tout, bool kInclusive>
-__global__ void __launch_bounds__(kScanThreads) k_tile_scan(const Tin* __restrict__ in, int64_t n,
-                                                            const Tout* __restrict__ tile_off,
+template <class In, class Tout, bool kInclusive>
+__global__ void __launch_bounds__(kScanThreads) k_tile_scan(In in, int64_t n, const Tout* __restrict__ tile_off,
                                                             Tout* __restrict__ out) {
     __shared__ Tout warp_tot[kScanThreads / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -81,25 +80,34 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const Tin* __restric
         out[n] = carry;
 }
 
-template <class Tin, class Tout, bool kInclusive>
-void scan_impl(const Tin* in, Tout* out, int64_t n, cudaStream_t s) {
+template <class In, class Tout, bool kInclusive>
+void scan_impl(In in, Tout* out, int64_t n, cudaStream_t s) {
     if (n == 0) {
         if (!kInclusive) VRB_CUDA(cudaMemsetAsync(out, 0, sizeof(Tout), s));
         return;
     }
     const int64_t tiles = ceil_div(n, kScanTile);
     if (tiles == 1) {
-        k_tile_scan<Tin, Tout, kInclusive><<<1, kScanThreads, 0, s>>>(in, n, nullptr, out);
+        k_tile_scan<In, Tout, kInclusive><<<1, kScanThreads, 0, s>>>(in, n, nullptr, out);
         VRB_LAUNCH_CHECK();
         return;
     }
     DBuf<Tout> sums(tiles, s), offs(tiles + 1, s);
-    k_tile_sums<Tin, Tout><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, n, sums.get());
+    k_tile_sums<In, Tout><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, n, sums.get());
     VRB_LAUNCH_CHECK();
-    scan_impl<Tout, Tout, false>(sums.get(), offs.get(), tiles, s);
-    k_tile_scan<Tin, Tout, kInclusive><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, n, offs.get(), out);
+    scan_impl<const Tout*, Tout, false>(sums.get(), offs.get(), tiles, s);
+    k_tile_scan<In, Tout, kInclusive><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, n, offs.get(), out);
     VRB_LAUNCH_CHECK();
 }
+
+// head flags of a sorted key array as a scan input: 1 where a run of equal
+// keys starts (dense ranks = their inclusive scan, reading A3)
+struct HeadFlags {
+    const uint64_t* key;
+    __device__ __forceinline__ uint32_t operator[](int64_t i) const {
+        return (i == 0 || __ldg(key + i) != __ldg(key + i - 1)) ? 1u : 0u;
+    }
+};
 
 __global__ void k_varying(const uint64_t* __restrict__ k, int64_t n, unsigned long long* out) {
     const uint64_t k0 = k[0];
@@ -156,13 +164,16 @@ unsigned grid_for(int64_t n, int threads) {
 }  // namespace
 
 void exclusive_scan(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
-    scan_impl<uint32_t, uint64_t, false>(in, out, n, s);
+    scan_impl<const uint32_t*, uint64_t, false>(in, out, n, s);
+}
+void dense_ranks(const uint64_t* sorted_keys, uint32_t* out, int64_t n, cudaStream_t s) {
+    scan_impl<HeadFlags, uint32_t, true>(HeadFlags{sorted_keys}, out, n, s);
 }
 void exclusive_scan(const uint64_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
-    scan_impl<uint64_t, uint64_t, false>(in, out, n, s);
+    scan_impl<const uint64_t*, uint64_t, false>(in, out, n, s);
 }
 void inclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
-    scan_impl<uint32_t, uint32_t, true>(in, out, n, s);
+    scan_impl<const uint32_t*, uint32_t, true>(in, out, n, s);
 }
 
 uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s) {

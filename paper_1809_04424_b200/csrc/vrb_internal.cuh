@@ -116,6 +116,9 @@ void exclusive_scan(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s
 void exclusive_scan(const uint64_t* in, uint64_t* out, int64_t n, cudaStream_t s);
 // out[i] = sum_{q<=i} in[q] (u32 result; the caller guarantees no overflow)
 void inclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s);
+// out[i] = 1-based dense rank of sorted_keys[i] (the inclusive scan of the
+// run-start flags, computed on the fly from the keys)
+void dense_ranks(const uint64_t* sorted_keys, uint32_t* out, int64_t n, cudaStream_t s);
 
 // Bitwise OR over i of (keys[i] ^ keys[0]): the key bits that vary.
 uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s);
