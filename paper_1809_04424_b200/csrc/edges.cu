@@ -248,9 +248,22 @@ uint32_t* sort_ids(DBuf<uint64_t>& k0, DBuf<uint64_t>& k1, DBuf<uint32_t>& v0, D
 // than 64 whose keys are not all equal sets *fallback (full sort needed).
 __global__ void k_fixup_runs(uint64_t* __restrict__ key, uint32_t* __restrict__ val, int64_t n, int shift,
                              int* __restrict__ fallback) {
-    GRID_STRIDE(p, n) {
-        const uint64_t hp = key[p] >> shift;
-        if (p > 0 && (key[p - 1] >> shift) == hp) continue;   // not the start of a run
+    // lanes hold consecutive keys: the neighbours come by shuffles, so the
+    // common case (a run of one) costs one coalesced load per key; only the
+    // starts of real runs walk them
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+        const int64_t p = base + lane;
+        const uint64_t k = p < n ? key[p] : ~0ull;
+        uint64_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
+        uint64_t knext = __shfl_down_sync(0xffffffffu, k, 1);
+        if (lane == 0) kprev = p > 0 && p < n ? key[p - 1] : ~0ull;
+        if (lane == 31) knext = p + 1 < n ? key[p + 1] : ~0ull;
+        if (p >= n) continue;
+        const uint64_t hp = k >> shift;
+        if (p > 0 && (kprev >> shift) == hp) continue;        // not the start of a run
+        if (p + 1 >= n || (knext >> shift) != hp) continue;   // a run of one
         int64_t q = p + 1;
         while (q < n && q - p <= VRB_EDGE_RUN_MAX && (key[q] >> shift) == hp) ++q;
         if (q - p < 2) continue;
