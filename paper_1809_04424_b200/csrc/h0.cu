@@ -252,26 +252,90 @@ __global__ void k_keep_flags(const uint32_t* __restrict__ forest, int64_t nf, ui
     GRID_STRIDE(q, nf) keep[forest[q]] = 0u;
 }
 
+__global__ void k_keep_bytes(const uint32_t* __restrict__ keep, int64_t E, uint8_t* __restrict__ out) {
+    GRID_STRIDE(e, E) out[e] = (uint8_t)keep[e];
+}
+
 __global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __restrict__ newidx, int64_t E,
                          uint32_t* __restrict__ rowmap) {
     GRID_STRIDE(e, E) if (keep[e]) rowmap[newidx[e]] = (uint32_t)e;
 }
 
-__global__ void k_col_counts(const uint32_t* __restrict__ rows, int64_t ncols, const uint32_t* __restrict__ keep,
-                             uint32_t* __restrict__ cnt) {
-    GRID_STRIDE(j, ncols) cnt[j] = keep[rows[3 * j]] + keep[rows[3 * j + 1]] + keep[rows[3 * j + 2]];
+// Columns in tiles of kCT: pass 1 sums each tile's kept rows, a scan of the
+// tile sums gives tile offsets, pass 2 scans the tile's column counts in the
+// block and writes colptr and the kept (renumbered) rows -- the D_2 rows are
+// read twice, colptr and the output written once, no per-column count array.
+constexpr int kCT = 2048;   // columns per tile: 256 threads x 8
+
+__device__ __forceinline__ uint32_t kept3(const uint32_t* __restrict__ rows, const uint8_t* __restrict__ keep,
+                                          int64_t j, uint32_t r[3]) {
+    const uint32_t* c = rows + 3 * j;
+    r[0] = __ldg(c);
+    r[1] = __ldg(c + 1);
+    r[2] = __ldg(c + 2);
+    return (uint32_t)keep[r[0]] + keep[r[1]] + keep[r[2]];
 }
 
-__global__ void k_col_fill(const uint32_t* __restrict__ rows, int64_t ncols, const uint32_t* __restrict__ keep,
-                           const uint64_t* __restrict__ newidx, const uint64_t* __restrict__ colptr,
-                           uint32_t* __restrict__ out) {
-    GRID_STRIDE(j, ncols) {
-        uint64_t o = colptr[j];
+__global__ void __launch_bounds__(256) k_col_tile_sums(const uint32_t* __restrict__ rows, int64_t ncols,
+                                                       const uint8_t* __restrict__ keep,
+                                                       unsigned long long* __restrict__ sums) {
+    __shared__ unsigned long long red[8];
+    const int64_t j0 = (int64_t)blockIdx.x * kCT;
+    unsigned long long a = 0;
+    for (int q = threadIdx.x; q < kCT; q += 256) {
+        const int64_t j = j0 + q;
+        uint32_t r[3];
+        if (j < ncols) a += kept3(rows, keep, j, r);
+    }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const uint32_t r = rows[3 * j + c];
-            if (keep[r]) out[o++] = (uint32_t)newidx[r];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_col_tile_fill(const uint32_t* __restrict__ rows, int64_t ncols,
+                                                       const uint8_t* __restrict__ keep,
+                                                       const uint64_t* __restrict__ newidx,
+                                                       const uint64_t* __restrict__ tile_off,
+                                                       uint64_t* __restrict__ colptr, uint32_t* __restrict__ out) {
+    __shared__ unsigned long long wt[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t j0 = (int64_t)blockIdx.x * kCT;
+    unsigned long long carry = tile_off[blockIdx.x];
+    for (int it = 0; it < kCT / 256; ++it) {
+        const int64_t j = j0 + it * 256 + threadIdx.x;
+        uint32_t r[3] = {0, 0, 0};
+        const uint32_t c = j < ncols ? kept3(rows, keep, j, r) : 0u;
+        unsigned long long x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
+        if (lane == 31) wt[wid] = x;
+        __syncthreads();
+        unsigned long long before = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const unsigned long long v = wt[w];
+            if (w < wid) before += v;
+            tot += v;
+        }
+        __syncthreads();
+        if (j < ncols) {
+            uint64_t o = carry + before + x - c;
+            colptr[j] = o;
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (keep[r[q]]) out[o++] = (uint32_t)newidx[r[q]];
+            if (j == ncols - 1) colptr[ncols] = o;
+        }
+        carry += tot;
     }
 }
 
@@ -282,7 +346,7 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
                     uint32_t** rowval_out, uint32_t** rowmap_out, int64_t* nrows_out) {
     *rowval_out = nullptr;
     *rowmap_out = nullptr;
-    DBuf<uint32_t> keep(std::max<int64_t>(E, 1), s);
+    DBuf<uint32_t> keep(std::max<int64_t>(E, 1), s);   // u32 flags for the scan ...
     fill_u32(keep.get(), 1u, E, s);
     if (nf) {
         k_keep_flags<<<grid_for(nf), 256, 0, s>>>(forest, nf, keep.get());
@@ -299,20 +363,27 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
         k_rowmap<<<grid_for(E), 256, 0, s>>>(keep.get(), newidx.get(), E, *rowmap_out);
         VRB_LAUNCH_CHECK();
     }
-    DBuf<uint32_t> cnt(std::max<int64_t>(ncols, 1), s);
-    if (ncols) {
-        k_col_counts<<<grid_for(ncols), 256, 0, s>>>(rows, ncols, keep.get(), cnt.get());
-        VRB_LAUNCH_CHECK();
+    DBuf<uint8_t> keep8(std::max<int64_t>(E, 1), s);   // ... and bytes for the column passes (L2-resident)
+    k_keep_bytes<<<grid_for(E), 256, 0, s>>>(keep.get(), E, keep8.get());
+    VRB_LAUNCH_CHECK();
+    keep.reset();
+    if (ncols == 0) {
+        VRB_CUDA(cudaMemsetAsync(colptr, 0, sizeof(uint64_t), s));
+        return 0;
     }
-    exclusive_scan(cnt.get(), colptr, ncols, s);
+    const int64_t tiles = ceil_div(ncols, kCT);
+    DBuf<unsigned long long> sums(tiles, s);
+    DBuf<uint64_t> toff(tiles + 1, s);
+    k_col_tile_sums<<<(unsigned)tiles, 256, 0, s>>>(rows, ncols, keep8.get(), sums.get());
+    VRB_LAUNCH_CHECK();
+    exclusive_scan(reinterpret_cast<const uint64_t*>(sums.get()), toff.get(), tiles, s);
     uint64_t nnz = 0;
-    VRB_CUDA(cudaMemcpyAsync(&nnz, colptr + ncols, sizeof(nnz), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(&nnz, toff.get() + tiles, sizeof(nnz), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *rowval_out = alloc_out((int64_t)nnz, ctx);
-    if (nnz) {
-        k_col_fill<<<grid_for(ncols), 256, 0, s>>>(rows, ncols, keep.get(), newidx.get(), colptr, *rowval_out);
-        VRB_LAUNCH_CHECK();
-    }
+    k_col_tile_fill<<<(unsigned)tiles, 256, 0, s>>>(rows, ncols, keep8.get(), newidx.get(), toff.get(), colptr,
+                                                    *rowval_out);
+    VRB_LAUNCH_CHECK();
     VRB_CUDA(cudaStreamSynchronize(s));
     return (int64_t)nnz;
 }
