@@ -618,14 +618,15 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
     return __reduce_add_sync(0xffffffffu, c);
 }
 
+template <bool kSmemBits = false>
 __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* __restrict__ map,
                                              WarpScratchB* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
                                              uint64_t offx, uint32_t degx, uint64_t bmo, uint64_t slot,
-                                             uint32_t filt) {
+                                             uint32_t filt, const uint32_t* smem_bits = nullptr) {
     const int lane = threadIdx.x & 31;
     const uint32_t nw = (degx + 31) >> 5;
     const uint32_t nchunks = (nw + 31) >> 5;
-    const uint32_t* __restrict__ in = A.bm + bmo;
+    const uint32_t* __restrict__ in = kSmemBits ? smem_bits : A.bm + bmo;
     const uint2* __restrict__ idx = A.idl + (A.debug == 3 ? 0 : offx);   // debug 3: ablation, one hot list
     // Windows of kWinB slots.  Each pass walks the bitmap in chunks of 32
     // words held in registers (lane = word): a warp scan of the popcounts
@@ -638,7 +639,7 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         for (uint32_t ch = 0; ch < nchunks; ++ch) {
             if (w0 > 0 && carry >= w1) break;
             const uint32_t wd = 32 * ch + lane;
-            uint32_t b = wd < nw ? __ldg(in + wd) : 0u;
+            uint32_t b = wd < nw ? (kSmemBits ? in[wd] : __ldg(in + wd)) : 0u;
             const uint32_t c = __popc(b);
             uint32_t incl = c;
 #pragma unroll
@@ -737,6 +738,37 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         __syncwarp();
     }
 }
+
+// Mark-in-fill (mode 4, VRB_TRI_PATH=markfill): the count stores nothing
+// but the counts; the fill marks the apex bitmap itself (as the bitmap count
+// does) in shared memory, then walks it as warp_fill_bm.
+struct WarpScratchM {
+    uint32_t bits[kBmWords];
+    WarpScratchB b;
+};
+
+__device__ __forceinline__ void warp_markfill(const TriArgs& A, const uint32_t* __restrict__ map,
+                                              WarpScratchM* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
+                                              uint64_t offx, uint32_t len, uint32_t degx, uint64_t slot,
+                                              uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (degx + 31) >> 5;
+    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
+    __syncwarp();
+    int mis;
+    const uint4* g = aligned_groups(A.nkr + offx, mis);
+    const int ngroups = (int)((len + mis + 3) >> 2);
+    auto mark = [&](uint32_t w, uint32_t) {
+        if (map[w & 0xFFFFu] < p) {
+            const uint32_t r = w >> 16;
+            atomicOr(&W->bits[r >> 5], 1u << (r & 31));
+        }
+    };
+    stream_prefix<kRegGroups>(g, ngroups, mis, len, mark);
+    __syncwarp();
+    warp_fill_bm<true>(A, map, &W->b, p, y, x, offx, degx, 0, slot, filt, W->bits);
+}
+
 
 // ---------------------------------------------------------------------------
 // Position-bitmap path (the default for single-rank-range builds with packed
@@ -1171,10 +1203,12 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
+        kBm == 4, WarpScratchM,
+        typename std::conditional<
         kBm >= 2, typename std::conditional<kFill, WarpScratchT, WarpScratchNone>::type,
         typename std::conditional<
             kBm == 1, typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
-            typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type>::type;
+            typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type>::type>::type;
     WS* scratch = reinterpret_cast<WS*>(smem + (A.gmap ? 0 : ((A.n * 4 + 15) / 16) * 16));
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
@@ -1241,7 +1275,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
             if (kFill) {
                 if (pl0.z) { slot0 = A.toff[pl0.x] - A.slot0; filt0 = A.efilt[pl0.x]; }
                 if (pl1.z) { slot1 = A.toff[pl1.x] - A.slot0; filt1 = A.efilt[pl1.x]; }
-                if (kBm) {
+                if (kBm && kBm != 4) {
                     if (pl0.z) bmo0 = A.bmoff[e0];
                     if (pl1.z) bmo1 = A.bmoff[e1];
                 }
@@ -1249,7 +1283,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
             while (e0 < end) {
                 const int64_t e2 = grab();
                 const uint4 pl2 = plan_of(e2);
-                if (kBm && kFill && pl1.z) {
+                if (kBm && kBm != 4 && kFill && pl1.z) {
                     // pull the next edge's bitmap into L2 while this edge runs
                     const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.bm + bmo1) & ~(uintptr_t)127;
                     const uintptr_t a1 =
@@ -1259,7 +1293,9 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                 }
                 if (pl0.z) {
                     const uint32_t p = pl0.x, x = pl0.y, len = pl0.z;
-                    if constexpr (kBm == 3 && !kFill) {
+                    if constexpr (kBm == 4 && kFill) {
+                        warp_markfill(A, map, scratch + wid, p, y, x, off0, len, pl0.w, slot0, filt0);
+                    } else if constexpr (kBm == 3 && !kFill) {
                         const uint32_t c = warp_count_rec(A, map, p, off0, len);
                         if (lane == 0) A.cnt[p] = c;
                     } else if constexpr (kBm == 2 && kFill) {
@@ -1291,7 +1327,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                 if (kFill && pl2.z) {
                     slot2 = A.toff[pl2.x] - A.slot0;
                     filt2 = A.efilt[pl2.x];
-                    if (kBm) bmo2 = A.bmoff[e2];
+                    if (kBm && kBm != 4) bmo2 = A.bmoff[e2];
                 }
                 e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1; bmo0 = bmo1;
                 e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2; bmo1 = bmo2;
@@ -1330,6 +1366,7 @@ void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap,
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
     TriArgs A = base;
     const bool packed = A.packed != 0;
+    const bool markfill = fill && A.bm_mode == 4;   // mark-in-fill (no stored bitmaps)
     const bool recm = A.rec != nullptr;   // x-major path: the count stores records
     const bool bm = A.bm != nullptr || recm;
     const bool tbm = (A.bm != nullptr && A.bm_mode == 2) || recm;
@@ -1337,7 +1374,8 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     // 16-warp CTAs, two per SM (shorter per-host barrier tails)
     // the host map goes to global memory when it would leave shared memory for
     // fewer than 8 warps of scratch (n above ~40-50k), or when forced (tests)
-    size_t per_warp = tbm ? (fill ? sizeof(WarpScratchT) : sizeof(WarpScratchNone))
+    size_t per_warp = markfill ? sizeof(WarpScratchM)
+                    : tbm ? (fill ? sizeof(WarpScratchT) : sizeof(WarpScratchNone))
                           : bm ? (fill ? sizeof(WarpScratchB) : sizeof(WarpScratchC)) : (fill ? scratch_bytes(packed) : 0);
     const char* fg = std::getenv("VRB_FORCE_GLOBAL_MAP");   // testing knob
     const bool gmap = (fg && fg[0] == '1') ||
@@ -1346,7 +1384,7 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     const size_t mapb = gmap ? 0 : map_bytes(A.n);
     const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)mapb - 1024;
     int warps;
-    if (bm) {
+    if (bm || markfill) {
         // count: 16-warp CTAs, 8 when the vertex map is small (more CTAs per SM)
         const int cw = mapb <= 32768 ? VRB_TRI_COUNT_WARPS / 2 : VRB_TRI_COUNT_WARPS;
         // fill: 32-warp CTAs (one per SM) when the host map is large (C5B:
@@ -1378,7 +1416,9 @@ void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts,
     VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     A.task_counter = counter.get();
     const int64_t cap = A.task_hi - A.task_lo;
-    if (recm) {
+    if (markfill) {
+        launch_k<true, true, 4>(A, threads, smem, cap, gmap, s);
+    } else if (recm) {
         launch_k<false, true, 3>(A, threads, smem, cap, gmap, s);
     } else if (tbm) {
         if (fill) launch_k<true, true, 2>(A, threads, smem, cap, gmap, s);
@@ -1436,9 +1476,17 @@ void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaSt
     launch(A, false, g.work, part, nparts, s);
 }
 
+// mark-in-fill (VRB_TRI_PATH=markfill): packed lists, degrees <= 8192, no
+// stored bitmaps (build_impl then runs the plain count)
+bool markfill_apply(const Graph& g) {
+    const char* m = std::getenv("VRB_TRI_PATH");
+    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && m && m[0] == 'm';
+}
+
 bool apex_bitmaps_apply(const Graph& g) {
     const char* off = std::getenv("VRB_NO_APEX_BITMAPS");   // testing knob: force the re-enumerating fill
-    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && !(off && off[0] == '1');
+    return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && !(off && off[0] == '1') &&
+           !markfill_apply(g);
 }
 
 void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words, cudaStream_t s) {
@@ -1587,7 +1635,7 @@ void fill_triangles(const Graph& g, const uint32_t* efilt, const uint64_t* toff,
     A.rows = rows;
     A.apex = g.n <= 65536 ? apex : nullptr;
     A.bm = const_cast<uint32_t*>(bm);
-    A.bm_mode = bm ? bitmap_mode() : 0;
+    A.bm_mode = bm ? bitmap_mode() : (markfill_apply(g) ? 4 : 0);
     A.bmoff = bmoff;
 #ifdef VRB_ABLATION
     // ablation timing of experiment builds only (tools/variants.py

@@ -98,6 +98,7 @@ void count_triangles(const Graph& g, uint32_t* cnt, int part, int nparts, cudaSt
 // (ceil(deg x / 32) words); the fill then emits from the bitmaps.
 constexpr uint32_t kApexBitmapMaxDeg = 8192;
 bool apex_bitmaps_apply(const Graph& g);
+bool markfill_apply(const Graph& g);
 void apex_bitmap_offsets(const Graph& g, DBuf<uint64_t>& bmoff, uint64_t& words, cudaStream_t s);
 void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint64_t* bmoff, cudaStream_t s);
 // Emit triangles of owner edges in [p_lo, p_hi) at slots toff[p] - slot0

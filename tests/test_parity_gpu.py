@@ -626,11 +626,12 @@ def test_full_size_c4_tetrahedra(vrb):
         torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("path", ["xmajor", "markfill", "bitmap"])
 @pytest.mark.parametrize("case", range(4))
-def test_xmajor_triangle_path(vrb, case, monkeypatch):
-    # the experimental x-major triangle path (VRB_TRI_PATH=xmajor) must be as
-    # exact as the default one
-    monkeypatch.setenv("VRB_TRI_PATH", "xmajor")
+def test_triangle_path_variants(vrb, case, path, monkeypatch):
+    # the experimental triangle paths (VRB_TRI_PATH=xmajor / markfill) must be
+    # as exact as the default one
+    monkeypatch.setenv("VRB_TRI_PATH", path)
     X, maxdim, radius = [(workloads.random_cloud(21, 300, 4, "gauss"), 1, 1.8),
                          (workloads.integer_lattice(4, 3), 2, 1.5),
                          (workloads.WORKLOADS["C2"].points(), 2, 0.45),
