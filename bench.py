@@ -290,16 +290,22 @@ def main():
         # F1 "clear and compress": D_2 without the H0 forest's rows,
         # on a build whose H0 is already computed (device-timed, not part of the step)
         if w.maxdim >= 1:
-            r = one_build(Xd)
-            r.h0()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            cp, rv, rm = r.compress_d2()
-            e1.record(s)
-            torch.cuda.synchronize()
+            cc_ms = []
+            for rep in range(2):   # the first call also grows the allocator's pool for its outputs
+                r = one_build(Xd)
+                r.h0()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                cp, rv, rm = r.compress_d2()
+                e1.record(s)
+                torch.cuda.synchronize()
+                cc_ms.append(e0.elapsed_time(e1))
+                if rep == 0:
+                    del r, cp, rv, rm
             T_ = counts[2][0]
-            h0["clear_compress"] = {"ms": e0.elapsed_time(e1), "d2_rows": int(counts[1][0]), "rows_kept": int(rm.numel()),
+            h0["clear_compress"] = {"ms": cc_ms[-1], "ms_first_call": cc_ms[0], "d2_rows": int(counts[1][0]),
+                                    "rows_kept": int(rm.numel()),
                                     "d2_nnz": int(3 * T_), "nnz_kept": int(rv.numel()),
                                     "nnz_removed_frac": (1.0 - rv.numel() / (3 * T_)) if T_ else 0.0}
             del r, cp, rv, rm

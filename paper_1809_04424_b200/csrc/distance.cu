@@ -530,7 +530,17 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     auto tidx = [&](int64_t ti) { return ti * nt - ti * (ti - 1) / 2; };   // first packed tile of tile row ti
     const int64_t mask_base = tidx(ti_lo);
     const int64_t ntiles = tidx(ti_hi) - mask_base;
-    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * 8);
+    // persistent CTAs: exactly the resident ones (a grid-stride loop over a
+    // grid larger than what fits would leave the extra CTAs a late second wave)
+    static int per_sm_mask = 0, per_sm_fill = 0;
+    if (!per_sm_mask) {
+        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_mask, k_dist_mask, kThreads, 0));
+        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fill, k_dist_fill, kThreads, 0));
+        per_sm_mask = std::max(per_sm_mask, 1);
+        per_sm_fill = std::max(per_sm_fill, 1);
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * per_sm_fill);
+    const unsigned grid_mask = (unsigned)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * per_sm_mask);
     if (all) {   // full filtration: no mask pass, closed-form slots
         auto start = [&](int64_t i) { return (uint64_t)(i * n - i * (i + 1) / 2); };   // lex slot of row i
         const uint64_t E = start(std::min(row_hi, n)) - start(row_lo);
@@ -553,7 +563,7 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
     DBuf<uint32_t> cnt((size_t)(nrows * nt), s);
     VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, ti_hi, mask_base,
+    k_dist_mask<<<grid_mask, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, ti_hi, mask_base,
                                           ntiles);
     VRB_LAUNCH_CHECK();
     DBuf<uint64_t> base((size_t)(nrows * nt + 1), s);
