@@ -56,21 +56,16 @@ __device__ __forceinline__ void tile_of_block(int64_t b, int64_t nt, int64_t ti_
 // Tile rows [ti_lo, ti_lo + gridDim.y) (a rank's row block);
 // masks are indexed from the block's first tile (mask_base) and the per
 // (row, tile) counts from its first row.
-struct MaskSmem {
-    double sA[kDC][kT];
-    double sB[kDC][kT];
-    unsigned long long mrow[kT];
-};
-
-__device__ __forceinline__ void mask_tile(MaskSmem& S, int64_t b, const double* __restrict__ X, int64_t n, int d,
-                                          int64_t nt, double thr, int all, unsigned long long* __restrict__ masks,
-                                          uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo, int64_t ti_hi,
-                                          int64_t mask_base) {
+__global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict__ X, int64_t n, int d,
+                                                        int64_t nt, double thr, int all,
+                                                        unsigned long long* __restrict__ masks,
+                                                        uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo,
+                                                        int64_t ti_hi, int64_t mask_base) {
     int64_t ti, tj;
-    tile_of_block(b, nt, ti_lo, ti_hi, mask_base, ti, tj);
-    auto& sA = S.sA;
-    auto& sB = S.sB;
-    auto& mrow = S.mrow;
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    __shared__ double sA[kDC][kT];
+    __shared__ double sB[kDC][kT];
+    __shared__ unsigned long long mrow[kT];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int64_t i0 = ti * kT, j0 = tj * kT;
     if (threadIdx.x < kT) mrow[threadIdx.x] = 0ull;
@@ -132,20 +127,6 @@ __device__ __forceinline__ void mask_tile(MaskSmem& S, int64_t b, const double* 
     }
 }
 
-// Persistent: CTAs stride over the tiles (a tile is ~1 us of work, so one
-// CTA per tile would pay a block launch per tile).
-__global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict__ X, int64_t n, int d,
-                                                        int64_t nt, double thr, int all,
-                                                        unsigned long long* __restrict__ masks,
-                                                        uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo,
-                                                        int64_t ti_hi, int64_t mask_base, int64_t ntiles) {
-    __shared__ MaskSmem S;
-    for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) {
-        mask_tile(S, b, X, n, d, nt, thr, all, masks, rowtile_cnt, ti_lo, ti_hi, mask_base);
-        __syncthreads();
-    }
-}
-
 // Full filtration (masks == null): every pair j > i is kept, so the row
 // bits and the lex slot are closed-form and the mask pass is skipped.
 __device__ __forceinline__ unsigned long long full_row_bits(int64_t i, int64_t j0, int64_t n) {
@@ -156,22 +137,17 @@ __device__ __forceinline__ unsigned long long full_row_bits(int64_t i, int64_t j
     return upto & ~((1ull << lo) - 1ull);
 }
 
-struct FillSmem {
-    double sA[kFillStageD][kT];
-    double sB[kFillStageD][kT];
-    uint32_t rstart[kT + 1];
-    uint16_t plist[kT * kT];
-    int s_any;
-};
-
-__device__ __forceinline__ void fill_tile(FillSmem& S, int64_t b, const double* __restrict__ X, int64_t n, int d,
-                                          int64_t nt, const unsigned long long* __restrict__ masks,
-                                          const uint64_t* __restrict__ slot_base, uint64_t* __restrict__ key,
-                                          uint32_t* __restrict__ ei, uint32_t* __restrict__ ej,
-                                          uint32_t* __restrict__ pij, int64_t ti_lo, int64_t ti_hi,
-                                          int64_t mask_base) {
+__global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict__ X, int64_t n, int d,
+                                                        int64_t nt,
+                                                        const unsigned long long* __restrict__ masks,
+                                                        const uint64_t* __restrict__ slot_base,
+                                                        uint64_t* __restrict__ key,
+                                                        uint32_t* __restrict__ ei,
+                                                        uint32_t* __restrict__ ej,
+                                                        uint32_t* __restrict__ pij, int64_t ti_lo,
+                                                        int64_t ti_hi, int64_t mask_base) {
     int64_t ti, tj;
-    tile_of_block(b, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
     const int64_t row_lo = ti_lo * kT;
@@ -179,9 +155,9 @@ __device__ __forceinline__ void fill_tile(FillSmem& S, int64_t b, const double* 
     // the tile's points, coordinate-major, when they fit (d <= kFillStageD):
     // the fold then reads shared memory (row point broadcast, column points
     // conflict-free) instead of strided global loads
-    auto& sA = S.sA;
-    auto& sB = S.sB;
-    int& s_any = S.s_any;
+    __shared__ double sA[kFillStageD][kT];
+    __shared__ double sB[kFillStageD][kT];
+    __shared__ int s_any;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
     if (threadIdx.x < kT && (m ? m[threadIdx.x] : full_row_bits(i0 + threadIdx.x, j0, n))) s_any = 1;
@@ -201,8 +177,8 @@ __device__ __forceinline__ void fill_tile(FillSmem& S, int64_t b, const double* 
         // so compact them first (row starts by a warp scan of the row
         // popcounts, then each row's set bits) and give every thread whole
         // pairs: no lane idles on a dropped pair
-        auto& rstart = S.rstart;
-        auto& plist = S.plist;
+        __shared__ uint32_t rstart[kT + 1];
+        __shared__ uint16_t plist[kT * kT];
         if (wid == 0) {
             uint32_t c0 = __popcll(m[lane]), c1 = __popcll(m[lane + 32]);
             uint32_t x0 = c0, x1 = c1;
@@ -287,22 +263,6 @@ __device__ __forceinline__ void fill_tile(FillSmem& S, int64_t b, const double* 
                 ej[slot] = (uint32_t)j;
             }
         }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict__ X, int64_t n, int d,
-                                                        int64_t nt,
-                                                        const unsigned long long* __restrict__ masks,
-                                                        const uint64_t* __restrict__ slot_base,
-                                                        uint64_t* __restrict__ key,
-                                                        uint32_t* __restrict__ ei,
-                                                        uint32_t* __restrict__ ej,
-                                                        uint32_t* __restrict__ pij, int64_t ti_lo,
-                                                        int64_t ti_hi, int64_t mask_base, int64_t ntiles) {
-    __shared__ FillSmem S;
-    for (int64_t b = blockIdx.x; b < ntiles; b += gridDim.x) {
-        fill_tile(S, b, X, n, d, nt, masks, slot_base, key, ei, ej, pij, ti_lo, ti_hi, mask_base);
-        __syncthreads();
     }
 }
 
@@ -530,17 +490,7 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
     auto tidx = [&](int64_t ti) { return ti * nt - ti * (ti - 1) / 2; };   // first packed tile of tile row ti
     const int64_t mask_base = tidx(ti_lo);
     const int64_t ntiles = tidx(ti_hi) - mask_base;
-    // persistent CTAs: exactly the resident ones (a grid-stride loop over a
-    // grid larger than what fits would leave the extra CTAs a late second wave)
-    static int per_sm_mask = 0, per_sm_fill = 0;
-    if (!per_sm_mask) {
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_mask, k_dist_mask, kThreads, 0));
-        VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fill, k_dist_fill, kThreads, 0));
-        per_sm_mask = std::max(per_sm_mask, 1);
-        per_sm_fill = std::max(per_sm_fill, 1);
-    }
-    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * per_sm_fill);
-    const unsigned grid_mask = (unsigned)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * per_sm_mask);
+    const unsigned grid = (unsigned)ntiles;
     if (all) {   // full filtration: no mask pass, closed-form slots
         auto start = [&](int64_t i) { return (uint64_t)(i * n - i * (i + 1) / 2); };   // lex slot of row i
         const uint64_t E = start(std::min(row_hi, n)) - start(row_lo);
@@ -556,15 +506,14 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
         }
         if (E == 0) return;
         k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, nullptr, nullptr, out.key.get(), out.ei.get(),
-                                              out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base, ntiles);
+                                              out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base);
         VRB_LAUNCH_CHECK();
         return;
     }
     DBuf<unsigned long long> masks((size_t)ntiles * kT, s);
     DBuf<uint32_t> cnt((size_t)(nrows * nt), s);
     VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-    k_dist_mask<<<grid_mask, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, ti_hi, mask_base,
-                                          ntiles);
+    k_dist_mask<<<grid, kThreads, 0, s>>>(X, n, d, nt, thr, all, masks.get(), cnt.get(), ti_lo, ti_hi, mask_base);
     VRB_LAUNCH_CHECK();
     DBuf<uint64_t> base((size_t)(nrows * nt + 1), s);
     exclusive_scan(cnt.get(), base.get(), nrows * nt, s);
@@ -583,7 +532,7 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
         out.ej.alloc(E, s);
     }
     k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, masks.get(), base.get(), out.key.get(),
-                                          out.ei.get(), out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base, ntiles);
+                                          out.ei.get(), out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base);
     VRB_LAUNCH_CHECK();
 }
 
