@@ -252,10 +252,6 @@ __global__ void k_keep_flags(const uint32_t* __restrict__ forest, int64_t nf, ui
     GRID_STRIDE(q, nf) keep[forest[q]] = 0u;
 }
 
-__global__ void k_keep_bytes(const uint32_t* __restrict__ keep, int64_t E, uint8_t* __restrict__ out) {
-    GRID_STRIDE(e, E) out[e] = (uint8_t)keep[e];
-}
-
 __global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __restrict__ newidx, int64_t E,
                          uint32_t* __restrict__ rowmap) {
     GRID_STRIDE(e, E) if (keep[e]) rowmap[newidx[e]] = (uint32_t)e;
@@ -264,78 +260,137 @@ __global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __re
 // Columns in tiles of kCT: pass 1 sums each tile's kept rows, a scan of the
 // tile sums gives tile offsets, pass 2 scans the tile's column counts in the
 // block and writes colptr and the kept (renumbered) rows -- the D_2 rows are
-// read twice, colptr and the output written once, no per-column count array.
+// read twice, colptr and the output written once.  Whether a row survives and
+// its new number come from the (sorted) forest itself, held in shared memory
+// with a coarse index: blk[b] = #forest positions below b * 1024, so a row r
+// scans forest[blk[r/1024], blk[r/1024 + 1]) -- a couple of entries (the
+// forest has n - c of E edges) -- instead of two random global lookups per
+// row.  Persistent CTAs load the index once and stride over the tiles.
 constexpr int kCT = 2048;   // columns per tile: 256 threads x 8
+constexpr int kBlkShift = 10;
 
-__device__ __forceinline__ uint32_t kept3(const uint32_t* __restrict__ rows, const uint8_t* __restrict__ keep,
-                                          int64_t j, uint32_t r[3]) {
+struct ForestIndex {
+    const uint32_t* f;     // sorted forest positions (shared)
+    const uint32_t* blk;   // coarse index (shared)
+    __device__ __forceinline__ bool kept(uint32_t r, uint32_t& newr) const {
+        const uint32_t b = r >> kBlkShift;
+        uint32_t lo = blk[b];
+        const uint32_t hi = blk[b + 1];
+        while (lo < hi && f[lo] < r) ++lo;
+        newr = r - lo;
+        return !(lo < hi && f[lo] == r);
+    }
+};
+
+__device__ __forceinline__ uint32_t kept3(const uint32_t* __restrict__ rows, const ForestIndex& FI, int64_t j,
+                                          uint32_t nr[3], bool k[3]) {
     const uint32_t* c = rows + 3 * j;
-    r[0] = __ldg(c);
-    r[1] = __ldg(c + 1);
-    r[2] = __ldg(c + 2);
-    return (uint32_t)keep[r[0]] + keep[r[1]] + keep[r[2]];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        k[q] = FI.kept(__ldg(c + q), nr[q]);
+        cnt += k[q] ? 1u : 0u;
+    }
+    return cnt;
+}
+
+__device__ __forceinline__ ForestIndex load_forest(unsigned char* smem, const uint32_t* __restrict__ forest,
+                                                   int64_t nf, const uint32_t* __restrict__ blk, int64_t nblk) {
+    uint32_t* f = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* b = f + nf;
+    for (int64_t q = threadIdx.x; q < nf; q += blockDim.x) f[q] = forest[q];
+    for (int64_t q = threadIdx.x; q <= nblk; q += blockDim.x) b[q] = blk[q];
+    __syncthreads();
+    return ForestIndex{f, b};
+}
+
+__global__ void k_forest_blocks(const uint32_t* __restrict__ forest, int64_t nf, int64_t nblk,
+                                uint32_t* __restrict__ blk) {
+    GRID_STRIDE(b, nblk + 1) {
+        const uint64_t v = (uint64_t)b << kBlkShift;
+        int64_t lo = 0, hi = nf;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((uint64_t)forest[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        blk[b] = (uint32_t)lo;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_col_tile_sums(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                       const uint8_t* __restrict__ keep,
+                                                       const uint32_t* __restrict__ forest, int64_t nf,
+                                                       const uint32_t* __restrict__ blk, int64_t nblk,
                                                        unsigned long long* __restrict__ sums) {
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long red[8];
-    const int64_t j0 = (int64_t)blockIdx.x * kCT;
-    unsigned long long a = 0;
-    for (int q = threadIdx.x; q < kCT; q += 256) {
-        const int64_t j = j0 + q;
-        uint32_t r[3];
-        if (j < ncols) a += kept3(rows, keep, j, r);
-    }
+    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk);
+    const int64_t tiles = (ncols + kCT - 1) / kCT;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t j0 = t * kCT;
+        unsigned long long a = 0;
+        for (int q = threadIdx.x; q < kCT; q += 256) {
+            const int64_t j = j0 + q;
+            uint32_t nr[3];
+            bool k[3];
+            if (j < ncols) a += kept3(rows, FI, j, nr, k);
+        }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < 8; ++w) t += red[w];
-        sums[blockIdx.x] = t;
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tt = 0;
+            for (int w = 0; w < 8; ++w) tt += red[w];
+            sums[t] = tt;
+        }
+        __syncthreads();
     }
 }
 
 __global__ void __launch_bounds__(256) k_col_tile_fill(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                       const uint8_t* __restrict__ keep,
-                                                       const uint64_t* __restrict__ newidx,
+                                                       const uint32_t* __restrict__ forest, int64_t nf,
+                                                       const uint32_t* __restrict__ blk, int64_t nblk,
                                                        const uint64_t* __restrict__ tile_off,
                                                        uint64_t* __restrict__ colptr, uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long wt[8];
+    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t j0 = (int64_t)blockIdx.x * kCT;
-    unsigned long long carry = tile_off[blockIdx.x];
-    for (int it = 0; it < kCT / 256; ++it) {
-        const int64_t j = j0 + it * 256 + threadIdx.x;
-        uint32_t r[3] = {0, 0, 0};
-        const uint32_t c = j < ncols ? kept3(rows, keep, j, r) : 0u;
-        unsigned long long x = c;
+    const int64_t tiles = (ncols + kCT - 1) / kCT;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t j0 = t * kCT;
+        unsigned long long carry = tile_off[t];
+        for (int it = 0; it < kCT / 256; ++it) {
+            const int64_t j = j0 + it * 256 + threadIdx.x;
+            uint32_t nr[3] = {0, 0, 0};
+            bool k[3] = {false, false, false};
+            const uint32_t c = j < ncols ? kept3(rows, FI, j, nr, k) : 0u;
+            unsigned long long x = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wt[wid] = x;
-        __syncthreads();
-        unsigned long long before = 0, tot = 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wt[wid] = x;
+            __syncthreads();
+            unsigned long long before = 0, tot = 0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const unsigned long long v = wt[w];
-            if (w < wid) before += v;
-            tot += v;
-        }
-        __syncthreads();
-        if (j < ncols) {
-            uint64_t o = carry + before + x - c;
-            colptr[j] = o;
+            for (int w = 0; w < 8; ++w) {
+                const unsigned long long v = wt[w];
+                if (w < wid) before += v;
+                tot += v;
+            }
+            __syncthreads();
+            if (j < ncols) {
+                uint64_t o = carry + before + x - c;
+                colptr[j] = o;
 #pragma unroll
-            for (int q = 0; q < 3; ++q)
-                if (keep[r[q]]) out[o++] = (uint32_t)newidx[r[q]];
-            if (j == ncols - 1) colptr[ncols] = o;
+                for (int q = 0; q < 3; ++q)
+                    if (k[q]) out[o++] = nr[q];
+                if (j == ncols - 1) colptr[ncols] = o;
+            }
+            carry += tot;
         }
-        carry += tot;
     }
 }
 
@@ -363,26 +418,35 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
         k_rowmap<<<grid_for(E), 256, 0, s>>>(keep.get(), newidx.get(), E, *rowmap_out);
         VRB_LAUNCH_CHECK();
     }
-    DBuf<uint8_t> keep8(std::max<int64_t>(E, 1), s);   // ... and bytes for the column passes (L2-resident)
-    k_keep_bytes<<<grid_for(E), 256, 0, s>>>(keep.get(), E, keep8.get());
-    VRB_LAUNCH_CHECK();
     keep.reset();
     if (ncols == 0) {
         VRB_CUDA(cudaMemsetAsync(colptr, 0, sizeof(uint64_t), s));
         return 0;
     }
+    const int64_t nblk = (E >> kBlkShift) + 1;
+    DBuf<uint32_t> blk(nblk + 1, s);
+    k_forest_blocks<<<grid_for(nblk + 1), 256, 0, s>>>(forest, nf, nblk, blk.get());
+    VRB_LAUNCH_CHECK();
+    const size_t smem = (size_t)4 * (nf + nblk + 1);
+    if ((int64_t)smem + 1024 > (int64_t)device_max_smem_optin())
+        fail(VRB_ENOTSUP, "clear and compress: the forest index (%zu bytes) exceeds shared memory", smem);
+    VRB_CUDA(cudaFuncSetAttribute(k_col_tile_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VRB_CUDA(cudaFuncSetAttribute(k_col_tile_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_tile_fill, 256, smem));
     const int64_t tiles = ceil_div(ncols, kCT);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)device_sm_count() * std::max(1, per_sm));
     DBuf<unsigned long long> sums(tiles, s);
     DBuf<uint64_t> toff(tiles + 1, s);
-    k_col_tile_sums<<<(unsigned)tiles, 256, 0, s>>>(rows, ncols, keep8.get(), sums.get());
+    k_col_tile_sums<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, sums.get());
     VRB_LAUNCH_CHECK();
     exclusive_scan(reinterpret_cast<const uint64_t*>(sums.get()), toff.get(), tiles, s);
     uint64_t nnz = 0;
     VRB_CUDA(cudaMemcpyAsync(&nnz, toff.get() + tiles, sizeof(nnz), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *rowval_out = alloc_out((int64_t)nnz, ctx);
-    k_col_tile_fill<<<(unsigned)tiles, 256, 0, s>>>(rows, ncols, keep8.get(), newidx.get(), toff.get(), colptr,
-                                                    *rowval_out);
+    k_col_tile_fill<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, toff.get(), colptr,
+                                            *rowval_out);
     VRB_LAUNCH_CHECK();
     VRB_CUDA(cudaStreamSynchronize(s));
     return (int64_t)nnz;
