@@ -296,6 +296,7 @@ __device__ __forceinline__ uint32_t kept3(const uint32_t* __restrict__ rows, con
 
 __device__ __forceinline__ ForestIndex load_forest(unsigned char* smem, const uint32_t* __restrict__ forest,
                                                    int64_t nf, const uint32_t* __restrict__ blk, int64_t nblk) {
+    if (nblk < 0) return ForestIndex{forest, blk};   // too large for shared memory: read it through L2
     uint32_t* f = reinterpret_cast<uint32_t*>(smem);
     uint32_t* b = f + nf;
     for (int64_t q = threadIdx.x; q < nf; q += blockDim.x) f[q] = forest[q];
@@ -427,9 +428,12 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
     DBuf<uint32_t> blk(nblk + 1, s);
     k_forest_blocks<<<grid_for(nblk + 1), 256, 0, s>>>(forest, nf, nblk, blk.get());
     VRB_LAUNCH_CHECK();
-    const size_t smem = (size_t)4 * (nf + nblk + 1);
-    if ((int64_t)smem + 1024 > (int64_t)device_max_smem_optin())
-        fail(VRB_ENOTSUP, "clear and compress: the forest index (%zu bytes) exceeds shared memory", smem);
+    size_t smem = (size_t)4 * (nf + nblk + 1);
+    int64_t nblk_arg = nblk;
+    if ((int64_t)smem + 2048 > (int64_t)device_max_smem_optin()) {   // large forests: index in global memory
+        smem = 0;
+        nblk_arg = -1;
+    }
     VRB_CUDA(cudaFuncSetAttribute(k_col_tile_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VRB_CUDA(cudaFuncSetAttribute(k_col_tile_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
@@ -438,14 +442,14 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)device_sm_count() * std::max(1, per_sm));
     DBuf<unsigned long long> sums(tiles, s);
     DBuf<uint64_t> toff(tiles + 1, s);
-    k_col_tile_sums<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, sums.get());
+    k_col_tile_sums<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk_arg, sums.get());
     VRB_LAUNCH_CHECK();
     exclusive_scan(reinterpret_cast<const uint64_t*>(sums.get()), toff.get(), tiles, s);
     uint64_t nnz = 0;
     VRB_CUDA(cudaMemcpyAsync(&nnz, toff.get() + tiles, sizeof(nnz), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *rowval_out = alloc_out((int64_t)nnz, ctx);
-    k_col_tile_fill<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, toff.get(), colptr,
+    k_col_tile_fill<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk_arg, toff.get(), colptr,
                                             *rowval_out);
     VRB_LAUNCH_CHECK();
     VRB_CUDA(cudaStreamSynchronize(s));
