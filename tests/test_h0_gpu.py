@@ -203,3 +203,27 @@ def test_compress_d2_vs_oracle(vrb, case):
     assert comp_pairs == full_pairs
     # the forest edges are never pivots of D_2
     assert not any(negative[r] for r, _ in full_pairs)
+
+
+def test_compress_d2_large_forest_index_in_global_memory(vrb):
+    # 60 000 points: the forest (~60 000 edges) is too large for the
+    # shared-memory index, so the column passes read it through L2; the
+    # result must still be D_2 without the forest rows, renumbered (checked
+    # against that definition on the GPU's own D_2 and forest, whose parity
+    # the tests above establish)
+    X = workloads.random_cloud(60, 60000, 3, "uniform")
+    res = vrb.build(X, maxdim=1, radius=0.03)
+    pos, _, _ = res.h0()
+    forest = np.sort(_u32(pos).astype(np.int64))
+    rows = _u32(res.boundary(2)).astype(np.int64)
+    cp, rv, rm = res.compress_d2()
+    cp, rv, rm = cp.cpu().numpy(), _u32(rv).astype(np.int64), _u32(rm).astype(np.int64)
+    E = res.count(1)[0]
+    keep = np.ones(E, dtype=bool)
+    keep[forest] = False
+    newidx = np.cumsum(keep) - 1
+    assert np.array_equal(rm, np.flatnonzero(keep))
+    kept = keep[rows]
+    assert np.array_equal(np.diff(cp), kept.sum(1))
+    assert np.array_equal(rv, newidx[rows][kept])
+    assert kept.sum(1).min() >= 1
