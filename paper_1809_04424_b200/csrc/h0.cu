@@ -257,141 +257,194 @@ __global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __re
     GRID_STRIDE(e, E) if (keep[e]) rowmap[newidx[e]] = (uint32_t)e;
 }
 
-// Columns in tiles of kCT: pass 1 sums each tile's kept rows, a scan of the
-// tile sums gives tile offsets, pass 2 scans the tile's column counts in the
-// block and writes colptr and the kept (renumbered) rows -- the D_2 rows are
-// read twice, colptr and the output written once.  Whether a row survives and
-// its new number come from the (sorted) forest itself, held in shared memory
-// with a coarse index: blk[b] = #forest positions below b * 1024, so a row r
-// scans forest[blk[r/1024], blk[r/1024 + 1]) -- a couple of entries (the
-// forest has n - c of E edges) -- instead of two random global lookups per
-// row.  Persistent CTAs load the index once and stride over the tiles.
-constexpr int kCT = 2048;   // columns per tile: 256 threads x 8
-constexpr int kBlkShift = 10;
+// Columns in tiles: a thread takes kCPT consecutive columns (3 kCPT rows,
+// read as 16-byte vectors), a CTA of kCTh threads one tile of kCT columns.
+// Pass 1 sums each tile's kept rows, a scan of the tile sums gives tile
+// offsets, pass 2 scans the threads' counts in the block and writes colptr
+// and the kept (renumbered) rows -- the D_2 rows are read twice, colptr and
+// the output written once.  Whether a row survives and its new number come
+// from the (sorted) forest itself, held in shared memory with a coarse
+// index: blk[b] = #forest positions below b << shift, so a row r searches
+// forest[blk[r >> shift], blk[(r >> shift) + 1]) -- with the shift chosen so
+// a block holds about one forest position on average (the forest has n - c
+// of E edges, most of them among the shortest) -- instead of two random
+// global lookups per row.  Persistent CTAs load the
+// index once and stride over the tiles.
+constexpr int kCTh = 1024;           // threads per CTA
+constexpr int kCPT = 8;              // columns per thread (24 rows = 6 uint4)
+constexpr int kCT = kCTh * kCPT;     // columns per tile
 
 struct ForestIndex {
-    const uint32_t* f;     // sorted forest positions (shared)
-    const uint32_t* blk;   // coarse index (shared)
+    const uint32_t* f;     // sorted forest positions
+    const uint32_t* blk;   // coarse index
+    int shift;
     __device__ __forceinline__ bool kept(uint32_t r, uint32_t& newr) const {
-        const uint32_t b = r >> kBlkShift;
-        uint32_t lo = blk[b];
-        const uint32_t hi = blk[b + 1];
-        while (lo < hi && f[lo] < r) ++lo;
+        const uint32_t b = r >> shift;
+        uint32_t lo = blk[b], hi = blk[b + 1];
+        const uint32_t end = hi;
+        // lower bound of r in the block's forest positions: the forest's
+        // (short) edges crowd the first blocks, so search, not scan
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (f[mid] < r) lo = mid + 1; else hi = mid;
+        }
         newr = r - lo;
-        return !(lo < hi && f[lo] == r);
+        return !(lo < end && f[lo] == r);
     }
 };
 
-__device__ __forceinline__ uint32_t kept3(const uint32_t* __restrict__ rows, const ForestIndex& FI, int64_t j,
-                                          uint32_t nr[3], bool k[3]) {
-    const uint32_t* c = rows + 3 * j;
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        k[q] = FI.kept(__ldg(c + q), nr[q]);
-        cnt += k[q] ? 1u : 0u;
-    }
-    return cnt;
-}
-
 __device__ __forceinline__ ForestIndex load_forest(unsigned char* smem, const uint32_t* __restrict__ forest,
-                                                   int64_t nf, const uint32_t* __restrict__ blk, int64_t nblk) {
-    if (nblk < 0) return ForestIndex{forest, blk};   // too large for shared memory: read it through L2
+                                                   int64_t nf, const uint32_t* __restrict__ blk, int64_t nblk,
+                                                   int shift, bool in_smem) {
+    if (!in_smem) return ForestIndex{forest, blk, shift};   // too large for shared memory: read it through L2
     uint32_t* f = reinterpret_cast<uint32_t*>(smem);
     uint32_t* b = f + nf;
     for (int64_t q = threadIdx.x; q < nf; q += blockDim.x) f[q] = forest[q];
     for (int64_t q = threadIdx.x; q <= nblk; q += blockDim.x) b[q] = blk[q];
     __syncthreads();
-    return ForestIndex{f, b};
+    return ForestIndex{f, b, shift};
 }
 
-__global__ void k_forest_blocks(const uint32_t* __restrict__ forest, int64_t nf, int64_t nblk,
+// the kCPT columns of thread slot j0 .. j0 + kCPT: kept flags, new rows, and
+// the number kept per column (columns >= ncols keep nothing)
+struct ColGroup {
+    uint32_t r[3 * kCPT];
+    uint32_t keepmask;   // bit 3 c + q: row q of column c kept
+};
+
+__device__ __forceinline__ uint32_t load_group(const uint32_t* __restrict__ rows, int64_t ncols, int64_t j0,
+                                               const ForestIndex& FI, ColGroup& G) {
+    if (j0 + kCPT <= ncols) {
+        const uint4* v = reinterpret_cast<const uint4*>(rows + 3 * j0);
+#pragma unroll
+        for (int q = 0; q < 3 * kCPT / 4; ++q) {
+            const uint4 w = __ldcs(v + q);
+            G.r[4 * q] = w.x; G.r[4 * q + 1] = w.y; G.r[4 * q + 2] = w.z; G.r[4 * q + 3] = w.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 3 * kCPT; ++q) G.r[q] = j0 + q / 3 < ncols ? __ldcs(rows + 3 * j0 + q) : 0u;
+    }
+    uint32_t mask = 0, cnt = 0;
+    uint32_t last = 0xFFFFFFFFu, lastnew = 0;
+    bool lastkept = false;
+#pragma unroll
+    for (int q = 0; q < 3 * kCPT; ++q) {
+        if (j0 + q / 3 >= ncols) continue;
+        uint32_t nr;
+        bool k;
+        if (G.r[q] == last) {   // the owner edge's row repeats along its triangles
+            nr = lastnew;
+            k = lastkept;
+        } else {
+            k = FI.kept(G.r[q], nr);
+            last = G.r[q];
+            lastnew = nr;
+            lastkept = k;
+        }
+        G.r[q] = nr;
+        if (k) { mask |= 1u << q; ++cnt; }
+    }
+    G.keepmask = mask;
+    return cnt;
+}
+
+__global__ void __launch_bounds__(kCTh) k_col_tile_sums(const uint32_t* __restrict__ rows, int64_t ncols,
+                                                        const uint32_t* __restrict__ forest, int64_t nf,
+                                                        const uint32_t* __restrict__ blk, int64_t nblk, int shift,
+                                                        int in_smem, unsigned long long* __restrict__ sums) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red[kCTh / 32];
+    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk, shift, in_smem != 0);
+    const int64_t tiles = (ncols + kCT - 1) / kCT;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        ColGroup G;
+        unsigned long long a = load_group(rows, ncols, t * kCT + (int64_t)threadIdx.x * kCPT, FI, G);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long v = red[threadIdx.x];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (threadIdx.x == 0) sums[t] = v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kCTh) k_col_tile_fill(const uint32_t* __restrict__ rows, int64_t ncols,
+                                                        const uint32_t* __restrict__ forest, int64_t nf,
+                                                        const uint32_t* __restrict__ blk, int64_t nblk, int shift,
+                                                        int in_smem, const uint64_t* __restrict__ tile_off,
+                                                        uint64_t* __restrict__ colptr, uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long wt[kCTh / 32];
+    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk, shift, in_smem != 0);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t tiles = (ncols + kCT - 1) / kCT;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t j0 = t * kCT + (int64_t)threadIdx.x * kCPT;
+        ColGroup G;
+        const uint32_t c = load_group(rows, ncols, j0, FI, G);
+        unsigned long long x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wt[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long v = wt[lane], s = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            wt[lane] = s - v;   // exclusive prefix of the warp totals
+        }
+        __syncthreads();
+        uint64_t o = tile_off[t] + wt[wid] + x - c;
+        if (j0 + kCPT <= ncols) {
+            uint64_t cp[kCPT];
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) {
+                cp[q] = o;
+#pragma unroll
+                for (int e = 0; e < 3; ++e)
+                    if ((G.keepmask >> (3 * q + e)) & 1u) out[o++] = G.r[3 * q + e];
+            }
+            ulonglong2* d = reinterpret_cast<ulonglong2*>(colptr + j0);
+#pragma unroll
+            for (int q = 0; q < kCPT / 2; ++q) __stcs(d + q, make_ulonglong2(cp[2 * q], cp[2 * q + 1]));
+            if (j0 + kCPT == ncols) colptr[ncols] = o;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kCPT; ++q) {
+                if (j0 + q >= ncols) break;
+                colptr[j0 + q] = o;
+#pragma unroll
+                for (int e = 0; e < 3; ++e)
+                    if ((G.keepmask >> (3 * q + e)) & 1u) out[o++] = G.r[3 * q + e];
+                if (j0 + q == ncols - 1) colptr[ncols] = o;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_forest_blocks(const uint32_t* __restrict__ forest, int64_t nf, int64_t nblk, int shift,
                                 uint32_t* __restrict__ blk) {
     GRID_STRIDE(b, nblk + 1) {
-        const uint64_t v = (uint64_t)b << kBlkShift;
+        const uint64_t v = (uint64_t)b << shift;
         int64_t lo = 0, hi = nf;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
             if ((uint64_t)forest[mid] < v) lo = mid + 1; else hi = mid;
         }
         blk[b] = (uint32_t)lo;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_col_tile_sums(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                       const uint32_t* __restrict__ forest, int64_t nf,
-                                                       const uint32_t* __restrict__ blk, int64_t nblk,
-                                                       unsigned long long* __restrict__ sums) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long red[8];
-    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk);
-    const int64_t tiles = (ncols + kCT - 1) / kCT;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t j0 = t * kCT;
-        unsigned long long a = 0;
-        for (int q = threadIdx.x; q < kCT; q += 256) {
-            const int64_t j = j0 + q;
-            uint32_t nr[3];
-            bool k[3];
-            if (j < ncols) a += kept3(rows, FI, j, nr, k);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long tt = 0;
-            for (int w = 0; w < 8; ++w) tt += red[w];
-            sums[t] = tt;
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256) k_col_tile_fill(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                       const uint32_t* __restrict__ forest, int64_t nf,
-                                                       const uint32_t* __restrict__ blk, int64_t nblk,
-                                                       const uint64_t* __restrict__ tile_off,
-                                                       uint64_t* __restrict__ colptr, uint32_t* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long wt[8];
-    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t tiles = (ncols + kCT - 1) / kCT;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t j0 = t * kCT;
-        unsigned long long carry = tile_off[t];
-        for (int it = 0; it < kCT / 256; ++it) {
-            const int64_t j = j0 + it * 256 + threadIdx.x;
-            uint32_t nr[3] = {0, 0, 0};
-            bool k[3] = {false, false, false};
-            const uint32_t c = j < ncols ? kept3(rows, FI, j, nr, k) : 0u;
-            unsigned long long x = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) wt[wid] = x;
-            __syncthreads();
-            unsigned long long before = 0, tot = 0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const unsigned long long v = wt[w];
-                if (w < wid) before += v;
-                tot += v;
-            }
-            __syncthreads();
-            if (j < ncols) {
-                uint64_t o = carry + before + x - c;
-                colptr[j] = o;
-#pragma unroll
-                for (int q = 0; q < 3; ++q)
-                    if (k[q]) out[o++] = nr[q];
-                if (j == ncols - 1) colptr[ncols] = o;
-            }
-            carry += tot;
-        }
     }
 }
 
@@ -424,33 +477,38 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
         VRB_CUDA(cudaMemsetAsync(colptr, 0, sizeof(uint64_t), s));
         return 0;
     }
-    const int64_t nblk = (E >> kBlkShift) + 1;
+    // coarse index granularity: about one forest position per block, as long
+    // as forest + index fit shared memory (else the index goes to L2)
+    const int64_t budget = (int64_t)device_max_smem_optin() - 4096;
+    int shift = 6;
+    while (shift < 31 && (((E >> shift) > 2 * nf + 1024) || 4 * (nf + (E >> shift) + 2) > budget)) ++shift;
+    const int64_t nblk = (E >> shift) + 1;
     DBuf<uint32_t> blk(nblk + 1, s);
-    k_forest_blocks<<<grid_for(nblk + 1), 256, 0, s>>>(forest, nf, nblk, blk.get());
+    k_forest_blocks<<<grid_for(nblk + 1), 256, 0, s>>>(forest, nf, nblk, shift, blk.get());
     VRB_LAUNCH_CHECK();
     size_t smem = (size_t)4 * (nf + nblk + 1);
-    int64_t nblk_arg = nblk;
-    if ((int64_t)smem + 2048 > (int64_t)device_max_smem_optin()) {   // large forests: index in global memory
+    int in_smem = 1;
+    if ((int64_t)smem > budget) {   // large forests: index in global memory
         smem = 0;
-        nblk_arg = -1;
+        in_smem = 0;
     }
     VRB_CUDA(cudaFuncSetAttribute(k_col_tile_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VRB_CUDA(cudaFuncSetAttribute(k_col_tile_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_tile_fill, 256, smem));
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_tile_fill, kCTh, smem));
     const int64_t tiles = ceil_div(ncols, kCT);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)device_sm_count() * std::max(1, per_sm));
     DBuf<unsigned long long> sums(tiles, s);
     DBuf<uint64_t> toff(tiles + 1, s);
-    k_col_tile_sums<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk_arg, sums.get());
+    k_col_tile_sums<<<grid, kCTh, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, shift, in_smem, sums.get());
     VRB_LAUNCH_CHECK();
     exclusive_scan(reinterpret_cast<const uint64_t*>(sums.get()), toff.get(), tiles, s);
     uint64_t nnz = 0;
     VRB_CUDA(cudaMemcpyAsync(&nnz, toff.get() + tiles, sizeof(nnz), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *rowval_out = alloc_out((int64_t)nnz, ctx);
-    k_col_tile_fill<<<grid, 256, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk_arg, toff.get(), colptr,
-                                            *rowval_out);
+    k_col_tile_fill<<<grid, kCTh, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, shift, in_smem, toff.get(),
+                                             colptr, *rowval_out);
     VRB_LAUNCH_CHECK();
     VRB_CUDA(cudaStreamSynchronize(s));
     return (int64_t)nnz;

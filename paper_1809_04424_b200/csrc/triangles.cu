@@ -292,6 +292,27 @@ __device__ __forceinline__ uint32_t rank_bits(WS* __restrict__ W, uint32_t lim) 
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+// Exclusive per-word prefix popcounts of nw bitmap words (any nw), warp-wide.
+__device__ __forceinline__ void rank_bits_n(const uint32_t* __restrict__ bits, uint32_t* __restrict__ wpre,
+                                            uint32_t nw) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    uint32_t carry = 0;
+    for (uint32_t w0 = 0; w0 < nw; w0 += 32) {
+        const uint32_t wd = w0 + lane;
+        const uint32_t c = wd < nw ? __popc(bits[wd]) : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (wd < nw) wpre[wd] = carry + incl - c;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+}
+
 // Write the staged window [s0, s0 + m), one lane per triangle, kU position
 // gathers in flight per lane: record -> (k, t); pos(x, k) = np[offx + t] (the
 // prefix just streamed: L1/L2), pos(y, k) = map[k].
@@ -958,84 +979,156 @@ __device__ __forceinline__ void warp_fill_tbm(const TriArgs& A, const uint32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// x-major path ("records"; an experiment behind VRB_TRI_PATH=xmajor, packed
-// lists and degrees <= kApexBitmapMaxDeg).
-//   count (hosted by y, as before): per owner edge p, ballots over the
-//          scanned prefix of x give one bit per candidate t (valid apex:
-//          pos(y, k) < p) -- 32 candidates per map lookup + vote, no shared
-//          atomics -- and the valid candidates' host positions pos(y, k) are
-//          appended in prefix order (a coalesced 4-byte store per valid lane).
-//   fill  (x-major): a CTA holds the scanned vertex x's whole position-
-//          ordered list (k | krank, pos(x, k)) in shared memory and its warps
-//          take x's owner edges; per edge the validity words say which prefix
-//          entries are apexes, their id ranks (in the list word) give the
-//          slots (a shared bitmap + prefix popcounts: the lex order), k and
-//          pos(x, k) come from shared memory and pos(y, k) from the appended
-//          records (contiguous).  No neighbourhood is re-read from DRAM per
-//          owner edge: the fill reads 4 B per triangle and a bit per candidate
-//          besides writing its 28 B per triangle.
+// x-major path ("records"; packed lists, degrees <= kApexBitmapMaxDeg).
+//   count (hosted by y, the host map on chip): per owner edge p, x's
+//          older-neighbour prefix is streamed as in the bitmap count; each
+//          step (32 lanes x one entry of their 16-byte groups) takes one map
+//          lookup and one ballot: the ballot word is the step's validity
+//          word (stored, 32 per coalesced store) and the valid lanes append
+//          the host positions pos(y, k) in step order (a coalesced run per
+//          step).  No shared atomics, no per-edge bitmap.
+//   fill  (x-major): a CTA holds the scanned vertex x's position-ordered
+//          list (krank << 16 | k, pos(x, k)) in shared memory and its warps
+//          take x's owner edges.  Per edge: the validity words give the
+//          valid prefix entries t in step order (= the records' order); a
+//          compaction puts them in a shared arrival list; their id ranks
+//          (in the list word) are marked in a shared bitmap and prefix-
+//          popcounted -- the slot of an apex is the number of valid apexes
+//          of smaller id (the lex order); each arrival is staged at its slot
+//          with pos(y, k) read from its record (coalesced), and the staged
+//          window is written as whole 16-byte chunks.  No neighbourhood is
+//          re-read from DRAM per owner edge: the fill reads 4 B per triangle
+//          and a bit per candidate besides writing its 28 B per triangle.
+// Step order: chunk c of 32 groups, entry e of the group, lane: step s =
+// 4 c + e covers the prefix entries t = 4 (32 c + lane) + e - mis.
 // ---------------------------------------------------------------------------
+template <int G, class F>
+__device__ __forceinline__ void stream_range_s(const uint4* __restrict__ g, int start, int stop, int ngroups, int mis,
+                                               uint32_t len, F&& f) {
+    const int lane = threadIdx.x & 31;
+    for (int i0 = start; i0 < stop; i0 += 32 * G) {
+        uint4 q[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int i = i0 + u * 32 + lane;
+            q[u] = i < ngroups ? ld_list(g + i) : no_group();
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int i = i0 + u * 32 + lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t t = (uint32_t)(4 * i + e - mis);
+                f(pick(q[u], e), t < len);   // every lane calls (ballots inside)
+            }
+        }
+    }
+}
+template <class F>
+__device__ __forceinline__ void stream_prefix_s(const uint4* __restrict__ g, int ngroups, int mis, uint32_t len,
+                                                F&& f) {
+    const int f4 = (ngroups / 128) * 128;
+    const int f2 = f4 + ((ngroups - f4) / 64) * 64;
+    stream_range_s<4>(g, 0, f4, ngroups, mis, len, f);
+    stream_range_s<2>(g, f4, f2, ngroups, mis, len, f);
+    stream_range_s<1>(g, f2, ngroups, ngroups, mis, len, f);
+}
+
+__host__ __device__ __forceinline__ uint32_t rec_steps(uint32_t len, uint32_t mis) {
+    const uint32_t ngroups = (len + mis + 3) >> 2;
+    return 4u * ((ngroups + 31u) >> 5);
+}
+
 __device__ __forceinline__ uint32_t warp_count_rec(const TriArgs& A, const uint32_t* __restrict__ map, uint32_t p,
                                                    uint64_t offx, uint32_t len) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t* __restrict__ lst = A.nkr + offx;
     uint32_t* __restrict__ rec = A.rec + __ldg(A.rec_off + p);
     uint32_t* __restrict__ tb = A.tb + __ldg(A.tb_off + p);
-    const uint32_t nch = (len + 31) >> 5;
-    uint32_t c = 0;
-    constexpr int U = 8;
-    for (uint32_t c0 = 0; c0 < nch; c0 += U) {
-        uint32_t w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t t = 32 * (c0 + u) + lane;
-            w[u] = t < len ? ld_list(lst + t) : 0u;
-        }
-        uint32_t mine = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t t = 32 * (c0 + u) + lane;
-            const uint32_t py = t < len ? map[w[u] & 0xFFFFu] : NONE32;
-            const bool v = py < p;
-            const uint32_t b = __ballot_sync(0xffffffffu, v);
-            if (v) __stcg(rec + c + __popc(b & lt), py);
-            if (lane == u) mine = b;
-            c += __popc(b);
-        }
-        if (lane < U && c0 + lane < nch) __stcg(tb + c0 + lane, mine);
+    int mis;
+    const uint4* g = aligned_groups(A.nkr + offx, mis);
+    const int ngroups = (int)((len + mis + 3) >> 2);
+    uint32_t na = 0, step = 0, mine = 0;
+    stream_prefix_s(g, ngroups, mis, len, [&](uint32_t w, bool in) {
+        const uint32_t py = in ? map[w & 0xFFFFu] : NONE32;
+        const bool v = py < p;
+        const uint32_t b = __ballot_sync(0xffffffffu, v);
+        if (v) __stcg(rec + na + __popc(b & lt), py);
+        na += __popc(b);
+        if ((step & 31u) == (uint32_t)lane) mine = b;
+        ++step;
+        if ((step & 31u) == 0) __stcg(tb + step - 32 + lane, mine);
+    });
+    if (step & 31u) {
+        if ((uint32_t)lane < (step & 31u)) __stcg(tb + (step & ~31u) + lane, mine);
     }
-    return c;
+    return na;
 }
 
-constexpr int kWinX = 256;
+#ifndef VRB_XM_WIN
+#define VRB_XM_WIN 1024
+#endif
+constexpr int kWinX = VRB_XM_WIN;   // slots per window of the x-major fill
 struct WarpScratchX {
-    uint32_t bits[kBmWords];   // valid apexes by id rank in x's list
-    uint32_t wpre[kBmWords];
-    uint16_t rk[kWinX];        // staged window: apex ...
-    uint32_t rpx[kWinX];       // ... pos(x, k) ...
-    uint32_t rpy[kWinX];       // ... pos(y, k)
-    alignas(16) uint32_t st[96];
-    alignas(16) uint32_t sr[96];
+    uint32_t rbits[kBmWords];   // valid apexes by id rank in x's list
+    uint32_t wpre[kBmWords];    // exclusive prefix popcount per word
+    uint32_t py[kWinX];         // staged: pos(y, k) by slot
+    uint16_t cand[kWinX];       // arrival list: prefix index t of the valid entries (record order)
+    uint16_t st[kWinX];         // staged: prefix index t by slot
+    alignas(16) uint32_t ov[96];   // 32 triangles' vertices, then D_2 rows: 16-byte chunks
+    alignas(16) uint32_t orw[96];
 };
 
-// store_window with pos(y, k) from the staging too: kpq(j) = (k, pos(x,k), pos(y,k))
-template <int kU, class KPQ>
-__device__ __forceinline__ void store_window3(const TriArgs& A, uint32_t* __restrict__ st, uint32_t* __restrict__ sr,
-                                              uint64_t s0, uint32_t m, uint32_t p, uint32_t y, uint32_t x,
-                                              uint32_t filt, KPQ&& kpq) {
+// every valid entry of the edge in record order: f(t, j) (lane-serial over
+// the set bits of lane-owned validity words; j = record index)
+template <class F>
+__device__ __forceinline__ void walk_valid(const uint32_t* __restrict__ tb, uint32_t nsteps, uint32_t mis, F&& f) {
     const int lane = threadIdx.x & 31;
-    auto tri = [&](uint32_t j, uint3 q, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0, uint32_t& r1) {
-        a0 = y; a1 = x; a2 = q.x;
+    uint32_t run = 0;
+    for (uint32_t s0 = 0; s0 < nsteps; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        uint32_t word = s < nsteps ? __ldg(tb + s) : 0u;
+        const uint32_t c = __popc(word);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        uint32_t j = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t tb0 = 4u * 32u * (s >> 2) + (s & 3u) - mis;   // t of bit 0
+        while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            f(tb0 + 4u * (uint32_t)b, j);
+            ++j;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t xm_slot(const WarpScratchX* __restrict__ W, uint32_t r) {
+    return W->wpre[r >> 5] + __popc(W->rbits[r >> 5] & ((1u << (r & 31)) - 1u));
+}
+
+// emit the staged window [0, m) at output slots s0 + [0, m)
+__device__ __forceinline__ void flush_x(const TriArgs& A, const uint32_t* __restrict__ lk,
+                                        const uint32_t* __restrict__ lp, WarpScratchX* __restrict__ W, uint64_t s0,
+                                        uint32_t m, uint32_t p, uint32_t y, uint32_t x, uint32_t filt) {
+    const int lane = threadIdx.x & 31;
+    auto tri = [&](uint32_t j, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0, uint32_t& r1) {
+        const uint32_t t = W->st[j];
+        const uint32_t k = lk[t] & 0xFFFFu, px = lp[t], py = W->py[j];
+        a0 = y; a1 = x; a2 = k;
         sort3(a0, a1, a2);
-        r0 = min(q.y, q.z);
-        r1 = max(q.y, q.z);
+        r0 = min(px, py);
+        r1 = max(px, py);
         __stcs(A.tf + s0 + j, filt);
-        if (A.apex) A.apex[s0 + j] = (uint16_t)q.x;
+        if (A.apex) A.apex[s0 + j] = (uint16_t)k;
     };
-    auto scalar = [&](uint32_t j, uint3 q) {
+    auto scalar = [&](uint32_t j) {
         uint32_t a0, a1, a2, r0, r1;
-        tri(j, q, a0, a1, a2, r0, r1);
+        tri(j, a0, a1, a2, r0, r1);
         uint32_t* tv = A.tv + 3 * (s0 + j);
         __stcs(tv, a0);
         __stcs(tv + 1, a1);
@@ -1048,97 +1141,89 @@ __device__ __forceinline__ void store_window3(const TriArgs& A, uint32_t* __rest
         }
     };
     const uint32_t h = min(m, (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u));
-    if ((uint32_t)lane < h) scalar(lane, kpq(lane));
-    for (uint32_t g0 = h; g0 < m; g0 += 32 * kU) {
-#pragma unroll
-        for (int q = 0; q < kU; ++q) {
-            const uint32_t g = g0 + 32 * q;
-            if (g >= m) break;
-            const uint32_t j = g + lane;
-            if (g + 32 <= m) {
-                uint32_t a0, a1, a2, r0, r1;
-                tri(j, kpq(j), a0, a1, a2, r0, r1);
-                st[3 * lane] = a0;
-                st[3 * lane + 1] = a1;
-                st[3 * lane + 2] = a2;
-                sr[3 * lane] = r0;
-                sr[3 * lane + 1] = r1;
-                sr[3 * lane + 2] = p;
-                __syncwarp();
-                if (lane < 24) {
-                    __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane, reinterpret_cast<const uint4*>(st)[lane]);
-                    if (A.rows)
-                        __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
-                               reinterpret_cast<const uint4*>(sr)[lane]);
-                }
-                __syncwarp();
-            } else if (j < m) {
-                scalar(j, kpq(j));
+    if ((uint32_t)lane < h) scalar(lane);
+    for (uint32_t g = h; g < m; g += 32) {
+        const uint32_t j = g + lane;
+        if (g + 32 <= m) {
+            uint32_t a0, a1, a2, r0, r1;
+            tri(j, a0, a1, a2, r0, r1);
+            W->ov[3 * lane] = a0;
+            W->ov[3 * lane + 1] = a1;
+            W->ov[3 * lane + 2] = a2;
+            W->orw[3 * lane] = r0;
+            W->orw[3 * lane + 1] = r1;
+            W->orw[3 * lane + 2] = p;
+            __syncwarp();
+            if (lane < 24) {
+                __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane, reinterpret_cast<const uint4*>(W->ov)[lane]);
+                if (A.rows)
+                    __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
+                           reinterpret_cast<const uint4*>(W->orw)[lane]);
             }
+            __syncwarp();
+        } else if (j < m) {
+            scalar(j);
         }
     }
 }
 
 __device__ __forceinline__ void warp_fill_x(const TriArgs& A, const uint32_t* __restrict__ lk,
                                             const uint32_t* __restrict__ lp, WarpScratchX* __restrict__ W, uint32_t p,
-                                            uint32_t y, uint32_t x, uint32_t len, uint32_t degx, uint64_t slot,
-                                            uint32_t filt) {
+                                            uint32_t y, uint32_t x, uint32_t len, uint32_t degx, uint32_t mis,
+                                            uint64_t slot, uint32_t count, uint32_t filt) {
     const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
     const uint32_t* __restrict__ tb = A.tb + __ldg(A.tb_off + p);
     const uint32_t* __restrict__ rec = A.rec + __ldg(A.rec_off + p);
-    const uint32_t nch = (len + 31) >> 5;
+    const uint32_t nsteps = rec_steps(len, mis);
     const uint32_t nw = (degx + 31) >> 5;
-    for (uint32_t w = lane; w < nw; w += 32) W->bits[w] = 0u;
-    __syncwarp();
-    // ---- mark the id ranks of the valid entries (lane j holds word c0 + j)
-    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
-        const uint32_t wl = c0 + lane < nch ? __ldg(tb + c0 + lane) : 0u;
-        const uint32_t nu = min(32u, nch - c0);
-        for (uint32_t u = 0; u < nu; ++u) {
-            const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
-            if ((word >> lane) & 1u) {
-                const uint32_t r = lk[32 * (c0 + u) + lane] >> 16;
-                atomicOr(&W->bits[r >> 5], 1u << (r & 31));
-            }
+    if (count <= (uint32_t)kWinX) {
+        // arrivals -> shared list, then mark, rank, place, flush
+        walk_valid(tb, nsteps, mis, [&](uint32_t t, uint32_t j) { W->cand[j] = (uint16_t)t; });
+        __syncwarp();
+        for (uint32_t j = lane; j < count; j += 32) {
+            const uint32_t r = lk[W->cand[j]] >> 16;
+            atomicOr(&W->rbits[r >> 5], 1u << (r & 31));
         }
-    }
-    const uint32_t count = rank_bits<kBmWords>(W, degx);
-    // ---- windows of kWinX slots: stage (k, pos(x,k), pos(y,k)) by slot, store
-    for (uint32_t w0 = 0; w0 < count; w0 += kWinX) {
-        uint32_t run = 0;   // records before this chunk (prefix order)
-        for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
-            const uint32_t wl = c0 + lane < nch ? __ldg(tb + c0 + lane) : 0u;
-            const uint32_t nu = min(32u, nch - c0);
-            for (uint32_t u = 0; u < nu; ++u) {
-                const uint32_t word = __shfl_sync(0xffffffffu, wl, u);
-                if ((word >> lane) & 1u) {
-                    const uint32_t t = 32 * (c0 + u) + lane;
-                    const uint32_t e = lk[t];
-                    const uint32_t r = e >> 16;
-                    const uint32_t wd = W->bits[r >> 5];
-                    const uint32_t sl = W->wpre[r >> 5] + __popc(wd & ((2u << (r & 31)) - 1u)) - 1u - w0;
-                    if (sl < (uint32_t)kWinX) {
-                        W->rk[sl] = (uint16_t)(e & 0xFFFFu);
-                        W->rpx[sl] = lp[t];
-                        W->rpy[sl] = __ldg(rec + run + __popc(word & lt));
-                    }
+        rank_bits_n(W->rbits, W->wpre, nw);
+        for (uint32_t j = lane; j < count; j += 32) {
+            const uint32_t t = W->cand[j];
+            const uint32_t s = xm_slot(W, lk[t] >> 16);
+            W->st[s] = (uint16_t)t;
+            W->py[s] = __ldcs(rec + j);
+        }
+        __syncwarp();
+        flush_x(A, lk, lp, W, slot, count, p, y, x, filt);
+    } else {
+        // more apexes than a window: mark from the validity words, then per
+        // window of slots place the arrivals that fall in it
+        walk_valid(tb, nsteps, mis, [&](uint32_t t, uint32_t) {
+            const uint32_t r = lk[t] >> 16;
+            atomicOr(&W->rbits[r >> 5], 1u << (r & 31));
+        });
+        rank_bits_n(W->rbits, W->wpre, nw);
+        for (uint32_t w0 = 0; w0 < count; w0 += kWinX) {
+            walk_valid(tb, nsteps, mis, [&](uint32_t t, uint32_t j) {
+                const uint32_t s = xm_slot(W, lk[t] >> 16) - w0;
+                if (s < (uint32_t)kWinX) {
+                    W->st[s] = (uint16_t)t;
+                    W->py[s] = __ldg(rec + j);
                 }
-                run += __popc(word);
-            }
+            });
+            __syncwarp();
+            flush_x(A, lk, lp, W, slot + w0, min((uint32_t)kWinX, count - w0), p, y, x, filt);
+            __syncwarp();
         }
-        __syncwarp();
-        const uint32_t m = min((uint32_t)kWinX, count - w0);
-        store_window3<4>(A, W->st, W->sr, slot + w0, m, p, y, x, filt,
-                         [&](uint32_t j) { return make_uint3(W->rk[j], W->rpx[j], W->rpy[j]); });
-        __syncwarp();
     }
+    __syncwarp();
+    for (uint32_t w = lane; w < nw; w += 32) W->rbits[w] = 0u;
+    __syncwarp();
 }
 
 // The x-major fill: CTAs take tasks (work-balanced ranges of fill-plan slots),
-// each slot range grouped by scanned vertex x; per x the CTA loads x's list
-// into shared memory once and its warps take x's owner edges.
-__global__ void __launch_bounds__(kThreads, 1) k_tri_fill_x(TriArgs A) {
+// each slot range grouped by scanned vertex x; per x the CTA loads x's
+// position-ordered list into shared memory once and its warps take x's owner
+// edges (the next edge's validity words and records are prefetched to L2).
+__global__ void __launch_bounds__(512, 1) k_tri_fill_x(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* lk = reinterpret_cast<uint32_t*>(smem);
     uint32_t* lp = lk + A.lists_cap;
@@ -1148,6 +1233,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tri_fill_x(TriArgs A) {
     __shared__ unsigned s_next;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nthreads = blockDim.x;
+    for (int q = lane; q < kBmWords; q += 32) scratch[wid].rbits[q] = 0u;
     for (;;) {
         if (threadIdx.x == 0) {
             const int64_t task = A.task_lo + (int64_t)atomicAdd(A.task_counter, 1ull);
@@ -1177,20 +1263,70 @@ __global__ void __launch_bounds__(kThreads, 1) k_tri_fill_x(TriArgs A) {
             const int64_t end = s_end;
             const uint64_t ox = A.off[x];
             const uint32_t degx = (uint32_t)(A.off[x + 1] - ox);
+            const uint32_t mis = (uint32_t)(ox & 3u);   // the lists are 16-byte aligned
             for (uint32_t t = threadIdx.x; t < degx; t += nthreads) {
                 lk[t] = A.nkr[ox + t];
                 lp[t] = A.np[ox + t];
             }
             __syncthreads();
-            for (;;) {
+            auto grab = [&]() -> int64_t {
                 unsigned my = 0;
                 if (lane == 0) my = atomicAdd(&s_next, 1u);
-                const int64_t e = seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
-                if (e >= end) break;
-                const uint4 pl = A.fplan[e];
-                const uint32_t p = pl.x, y = pl.y, len = pl.z;
-                if (len == 0 || (int64_t)p < A.p_lo || (int64_t)p >= A.p_hi) continue;
-                warp_fill_x(A, lk, lp, scratch + wid, p, y, x, len, degx, A.toff[p] - A.slot0, A.efilt[p]);
+                return seg + (int64_t)__shfl_sync(0xffffffffu, my, 0);
+            };
+            // software pipeline over x's owner edges: plans three ahead, the
+            // per-edge offsets two ahead, the L2 prefetch of the validity
+            // words and records one ahead of the edge being filled
+            struct Meta {
+                uint64_t t0, tbo, reco;
+                uint32_t count, filt;
+            };
+            auto plan_of = [&](int64_t e) -> uint4 {
+                uint4 pl = e < end ? A.fplan[e] : make_uint4(0, 0, 0, 0);
+                if ((int64_t)pl.x < A.p_lo || (int64_t)pl.x >= A.p_hi) pl.z = 0;
+                return pl;
+            };
+            auto meta_of = [&](const uint4& pl) -> Meta {
+                Meta m{0, 0, 0, 0, 0};
+                if (pl.z) {
+                    m.t0 = A.toff[pl.x];
+                    m.count = (uint32_t)(A.toff[pl.x + 1] - m.t0);
+                    m.filt = A.efilt[pl.x];
+                    m.tbo = A.tb_off[pl.x];
+                    m.reco = A.rec_off[pl.x];
+                }
+                return m;
+            };
+            auto prefetch = [&](const uint4& pl, const Meta& m) {
+                if (!pl.z || !m.count) return;
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.tb + m.tbo) & ~(uintptr_t)127;
+                const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.tb + m.tbo + rec_steps(pl.z, mis));
+                for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a < a1; a += 128 * 32)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                const uintptr_t b0 = reinterpret_cast<uintptr_t>(A.rec + m.reco) & ~(uintptr_t)127;
+                const uintptr_t b1 = reinterpret_cast<uintptr_t>(A.rec + m.reco + m.count);
+                for (uintptr_t a = b0 + 128 * (uintptr_t)lane; a < b1; a += 128 * 32)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+            };
+            int64_t e0 = grab();
+            uint4 pl0 = plan_of(e0);
+            int64_t e1 = grab();
+            uint4 pl1 = plan_of(e1);
+            int64_t e2 = grab();
+            uint4 pl2 = plan_of(e2);
+            Meta m0 = meta_of(pl0), m1 = meta_of(pl1);
+            prefetch(pl0, m0);
+            while (e0 < end) {
+                const int64_t e3 = grab();
+                const uint4 pl3 = plan_of(e3);
+                const Meta m2 = meta_of(pl2);
+                prefetch(pl1, m1);
+                if (pl0.z && m0.count)
+                    warp_fill_x(A, lk, lp, scratch + wid, pl0.x, pl0.y, x, pl0.z, degx, mis, m0.t0 - A.slot0,
+                                m0.count, m0.filt);
+                e0 = e1; pl0 = pl1; m0 = m1;
+                e1 = e2; pl1 = pl2; m1 = m2;
+                e2 = e3; pl2 = pl3;
             }
             __syncthreads();
             seg = end;
@@ -1199,7 +1335,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tri_fill_x(TriArgs A) {
 }
 
 template <bool kFill, bool kPacked, int kBm>
-__global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2), 1) k_triangles(TriArgs A) {
+__global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2),
+                                   (!kFill && kBm == 3) ? 2 : 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
@@ -1519,20 +1656,25 @@ void count_triangles_bm(const Graph& g, uint32_t* cnt, uint32_t* bm, const uint6
 }
 
 namespace {
-__global__ void k_rec_words(const uint32_t* __restrict__ scan_len, int64_t E, int64_t p_lo, int64_t p_hi,
+__global__ void k_rec_words(const uint32_t* __restrict__ scan_len, const uint32_t* __restrict__ scan_v,
+                            const uint64_t* __restrict__ off, int64_t E, int64_t p_lo, int64_t p_hi,
                             uint32_t* __restrict__ nrec, uint32_t* __restrict__ nwords) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t len = (p >= p_lo && p < p_hi) ? scan_len[p] : 0u;
-        nrec[p] = len;
-        nwords[p] = (len + 31u) >> 5;
+        nrec[p] = len;   // capacity: a record per candidate at most
+        nwords[p] = len ? rec_steps(len, (uint32_t)(off[scan_v[p]] & 3u)) : 0u;
     }
 }
 }  // namespace
 
 // The x-major path is an experiment (VRB_TRI_PATH=xmajor): correct, but
-// measured slower than the apex-bitmap path on C5B (count 16.7 ms against
-// 9.0, fill 45.4 against 22.5) -- the fill touches
-// every candidate twice instead of only the valid apexes.
+// measured slower than the apex-bitmap path on C5B (round 2, second version:
+// ballot-compacted records, arrival lists, a 3-deep software pipeline and L2
+// prefetch in the fill -- count 12.6 ms against 9.0, fill 30.0 against 22.5;
+// C3 fill 30.6 against 8.9, most of its edges exceeding a 1024-slot window).
+// Both fills are bound by per-owner-edge work (ncu: 14.0e9 instructions for
+// 9.7e6 edges and 2.0e9 triangles), not by the gathers the x-major layout
+// removes.
 bool records_apply(const Graph& g) {
     const char* m = std::getenv("VRB_TRI_PATH");
     return g.packed && g.idl.get() && g.max_deg <= kApexBitmapMaxDeg && m && m[0] == 'x';
@@ -1548,7 +1690,7 @@ void count_triangles_rec(const Graph& g, const uint32_t* ev, int64_t p_lo, int64
     {
         DBuf<uint32_t> a(E, s), b(E, s);
         k_rec_words<<<(unsigned)std::min<int64_t>(ceil_div(E, 256), (int64_t)device_sm_count() * 16), 256, 0, s>>>(
-            g.scan_len.get(), E, p_lo, p_hi, a.get(), b.get());
+            g.scan_len.get(), g.scan_v.get(), g.off.get(), E, p_lo, p_hi, a.get(), b.get());
         VRB_LAUNCH_CHECK();
         exclusive_scan(a.get(), R.rec_off.get(), E, s);
         exclusive_scan(b.get(), R.tb_off.get(), E, s);
@@ -1596,7 +1738,7 @@ void fill_triangles_x(const Graph& g, const TriRecords& R, const uint32_t* efilt
     const size_t lists = (size_t)8 * A.lists_cap;
     const int64_t avail = (int64_t)device_max_smem_optin() - (int64_t)lists - 1024;
     const char* fw = std::getenv("VRB_TRI_FILL_WARPS");
-    int warps = (int)std::min<int64_t>(fw ? std::max(4, std::min(kWarps, std::atoi(fw))) : kWarps,
+    int warps = (int)std::min<int64_t>(fw ? std::max(4, std::min(16, std::atoi(fw))) : 16,
                                        avail / (int64_t)sizeof(WarpScratchX));
     if (warps < 4) fail(VRB_ENOTSUP, "x-major triangle fill: degree %u leaves no shared memory", g.max_deg);
     const int threads = warps * 32;

@@ -629,7 +629,7 @@ def test_full_size_c4_tetrahedra(vrb):
 @pytest.mark.parametrize("path", ["xmajor", "markfill", "bitmap"])
 @pytest.mark.parametrize("case", range(4))
 def test_triangle_path_variants(vrb, case, path, monkeypatch):
-    # the experimental triangle paths (VRB_TRI_PATH=xmajor / markfill) must be
+    # every triangle path (VRB_TRI_PATH=xmajor / markfill / bitmap) must be
     # as exact as the default one
     monkeypatch.setenv("VRB_TRI_PATH", path)
     X, maxdim, radius = [(workloads.random_cloud(21, 300, 4, "gauss"), 1, 1.8),
