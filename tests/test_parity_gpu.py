@@ -308,6 +308,20 @@ def test_edge_sort_high_bit_runs_fallback(vrb):
         compare(vrb, X, 1, 1.0 + 1e-9)
 
 
+@pytest.mark.parametrize("m", [20, 50])
+def test_edge_sort_high_bit_runs_with_ties(vrb, m):
+    # as above, every ring point twice: each run of equal high bits mixes
+    # equal lengths (a dense-rank level of 2+ edges) with distinct ones, so
+    # the fused ranking pass must count distinct keys per run and keep equal
+    # keys in (i, j) order
+    theta = np.linspace(0.0, 2.0 * np.pi, m, endpoint=False)
+    rad = 1.0 + np.arange(m)[::-1] * 1e-12
+    ring = np.stack([rad * np.cos(theta), rad * np.sin(theta)], axis=1)
+    X = np.concatenate([np.zeros((1, 2)), ring, ring[::-1], [[1000.0, 0.0]]])
+    compare(vrb, X, 0, math.inf)
+    compare(vrb, X, 1, 1.0 + 1e-9)
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_global_host_map_forced(vrb, monkeypatch, seed):
     # the host map in global memory (used when n is too large for shared
