@@ -266,6 +266,97 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
     }
 }
 
+// Full filtration (r = inf, inclusive): every pair j > i is kept and the lex
+// slot of (i, j) is closed-form, so one register-tiled pass computes and
+// writes them (4 x 4 pairs per thread: 8 shared loads per coordinate serve
+// 16 folds, as in k_dist_mask).  The fold is the same RN sequence
+// (t = x_ic - x_jc; acc = acc + t * t; len = sqrt(acc)).  The pass also
+// reduces min / max / OR of the length bits for the edge sort (key_range).
+__global__ void __launch_bounds__(kThreads) k_dist_full(const double* __restrict__ X, int64_t n, int d, int64_t nt,
+                                                        uint64_t* __restrict__ key, uint32_t* __restrict__ ei,
+                                                        uint32_t* __restrict__ ej, uint32_t* __restrict__ pij,
+                                                        int64_t ti_lo, int64_t ti_hi, int64_t mask_base,
+                                                        unsigned long long* __restrict__ range) {
+    int64_t ti, tj;
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    __shared__ double sA[kDC][kT];
+    __shared__ double sB[kDC][kT];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = ti * kT, j0 = tj * kT;
+    const int64_t row_lo = ti_lo * kT;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int c0 = 0; c0 < d; c0 += kDC) {
+        const int dc = min(kDC, d - c0);
+        __syncthreads();
+        for (int q = threadIdx.x; q < kT * kDC; q += kThreads) {
+            const int r = q / kDC, c = q % kDC;
+            double va = 0.0, vb = 0.0;
+            if (c < dc) {
+                if (i0 + r < n) va = X[(i0 + r) * d + c0 + c];
+                if (j0 + r < n) vb = X[(j0 + r) * d + c0 + c];
+            }
+            sA[c][r] = va;
+            sB[c][r] = vb;
+        }
+        __syncthreads();
+        for (int c = 0; c < dc; ++c) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { a[q] = sA[c][ty + 16 * q]; b[q] = sB[c][tx + 16 * q]; }
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double t = __dsub_rn(a[p], b[q]);
+                    acc[p][q] = __dadd_rn(acc[p][q], __dmul_rn(t, t));
+                }
+        }
+    }
+    uint64_t mn = ~0ull, mx = 0ull, orr = 0ull;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int64_t i = i0 + ty + 16 * p;
+        if (i >= n) continue;
+        // row i starts at lex slot i n - i (i + 1) / 2 (less the block's first row)
+        const uint64_t rbase = (uint64_t)(i * n - i * (i + 1) / 2 - (row_lo * n - row_lo * (row_lo + 1) / 2));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t j = j0 + tx + 16 * q;
+            if (j <= i || j >= n) continue;
+            const uint64_t bits = (uint64_t)__double_as_longlong(__dsqrt_rn(acc[p][q]));
+            const uint64_t slot = rbase + (uint64_t)(j - i - 1);
+            __stcs(reinterpret_cast<unsigned long long*>(key + slot), (unsigned long long)bits);
+            if (pij) {
+                __stcs(pij + slot, ((uint32_t)i << 16) | (uint32_t)j);
+            } else {
+                ei[slot] = (uint32_t)i;
+                ej[slot] = (uint32_t)j;
+            }
+            mn = bits < mn ? bits : mn;
+            mx = bits > mx ? bits : mx;
+            orr |= bits;
+        }
+    }
+    if (range) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t a = __shfl_down_sync(0xffffffffu, mn, o), b = __shfl_down_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+            orr |= __shfl_down_sync(0xffffffffu, orr, o);
+        }
+        if ((threadIdx.x & 31) == 0 && orr | mx) {
+            atomicMin(&range[0], (unsigned long long)mn);
+            atomicMax(&range[1], (unsigned long long)mx);
+            atomicOr(&range[2], (unsigned long long)orr);
+        }
+    }
+}
+
 __global__ void k_check_points(const double* __restrict__ X, int64_t total, int* bad) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
          q += (int64_t)gridDim.x * blockDim.x)
@@ -505,8 +596,12 @@ void build_kept_edges(const double* X, int64_t n, int d, double radius, bool str
             out.ej.alloc(E, s);
         }
         if (E == 0) return;
-        k_dist_fill<<<grid, kThreads, 0, s>>>(X, n, d, nt, nullptr, nullptr, out.key.get(), out.ei.get(),
-                                              out.ej.get(), out.pij.get(), ti_lo, ti_hi, mask_base);
+        // the key range (min, max, OR of the length bits) comes with the pass
+        out.range.alloc(3, s);
+        const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+        VRB_CUDA(cudaMemcpyAsync(out.range.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_dist_full<<<grid, kThreads, 0, s>>>(X, n, d, nt, out.key.get(), out.ei.get(), out.ej.get(), out.pij.get(),
+                                              ti_lo, ti_hi, mask_base, out.range.get());
         VRB_LAUNCH_CHECK();
         return;
     }

@@ -289,12 +289,17 @@ __global__ void k_fixup_runs(uint64_t* __restrict__ key, uint32_t* __restrict__ 
 }
 
 // Sort the kept edges by (len, i, j): a stable radix sort of the length bits
-// (the input is in lex order).  Results: so.key[q] + so.bias = length bits of
-// the q-th edge, so.val[q] = its packed (i, j) (ke.packed) or lex index.
-void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so) {
+// (the input is in lex order), on the 4 highest varying digits only.  Results:
+// so.key[q] + so.bias = length bits of the q-th edge, so.val[q] = its packed
+// (i, j) (ke.packed) or lex index.  *shift_out > 0: the keys are ordered by
+// (key >> shift) only -- runs of equal high bits still need their full-key
+// order (k_fixup_runs, or the fused ranking pass).
+static void sort_edges_top(KeptEdges& ke, cudaStream_t s, SortedEdges& so, int* shift_out, bool* alt_out) {
     const int64_t E = ke.E;
     so.E = E;
     so.packed = ke.packed;
+    *shift_out = 0;
+    *alt_out = false;
     if (E == 0) return;
     DBuf<uint64_t>& key_alt = so.key_alt;
     key_alt.alloc(E, s);
@@ -310,55 +315,340 @@ void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so) {
     }
     // sort (len bits - min): only the digits of (max - min) vary
     uint64_t kmin = 0;
-    const uint64_t vary = key_range(ke.key.get(), E, s, &kmin);
+    const uint64_t vary = key_range(ke.key.get(), E, s, &kmin, ke.range.get());
     // radix passes on the 4 highest varying digits only (~31+ significant
-    // bits); the few runs left with equal high bits are finished in place
+    // bits); the runs left with equal high bits are finished afterwards
     int hi_digit = -1;
     for (int dg = 7; dg >= 0; --dg)
         if ((vary >> (8 * dg)) & 0xFFull) { hi_digit = dg; break; }
     const int shift = hi_digit >= VRB_EDGE_TOP_DIGITS ? 8 * (hi_digit - (VRB_EDGE_TOP_DIGITS - 1)) : 0;
     const uint64_t vary_top = shift ? (vary & ~((1ull << shift) - 1ull)) : vary;
     bool biased = false;
-    bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary_top, s, kmin, &biased);
-    const uint64_t bias = biased ? kmin : 0ull;
-    if (shift && (vary & ((1ull << shift) - 1ull))) {   // varying bits below the sorted digits
-        uint64_t* k1 = alt ? key_alt.get() : ke.key.get();
-        uint32_t* v1 = alt ? perm_alt.get() : vals;
-        DBuf<int> fb(1, s);
-        VRB_CUDA(cudaMemsetAsync(fb.get(), 0, sizeof(int), s));
-        k_fixup_runs<<<grid_for(E, 256), 256, 0, s>>>(k1, v1, E, shift, fb.get());
-        VRB_LAUNCH_CHECK();
-        int h = 0;
-        VRB_CUDA(cudaMemcpyAsync(&h, fb.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-        VRB_CUDA(cudaStreamSynchronize(s));
-        if (h) {   // heavy clustering of the high bits: complete the sort on every digit
-            uint64_t* k2 = alt ? ke.key.get() : key_alt.get();
-            uint32_t* v2 = alt ? vals : perm_alt.get();
-            const bool alt2 = radix_sort_pairs(k1, k2, v1, v2, E, vary, s);
-            if (alt2) alt = !alt;
-        }
-    }
+    const bool alt = radix_sort_pairs(ke.key.get(), key_alt.get(), vals, perm_alt.get(), E, vary_top, s, kmin, &biased);
     so.key = alt ? key_alt.get() : ke.key.get();
     so.val = alt ? perm_alt.get() : vals;
-    so.bias = bias;
+    so.bias = biased ? kmin : 0ull;
+    *shift_out = (shift && (vary & ((1ull << shift) - 1ull))) ? shift : 0;   // varying bits below the sorted digits
+    *alt_out = alt;
 }
+
+// Complete the order by a full-key radix sort (the fallback when a run of
+// equal high bits is too long for the in-place fix-up).
+static void sort_edges_full(KeptEdges& ke, cudaStream_t s, SortedEdges& so, bool alt) {
+    const int64_t E = ke.E;
+    uint64_t* k1 = const_cast<uint64_t*>(so.key);
+    uint32_t* v1 = const_cast<uint32_t*>(so.val);
+    uint32_t* vals0 = ke.packed ? ke.pij.get() : so.perm.get();
+    uint64_t* k2 = alt ? ke.key.get() : so.key_alt.get();
+    uint32_t* v2 = alt ? vals0 : so.perm_alt.get();
+    const uint64_t vary = varying_bits(k1, E, s);
+    const bool alt2 = radix_sort_pairs(k1, k2, v1, v2, E, vary, s);
+    if (alt2) {
+        so.key = k2;
+        so.val = v2;
+    }
+}
+
+void sort_edges(KeptEdges& ke, cudaStream_t s, SortedEdges& so) {
+    int shift = 0;
+    bool alt = false;
+    sort_edges_top(ke, s, so, &shift, &alt);
+    if (!shift) return;
+    const int64_t E = ke.E;
+    DBuf<int> fb(1, s);
+    VRB_CUDA(cudaMemsetAsync(fb.get(), 0, sizeof(int), s));
+    k_fixup_runs<<<grid_for(E, 256), 256, 0, s>>>(const_cast<uint64_t*>(so.key), const_cast<uint32_t*>(so.val), E,
+                                                  shift, fb.get());
+    VRB_LAUNCH_CHECK();
+    int h = 0;
+    VRB_CUDA(cudaMemcpyAsync(&h, fb.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaStreamSynchronize(s));
+    if (h) sort_edges_full(ke, s, so, alt);   // heavy clustering of the high bits: every digit
+}
+
+namespace {
+// Fused S3 epilogue (one pass over the high-bit-sorted keys, in place of the
+// run fix-up, the two-pass head-flag scan and the output kernel).  A tile
+// of 2048 positions is staged in shared memory with halos; every run of
+// equal high bits (C5A: 47% of the edges sit in runs of 2..10) is put in
+// full-key order by ranking each item within its run (stable: equal keys
+// keep their lex order) -- a run belongs to the tile it starts in, a run
+// longer than kRkRunMax must hold equal keys (its order stands; otherwise
+// the caller re-sorts).  Heads of equal-length runs are counted by warp
+// ballots, turned into dense ranks by a chained scan over tiles (decoupled
+// look-back, tiles taken in order), and each warp writes its positions'
+// (i, j), filt and value_of_rank in lane-consecutive (coalesced) rounds.
+constexpr int kRkThreads = 256;
+constexpr int kRkWarps = kRkThreads / 32;
+constexpr int kRkTile = 2048;
+constexpr int kRkRunMax = 64;
+constexpr int kRkHalo = kRkRunMax + 1;
+constexpr int kRkStage = kRkTile + 2 * kRkHalo;
+constexpr unsigned long long kRkAgg = 1ull << 62, kRkPre = 2ull << 62, kRkVal = (1ull << 62) - 1;
+
+struct RankArgs {
+    const uint64_t* key;   // + bias = length bits
+    const uint32_t* val;   // packed (i << 16 | j), or the lex index into ei / ej
+    int64_t E;
+    int shift;             // > 0: ordered only by key >> shift so far
+    uint64_t bias;
+    const uint32_t* ei;
+    const uint32_t* ej;    // null when packed
+    uint32_t* ev;
+    uint32_t* efilt;
+    double* vor;
+    unsigned long long* status;
+    unsigned* tile_counter;
+    int* fallback;
+};
+
+__device__ __forceinline__ uint2 edge_of(const RankArgs& A, uint32_t v) {
+    return A.ej ? make_uint2(__ldg(A.ei + v), __ldg(A.ej + v)) : make_uint2(v >> 16, v & 0xFFFFu);
+}
+
+__global__ void __launch_bounds__(kRkThreads) k_rank_edges(RankArgs A) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_wtot[kRkWarps];
+    __shared__ unsigned long long s_prefix;
+    __shared__ unsigned s_own_lo, s_own_hi;         // owned positions, relative to t0
+    __shared__ uint64_t s_key[kRkStage];            // window [t0 - halo, t1 + halo), as sorted so far
+    __shared__ uint32_t s_val[kRkStage];
+    __shared__ uint16_t s_perm[kRkTile + kRkHalo];  // owned positions (from t0) -> window index
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(A.tile_counter, 1u);
+        s_own_lo = 0xFFFFFFFFu;
+        s_own_hi = 0u;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t E = A.E;
+    const int sh = A.shift;
+    const int64_t t0 = (int64_t)tile * kRkTile;
+    const int64_t wb = t0 - kRkHalo;                 // window base (may be negative)
+    const int t1r = (int)(min(t0 + kRkTile, E) - t0);   // tile length
+    const int h0r = (int)(max(t0 - kRkHalo, (int64_t)0) - wb), h1r = (int)(min(t0 + kRkTile + kRkHalo, E) - wb);
+    for (int w = h0r + threadIdx.x; w < h1r; w += kRkThreads) {
+        s_key[w] = __ldcs(A.key + wb + w);
+        s_val[w] = __ldcs(A.val + wb + w);
+    }
+    __syncthreads();
+    const int T0 = kRkHalo, T1 = kRkHalo + t1r;      // the tile in window coordinates
+    // ---- final places (s_perm) of the owned items
+    unsigned my_lo = 0xFFFFFFFFu, my_hi = 0u;
+    for (int w = T0 + threadIdx.x; w < h1r; w += kRkThreads) {
+        const uint64_t kq = s_key[w];
+        if (!sh) {   // fully sorted: every item in place
+            if (w < T1) {
+                s_perm[w - T0] = (uint16_t)w;
+                my_lo = min(my_lo, (unsigned)(w - T0));
+                my_hi = max(my_hi, (unsigned)(w - T0 + 1));
+            }
+            continue;
+        }
+        const uint64_t top = kq >> sh;
+        const int64_t q = wb + w;
+        const bool starts = q == 0 || (s_key[w - 1] >> sh) != top;
+        const bool ends = q + 1 >= E || (w + 1 < h1r ? (s_key[w + 1] >> sh) : (A.key[q + 1] >> sh)) != top;
+        if (starts && ends) {   // a run of one (the common case)
+            if (w < T1) {
+                s_perm[w - T0] = (uint16_t)w;
+                my_lo = min(my_lo, (unsigned)(w - T0));
+                my_hi = max(my_hi, (unsigned)(w - T0 + 1));
+            }
+            continue;
+        }
+        int rs = w, re = w + 1;
+        bool lng = false;
+        while (rs > h0r && (s_key[rs - 1] >> sh) == top) {
+            --rs;
+            if (w - rs >= kRkRunMax) { lng = true; break; }
+        }
+        if (!lng && rs >= T1) continue;   // a run of a later tile (long or short: not ours)
+        if (!lng) {
+            while (re < h1r && (s_key[re] >> sh) == top) {
+                ++re;
+                if (re - rs > kRkRunMax) { lng = true; break; }
+            }
+            if (!lng && re == h1r && wb + h1r < E && (A.key[wb + h1r] >> sh) == top) lng = true;
+        }
+        if (lng) {
+            // a long run: every key must be equal (then the lex order of the
+            // stable radix passes stands); otherwise the caller re-sorts
+            if ((w > h0r && (s_key[w - 1] >> sh) == top && s_key[w - 1] != kq) ||
+                (w + 1 < h1r && (s_key[w + 1] >> sh) == top && s_key[w + 1] != kq))
+                atomicOr(A.fallback, 1);
+            if (w < T1) {
+                s_perm[w - T0] = (uint16_t)w;
+                my_lo = min(my_lo, (unsigned)(w - T0));
+                my_hi = max(my_hi, (unsigned)(w - T0 + 1));
+            }
+            continue;
+        }
+        if (rs < T0) continue;   // a short run of an earlier tile
+        int pos = rs;
+        for (int a = rs; a < re; ++a) {
+            const uint64_t ka = s_key[a];
+            pos += (ka < kq || (ka == kq && a < w)) ? 1 : 0;
+        }
+        s_perm[pos - T0] = (uint16_t)w;
+        my_lo = min(my_lo, (unsigned)(w - T0));
+        my_hi = max(my_hi, (unsigned)(w - T0 + 1));
+    }
+    my_lo = __reduce_min_sync(0xffffffffu, my_lo);
+    my_hi = __reduce_max_sync(0xffffffffu, my_hi);
+    if (lane == 0) {
+        atomicMin(&s_own_lo, my_lo);
+        atomicMax(&s_own_hi, my_hi);
+    }
+    __syncthreads();
+    const int olo = s_own_lo == 0xFFFFFFFFu ? 0 : (int)s_own_lo;   // owned [olo, ohi), relative to t0
+    const int ohi = s_own_lo == 0xFFFFFFFFu ? 0 : (int)s_own_hi;
+    // ---- heads in the final order, per warp over a contiguous chunk of the
+    // owned positions (32 per round).  The position before olo holds the
+    // previous run's item: it differs in its high bits, or is equal within a
+    // long run, so the staged key (any order) decides.
+    const int nown = ohi - olo;
+    const int chunk = ((nown + kRkWarps - 1) / kRkWarps + 31) & ~31;
+    const int c0 = min(olo + wid * chunk, ohi), c1 = min(c0 + chunk, ohi);
+    auto key_final = [&](int r) -> uint64_t { return s_key[s_perm[r]]; };
+    auto head_at = [&](int r, uint64_t kq) -> bool {
+        const int64_t q = t0 + r;
+        if (q == 0) return true;
+        const uint64_t kp = r == olo ? (T0 + r - 1 >= h0r ? s_key[T0 + r - 1] : A.key[q - 1]) : key_final(r - 1);
+        return kq != kp;
+    };
+    uint32_t wheads = 0;
+    for (int r0 = c0; r0 < c1; r0 += 32) {
+        const int r = r0 + lane;
+        const bool h = r < c1 && head_at(r, key_final(r));
+        wheads += __popc(__ballot_sync(0xffffffffu, h));
+    }
+    if (lane == 0) s_wtot[wid] = wheads;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t v = lane < kRkWarps ? s_wtot[lane] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < kRkWarps; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, kRkWarps - 1);
+        volatile unsigned long long* st = A.status;
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0) st[0] = kRkPre | (unsigned long long)total;
+        } else {
+            if (lane == 0) st[tile] = kRkAgg | (unsigned long long)total;
+            // look-back: the warp reads 32 predecessors' status words at a time
+            int64_t j = (int64_t)tile - 1;
+            for (;;) {
+                const int64_t jj = j - lane;
+                unsigned long long sv = kRkPre;   // below tile 0: an inclusive prefix of 0
+                if (jj >= 0) {
+                    sv = st[jj];
+                    while ((sv & (kRkAgg | kRkPre)) == 0) sv = st[jj];
+                }
+                const unsigned pre = __ballot_sync(0xffffffffu, (sv & kRkPre) != 0);
+                const int first = pre ? __ffs(pre) - 1 : 32;   // nearest predecessor with a prefix
+                unsigned long long part = lane <= first ? (sv & kRkVal) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                excl += part;
+                if (pre) break;
+                j -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                st[tile] = kRkPre | (excl + total);
+            }
+        }
+        if (lane < kRkWarps) s_wtot[lane] = incl - v;   // exclusive per warp
+        if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    // ---- outputs: lane-consecutive rounds, ranks by ballot prefix counts
+    uint32_t run = (uint32_t)(s_prefix + s_wtot[wid]);
+    const unsigned lle = (2u << lane) - 1u;   // lanes <= this one
+    for (int r0 = c0; r0 < c1; r0 += 32) {
+        const int r = r0 + lane;
+        const bool in = r < c1;
+        const int w = in ? s_perm[r] : 0;
+        const uint64_t kq = in ? s_key[w] : 0ull;
+        const bool h = in && head_at(r, kq);
+        const unsigned b = __ballot_sync(0xffffffffu, h);
+        if (in) {
+            const uint32_t filt = run + __popc(b & lle);
+            if (h) A.vor[filt - 1] = __longlong_as_double((long long)(kq + A.bias));
+            const int64_t q = t0 + r;
+            __stcs(reinterpret_cast<uint2*>(A.ev) + q, edge_of(A, s_val[w]));
+            __stcs(A.efilt + q, filt);
+        }
+        run += __popc(b);
+    }
+}
+}  // namespace
 
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
     const int64_t E = ke.E;
     if (E == 0) return 0;
     SortedEdges so;
-    sort_edges(ke, s, so);
-    const uint64_t* skey = so.key;
-    const uint32_t* sval = so.val;
-    const uint64_t bias = so.bias;
-    dense_ranks(skey, efilt, E, s);   // heads + inclusive scan in one pass over the keys
-    if (ke.packed)
-        k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, efilt, E, reinterpret_cast<uint2*>(ev),
-                                                               vor, bias);
-    else
-        k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(skey, sval, ke.ei.get(), ke.ej.get(), efilt, E, ev, vor,
-                                                        bias);
-    VRB_LAUNCH_CHECK();
+    const char* un = std::getenv("VRB_EDGE_UNFUSED");   // experiment knob: the three-kernel epilogue
+    if (un && un[0] == '1') {
+        sort_edges(ke, s, so);
+        dense_ranks(so.key, efilt, E, s);
+        if (ke.packed)
+            k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(so.key, so.val, efilt, E,
+                                                                   reinterpret_cast<uint2*>(ev), vor, so.bias);
+        else
+            k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(so.key, so.val, ke.ei.get(), ke.ej.get(), efilt, E, ev,
+                                                            vor, so.bias);
+        VRB_LAUNCH_CHECK();
+    } else {
+        int shift = 0;
+        bool alt = false;
+        sort_edges_top(ke, s, so, &shift, &alt);
+        const int64_t tiles = ceil_div(E, kRkTile);
+        DBuf<unsigned long long> status(tiles, s);
+        DBuf<unsigned> counter(1, s);
+        DBuf<int> fb(1, s);
+        VRB_CUDA(cudaMemsetAsync(status.get(), 0, tiles * sizeof(unsigned long long), s));
+        VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned), s));
+        VRB_CUDA(cudaMemsetAsync(fb.get(), 0, sizeof(int), s));
+        RankArgs A{};
+        A.key = so.key;
+        A.val = so.val;
+        A.E = E;
+        A.shift = shift;
+        A.bias = so.bias;
+        A.ei = ke.packed ? nullptr : ke.ei.get();
+        A.ej = ke.packed ? nullptr : ke.ej.get();
+        A.ev = ev;
+        A.efilt = efilt;
+        A.vor = vor;
+        A.status = status.get();
+        A.tile_counter = counter.get();
+        A.fallback = fb.get();
+        k_rank_edges<<<(unsigned)tiles, kRkThreads, 0, s>>>(A);
+        VRB_LAUNCH_CHECK();
+        int h = 0;
+        VRB_CUDA(cudaMemcpyAsync(&h, fb.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        VRB_CUDA(cudaStreamSynchronize(s));
+        if (h) {
+            // a run of equal high bits too long for the in-place sort: complete
+            // the order on every digit, then the three-kernel epilogue
+            sort_edges_full(ke, s, so, alt);
+            dense_ranks(so.key, efilt, E, s);
+            if (ke.packed)
+                k_edge_outputs_packed<<<grid_for(E, 256), 256, 0, s>>>(so.key, so.val, efilt, E,
+                                                                       reinterpret_cast<uint2*>(ev), vor, so.bias);
+            else
+                k_edge_outputs<<<grid_for(E, 256), 256, 0, s>>>(so.key, so.val, ke.ei.get(), ke.ej.get(), efilt, E,
+                                                                ev, vor, so.bias);
+            VRB_LAUNCH_CHECK();
+        }
+    }
     uint32_t nvals = 0;
     VRB_CUDA(cudaMemcpyAsync(&nvals, efilt + E - 1, sizeof(nvals), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));

@@ -188,16 +188,20 @@ uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s) {
     return (uint64_t)h;
 }
 
-uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin) {
+uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin,
+                   const unsigned long long* reduced) {
     *kmin = 0;
     if (n <= 0) return 0;
-    DBuf<unsigned long long> acc(3, s);
-    const unsigned long long init[3] = {~0ull, 0ull, 0ull};
-    VRB_CUDA(cudaMemcpyAsync(acc.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
-    k_minmax<<<grid_for(n, 256), 256, 0, s>>>(keys, n, acc.get());
-    VRB_LAUNCH_CHECK();
+    DBuf<unsigned long long> acc;
+    if (!reduced) {
+        acc.alloc(3, s);
+        const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+        VRB_CUDA(cudaMemcpyAsync(acc.get(), init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_minmax<<<grid_for(n, 256), 256, 0, s>>>(keys, n, acc.get());
+        VRB_LAUNCH_CHECK();
+    }
     unsigned long long h[3] = {0, 0, 0};
-    VRB_CUDA(cudaMemcpyAsync(h, acc.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    VRB_CUDA(cudaMemcpyAsync(h, reduced ? reduced : acc.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     *kmin = h[0];
     uint64_t d = h[1] - h[0], mask = 0;

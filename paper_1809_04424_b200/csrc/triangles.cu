@@ -592,7 +592,10 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 #define VRB_TRI_COUNT_WARPS 16
 #endif
 constexpr int kBmWords = (int)(kApexBitmapMaxDeg / 32);
-constexpr int kWinB = 512;
+#ifndef VRB_WINB
+#define VRB_WINB 512
+#endif
+constexpr int kWinB = VRB_WINB;   // slots per window of the bitmap fill
 struct WarpScratchC {              // count
     uint32_t bits[kBmWords];
 };
@@ -686,11 +689,19 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         if (A.debug != 2) {
             const uint64_t s0 = slot + w0;
             // one triangle: slot j of the window, (k, pos(x, k)) gathered
+            const uint32_t vlo = min(x, y), vhi = max(x, y);
             auto tri = [&](uint32_t j, uint2 kp, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0,
                            uint32_t& r1) {
                 const uint32_t k = kp.x, px = kp.y, py = map[k];
+#ifdef VRB_SORT3
                 a0 = y; a1 = x; a2 = k;
                 sort3(a0, a1, a2);
+#else
+                // the owner edge's ends are fixed: place the apex among them
+                a0 = k < vlo ? k : vlo;
+                a1 = k < vlo ? vlo : (k < vhi ? k : vhi);
+                a2 = k < vhi ? vhi : k;
+#endif
                 r0 = min(px, py);
                 r1 = max(px, py);
                 __stcs(A.tf + s0 + j, filt);

@@ -125,7 +125,8 @@ uint64_t varying_bits(const uint64_t* keys, int64_t n, cudaStream_t s);
 
 // (max - min) of the keys as a bit mask of its length (every key - min fits
 // in it); *kmin = min.  A sort of (key - kmin) needs only those digits.
-uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin);
+uint64_t key_range(const uint64_t* keys, int64_t n, cudaStream_t s, uint64_t* kmin,
+                   const unsigned long long* reduced = nullptr);
 
 // Stable ascending LSD radix sort of (keys, vals) on the bit range [0, 64)
 // restricted to the 8-bit digits that contain a bit of `varying`.  Uses

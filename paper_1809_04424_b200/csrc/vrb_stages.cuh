@@ -22,6 +22,7 @@ struct KeptEdges {
     DBuf<uint64_t> key;   // bit pattern of len (non-negative doubles order as u64)
     bool packed = false;  // n <= 65536: (i << 16 | j) in pij, else i, j in ei, ej
     DBuf<uint32_t> ei, ej, pij;
+    DBuf<unsigned long long> range;   // when set: min, max, OR of the key bits (reduced by the distance pass)
 };
 // Rows [row_lo, row_hi) only (a rank's row block; row_lo and row_hi < n
 // multiples of edge_tile(); row_hi = -1: to n): their pairs j > i.
