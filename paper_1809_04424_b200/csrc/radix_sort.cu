@@ -31,6 +31,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef VRB_SORT_MINB
 #define VRB_SORT_MINB 4
 #endif
+#ifndef VRB_SORT_BALLOT
+#define VRB_SORT_BALLOT 0
+#endif
 #ifndef VRB_SORT_LOOK
 #define VRB_SORT_LOOK 4
 #endif
@@ -127,7 +130,23 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
         const int64_t i = base + r * 32 + lane;
         const bool ok = i < n;
         const uint32_t dg = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : (uint32_t)(kBins + lane);
+#if VRB_SORT_BALLOT
+        // experiment (VRB_SORT_BALLOT=1): peers by one ballot per digit bit
+        // (and one for the past-the-end lanes, whose digits are unique)
+        // instead of match.any -- measured slower for the edge sort (C5A
+        // edge rank 12.7 -> 13.6 ms), slightly faster for HIV's keys-only
+        // tie sort with 3 CTAs per SM (14.5 -> 14.0 ms)
+        uint32_t peers = __ballot_sync(0xffffffffu, ok);
+        if (!ok) peers = ~peers;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const bool bit = (dg >> b) & 1u;
+            const uint32_t vote = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? vote : ~vote;
+        }
+#else
         const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+#endif
         const uint32_t before = ok ? S.woff[wid][dg] : 0u;
         __syncwarp();
         rk[r] = before + __popc(peers & lt);
