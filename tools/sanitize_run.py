@@ -46,6 +46,17 @@ os.environ.pop("VRB_FORCE_SPARSE_TETS")
 H = workloads.hamming_matrix(workloads.hamming_sequences(3, n=140, length=120, clades=4))
 vrb.build_dm(H, maxdim=1, radius=math.inf)
 vrb.build_dm(H, maxdim=2, radius=60.0)
+# round 2, second session: the x-major triangle path; the fused edge
+# epilogue over several tiles with runs of equal high bits (tied and
+# distinct lengths) and a fallback run longer than 64
+os.environ["VRB_TRI_PATH"] = "xmajor"
+vrb.build(workloads.random_cloud(11, 300, 4, "gauss"), maxdim=1, radius=1.8)
+os.environ.pop("VRB_TRI_PATH")
+for m in (50, 150):
+    theta = np.linspace(0.0, 2.0 * np.pi, m, endpoint=False)
+    rad = 1.0 + np.arange(m)[::-1] * 1e-12
+    ring = np.stack([rad * np.cos(theta), rad * np.sin(theta)], axis=1)
+    vrb.build(np.concatenate([np.zeros((1, 2)), ring, ring[::-1], [[1000.0, 0.0]]]), maxdim=1, radius=math.inf)
 vrb.latlon2euc(torch.rand(100, 2, dtype=torch.float64, device="cuda") * 90)
 vrb.sortperm_f64(torch.randn(5000, dtype=torch.float64, device="cuda"))
 cp = torch.tensor([0, 2, 3], dtype=torch.int64, device="cuda")
