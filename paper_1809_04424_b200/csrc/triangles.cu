@@ -642,16 +642,20 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
     return __reduce_add_sync(0xffffffffu, c);
 }
 
-template <bool kSmemBits = false>
+// known_count: the edge's triangle count when the caller has it (toff), else
+// ~0u; a count within one window takes a walk with no window tests
+template <bool kSmemBits = false, bool kApex = true>
 __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* __restrict__ map,
                                              WarpScratchB* __restrict__ W, uint32_t p, uint32_t y, uint32_t x,
                                              uint64_t offx, uint32_t degx, uint64_t bmo, uint64_t slot,
-                                             uint32_t filt, const uint32_t* smem_bits = nullptr) {
+                                             uint32_t filt, const uint32_t* smem_bits = nullptr,
+                                             uint32_t known_count = ~0u) {
     const int lane = threadIdx.x & 31;
     const uint32_t nw = (degx + 31) >> 5;
     const uint32_t nchunks = (nw + 31) >> 5;
     const uint32_t* __restrict__ in = kSmemBits ? smem_bits : A.bm + bmo;
     const uint2* __restrict__ idx = A.idl + (A.debug == 3 ? 0 : offx);   // debug 3: ablation, one hot list
+    if (known_count == 0) return;
     // Windows of kWinB slots.  Each pass walks the bitmap in chunks of 32
     // words held in registers (lane = word): a warp scan of the popcounts
     // gives every word's first slot, and each lane stages the ranks of its
@@ -659,6 +663,7 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
     uint32_t count = 0;
     for (uint32_t w0 = 0; w0 == 0 || w0 < count; w0 += kWinB) {
         const uint32_t w1 = w0 + kWinB;
+        const bool one_window = known_count <= (uint32_t)kWinB;
         uint32_t carry = 0;
         for (uint32_t ch = 0; ch < nchunks; ++ch) {
             if (w0 > 0 && carry >= w1) break;
@@ -673,7 +678,13 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
             }
             uint32_t s = carry + incl - c;
             carry += __shfl_sync(0xffffffffu, incl, 31);
-            if (s < w1 && s + c > w0) {
+            if (one_window) {   // every slot is in the window
+                const uint32_t base = 32 * wd;
+                while (b) {
+                    W->rec[s++] = (uint16_t)(base + (uint32_t)(__ffs(b) - 1));
+                    b &= b - 1;
+                }
+            } else if (s < w1 && s + c > w0) {
                 while (b) {
                     const int bit = __ffs(b) - 1;
                     b &= b - 1;
@@ -705,7 +716,7 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
                 r0 = min(px, py);
                 r1 = max(px, py);
                 __stcs(A.tf + s0 + j, filt);
-                if (A.apex) A.apex[s0 + j] = (uint16_t)k;
+                if (kApex && A.apex) A.apex[s0 + j] = (uint16_t)k;
             };
             auto scalar = [&](uint32_t j, uint2 kp) {
                 uint32_t a0, a1, a2, r0, r1;
@@ -1419,10 +1430,19 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
             uint64_t off0 = pl0.z ? A.off[pl0.y] : 0, off1 = pl1.z ? A.off[pl1.y] : 0;
             uint64_t slot0 = 0, slot1 = 0;
             uint32_t filt0 = 0, filt1 = 0;
+            uint32_t tc0 = 0, tc1 = 0;     // the pipelined edges' triangle counts
             uint64_t bmo0 = 0, bmo1 = 0;   // bitmap fill: word offsets of the pipelined edges' bitmaps
             if (kFill) {
-                if (pl0.z) { slot0 = A.toff[pl0.x] - A.slot0; filt0 = A.efilt[pl0.x]; }
-                if (pl1.z) { slot1 = A.toff[pl1.x] - A.slot0; filt1 = A.efilt[pl1.x]; }
+                if (pl0.z) {
+                    slot0 = A.toff[pl0.x] - A.slot0;
+                    tc0 = (uint32_t)(A.toff[pl0.x + 1] - A.toff[pl0.x]);
+                    filt0 = A.efilt[pl0.x];
+                }
+                if (pl1.z) {
+                    slot1 = A.toff[pl1.x] - A.slot0;
+                    tc1 = (uint32_t)(A.toff[pl1.x + 1] - A.toff[pl1.x]);
+                    filt1 = A.efilt[pl1.x];
+                }
                 if (kBm && kBm != 4) {
                     if (pl0.z) bmo0 = A.bmoff[e0];
                     if (pl1.z) bmo1 = A.bmoff[e1];
@@ -1431,7 +1451,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
             while (e0 < end) {
                 const int64_t e2 = grab();
                 const uint4 pl2 = plan_of(e2);
-                if (kBm && kBm != 4 && kFill && pl1.z) {
+                if (kBm && kBm != 4 && kFill && pl1.z && (kBm != 1 || tc1)) {
                     // pull the next edge's bitmap into L2 while this edge runs
                     const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.bm + bmo1) & ~(uintptr_t)127;
                     const uintptr_t a1 =
@@ -1452,7 +1472,12 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                         const uint32_t c = warp_count_tbm(A, map, p, off0, len, e0);
                         if (lane == 0) A.cnt[p] = c;
                     } else if constexpr (kBm && kFill) {
-                        warp_fill_bm(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0, filt0);
+                        if (A.apex)
+                            warp_fill_bm<false, true>(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0,
+                                                      filt0, nullptr, tc0);
+                        else
+                            warp_fill_bm<false, false>(A, map, scratch + wid, p, y, x, off0, pl0.w, bmo0, slot0,
+                                                       filt0, nullptr, tc0);
                     } else if constexpr (kBm) {
                         const uint32_t c = warp_count_bm(A, map, scratch + wid, p, off0, len, pl0.w, e0);
                         if (lane == 0) A.cnt[p] = c;
@@ -1471,14 +1496,15 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
                     }
                 }
                 uint64_t off2 = pl2.z ? A.off[pl2.y] : 0, slot2 = 0, bmo2 = 0;
-                uint32_t filt2 = 0;
+                uint32_t filt2 = 0, tc2 = 0;
                 if (kFill && pl2.z) {
                     slot2 = A.toff[pl2.x] - A.slot0;
+                    tc2 = (uint32_t)(A.toff[pl2.x + 1] - A.toff[pl2.x]);
                     filt2 = A.efilt[pl2.x];
                     if (kBm && kBm != 4) bmo2 = A.bmoff[e2];
                 }
-                e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1; bmo0 = bmo1;
-                e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2; bmo1 = bmo2;
+                e0 = e1; pl0 = pl1; off0 = off1; slot0 = slot1; filt0 = filt1; bmo0 = bmo1; tc0 = tc1;
+                e1 = e2; pl1 = pl2; off1 = off2; slot1 = slot2; filt1 = filt2; bmo1 = bmo2; tc1 = tc2;
             }
             __syncthreads();
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
