@@ -25,22 +25,32 @@ namespace {
 #endif
 constexpr int kThreads = VRB_SORT_THREADS;   // >= 256, a multiple of 32
 constexpr int kWarps = kThreads / 32;
-#ifndef VRB_SORT_ITEMS
-#define VRB_SORT_ITEMS 12
-#endif
 #ifndef VRB_SORT_MINB
 #define VRB_SORT_MINB 4
 #endif
 #ifndef VRB_SORT_BALLOT
 #define VRB_SORT_BALLOT 0
 #endif
+#ifndef VRB_SORT_MINB_KEYS
+#define VRB_SORT_MINB_KEYS 4
+#endif
 #ifndef VRB_SORT_LOOK
 #define VRB_SORT_LOOK 4
 #endif
 constexpr int kLook = VRB_SORT_LOOK;         // tiles read per look-back step
-constexpr int kItems = VRB_SORT_ITEMS;       // per thread
-constexpr int kTile = kThreads * kItems;     // 3072 items per tile
-constexpr int kWarpItems = 32 * kItems;      // contiguous items per warp
+// items per thread: (key, value) pairs 8, keys only 20 (B200 sweep: the
+// C5A edge sort 12.7 -> 12.4 ms at 8 instead of 12; HIV's keys-only tie
+// sort 14.5 -> 13.5 / 12.7 ms at 16 / 20)
+#ifndef VRB_SORT_ITEMS_PAIRS
+#define VRB_SORT_ITEMS_PAIRS 8
+#endif
+#ifndef VRB_SORT_ITEMS_KEYS
+#define VRB_SORT_ITEMS_KEYS 20
+#endif
+template <bool kVals>
+__host__ __device__ constexpr int items_per_thread() { return kVals ? VRB_SORT_ITEMS_PAIRS : VRB_SORT_ITEMS_KEYS; }
+template <bool kVals>
+__host__ __device__ constexpr int tile_items() { return kThreads * items_per_thread<kVals>(); }
 constexpr int kBins = 256;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
@@ -86,8 +96,8 @@ __global__ void k_scan_bins(unsigned long long* __restrict__ hist) {
 
 template <bool kVals>
 struct SweepSmem {
-    uint64_t key[kTile];
-    uint32_t val[kVals ? kTile : 1];
+    uint64_t key[tile_items<kVals>()];
+    uint32_t val[kVals ? tile_items<kVals>() : 1];
     uint32_t woff[kWarps][kBins];   // per-warp digit counts -> tile-local start per warp
     uint32_t tstart[kBins];         // tile-local start of each digit
     unsigned long long gstart[kBins];   // global position of the tile's run of each digit
@@ -97,7 +107,7 @@ struct SweepSmem {
 
 // kVals = false: keys only (vals_in / vals_out unused)
 template <bool kVals>
-__global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint64_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kThreads, kVals ? VRB_SORT_MINB : VRB_SORT_MINB_KEYS) k_onesweep(const uint64_t* __restrict__ keys_in,
                                                        const uint32_t* __restrict__ vals_in,
                                                        uint64_t* __restrict__ keys_out,
                                                        uint32_t* __restrict__ vals_out, int64_t n, int shift,
@@ -106,6 +116,9 @@ __global__ void __launch_bounds__(kThreads, VRB_SORT_MINB) k_onesweep(const uint
                                                        unsigned* __restrict__ tile_counter, uint64_t bias) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SweepSmem<kVals>& S = *reinterpret_cast<SweepSmem<kVals>*>(smem_raw);
+    constexpr int kItems = items_per_thread<kVals>();
+    constexpr int kTile = tile_items<kVals>();
+    constexpr int kWarpItems = 32 * kItems;   // contiguous items per warp
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) S.tile_id = atomicAdd(tile_counter, 1u);
     for (int q = threadIdx.x; q < kWarps * kBins; q += kThreads) (&S.woff[0][0])[q] = 0;
@@ -245,7 +258,7 @@ bool radix_sort_impl(uint64_t* keys, uint64_t* keys_alt, uint32_t* vals, uint32_
     uint32_t digit_mask = 0;
     for (int d = 0; d < 8; ++d)
         if ((varying >> (8 * d)) & 0xFFull) digit_mask |= 1u << d;
-    const int64_t ntiles = ceil_div(n, kTile);
+    const int64_t ntiles = ceil_div(n, (int64_t)tile_items<kVals>());
     DBuf<unsigned long long> hist(8 * kBins, s);
     VRB_CUDA(cudaMemsetAsync(hist.get(), 0, hist.bytes(), s));
     const unsigned hg = (unsigned)std::min<int64_t>(ceil_div(n, kThreads), (int64_t)device_sm_count() * 8);
