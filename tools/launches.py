@@ -19,6 +19,16 @@ def load(path):
 
 def main(path, nbuilds=2):
     data = load(path)
+    if data and "Metric Name" in data[0]:   # several metrics per launch: durations only, DRAM bytes beside
+        dram = collections.defaultdict(float)
+        for d in data:
+            if d["Metric Name"].startswith("dram__bytes"):
+                dram[d.get("ID")] += float(d["Metric Value"].replace(",", "")) * (
+                    1e9 if d["Metric Unit"] == "Gbyte" else 1e6 if d["Metric Unit"] == "Mbyte" else
+                    1e3 if d["Metric Unit"] == "Kbyte" else 1.0)
+        data = [d for d in data if d["Metric Name"] == "gpu__time_duration.sum"]
+        for d in data:
+            d["_dram"] = dram.get(d.get("ID"), 0.0)
     per = len(data) // nbuilds
     last = data[-per:]
     agg = collections.OrderedDict()
@@ -26,12 +36,14 @@ def main(path, nbuilds=2):
     for d in last:
         name = d["Kernel Name"].split("(")[0][-48:]
         v = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1e-6)
-        a = agg.setdefault(name, [0, 0.0])
+        a = agg.setdefault(name, [0, 0.0, 0.0])
         a[0] += 1
         a[1] += v
+        a[2] += d.get("_dram", 0.0)
     tot = sum(v[1] for v in agg.values())
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{v[1]:9.3f} ms {100 * v[1] / tot:5.1f}% x{v[0]:3d} {k}")
+        extra = f"  DRAM {v[2] / 1e9:7.2f} GB ({v[2] / 1e6 / max(v[1], 1e-9):6.0f} GB/s)" if v[2] else ""
+        print(f"{v[1]:9.3f} ms {100 * v[1] / tot:5.1f}% x{v[0]:3d} {k}{extra}")
     print(f"total {tot:.3f} ms over {len(last)} launches")
 
 
