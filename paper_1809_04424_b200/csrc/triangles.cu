@@ -588,6 +588,18 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 // flushes one lane per triangle with (k, pos(x, k)) = idl[off x + r] -- a
 // gather in rank order, so a warp's 32 loads fall in a few sectors.
 // ---------------------------------------------------------------------------
+#ifndef VRB_BATCH_DIV
+#define VRB_BATCH_DIV 2
+#endif
+#ifndef VRB_BATCH_MAX
+#define VRB_BATCH_MAX 32
+#endif
+#ifndef VRB_COUNT_BATCH
+#define VRB_COUNT_BATCH 1
+#endif
+#ifndef VRB_FILL_BATCH
+#define VRB_FILL_BATCH 1
+#endif
 #ifndef VRB_TRI_COUNT_WARPS
 #define VRB_TRI_COUNT_WARPS 16
 #endif
@@ -1410,6 +1422,111 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
             const uint64_t oy = A.off[y], oy1 = A.off[y + 1];
             for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = A.np[t];
             __syncthreads();
+#if VRB_COUNT_BATCH
+            if constexpr (kBm == 1 && !kFill) {
+                // the bitmap count in batches (as the bitmap fill below)
+                const int nwarps = nthreads >> 5;
+                for (;;) {
+                    unsigned my = 0, bb = 0;
+                    if (lane == 0) {
+                        const int64_t rem = end - seg - (int64_t)*(volatile unsigned*)&s_next;
+                        const int64_t want = rem / (VRB_BATCH_DIV * nwarps);
+                        bb = want < 1 ? 1u : (want > VRB_BATCH_MAX ? (unsigned)VRB_BATCH_MAX : (unsigned)want);
+                        my = atomicAdd(&s_next, bb);
+                    }
+                    my = __shfl_sync(0xffffffffu, my, 0);
+                    bb = __shfl_sync(0xffffffffu, bb, 0);
+                    const int64_t eb = seg + (int64_t)my;
+                    if (eb >= end) break;
+                    const int nb = (int)(end - eb < (int64_t)bb ? end - eb : (int64_t)bb);
+                    uint4 pl = make_uint4(0, 0, 0, 0);
+                    uint64_t offx = 0;
+                    if (lane < nb) {
+                        pl = A.plan[eb + lane];
+                        if (pl.z) offx = A.off[pl.y];
+                    }
+                    for (int i = 0; i < nb; ++i) {
+                        const uint32_t len = __shfl_sync(0xffffffffu, pl.z, i);
+                        if (!len) continue;
+                        const uint32_t p = __shfl_sync(0xffffffffu, pl.x, i), degx = __shfl_sync(0xffffffffu, pl.w, i);
+                        const uint64_t oi = __shfl_sync(0xffffffffu, offx, i);
+                        const uint32_t c = warp_count_bm(A, map, scratch + wid, p, oi, len, degx, eb + i);
+                        if (lane == 0) A.cnt[p] = c;
+                    }
+                }
+                __syncthreads();
+                for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
+                __syncthreads();
+                seg = end;
+                continue;
+            }
+#endif
+#if VRB_FILL_BATCH
+            if constexpr (kBm == 1 && kFill) {
+                // The bitmap fill takes the host's edges in batches (up to 32,
+                // shrinking with what is left so the warps stay balanced): one
+                // shared atomic per batch, the batch's plans, offsets, counts
+                // and bitmap offsets loaded lane-parallel, the batch's bitmaps
+                // prefetched to L2 together; the edges then run one by one
+                // with their parameters broadcast from the lanes.
+                const int nwarps = nthreads >> 5;
+                for (;;) {
+                    unsigned my = 0, bb = 0;
+                    if (lane == 0) {
+                        const int64_t rem = end - seg - (int64_t)*(volatile unsigned*)&s_next;
+                        const int64_t want = rem / (VRB_BATCH_DIV * nwarps);
+                        bb = want < 1 ? 1u : (want > VRB_BATCH_MAX ? (unsigned)VRB_BATCH_MAX : (unsigned)want);
+                        my = atomicAdd(&s_next, bb);
+                    }
+                    my = __shfl_sync(0xffffffffu, my, 0);
+                    bb = __shfl_sync(0xffffffffu, bb, 0);
+                    const int64_t eb = seg + (int64_t)my;
+                    if (eb >= end) break;
+                    const int nb = (int)(end - eb < (int64_t)bb ? end - eb : (int64_t)bb);
+                    uint4 pl = make_uint4(0, 0, 0, 0);
+                    uint64_t offx = 0, slot = 0, bmo = 0;
+                    uint32_t filt = 0, tc = 0;
+                    if (lane < nb) {
+                        pl = A.plan[eb + lane];
+                        if ((int64_t)pl.x < A.p_lo || (int64_t)pl.x >= A.p_hi) pl.z = 0;
+                        if (pl.z) {
+                            offx = A.off[pl.y];
+                            const uint64_t t0 = A.toff[pl.x];
+                            slot = t0 - A.slot0;
+                            tc = (uint32_t)(A.toff[pl.x + 1] - t0);
+                            filt = A.efilt[pl.x];
+                            bmo = A.bmoff[eb + lane];
+                        }
+                        if (pl.z && tc) {
+                            const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.bm + bmo) & ~(uintptr_t)127;
+                            const uintptr_t a1 = reinterpret_cast<uintptr_t>(A.bm + bmo + ((pl.w + 31) >> 5));
+                            for (uintptr_t a = a0; a < a1; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                        }
+                    }
+                    for (int i = 0; i < nb; ++i) {
+                        const uint32_t len = __shfl_sync(0xffffffffu, pl.z, i);
+                        const uint32_t tci = __shfl_sync(0xffffffffu, tc, i);
+                        if (!len || !tci) continue;
+                        const uint32_t p = __shfl_sync(0xffffffffu, pl.x, i), x = __shfl_sync(0xffffffffu, pl.y, i),
+                                       degx = __shfl_sync(0xffffffffu, pl.w, i),
+                                       fi = __shfl_sync(0xffffffffu, filt, i);
+                        const uint64_t oi = __shfl_sync(0xffffffffu, offx, i), si = __shfl_sync(0xffffffffu, slot, i),
+                                       bi = __shfl_sync(0xffffffffu, bmo, i);
+                        if (A.apex)
+                            warp_fill_bm<false, true>(A, map, scratch + wid, p, y, x, oi, degx, bi, si, fi, nullptr,
+                                                      tci);
+                        else
+                            warp_fill_bm<false, false>(A, map, scratch + wid, p, y, x, oi, degx, bi, si, fi, nullptr,
+                                                       tci);
+                    }
+                }
+                __syncthreads();
+                for (uint64_t t = oy + threadIdx.x; t < oy1; t += nthreads) map[A.nkr[t] & kmask] = NONE32;
+                __syncthreads();
+                seg = end;
+                continue;
+            }
+#endif
             // Edges of this host, longest prefix first, grabbed dynamically and
             // software-pipelined two deep: while edge e0 is processed, the
             // plan of e2 and the offsets of e1 are in flight.
