@@ -573,6 +573,24 @@ def test_c5a_edges_full(vrb):
     ll = lens[torch.from_numpy(idx).cuda()].cpu().numpy()
     for (i, j), L in zip(vv, ll):
         assert oracle.length(X, int(i), int(j)) == L
+    # every element: the oracle's full (len, i, j) order, levels and
+    # value_of_rank, as SHA-256 digests (tests/golden/c5a_edges.json, written
+    # by tools/make_golden.py from oracle/ only)
+    g = json.load(open(os.path.join(GOLDEN, "c5a_edges.json")))
+    assert g["points_sha256"] == hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest()
+    assert g["E"] == E and g["nvals"] == vor.shape[0]
+    del v, f, code, lens, dl, tie
+    h = hashlib.sha256()
+    gvc = gv.cpu()
+    step = 1 << 24
+    for a in range(0, E, step):
+        h.update(gvc[a:a + step].numpy().view(np.uint32).ravel().astype(np.uint64).tobytes())
+    del gvc
+    gfc = gf.cpu()
+    for a in range(0, E, step):
+        h.update(gfc[a:a + step].numpy().view(np.uint32).astype(np.uint64).tobytes())
+    assert h.hexdigest() == g["edges_sha256"]
+    assert hashlib.sha256(vor.cpu().numpy().tobytes()).hexdigest() == g["value_of_rank_sha256"]
 
 
 def test_full_size_c4_tetrahedra(vrb):

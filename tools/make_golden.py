@@ -53,8 +53,37 @@ def digest(config: str, k: int = 2) -> dict:
     }
 
 
+def digest_edges(config: str) -> dict:
+    # edges only (maxdim 0: C5A's 2e8 edges, full filtration)
+    w = workloads.WORKLOADS[config]
+    X = w.points()
+    t0 = time.time()
+    o = oracle.Oracle(X, w.radius)
+    ev, ef, el, vor = o.edges()
+    t1 = time.time()
+    edges = np.concatenate([ev.ravel().astype(np.uint64), ef.astype(np.uint64)])
+    return {
+        "config": config,
+        "citation": "computed by tools/make_golden.py with oracle/ only (SURVEY 8(c) steps 1-4): "
+                    "SHA-256 of the oracle's (i, j) pairs and levels in (len, i, j) order, and of value_of_rank",
+        "points_sha256": hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest(),
+        "E": int(o.E),
+        "nvals": int(o.nvals),
+        "edges_sha256": hashlib.sha256(edges.tobytes()).hexdigest(),
+        "value_of_rank_sha256": hashlib.sha256(vor.tobytes()).hexdigest(),
+        "oracle_seconds": {"edges": round(t1 - t0, 2)},
+    }
+
+
 if __name__ == "__main__":
     for cfg in sys.argv[1:] or ["C3", "C5B", "C4"]:
+        if workloads.WORKLOADS[cfg].maxdim == 0:
+            d = digest_edges(cfg)
+            path = os.path.join(ROOT, "tests", "golden", f"{cfg.lower()}_edges.json")
+            with open(path, "w") as f:
+                json.dump(d, f, indent=1)
+            print(cfg, d["E"], d["oracle_seconds"])
+            continue
         d = digest(cfg, k=3 if workloads.WORKLOADS[cfg].maxdim >= 2 else 2)
         path = os.path.join(ROOT, "tests", "golden", f"{cfg.lower()}_levels.json")
         with open(path, "w") as f:
