@@ -1368,11 +1368,14 @@ __global__ void __launch_bounds__(512, 1) k_tri_fill_x(TriArgs A) {
     }
 }
 
-template <bool kFill, bool kPacked, int kBm>
+// kGmap: the host map is a per-CTA slice of global memory (large n); else it
+// is in shared memory, and the compile-time choice lets every map lookup be
+// an LDS with a 32-bit address instead of a generic 64-bit load
+template <bool kFill, bool kPacked, int kBm, bool kGmap>
 __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS * 32 : kThreads / 2),
                                    (!kFill && kBm == 3) ? 2 : 1) k_triangles(TriArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t* map = A.gmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
+    uint32_t* map = kGmap ? A.gmap + (size_t)blockIdx.x * (size_t)A.n : reinterpret_cast<uint32_t*>(smem);
     using WS = typename std::conditional<
         kBm == 4, WarpScratchM,
         typename std::conditional<
@@ -1380,7 +1383,7 @@ __global__ void __launch_bounds__(kFill ? kThreads : (kBm ? VRB_TRI_COUNT_WARPS 
         typename std::conditional<
             kBm == 1, typename std::conditional<kFill, WarpScratchB, WarpScratchC>::type,
             typename std::conditional<kPacked && VRB_TRI_MODE == 3, WarpScratch3, WarpScratch>::type>::type>::type>::type;
-    WS* scratch = reinterpret_cast<WS*>(smem + (A.gmap ? 0 : ((A.n * 4 + 15) / 16) * 16));
+    WS* scratch = reinterpret_cast<WS*>(smem + (kGmap ? 0 : ((A.n * 4 + 15) / 16) * 16));
     __shared__ int64_t s_lo, s_hi, s_end;
     __shared__ uint32_t s_y;
     __shared__ unsigned s_next;
@@ -1637,21 +1640,32 @@ size_t scratch_bytes(bool packed) {
     return packed && VRB_TRI_MODE == 3 ? sizeof(WarpScratch3) : sizeof(WarpScratch);
 }
 
-template <bool kFill, bool kPacked, int kBm>
-void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap, cudaStream_t s) {
-    VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked, kBm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+template <bool kFill, bool kPacked, int kBm, bool kGmap>
+void launch_kg(TriArgs A, int threads, size_t smem, int64_t nctas_cap, cudaStream_t s) {
+    VRB_CUDA(cudaFuncSetAttribute(k_triangles<kFill, kPacked, kBm, kGmap>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked, kBm>, threads, smem));
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangles<kFill, kPacked, kBm, kGmap>, threads,
+                                                           smem));
     if (per_sm < 1) fail(VRB_ENOTSUP, "triangle kernel does not fit (n = %lld)", (long long)A.n);
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)device_sm_count() * per_sm, nctas_cap);
     DBuf<uint32_t> maps;
-    if (gmap) {   // one n-entry host map per CTA in global memory (L2-resident for moderate n)
+    if (kGmap) {   // one n-entry host map per CTA in global memory (L2-resident for moderate n)
         maps.alloc((size_t)grid * (size_t)A.n, s);
         A.gmap = maps.get();
+    } else {
+        A.gmap = nullptr;
     }
-    k_triangles<kFill, kPacked, kBm><<<grid, threads, smem, s>>>(A);
+    k_triangles<kFill, kPacked, kBm, kGmap><<<grid, threads, smem, s>>>(A);
     VRB_LAUNCH_CHECK();
+}
+
+template <bool kFill, bool kPacked, int kBm>
+void launch_k(TriArgs A, int threads, size_t smem, int64_t nctas_cap, bool gmap, cudaStream_t s) {
+    if (gmap)
+        launch_kg<kFill, kPacked, kBm, true>(A, threads, smem, nctas_cap, s);
+    else
+        launch_kg<kFill, kPacked, kBm, false>(A, threads, smem, nctas_cap, s);
 }
 
 void launch(const TriArgs& base, bool fill, uint64_t work, int part, int nparts, cudaStream_t s) {
