@@ -594,6 +594,9 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 #ifndef VRB_BATCH_MAX
 #define VRB_BATCH_MAX 32
 #endif
+#ifndef VRB_COUNT_PRED
+#define VRB_COUNT_PRED 1
+#endif
 #ifndef VRB_COUNT_BATCH
 #define VRB_COUNT_BATCH 1
 #endif
@@ -629,17 +632,53 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
     int mis;
     const uint4* g = aligned_groups(A.nkr + offx, mis);
     const int ngroups = (int)((len + mis + 3) >> 2);
+#if VRB_COUNT_PRED
+    // branch-free marking: every lane looks its entry up (entries past the
+    // prefix, or of a missing group (word 0, vertex 0), are looked up too and
+    // masked out), so the loop carries no divergent branches
+    auto run = [&](auto G_) {
+        constexpr int G = decltype(G_)::value;
+        return [&](int start, int stop) {
+            for (int i0 = start; i0 < stop; i0 += 32 * G) {
+                uint4 q[G];
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const int i = i0 + u * 32 + lane;
+                    q[u] = i < ngroups ? ld_list(g + i) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const int i = i0 + u * 32 + lane;
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const uint32_t t = (uint32_t)(4 * i + e2 - mis);
+                        const uint32_t w = pick(q[u], e2);
+                        const uint32_t py = map[w & 0xFFFFu];
+                        const uint32_t ok = (uint32_t)(t < len) & (uint32_t)(py < p);
+                        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&W->bits[w >> 21]);
+                        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
+                                     ::"r"(addr), "r"(1u << ((w >> 16) & 31u)), "r"(ok) : "memory");
+                    }
+                }
+            }
+        };
+    };
+    {
+        const int f4 = (ngroups / 128) * 128;
+        const int f2 = f4 + ((ngroups - f4) / 64) * 64;
+        run(std::integral_constant<int, 4>())(0, f4);
+        run(std::integral_constant<int, 2>())(f4, f2);
+        run(std::integral_constant<int, 1>())(f2, ngroups);
+    }
+#else
     auto mark = [&](uint32_t w, uint32_t) {
-#ifndef VRB_ABL_NOATOM
         if (map[w & 0xFFFFu] < p) {
             const uint32_t r = w >> 16;
             atomicOr(&W->bits[r >> 5], 1u << (r & 31));
         }
-#else
-        if (map[w & 0xFFFFu] < p) W->bits[0] += 1u;
-#endif
     };
     stream_prefix<kRegGroups>(g, ngroups, mis, len, mark);
+#endif
     __syncwarp();
     uint32_t c = 0;
     for (uint32_t w = lane; w < nw; w += 32) {
