@@ -750,6 +750,10 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
         const uint32_t m = min((uint32_t)kWinB, count - w0);
         if (A.debug != 2) {
             const uint64_t s0 = slot + w0;
+            // the window's output pointers (32-bit offsets from here on)
+            uint32_t* __restrict__ const tfw = A.tf + s0;
+            uint32_t* __restrict__ const tvw = A.tv + 3 * s0;
+            uint32_t* __restrict__ const rww = A.rows ? A.rows + 3 * s0 : nullptr;
             // one triangle: slot j of the window, (k, pos(x, k)) gathered
             const uint32_t vlo = min(x, y), vhi = max(x, y);
             auto tri = [&](uint32_t j, uint2 kp, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& r0,
@@ -766,18 +770,18 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
 #endif
                 r0 = min(px, py);
                 r1 = max(px, py);
-                __stcs(A.tf + s0 + j, filt);
+                __stcs(tfw + j, filt);
                 if (kApex && A.apex) A.apex[s0 + j] = (uint16_t)k;
             };
             auto scalar = [&](uint32_t j, uint2 kp) {
                 uint32_t a0, a1, a2, r0, r1;
                 tri(j, kp, a0, a1, a2, r0, r1);
-                uint32_t* tv = A.tv + 3 * (s0 + j);
+                uint32_t* tv = tvw + 3 * j;
                 __stcs(tv, a0);
                 __stcs(tv + 1, a1);
                 __stcs(tv + 2, a2);
-                if (A.rows) {
-                    uint32_t* rw = A.rows + 3 * (s0 + j);
+                if (rww) {
+                    uint32_t* rw = rww + 3 * j;
                     __stcs(rw, r0);
                     __stcs(rw + 1, r1);
                     __stcs(rw + 2, p);
@@ -816,10 +820,10 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
                         W->sr[3 * lane + 2] = p;
                         __syncwarp();
                         if (lane < 24) {
-                            __stcs(reinterpret_cast<uint4*>(A.tv + 3 * (s0 + g)) + lane,
+                            __stcs(reinterpret_cast<uint4*>(tvw + 3 * g) + lane,
                                    reinterpret_cast<const uint4*>(W->st)[lane]);
-                            if (A.rows)
-                                __stcs(reinterpret_cast<uint4*>(A.rows + 3 * (s0 + g)) + lane,
+                            if (rww)
+                                __stcs(reinterpret_cast<uint4*>(rww + 3 * g) + lane,
                                        reinterpret_cast<const uint4*>(W->sr)[lane]);
                         }
                         __syncwarp();
