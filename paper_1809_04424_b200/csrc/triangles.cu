@@ -633,6 +633,7 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
     const uint4* g = aligned_groups(A.nkr + offx, mis);
     const int ngroups = (int)((len + mis + 3) >> 2);
 #if VRB_COUNT_PRED
+    const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(W->bits);
     // branch-free marking: every lane looks its entry up (entries past the
     // prefix, or of a missing group (word 0, vertex 0), are looked up too and
     // masked out), so the loop carries no divergent branches
@@ -655,7 +656,7 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
                         const uint32_t w = pick(q[u], e2);
                         const uint32_t py = map[w & 0xFFFFu];
                         const uint32_t ok = (uint32_t)(t < len) & (uint32_t)(py < p);
-                        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&W->bits[w >> 21]);
+                        const uint32_t addr = bits_s + ((w >> 19) & ~3u);   // word r >> 5 of the bitmap
                         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
                                      ::"r"(addr), "r"(1u << ((w >> 16) & 31u)), "r"(ok) : "memory");
                     }
