@@ -702,6 +702,9 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     g.packed = n <= 65536 && g.max_deg <= 65536 && !(force_wide && force_wide[0] == '1');
     // +4 entries: the enumeration kernels read lists in aligned 16-byte groups
     g.nkr.alloc(n2 + 4, s);
+    // the padding is read by the last list's 16-byte groups: vertex 0, rank 0
+    // (the triangle count looks every word of a group up before masking)
+    VRB_CUDA(cudaMemsetAsync(g.nkr.get() + n2, 0, 4 * sizeof(uint32_t), s));
     if (!g.packed) g.nr.alloc(n2 + 4, s);
     g.np.alloc(n2 + 4, s);
     g.listidx.alloc(n2, s);

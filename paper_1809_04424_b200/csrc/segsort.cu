@@ -146,6 +146,20 @@ __device__ __forceinline__ int64_t seg_of(const uint64_t* __restrict__ segoff, i
     return lo;
 }
 
+// the same with a per-thread cached segment: grid-stride steps mostly land in
+// the same or the next segment (segments are long), so the binary search
+// (a chain of dependent loads) is the exception
+__device__ __forceinline__ int64_t seg_cached(const uint64_t* __restrict__ segoff, int64_t nseg, uint64_t q,
+                                              int64_t& g) {
+    if (g >= 0 && g < nseg) {
+        const uint64_t a = __ldg(segoff + g), b = __ldg(segoff + g + 1);
+        if (q >= a && q < b) return g;
+        if (q >= b && g + 1 < nseg && q < __ldg(segoff + g + 2)) return ++g;
+    }
+    g = seg_of(segoff, nseg, q);
+    return g;
+}
+
 #define ELEM_STRIDE(q, M) \
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (uint64_t)(M); \
          q += (uint64_t)gridDim.x * blockDim.x)
@@ -157,8 +171,9 @@ template <int K>
 __global__ void k_big_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
                            int64_t M, const uint32_t* __restrict__ verts, int cbits, int packed,
                            uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+    int64_t gc = -1;
     ELEM_STRIDE(q, M) {
-        const int64_t g = seg_of(segoff, nseg, q);
+        const int64_t g = seg_cached(segoff, nseg, q, gc);
         const uint64_t slot = segs[g].start + (q - segoff[g]);
         const uint64_t code = Code<K>::pack(verts + (K + 1) * slot);
         key[q] = packed ? (((uint64_t)g << cbits) | code) : code;
@@ -198,8 +213,9 @@ template <int K>
 __global__ void k_big_apply(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
                             int64_t M, const uint64_t* __restrict__ codes, const uint32_t* __restrict__ rcopy,
                             uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
+    int64_t gc = -1;
     ELEM_STRIDE(q, M) {
-        const int64_t g = seg_of(segoff, nseg, q);
+        const int64_t g = seg_cached(segoff, nseg, q, gc);
         const uint64_t slot = segs[g].start + (q - segoff[g]);
         uint32_t v[K + 1];
         Code<K>::unpack(codes[q], v);
@@ -238,8 +254,9 @@ __global__ void k_tab_positions(const uint32_t* __restrict__ ev, int64_t E, int6
 
 __global__ void k_tri_keys(const Seg* __restrict__ segs, const uint64_t* __restrict__ segoff, int64_t nseg,
                            int64_t M, const uint32_t* __restrict__ verts, int vb, uint64_t* __restrict__ key) {
+    int64_t gc = -1;
     ELEM_STRIDE(q, M) {
-        const int64_t g = seg_of(segoff, nseg, q);
+        const int64_t g = seg_cached(segoff, nseg, q, gc);
         const uint32_t* v = verts + 3 * (segs[g].start + (q - segoff[g]));
         key[q] = ((uint64_t)g << (3 * vb)) | ((uint64_t)v[0] << (2 * vb)) | ((uint64_t)v[1] << vb) | v[2];
     }
@@ -249,8 +266,9 @@ __global__ void k_tri_apply(const Seg* __restrict__ segs, const uint64_t* __rest
                             int64_t M, const uint64_t* __restrict__ key, int vb, const uint32_t* __restrict__ tab,
                             int64_t n, uint32_t* __restrict__ verts, uint32_t* __restrict__ rows) {
     const uint64_t m = (1ull << vb) - 1ull;
+    int64_t gc = -1;
     ELEM_STRIDE(q, M) {
-        const int64_t g = seg_of(segoff, nseg, q);
+        const int64_t g = seg_cached(segoff, nseg, q, gc);
         const uint64_t slot = segs[g].start + (q - segoff[g]);
         const uint64_t kk = key[q];
         const uint32_t a = (uint32_t)((kk >> (2 * vb)) & m), b = (uint32_t)((kk >> vb) & m), c = (uint32_t)(kk & m);
