@@ -79,15 +79,23 @@ __global__ void k_offsets_from_sorted(const uint64_t* __restrict__ skey, int64_t
 }
 
 // position-ordered lists: slot s holds entry q = sorted[s] of vertex skey[s]
+// listidx (entry -> its index in the vertex's list) is written only when the
+// large-n rank path needs it; the scanned-endpoint choice instead takes, per
+// edge, the minimum of (index << 1 | side) over its two entries (a shared-
+// nothing atomicMin into an L2-resident word per edge, where the scatter of
+// listidx made partial-sector DRAM writes)
 __global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ skey,
                             const uint32_t* __restrict__ ev, const uint64_t* __restrict__ off, int64_t n2,
-                            uint32_t* __restrict__ nkr, uint32_t* __restrict__ np, uint32_t* __restrict__ listidx) {
+                            uint32_t* __restrict__ nkr, uint32_t* __restrict__ np, uint32_t* __restrict__ listidx,
+                            unsigned* __restrict__ scanpack) {
     GRID_STRIDE(s, n2) {
         const uint32_t q = sorted[s];
         const uint32_t v = (uint32_t)skey[s];
         nkr[s] = ev[q ^ 1];
         np[s] = q >> 1;
-        listidx[q] = (uint32_t)(s - (int64_t)off[v]);
+        const uint32_t t = (uint32_t)(s - (int64_t)off[v]);
+        if (listidx) listidx[q] = t;
+        atomicMin(scanpack + (q >> 1), (t << 1) | (q & 1u));
     }
 }
 
@@ -163,14 +171,13 @@ __global__ void __launch_bounds__(256) k_ranks_bitmap(const uint64_t* __restrict
     }
 }
 
-__global__ void k_assign(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ listidx, int64_t E,
+// the endpoint with the shorter prefix (ties: the first endpoint)
+__global__ void k_assign(const uint32_t* __restrict__ ev, const unsigned* __restrict__ scanpack, int64_t E,
                          uint32_t* __restrict__ scan_v, uint32_t* __restrict__ scan_len) {
     GRID_STRIDE(p, E) {
-        const uint32_t la = listidx[2 * p], lb = listidx[2 * p + 1];
-        const uint32_t a = ev[2 * p], b = ev[2 * p + 1];
-        const bool scan_a = la <= lb;
-        scan_v[p] = scan_a ? a : b;
-        scan_len[p] = scan_a ? la : lb;
+        const unsigned w = scanpack[p];
+        scan_v[p] = ev[2 * p + (w & 1u)];
+        scan_len[p] = w >> 1;
     }
 }
 
@@ -707,22 +714,25 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     VRB_CUDA(cudaMemsetAsync(g.nkr.get() + n2, 0, 4 * sizeof(uint32_t), s));
     if (!g.packed) g.nr.alloc(n2 + 4, s);
     g.np.alloc(n2 + 4, s);
-    g.listidx.alloc(n2, s);
+    const char* force_sort = std::getenv("VRB_FORCE_SORT_RANKS");   // testing knob
+    const bool bitmap_ranks = n <= kRankBitmapMax && !(force_sort && force_sort[0] == '1');
+    if (!bitmap_ranks) g.listidx.alloc(n2, s);
     g.scan_v.alloc(E, s);
     g.scan_len.alloc(E, s);
     if (E == 0) return;
+    DBuf<unsigned> scanpack(E, s);
+    VRB_CUDA(cudaMemsetAsync(scanpack.get(), 0xFF, E * sizeof(unsigned), s));
     {
         DBuf<uint64_t>& k0 = lk0;
         DBuf<uint64_t>& k1 = lk1;
         DBuf<uint32_t>& v0 = lv0;
         DBuf<uint32_t>& v1 = lv1;
         k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(lsorted, lskeys, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
-                                                       g.listidx.get());
+                                                       g.listidx.get(), scanpack.get());
         VRB_LAUNCH_CHECK();
         const uint32_t* sorted = nullptr;
         // (b) ranks in neighbour-id order
-        const char* force_sort = std::getenv("VRB_FORCE_SORT_RANKS");   // testing knob
-        if (n <= kRankBitmapMax && !(force_sort && force_sort[0] == '1')) {
+        if (bitmap_ranks) {
             const size_t smem = (size_t)2 * ((n + 31) >> 5) * sizeof(uint32_t);
             VRB_CUDA(cudaFuncSetAttribute(k_ranks_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)device_sm_count() * 8);
@@ -748,7 +758,7 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     }
     // (c) scanned endpoint of every edge: the one with the shorter prefix of
     // neighbours older than the edge
-    k_assign<<<grid_for(E, 256), 256, 0, s>>>(ev, g.listidx.get(), E, g.scan_v.get(), g.scan_len.get());
+    k_assign<<<grid_for(E, 256), 256, 0, s>>>(ev, scanpack.get(), E, g.scan_v.get(), g.scan_len.get());
     VRB_LAUNCH_CHECK();
 }
 
