@@ -182,25 +182,28 @@ __global__ void k_assign(const uint32_t* __restrict__ ev, const unsigned* __rest
 }
 
 // plan sort key of the owner edges p_lo + [0, m): host, then longest prefix
-// first (LPT order inside a host)
+// first (LPT order inside a host, by prefix length in buckets of 2^lsh so
+// that host and length fit 24 bits: three radix passes)
 __global__ void k_host_keys(const uint32_t* __restrict__ ev, const uint32_t* __restrict__ scan_v,
-                            const uint32_t* __restrict__ scan_len, int64_t p_lo, int64_t m,
+                            const uint32_t* __restrict__ scan_len, int64_t p_lo, int64_t m, int lbits, int lsh,
                             uint64_t* __restrict__ host_key) {
+    const uint32_t lmax = (1u << lbits) - 1u;
     GRID_STRIDE(q, m) {
         const int64_t p = p_lo + q;
         const uint32_t a = ev[2 * p], b = ev[2 * p + 1], x = scan_v[p];
-        host_key[q] = ((uint64_t)(x == a ? b : a) << 32) | (uint32_t)~scan_len[p];
+        const uint32_t lb = min(scan_len[p] >> lsh, lmax);
+        host_key[q] = ((uint64_t)(x == a ? b : a) << lbits) | (lmax - lb);
     }
 }
 
 __global__ void k_hosted_work(const uint32_t* __restrict__ hosted, const uint64_t* __restrict__ host_key,
                               const uint32_t* __restrict__ scan_v, const uint32_t* __restrict__ scan_len,
-                              const uint64_t* __restrict__ off, int64_t E, int64_t p_lo,
+                              const uint64_t* __restrict__ off, int64_t E, int64_t p_lo, int lbits,
                               uint32_t* __restrict__ hosted_v, uint4* __restrict__ plan, uint32_t* __restrict__ work) {
     GRID_STRIDE(i, E) {
         const uint32_t p = (uint32_t)(p_lo + hosted[i]);
         const uint32_t x = scan_v[p], len = scan_len[p];
-        hosted_v[i] = (uint32_t)(host_key[i] >> 32);
+        hosted_v[i] = (uint32_t)(host_key[i] >> lbits);
         plan[i] = make_uint4(p, x, len, (uint32_t)(off[x + 1] - off[x]));
         work[i] = len;
     }
@@ -829,13 +832,17 @@ void build_plan(const uint32_t* ev, int64_t p_lo, int64_t p_hi, cudaStream_t s, 
     }
     DBuf<uint64_t> k0(m, s), k1(m, s);
     DBuf<uint32_t> v0(m, s), v1(m, s);
-    k_host_keys<<<grid_for(m, 256), 256, 0, s>>>(ev, g.scan_v.get(), g.scan_len.get(), p_lo, m, k0.get());
+    auto bits_of = [](uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; };
+    const int hbits = std::max(1, bits_of((uint64_t)std::max<int64_t>(g.n - 1, 1)));
+    const int lbits = std::max(1, 24 - hbits);
+    const int lsh = std::max(0, bits_of(g.max_deg) - lbits);
+    k_host_keys<<<grid_for(m, 256), 256, 0, s>>>(ev, g.scan_v.get(), g.scan_len.get(), p_lo, m, lbits, lsh, k0.get());
     VRB_LAUNCH_CHECK();
     uint64_t* skeys = nullptr;
     const uint32_t* sorted = sort_ids(k0, k1, v0, v1, m, s, &skeys);
     DBuf<uint32_t> work(m, s);
     k_hosted_work<<<grid_for(m, 256), 256, 0, s>>>(sorted, skeys, g.scan_v.get(), g.scan_len.get(), g.off.get(), m,
-                                                   p_lo, g.hosted_v.get(), g.plan.get(), work.get());
+                                                   p_lo, lbits, g.hosted_v.get(), g.plan.get(), work.get());
     VRB_LAUNCH_CHECK();
     exclusive_scan(work.get(), g.work_pre.get(), m, s);
     VRB_CUDA(cudaMemcpyAsync(&g.work, g.work_pre.get() + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
