@@ -56,8 +56,10 @@ __global__ void k_edge_outputs_packed(const uint64_t* __restrict__ key, const ui
     }
 }
 
+// (vertex << 32 | entry): a keys-only sort on the vertex bits, stable, keeps
+// each vertex's entries in position order
 __global__ void k_keys_vertex(const uint32_t* __restrict__ ev, int64_t n2, uint64_t* __restrict__ key) {
-    GRID_STRIDE(q, n2) key[q] = ev[q];
+    GRID_STRIDE(q, n2) key[q] = ((uint64_t)ev[q] << 32) | (uint64_t)q;
 }
 
 __global__ void k_keys_vertex_nbr(const uint32_t* __restrict__ ev, int64_t n2, uint64_t* __restrict__ key) {
@@ -72,7 +74,7 @@ __global__ void k_offsets_from_sorted(const uint64_t* __restrict__ skey, int64_t
         int64_t lo = 0, hi = n2;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            if (skey[mid] < (uint64_t)u) lo = mid + 1; else hi = mid;
+            if ((skey[mid] >> 32) < (uint64_t)u) lo = mid + 1; else hi = mid;
         }
         off[u] = (uint64_t)lo;
     }
@@ -84,13 +86,14 @@ __global__ void k_offsets_from_sorted(const uint64_t* __restrict__ skey, int64_t
 // edge, the minimum of (index << 1 | side) over its two entries (a shared-
 // nothing atomicMin into an L2-resident word per edge, where the scatter of
 // listidx made partial-sector DRAM writes)
-__global__ void k_pos_lists(const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ skey,
-                            const uint32_t* __restrict__ ev, const uint64_t* __restrict__ off, int64_t n2,
-                            uint32_t* __restrict__ nkr, uint32_t* __restrict__ np, uint32_t* __restrict__ listidx,
+__global__ void k_pos_lists(const uint64_t* __restrict__ skey, const uint32_t* __restrict__ ev,
+                            const uint64_t* __restrict__ off, int64_t n2, uint32_t* __restrict__ nkr,
+                            uint32_t* __restrict__ np, uint32_t* __restrict__ listidx,
                             unsigned* __restrict__ scanpack) {
     GRID_STRIDE(s, n2) {
-        const uint32_t q = sorted[s];
-        const uint32_t v = (uint32_t)skey[s];
+        const uint64_t kk = skey[s];
+        const uint32_t q = (uint32_t)kk;
+        const uint32_t v = (uint32_t)(kk >> 32);
         nkr[s] = ev[q ^ 1];
         np[s] = q >> 1;
         const uint32_t t = (uint32_t)(s - (int64_t)off[v]);
@@ -677,20 +680,19 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
     g.off.alloc(n + 1, s);
     // (a) lists in edge-position order: stable sort of the 2E entries by
     // vertex; the list offsets are the run starts of the sorted keys
+    if (n2 >= (int64_t)1 << 32) fail(VRB_EOVERFLOW, "%lld list entries exceed u32 entry ids", (long long)n2);
     DBuf<uint64_t> lk0, lk1;
     DBuf<uint32_t> lv0, lv1;
-    const uint32_t* lsorted = nullptr;
     const uint64_t* lskeys = nullptr;
     if (n2) {
         lk0.alloc(n2, s);
         lk1.alloc(n2, s);
-        lv0.alloc(n2, s);
-        lv1.alloc(n2, s);
         k_keys_vertex<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, lk0.get());
         VRB_LAUNCH_CHECK();
-        uint64_t* sk = nullptr;
-        lsorted = sort_ids(lk0, lk1, lv0, lv1, n2, s, &sk);
-        lskeys = sk;
+        int vb = 1;
+        while (vb < 32 && ((uint64_t)(n - 1) >> vb)) ++vb;
+        const bool alt = radix_sort_keys(lk0.get(), lk1.get(), n2, ((1ull << vb) - 1ull) << 32, s);
+        lskeys = alt ? lk1.get() : lk0.get();
         k_offsets_from_sorted<<<grid_for(n + 1, 256), 256, 0, s>>>(lskeys, n2, n, g.off.get());
         VRB_LAUNCH_CHECK();
     } else {
@@ -730,7 +732,7 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
         DBuf<uint64_t>& k1 = lk1;
         DBuf<uint32_t>& v0 = lv0;
         DBuf<uint32_t>& v1 = lv1;
-        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(lsorted, lskeys, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
+        k_pos_lists<<<grid_for(n2, 256), 256, 0, s>>>(lskeys, ev, g.off.get(), n2, g.nkr.get(), g.np.get(),
                                                        g.listidx.get(), scanpack.get());
         VRB_LAUNCH_CHECK();
         const uint32_t* sorted = nullptr;
@@ -745,6 +747,8 @@ void build_lists(const uint32_t* ev, int64_t n, int64_t E, cudaStream_t s, Graph
             VRB_LAUNCH_CHECK();
         } else {
             // large n: sort entries by (vertex, neighbour)
+            v0.alloc(n2, s);
+            v1.alloc(n2, s);
             k_keys_vertex_nbr<<<grid_for(n2, 256), 256, 0, s>>>(ev, n2, k0.get());
             VRB_LAUNCH_CHECK();
             sorted = sort_ids(k0, k1, v0, v1, n2, s);
