@@ -594,6 +594,9 @@ __device__ __forceinline__ void warp_fill_kp(const TriArgs& A, const uint32_t* _
 #ifndef VRB_BATCH_MAX
 #define VRB_BATCH_MAX 32
 #endif
+#ifndef VRB_COUNT_OR0
+#define VRB_COUNT_OR0 0
+#endif
 #ifndef VRB_COUNT_PRED
 #define VRB_COUNT_PRED 1
 #endif
@@ -657,8 +660,14 @@ __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32
                         const uint32_t py = map[w & 0xFFFFu];
                         const uint32_t ok = (uint32_t)(t < len) & (uint32_t)(py < p);
                         const uint32_t addr = bits_s + ((w >> 19) & ~3u);   // word r >> 5 of the bitmap
+#if VRB_COUNT_OR0
+                        // every lane ORs (a zero when not an apex): no branch at all
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"((0u - ok) & (1u << ((w >> 16) & 31u)))
+                                     : "memory");
+#else
                         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
                                      ::"r"(addr), "r"(1u << ((w >> 16) & 31u)), "r"(ok) : "memory");
+#endif
                     }
                 }
             }
