@@ -617,11 +617,37 @@ constexpr int kWinB = VRB_WINB;   // slots per window of the bitmap fill
 struct WarpScratchC {              // count
     uint32_t bits[kBmWords];
 };
+#ifndef VRB_FILL_BULK
+#define VRB_FILL_BULK 0
+#endif
 struct WarpScratchB {              // fill: the staged window (apex ranks by slot)
     uint16_t rec[kWinB];
+#if VRB_FILL_BULK
+    alignas(16) uint32_t st[2][96];   // double-buffered: one bulk copy in flight per buffer
+    alignas(16) uint32_t sr[2][96];
+#else
     alignas(16) uint32_t st[96];   // 32 triangles' vertices, then D_2 rows: re-cut into
     alignas(16) uint32_t sr[96];   // 16-byte chunks for full-sector vector stores
+#endif
 };
+
+#if VRB_FILL_BULK
+// TMA bulk store (cp.async.bulk shared::cta -> global, one issuing lane):
+// the staged 384-byte group leaves shared memory without passing through
+// registers; bulk groups are per thread, so lane 0 issues, commits and waits.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+#endif
 
 __device__ __forceinline__ uint32_t warp_count_bm(const TriArgs& A, const uint32_t* __restrict__ map,
                                                   WarpScratchC* __restrict__ W, uint32_t p, uint64_t offx,
@@ -799,6 +825,9 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
             };
             // head: slots before the first multiple of 4 (16-byte aligned triples)
             const uint32_t h = min(m, (uint32_t)((4u - (uint32_t)(s0 & 3u)) & 3u));
+#if VRB_FILL_BULK
+            uint32_t nbulk = 0;
+#endif
             if ((uint32_t)lane < h) scalar(lane, ld_idl(idx + W->rec[lane]));
 #ifndef VRB_TRI_BM_UNROLL
 #define VRB_TRI_BM_UNROLL 8
@@ -822,6 +851,27 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
                     if (g + 32 <= m) {
                         uint32_t a0, a1, a2, r0, r1;
                         tri(j, kq[q], a0, a1, a2, r0, r1);
+#if VRB_FILL_BULK
+                        // buffer nb was last read by the copy issued two groups ago
+                        if (lane == 0 && nbulk >= 2) bulk_wait_read<1>();
+                        __syncwarp();
+                        uint32_t* st = W->st[nbulk & 1];
+                        uint32_t* sr = W->sr[nbulk & 1];
+                        st[3 * lane] = a0;
+                        st[3 * lane + 1] = a1;
+                        st[3 * lane + 2] = a2;
+                        sr[3 * lane] = r0;
+                        sr[3 * lane + 1] = r1;
+                        sr[3 * lane + 2] = p;
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            bulk_s2g(tvw + 3 * g, st, 384u);
+                            if (rww) bulk_s2g(rww + 3 * g, sr, 384u);
+                            bulk_commit();
+                        }
+                        ++nbulk;
+#else
                         W->st[3 * lane] = a0;
                         W->st[3 * lane + 1] = a1;
                         W->st[3 * lane + 2] = a2;
@@ -837,11 +887,16 @@ __device__ __forceinline__ void warp_fill_bm(const TriArgs& A, const uint32_t* _
                                        reinterpret_cast<const uint4*>(W->sr)[lane]);
                         }
                         __syncwarp();
+#endif
                     } else if (j < m) {
                         scalar(j, kq[q]);
                     }
                 }
             }
+#if VRB_FILL_BULK
+            // the staging buffers are reused by the next window / owner edge
+            if (lane == 0 && nbulk) bulk_wait_read<0>();
+#endif
         }
         __syncwarp();
     }
