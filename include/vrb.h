@@ -298,6 +298,13 @@ vrb_status vrb_set_profiling(int32_t enable);
 vrb_status vrb_last_stage_ms(double* ms8);
 vrb_status vrb_last_stage_ms_n(double* ms, int32_t n);
 
+/* Which S3 edge-ranking path the last vrb_build / vrb_build_dm on this thread
+ * took: 1 = bucket scatter + on-chip finish (SURVEY 8(d) "Edges work the
+ * same way"; edge_buckets.cu), 0 = LSD radix passes (ties or spiky length
+ * distributions: a bucket over 2048 edges), -1 = no build yet or no edges.
+ * Both give the same arrays (the (len, i, j) order of P:929-936, A3/A4). */
+int32_t vrb_last_edge_path(void);
+
 /* Number of kernels this library has launched in this process (monotonic;
  * the difference across a region is the number of launches inside it). */
 unsigned long long vrb_launch_count(void);

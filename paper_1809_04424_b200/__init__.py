@@ -34,7 +34,7 @@ VRB_SKIP_BOUNDARY = 0x8
 # Every symbol include/vrb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("vrb_abi_version", "vrb_last_error", "vrb_set_allocator", "vrb_build", "vrb_build_dist",
            "vrb_count", "vrb_simplices", "vrb_rank_values", "vrb_boundary", "vrb_boundary_colptr",
-           "vrb_free", "vrb_sortperm_f64", "vrb_partition_bounds", "vrb_compress_d2", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_h0",
+           "vrb_free", "vrb_sortperm_f64", "vrb_partition_bounds", "vrb_compress_d2", "vrb_set_profiling", "vrb_last_stage_ms", "vrb_last_stage_ms_n", "vrb_launch_count", "vrb_last_edge_path", "vrb_h0",
            "vrb_build_dm",
            "vrb_latlon2euc", "vrb_gf2_blockprodsum", "vrb_gf2_csc", "vrb_gf2_free")
 
@@ -111,6 +111,8 @@ def lib() -> ctypes.CDLL:
     L.vrb_last_stage_ms_n.argtypes = [P(ctypes.c_double), ctypes.c_int32]
     L.vrb_launch_count.restype = ctypes.c_ulonglong
     L.vrb_launch_count.argtypes = []
+    L.vrb_last_edge_path.restype = ctypes.c_int32
+    L.vrb_last_edge_path.argtypes = []
     L.vrb_build_dm.restype = ctypes.c_int
     L.vrb_build_dm.argtypes = [p, i64, P(vrb_opts), p, P(p)]
     L.vrb_latlon2euc.restype = ctypes.c_int
@@ -183,6 +185,11 @@ def set_profiling(enable: bool):
 def launch_count() -> int:
     """Kernels launched by libvrb.so so far in this process."""
     return int(lib().vrb_launch_count())
+
+
+def last_edge_path() -> str:
+    """S3 path of the last build on this thread: "bucket", "radix" or "none"."""
+    return {1: "bucket", 0: "radix"}.get(int(lib().vrb_last_edge_path()), "none")
 
 
 def last_stage_ms() -> dict:

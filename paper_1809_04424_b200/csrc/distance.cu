@@ -487,6 +487,7 @@ void place_matrix(const double* D, int64_t n, uint32_t flags, cudaStream_t s, DB
 
 void build_kept_edges_dm(const double* D, int64_t n, double radius, bool strict, cudaStream_t s, KeptEdges& out) {
     out.E = 0;
+    out.n = n;
     if (n < 2) return;
     DBuf<uint32_t> cnt(n, s);
     DBuf<uint64_t> off(n + 1, s);
@@ -568,6 +569,7 @@ int64_t edge_tile() { return kT; }
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
                       KeptEdges& out, int64_t row_lo, int64_t row_hi) {
     out.E = 0;
+    out.n = n;
     if (row_hi < 0 || row_hi > n) row_hi = n;
     if (n < 2 || row_lo >= row_hi) return;
     if (row_lo % kT) fail(VRB_EINVAL, "row block must start at a multiple of %d", kT);

@@ -603,9 +603,24 @@ __global__ void __launch_bounds__(kRkThreads) k_rank_edges(RankArgs A) {
 }
 }  // namespace
 
+static thread_local int t_edge_path = -1;
+int last_edge_path() { return t_edge_path; }
+
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s) {
     const int64_t E = ke.E;
+    t_edge_path = -1;
     if (E == 0) return 0;
+    // the bucket path (edge_buckets.cu) unless the distribution does not
+    // allow it; VRB_EDGE_PATH=radix forces the radix path (tests, experiments)
+    const char* ep = std::getenv("VRB_EDGE_PATH");
+    if (!(ep && ep[0] == 'r')) {
+        int64_t nv = 0;
+        if (rank_edges_buckets(ke, ke.n, ev, efilt, vor, s, &nv)) {
+            t_edge_path = 1;
+            return nv;
+        }
+    }
+    t_edge_path = 0;
     SortedEdges so;
     const char* un = std::getenv("VRB_EDGE_UNFUSED");   // experiment knob: the three-kernel epilogue
     if (un && un[0] == '1') {

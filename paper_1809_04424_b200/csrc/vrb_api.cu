@@ -806,6 +806,8 @@ vrb_status vrb_sortperm_f64(const double* keys_dev, int64_t n, int64_t* perm_dev
 
 unsigned long long vrb_launch_count(void) { return vrb::g_launches.load(); }
 
+int32_t vrb_last_edge_path(void) { return vrb::last_edge_path(); }
+
 vrb_status vrb_set_profiling(int32_t enable) {
     vrb::g_profiling = enable != 0;
     return VRB_OK;

@@ -20,6 +20,7 @@ double cap_threshold(double r, bool strict);
 struct KeptEdges {
     int64_t E = 0;
     DBuf<uint64_t> key;   // bit pattern of len (non-negative doubles order as u64)
+    int64_t n = 0;
     bool packed = false;  // n <= 65536: (i << 16 | j) in pij, else i, j in ei, ej
     DBuf<uint32_t> ei, ej, pij;
     DBuf<unsigned long long> range;   // when set: min, max, OR of the key bits (reduced by the distance pass)
@@ -43,6 +44,11 @@ void latlon2euc(const double* latlon, int64_t n, double* xyz, cudaStream_t s);
 //   efilt : E u32 dense rank, 1-based                    (caller-allocated)
 //   vor   : >= nvals f64, vor[f-1] = length of level f  (caller-allocated, E entries)
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s);
+int last_edge_path();   // vrb_last_edge_path (this thread)
+// The bucket path of rank_edges (edge_buckets.cu); false when it does not
+// apply (then nothing was written and the radix path runs).
+bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s,
+                        int64_t* nvals);
 // The sort of rank_edges alone: key[q] + bias = length bits of the q-th edge
 // in (len, i, j) order; val[q] = packed (i << 16 | j) when packed, else the
 // lex index into ke.ei / ke.ej.  Buffers owned here or by ke (keep both alive).

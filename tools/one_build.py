@@ -23,5 +23,6 @@ for _ in range(reps):
     r = (vrb.build_dm(X, maxdim=w.maxdim, radius=w.radius) if w.kind == "matrix"
          else vrb.build(X, maxdim=w.maxdim, radius=w.radius))
     torch.cuda.synchronize()
+    print("edge path", vrb.last_edge_path())
     del r
 print("done", cfg, reps)
