@@ -482,7 +482,7 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
     // the scatter in slices of the bucket range, so that the sectors it
     // writes partially (one per bucket) stay L2-resident until complete
     const int64_t frontier = nb * 32;   // bytes of partial sectors if all buckets were active
-    int passes = (int)std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(frontier, (int64_t)32 << 20)));
+    int passes = (int)std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(frontier, (int64_t)16 << 20)));
     if (const char* ev = std::getenv("VRB_BK_PASSES")) passes = std::max(1, std::atoi(ev));
     DBuf<uint32_t> slices(passes + 1, s);
     k_bk_chunks<<<1, 32, 0, s>>>(off.get(), nb, passes, (uint64_t)ceil_div(E, passes), slices.get());
