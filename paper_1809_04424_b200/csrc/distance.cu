@@ -272,19 +272,12 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
 // 16 folds, as in k_dist_mask).  The fold is the same RN sequence
 // (t = x_ic - x_jc; acc = acc + t * t; len = sqrt(acc)).  The pass also
 // reduces min / max / OR of the length bits for the edge sort (key_range).
-__global__ void __launch_bounds__(kThreads) k_dist_full(const double* __restrict__ X, int64_t n, int d, int64_t nt,
-                                                        uint64_t* __restrict__ key, uint32_t* __restrict__ ei,
-                                                        uint32_t* __restrict__ ej, uint32_t* __restrict__ pij,
-                                                        int64_t ti_lo, int64_t ti_hi, int64_t mask_base,
-                                                        unsigned long long* __restrict__ range) {
-    int64_t ti, tj;
-    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
-    __shared__ double sA[kDC][kT];
-    __shared__ double sB[kDC][kT];
+// The 4 x 4 register-tiled fold of the 64 x 64 tile (i0, j0): thread
+// (tx, ty) holds the squared lengths of rows i0 + ty + 16 p, columns
+// j0 + tx + 16 q (the same RN sequence t = x_ic - x_jc; acc = acc + t * t).
+__device__ __forceinline__ void fold_tile(const double* __restrict__ X, int64_t n, int d, int64_t i0, int64_t j0,
+                                          double (&sA)[kDC][kT], double (&sB)[kDC][kT], double (&acc)[4][4]) {
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t i0 = ti * kT, j0 = tj * kT;
-    const int64_t row_lo = ti_lo * kT;
-    double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -316,6 +309,22 @@ __global__ void __launch_bounds__(kThreads) k_dist_full(const double* __restrict
                 }
         }
     }
+}
+
+__global__ void __launch_bounds__(kThreads) k_dist_full(const double* __restrict__ X, int64_t n, int d, int64_t nt,
+                                                        uint64_t* __restrict__ key, uint32_t* __restrict__ ei,
+                                                        uint32_t* __restrict__ ej, uint32_t* __restrict__ pij,
+                                                        int64_t ti_lo, int64_t ti_hi, int64_t mask_base,
+                                                        unsigned long long* __restrict__ range) {
+    int64_t ti, tj;
+    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    __shared__ double sA[kDC][kT];
+    __shared__ double sB[kDC][kT];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = ti * kT, j0 = tj * kT;
+    const int64_t row_lo = ti_lo * kT;
+    double acc[4][4];
+    fold_tile(X, n, d, i0, j0, sA, sB, acc);
     uint64_t mn = ~0ull, mx = 0ull, orr = 0ull;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -565,6 +574,7 @@ bool place_points(const double* X, int64_t n, int d, uint32_t flags, cudaStream_
 }
 
 int64_t edge_tile() { return kT; }
+
 
 void build_kept_edges(const double* X, int64_t n, int d, double radius, bool strict, cudaStream_t s,
                       KeptEdges& out, int64_t row_lo, int64_t row_hi) {

@@ -30,6 +30,7 @@
 // record that would not fit 64 bits: the caller runs the radix path.
 #include <algorithm>
 #include <cstdlib>
+#include <functional>
 
 #include "vrb_internal.cuh"
 #include "vrb_stages.cuh"
@@ -425,13 +426,24 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
 
 }  // namespace
 
-bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s,
-                        int64_t* nvals) {
-    const int64_t E = ke.E;
-    if (E < 2) return false;
-    uint64_t kmin = 0;
-    const uint64_t vary = key_range(ke.key.get(), E, s, &kmin, ke.range.get());
-    if (!vary) return false;   // one length: the radix path is trivial
+namespace {
+// The bucket parameters and the common finish (scan, scatter passes, chunk
+// ranking) of both front ends: hist(shift, cnt) counts the buckets of
+// (key - kmin) >> shift; scatter(P, cur, rec, slices, slice) writes the
+// records of the buckets in the slice.
+struct BkPlan {
+    int64_t E = 0, n = 0;
+    uint64_t kmin = 0, vary = 0;
+    int bn_avail = 0;      // > 0: packed ids of bn bits available for the record
+};
+using HistFn = std::function<void(const FoldBk&)>;
+using ScatterFn = std::function<void(const FoldBk&)>;
+
+bool bucket_rank(const BkPlan& P, const HistFn& hist, const ScatterFn& scatter, const KeptEdges* ke, uint32_t* ev,
+                 uint32_t* efilt, double* vor, cudaStream_t s, int64_t* nvals) {
+    const int64_t E = P.E;
+    const uint64_t vary = P.vary, kmin = P.kmin;
+    if (E < 2 || !vary) return false;   // one length: the radix path is trivial
     const int blen = 64 - __builtin_clzll(vary);
     const int tz = __builtin_ctzll(vary);
     int lgE = 0;
@@ -444,14 +456,16 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
     int vb = 1;
     while (vb < 64 && ((uint64_t)(E - 1) >> vb)) ++vb;
     int bn = 0;
-    if (ke.packed) {
-        int b = 1;
-        while (((uint64_t)(n - 1) >> b)) ++b;
-        if ((shift - tz) + 2 * b <= 64 || E > ((int64_t)1 << 26)) bn = b;
-    }
+    if (P.bn_avail && ((shift - tz) + 2 * P.bn_avail <= 64 || E > ((int64_t)1 << 26)))
+        bn = P.bn_avail;
     if (bn) vb = 2 * bn;
     if ((shift - tz) + vb > 64) shift = (64 - vb) + tz;   // more buckets so the record fits
     if (blen - shift > kBkMaxLogNB) return false;
+    FoldBk F;
+    F.kmin = kmin;
+    F.tz = tz;
+    F.vb = vb;
+    F.bn = bn;
     DBuf<uint32_t> cnt;
     DBuf<unsigned> mx(1, s);
     int64_t nb = 0;
@@ -460,8 +474,10 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
         cnt.alloc(nb, s);
         VRB_CUDA(cudaMemsetAsync(cnt.get(), 0, nb * sizeof(uint32_t), s));
         VRB_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned), s));
-        k_bk_hist<4><<<grid_cap(E, 256 * 4), 256, 0, s>>>(ke.key.get(), E, kmin, shift, cnt.get());
-        VRB_LAUNCH_CHECK();
+        F.shift = shift;
+        F.nb = nb;
+        F.cnt = cnt.get();
+        hist(F);
         k_bk_max<<<grid_cap(nb, 256), 256, 0, s>>>(cnt.get(), nb, mx.get());
         VRB_LAUNCH_CHECK();
         unsigned h = 0;
@@ -483,18 +499,16 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
     // writes partially (one per bucket) stay L2-resident until complete
     const int64_t frontier = nb * 32;   // bytes of partial sectors if all buckets were active
     int passes = (int)std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(frontier, (int64_t)16 << 20)));
-    if (const char* ev = std::getenv("VRB_BK_PASSES")) passes = std::max(1, std::atoi(ev));
+    if (const char* ep = std::getenv("VRB_BK_PASSES")) passes = std::max(1, std::atoi(ep));
     DBuf<uint32_t> slices(passes + 1, s);
     k_bk_chunks<<<1, 32, 0, s>>>(off.get(), nb, passes, (uint64_t)ceil_div(E, passes), slices.get());
     VRB_LAUNCH_CHECK();
+    F.cnt = cnt.get();
+    F.rec = rec.get();
+    F.slices = slices.get();
     for (int sl = 0; sl < passes; ++sl) {
-        if (bn)
-            k_bk_scatter<VRB_BK_ITEMS, true><<<grid_cap(E, 256 * VRB_BK_ITEMS), 256, 0, s>>>(
-                ke.key.get(), E, kmin, shift, tz, vb, ke.pij.get(), bn, cnt.get(), rec.get(), slices.get(), sl);
-        else
-            k_bk_scatter<VRB_BK_ITEMS, false><<<grid_cap(E, 256 * VRB_BK_ITEMS), 256, 0, s>>>(
-                ke.key.get(), E, kmin, shift, tz, vb, nullptr, 0, cnt.get(), rec.get(), slices.get(), sl);
-        VRB_LAUNCH_CHECK();
+        F.slice = sl;
+        scatter(F);
     }
     cnt.reset();
     const int64_t nchunks = ceil_div(E, kBkC);
@@ -510,15 +524,17 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
     A.rec = rec.get();
     A.off = off.get();
     A.cb = cb.get();
-    A.n = n;
+    A.n = P.n;
     A.kmin = kmin;
     A.shift = shift;
     A.tz = tz;
     A.vb = vb;
     A.bn = bn;
-    A.pij = ke.packed ? ke.pij.get() : nullptr;
-    A.ei = ke.packed ? nullptr : ke.ei.get();
-    A.ej = ke.packed ? nullptr : ke.ej.get();
+    if (!bn) {   // lex-index records: the ids are gathered
+        A.pij = ke->packed ? ke->pij.get() : nullptr;
+        A.ei = ke->packed ? nullptr : ke->ei.get();
+        A.ej = ke->packed ? nullptr : ke->ej.get();
+    }
     A.ev = ev;
     A.efilt = efilt;
     A.vor = vor;
@@ -531,6 +547,40 @@ bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt,
     VRB_CUDA(cudaStreamSynchronize(s));
     *nvals = nv;
     return true;
+}
+
+int bits_of(int64_t n) {
+    int b = 1;
+    while (((uint64_t)(n - 1) >> b)) ++b;
+    return b;
+}
+}  // namespace
+
+bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s,
+                        int64_t* nvals) {
+    const int64_t E = ke.E;
+    if (E < 2) return false;
+    BkPlan P;
+    P.E = E;
+    P.n = n;
+    P.vary = key_range(ke.key.get(), E, s, &P.kmin, ke.range.get());
+    P.bn_avail = ke.packed ? bits_of(n) : 0;
+    const uint64_t* key = ke.key.get();
+    const uint32_t* pij = ke.pij.get();
+    auto hist = [&](const FoldBk& F) {
+        k_bk_hist<4><<<grid_cap(E, 256 * 4), 256, 0, s>>>(key, E, F.kmin, F.shift, F.cnt);
+        VRB_LAUNCH_CHECK();
+    };
+    auto scatter = [&](const FoldBk& F) {
+        if (F.bn)
+            k_bk_scatter<VRB_BK_ITEMS, true><<<grid_cap(E, 256 * VRB_BK_ITEMS), 256, 0, s>>>(
+                key, E, F.kmin, F.shift, F.tz, F.vb, pij, F.bn, F.cnt, F.rec, F.slices, F.slice);
+        else
+            k_bk_scatter<VRB_BK_ITEMS, false><<<grid_cap(E, 256 * VRB_BK_ITEMS), 256, 0, s>>>(
+                key, E, F.kmin, F.shift, F.tz, F.vb, nullptr, 0, F.cnt, F.rec, F.slices, F.slice);
+        VRB_LAUNCH_CHECK();
+    };
+    return bucket_rank(P, hist, scatter, &ke, ev, efilt, vor, s, nvals);
 }
 
 }  // namespace vrb

@@ -45,10 +45,24 @@ void latlon2euc(const double* latlon, int64_t n, double* xyz, cudaStream_t s);
 //   vor   : >= nvals f64, vor[f-1] = length of level f  (caller-allocated, E entries)
 int64_t rank_edges(KeptEdges& ke, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s);
 int last_edge_path();   // vrb_last_edge_path (this thread)
+void note_edge_path(int path);
+bool fused_edges_enabled();   // VRB_EDGE_PATH unset or "fused"
 // The bucket path of rank_edges (edge_buckets.cu); false when it does not
 // apply (then nothing was written and the radix path runs).
 bool rank_edges_buckets(KeptEdges& ke, int64_t n, uint32_t* ev, uint32_t* efilt, double* vor, cudaStream_t s,
                         int64_t* nvals);
+// Bucket parameters handed to the count and scatter passes of the bucket
+// path (edge_buckets.cu): counts cnt[(bits - kmin) >> shift]; records of the
+// buckets in [slices[slice], slices[slice + 1]) at atomicAdd(&cnt[b], 1).
+struct FoldBk {
+    uint64_t kmin = 0;
+    int shift = 0, tz = 0, vb = 0, bn = 0;
+    int64_t nb = 0;
+    uint32_t* cnt = nullptr;
+    uint64_t* rec = nullptr;
+    const uint32_t* slices = nullptr;
+    int slice = 0;
+};
 // The sort of rank_edges alone: key[q] + bias = length bits of the q-th edge
 // in (len, i, j) order; val[q] = packed (i << 16 | j) when packed, else the
 // lex index into ke.ei / ke.ej.  Buffers owned here or by ke (keep both alive).
