@@ -244,6 +244,7 @@ def main():
 
     vrb.set_profiling(True)
     step_ms, fill_ms, tet_ms, stage_acc = [], [], [], {}
+    edge_path = None
     counts = None
     launches = 0
     s = torch.cuda.current_stream()
@@ -266,6 +267,7 @@ def main():
                 stage_acc[k] = stage_acc.get(k, 0.0) + v
             if counts is None:
                 counts = [r.count(k) for k in range(w.maxdim + 2)]
+                edge_path = vrb.last_edge_path()
             del r
     vrb.set_profiling(False)
     # F1 (outside the step): dimension-0 persistence of a build, device-timed;
@@ -331,6 +333,11 @@ def main():
         bytes_per_launch, kern_ms = TET_OUT_BYTES * Q_local, tet_avg
     elif T_local and fill_avg > 0:
         kname, bytes_per_launch, kern_ms = "k_triangles<fill>", TRI_OUT_BYTES * T_local, fill_avg
+    elif w.maxdim == 0 and stage_acc.get("edge_rank", 0.0) > 0:
+        # edges only (C5A): S3 as a whole against SURVEY 8(d)'s 44 B per edge
+        # (sort payload written and read once + the edge outputs)
+        kname = "S3 edge rank (" + edge_path + " path)"
+        bytes_per_launch, kern_ms = SURVEY_BALG["edge_k1"] * counts[1][2], stage_acc["edge_rank"] / args.steps
     else:
         kname = None
     if kname:
@@ -409,6 +416,7 @@ def main():
             "path_roofline": {"survey_balg_bytes": int(balg), "achieved_gbs": path_gbs, "peak": peak,
                               "frac": path_gbs / peak},
             "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
+            "edge_path": edge_path,
             "clocks": clocks.summary(),
             "h0_barcodes": h0,
             "e2e": e2e,

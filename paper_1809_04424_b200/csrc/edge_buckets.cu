@@ -50,6 +50,15 @@ namespace {
 #ifndef VRB_BK_THREADS
 #define VRB_BK_THREADS 512
 #endif
+// -DVRB_BK_CHECKS: device asserts on every shared-memory index and scatter
+// slot (an experiment build, tests/test_edge_buckets_gpu.py under it; the
+// pool has no compute-sanitizer)
+#ifdef VRB_BK_CHECKS
+#include <cassert>
+#define BK_ASSERT(c) assert(c)
+#else
+#define BK_ASSERT(c) ((void)0)
+#endif
 constexpr int kBkC = VRB_BK_C;          // chunk k = the buckets whose first item lies in [k C, (k+1) C)
 constexpr int kBkMax = 2 * kBkC;        // items of a chunk: < C + largest bucket <= 2 C
 constexpr int kBkThreads = VRB_BK_THREADS;
@@ -164,6 +173,7 @@ __global__ void __launch_bounds__(256) k_bk_scatter(const uint64_t* __restrict__
             if (inr[u]) {
                 const uint64_t d = k[u] - kmin;
                 const uint64_t r = (((d & low) >> tz) << lowbits) | idv[u];
+                BK_ASSERT(slot[u] < (uint64_t)E);
                 if (VRB_BK_KEEP)
                     st_keep(rec + slot[u], r, pol);
                 else
@@ -233,6 +243,7 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
     const int64_t p0 = (int64_t)A.off[ba];
     const int m = (int)((int64_t)A.off[bb] - p0);
     const uint32_t nbk = bb - ba;
+    BK_ASSERT(m >= 0 && m <= kBkMax);
     const bool staged = nbk <= (uint32_t)kBkOffStage;
     if (staged)
         for (int t = tid; t <= (int)nbk; t += kBkThreads) s_off[t] = (uint16_t)(A.off[ba + t] - p0);
@@ -257,6 +268,7 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
         const uint64_t res = s_rec[t] >> vb;
         const uint32_t sub = L >= rbits ? (uint32_t)(res << (L - rbits)) : (uint32_t)(res >> (rbits - L));
         const uint32_t sb = 4u * (uint32_t)st + sub;
+        BK_ASSERT(st <= t && t < st + mb && sub < (1u << L) && sb < 4u * (uint32_t)(st + mb));
         s_sb[t] = (uint16_t)sb;
         s_bl[t] = lo;
         atomicAdd(&s_cw[sb >> 1], 1u << (16 * (sb & 1)));
@@ -303,7 +315,9 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
     // ---- counting-sort scatter by sub-bucket; afterwards s_c16[x] = end of x
     for (int t = tid; t < m; t += kBkThreads) {
         const uint32_t sb = s_sb[t], sh = 16 * (sb & 1);
-        s_tmp[(atomicAdd(&s_cw[sb >> 1], 1u << sh) >> sh) & 0xFFFFu] = (uint16_t)t;
+        const uint32_t slot = (atomicAdd(&s_cw[sb >> 1], 1u << sh) >> sh) & 0xFFFFu;
+        BK_ASSERT(slot < (uint32_t)m);
+        s_tmp[slot] = (uint16_t)t;
     }
     __syncthreads();
     // ---- final place: rank inside the sub-bucket (records are distinct)
@@ -313,6 +327,7 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
         const uint64_t r = s_rec[t];
         int pos = lo;
         for (int u = lo; u < hi; ++u) pos += s_rec[s_tmp[u]] < r ? 1 : 0;
+        BK_ASSERT(lo <= pos && pos < hi && hi <= m);
         s_perm[pos] = (uint16_t)t;
     }
     __syncthreads();

@@ -43,6 +43,13 @@ def edges_equal(vrb, X, radius, strict=False, maxdim=0):
     return path, res
 
 
+@pytest.fixture(autouse=True)
+def _bucket_path(monkeypatch):
+    # the library takes the bucket path by default from 2^24 edges; these
+    # cases force it (tests that want the radix path set it themselves)
+    monkeypatch.setenv("VRB_EDGE_PATH", "bucket")
+
+
 @pytest.mark.parametrize("seed", range(24))
 def test_bucket_path_random(vrb, seed, monkeypatch):
     # continuous clouds: the bucket path must run and agree with the oracle
@@ -92,7 +99,7 @@ def test_full_filtration_both_paths(vrb):
     try:
         path, _ = edges_equal(vrb, X, math.inf)
     finally:
-        del os.environ["VRB_EDGE_PATH"]
+        os.environ["VRB_EDGE_PATH"] = "bucket"
     assert path == "radix"
 
 
@@ -145,6 +152,14 @@ def test_bucket_path_triangles(vrb):
     X = workloads.random_cloud(7600, 400, 4, "gauss")
     res, _ = compare(vrb, X, 1, 2.0)
     assert vrb.last_edge_path() == "bucket"
+
+
+def test_default_choice(vrb, monkeypatch):
+    # unset: small builds take the radix passes
+    monkeypatch.delenv("VRB_EDGE_PATH")
+    X = workloads.random_cloud(7800, 500, 3, "uniform")
+    path, _ = edges_equal(vrb, X, math.inf)
+    assert path == "radix"
 
 
 def test_tiny(vrb):

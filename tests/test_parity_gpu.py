@@ -548,6 +548,7 @@ def test_c5a_edges_full(vrb):
     w = workloads.WORKLOADS["C5A"]
     X = w.points()
     res = vrb.build(torch.from_numpy(X).cuda(), maxdim=0, radius=math.inf)
+    assert vrb.last_edge_path() == "bucket"   # the path bench.py times for C5A
     n = X.shape[0]
     E = n * (n - 1) // 2
     assert res.count(1)[0] == E

@@ -64,3 +64,17 @@ rv = torch.tensor([0, 1, 1], dtype=torch.int32, device="cuda")
 vrb.gf2_blockprodsum(2, (cp, rv), (cp, rv), (cp, rv))
 torch.cuda.synchronize()
 print("sanitize run ok")
+# round 2, third session: the S3 bucket path (several chunks, refinement,
+# sliced scatter) and the forced radix path on the same cloud
+Xb = workloads.random_cloud(11, 2500, 10, "gauss")
+vrb.build(Xb, maxdim=0, radius=math.inf)
+vrb.build(Xb, maxdim=1, radius=2.0)
+os.environ["VRB_BK_PASSES"] = "3"
+vrb.build(Xb, maxdim=0, radius=math.inf)
+del os.environ["VRB_BK_PASSES"]
+os.environ["VRB_EDGE_PATH"] = "radix"
+vrb.build(Xb, maxdim=0, radius=math.inf)
+del os.environ["VRB_EDGE_PATH"]
+torch.cuda.synchronize()
+print("sanitize_run done")
+
