@@ -320,17 +320,40 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
         s_tmp[slot] = (uint16_t)t;
     }
     __syncthreads();
-    // ---- final place: rank inside the sub-bucket (records are distinct)
+    // ---- final place: rank inside the sub-bucket (records are distinct);
+    // an item with an equal residual (an equal length: same bucket, same
+    // sub-bucket) and a smaller record is not a head of its level
+    uint32_t dups = 0;
     for (int t = tid; t < m; t += kBkThreads) {
         const uint32_t sb = s_sb[t];
         const int lo = sb ? (int)s_c16[sb - 1] : 0, hi = (int)s_c16[sb];
         const uint64_t r = s_rec[t];
         int pos = lo;
-        for (int u = lo; u < hi; ++u) pos += s_rec[s_tmp[u]] < r ? 1 : 0;
+        bool dup = false;
+        for (int u = lo; u < hi; ++u) {
+            const uint64_t ru = s_rec[s_tmp[u]];
+            pos += ru < r ? 1 : 0;
+            dup |= ru < r && (ru >> vb) == (r >> vb);
+        }
         BK_ASSERT(lo <= pos && pos < hi && hi <= m);
         s_perm[pos] = (uint16_t)t;
+        dups += dup ? 1u : 0u;
     }
+    dups = __reduce_add_sync(0xffffffffu, dups);
+    if (lane == 0) s_hm[wid] = dups;   // (s_hm reused below for head ballots)
     __syncthreads();
+    // the chunk's distinct-length count goes out first (successors look back
+    // on it); then every warp records its head ballots and writes its (i, j)
+    // -- they need no rank offset -- and warp 0 looks back for the prefix
+    volatile unsigned long long* st = A.status;
+    uint32_t total = 0;
+    if (wid == 0) {
+        uint32_t dsum = lane < kBkWarps ? s_hm[lane] : 0u;
+        dsum = __reduce_add_sync(0xffffffffu, dsum);
+        total = (uint32_t)m - dsum;
+        if (lane == 0) st[tile] = (tile == 0 ? kBkPre : kBkAgg) | (unsigned long long)total;
+    }
+    __syncthreads();   // s_hm free again
     // ---- heads in the final order: a bucket start (the chunk's first item
     // too: the previous chunk ends with another bucket) or a new residual
     const int chunk = ((m + kBkWarps - 1) / kBkWarps + 31) & ~31;
@@ -341,41 +364,18 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
         return s_bl[w] != s_bl[wp] || (s_rec[w] >> vb) != (s_rec[wp] >> vb);
     };
     uint32_t wheads = 0;
-    for (int r0 = c0; r0 < c1; r0 += 32) {   // r0: a multiple of 32
-        const int t = r0 + lane;
-        const bool h = t < c1 && head_at(t, s_perm[t]);
-        const unsigned bal = __ballot_sync(0xffffffffu, h);
-        if (lane == 0) s_hm[r0 >> 5] = bal;
-        wheads += __popc(bal);
-    }
-    __syncthreads();   // s_wtot is reused
-    if (lane == 0) s_wtot[wid] = wheads;
-    __syncthreads();
-    // the chunk's distinct-length count goes out first (successors look back
-    // on it), then every warp writes its (i, j) -- they need no rank offset --
-    // while warp 0 looks back for the chunk's dense-rank prefix
-    volatile unsigned long long* st = A.status;
-    uint32_t total = 0;
-    if (wid == 0) {
-        const uint32_t v = lane < kBkWarps ? s_wtot[lane] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane == 0) st[tile] = (tile == 0 ? kBkPre : kBkAgg) | (unsigned long long)total;
-        __syncwarp();
-        if (lane < kBkWarps) s_wtot[lane] = incl - v;   // exclusive per warp (read after the next barrier)
-    }
     {
         const uint64_t qmask = (1ull << vb) - 1ull;
         const uint64_t jmask = (1ull << A.bn) - 1ull;
-        for (int r0 = c0; r0 < c1; r0 += 32) {
+        for (int r0 = c0; r0 < c1; r0 += 32) {   // r0: a multiple of 32
             const int t = r0 + lane;
+            const int w = t < c1 ? s_perm[t] : 0;
+            const bool h = t < c1 && head_at(t, w);
+            const unsigned bal = __ballot_sync(0xffffffffu, h);
+            if (lane == 0) s_hm[r0 >> 5] = bal;
+            wheads += __popc(bal);
             if (t < c1) {
-                const uint64_t q = s_rec[s_perm[t]] & qmask;
+                const uint64_t q = s_rec[w] & qmask;
                 uint2 e;
                 if (A.bn) {
                     e = make_uint2((uint32_t)(q >> A.bn), (uint32_t)(q & jmask));
@@ -388,6 +388,19 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
                 __stcs(reinterpret_cast<uint2*>(A.ev) + p0 + t, e);
             }
         }
+    }
+    if (lane == 0) s_wtot[wid] = wheads;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t v = lane < kBkWarps ? s_wtot[lane] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        BK_ASSERT(__shfl_sync(0xffffffffu, incl, 31) == total);
+        if (lane < kBkWarps) s_wtot[lane] = incl - v;   // exclusive per warp
     }
     if (wid == 0) {
         unsigned long long excl = 0;
