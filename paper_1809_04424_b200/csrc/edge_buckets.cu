@@ -68,7 +68,10 @@ constexpr int kBkOffStage = 1024;       // a chunk's bucket offsets staged in sh
 constexpr int kBkMaxLogNB = 23;
 constexpr unsigned long long kBkAgg = 1ull << 62, kBkPre = 2ull << 62, kBkVal = (1ull << 62) - 1;
 
-constexpr size_t kBkSmem = kBkMax * sizeof(uint64_t)          // s_rec
+#ifndef VRB_BK_TMA
+#define VRB_BK_TMA 1   // the chunk's records come in by one cp.async.bulk (TMA) copy on an mbarrier
+#endif
+constexpr size_t kBkSmem = (kBkMax + 2) * sizeof(uint64_t)    // s_rec (+ 16-byte alignment slack)
                            + 4 * kBkMax * sizeof(uint16_t)    // s_c16 (sub-bucket counts, then ends; packed u16)
                            + kBkMax * sizeof(uint32_t)        // s_bl (bucket of an item, chunk-relative)
                            + 3 * kBkMax * sizeof(uint16_t)    // s_sb, s_tmp, s_perm
@@ -223,8 +226,8 @@ struct BkArgs {
 
 __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) {
     extern __shared__ __align__(16) unsigned char bk_smem[];
-    uint64_t* s_rec = reinterpret_cast<uint64_t*>(bk_smem);
-    uint32_t* s_cw = reinterpret_cast<uint32_t*>(s_rec + kBkMax);   // 4 kBkMax u16 counters, two per word
+    uint64_t* s_raw = reinterpret_cast<uint64_t*>(bk_smem);
+    uint32_t* s_cw = reinterpret_cast<uint32_t*>(s_raw + kBkMax + 2);   // 4 kBkMax u16 counters, two per word
     uint16_t* s_c16 = reinterpret_cast<uint16_t*>(s_cw);
     uint32_t* s_bl = s_cw + 2 * kBkMax;
     uint16_t* s_sb = reinterpret_cast<uint16_t*>(s_bl + kBkMax);
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
     __shared__ uint32_t s_wtot[kBkWarps];
     __shared__ unsigned long long s_prefix;
     __shared__ uint32_t s_hm[kBkMax / 32];   // head flags of the final order, one ballot per 32 positions
+    __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(A.counter, 1u);
     __syncthreads();
@@ -243,14 +247,44 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
     const int64_t p0 = (int64_t)A.off[ba];
     const int m = (int)((int64_t)A.off[bb] - p0);
     const uint32_t nbk = bb - ba;
+#if VRB_BK_TMA
+    // records [p0, p0 + m) by one bulk copy from the 16-byte aligned address
+    // at or below (rec is padded by two records), while the threads stage the
+    // offsets and clear the counters
+    const uint64_t* src = A.rec + p0;
+    const int lead = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    uint64_t* s_rec = s_raw + lead;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    if (tid == 0 && m > 0) {
+        const uint32_t bytes = (uint32_t)(((m + lead) * 8 + 15) & ~15);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(s_raw)), "l"(src - lead), "r"(bytes), "r"(bar)
+                     : "memory");
+    }
+#else
+    uint64_t* s_rec = s_raw;
+#endif
     BK_ASSERT(m >= 0 && m <= kBkMax);
     const bool staged = nbk <= (uint32_t)kBkOffStage;
     if (staged)
         for (int t = tid; t <= (int)nbk; t += kBkThreads) s_off[t] = (uint16_t)(A.off[ba + t] - p0);
+#if !VRB_BK_TMA
     for (int t = tid; t < m; t += kBkThreads)
         s_rec[t] = __ldcs(reinterpret_cast<const unsigned long long*>(A.rec) + p0 + t);
+#endif
     for (int t = tid; t < 2 * m; t += kBkThreads) s_cw[t] = 0u;   // 4m u16 counters
-    __syncthreads();
+    __syncthreads();   // (the barrier is initialised before any thread waits on it)
+#if VRB_BK_TMA
+    if (m > 0) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                         "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(bar) : "memory");
+    }
+#endif
     auto off_of = [&](uint32_t bl) -> int { return staged ? (int)s_off[bl] : (int)((int64_t)A.off[ba + bl] - p0); };
     const int vb = A.vb;
     const int rbits = A.shift - A.tz;   // residual bits
@@ -522,7 +556,7 @@ bool bucket_rank(const BkPlan& P, const HistFn& hist, const ScatterFn& scatter, 
     exclusive_scan(cnt.get(), off.get(), nb, s);
     k_bk_cursor<<<grid_cap(nb, 256), 256, 0, s>>>(off.get(), nb, cnt.get());   // cnt becomes the cursors
     VRB_LAUNCH_CHECK();
-    DBuf<uint64_t> rec(E, s);
+    DBuf<uint64_t> rec(E + 2, s);   // + 2: the chunk copies round to 16 bytes
     // the scatter in slices of the bucket range, so that the sectors it
     // writes partially (one per bucket) stay L2-resident until complete
     const int64_t frontier = nb * 32;   // bytes of partial sectors if all buckets were active
