@@ -53,29 +53,54 @@ __device__ __forceinline__ void tile_of_block(int64_t b, int64_t nt, int64_t ti_
     tj = ti + (q - tile_index(ti, ti, nt));
 }
 
+// The same, computed once per CTA (thread 0) and broadcast: the search is
+// ~90 instructions per thread when every thread runs it.
+__device__ __forceinline__ void tile_of_cta(int64_t nt, int64_t ti_lo, int64_t ti_hi, int64_t mask_base, int64_t& ti,
+                                            int64_t& tj) {
+    __shared__ int64_t s_tile[2];
+    if (threadIdx.x == 0) tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, s_tile[0], s_tile[1]);
+    __syncthreads();
+    ti = s_tile[0];
+    tj = s_tile[1];
+}
+
 // Tile rows [ti_lo, ti_lo + gridDim.y) (a rank's row block);
 // masks are indexed from the block's first tile (mask_base) and the per
 // (row, tile) counts from its first row.
+// The cap decision per pair, d2 <= thr (thr = T(r), reading A1), taken on
+// an FP32 fold of the coordinates rounded to float, with a rigorous error
+// bound, and by the exact FP64 fold of the fixed RN sequence only when the
+// FP32 value lies within the bound of thr:
+//   x' = fl32(x): |x' - x| <= u|x|, u = 2^-24; t' = fl(x'_i - x'_j):
+//   |t' - t| <= 2.1 u (|x_i| + |x_j|) <= 4.2 u M (M = max |coordinate| over
+//   the tile's points); |t'^2 - t^2| <= 4.2 u M (4M + 1) <= 17 u M^2 + 4.2 u M;
+//   FMA accumulation of d terms: |s' - sum t'^2| <= 1.01 d u sum t'^2.
+//   So |s' - d2| <= d (17 u M^2 + 4.2 u M) + 1.05 d u s' (+ the FP64 fold's
+//   own rounding, < 1e-15 d d2, and subnormal slack): B below doubles it.
+// The FP32 fold costs 2 FP32 ops per coordinate against 3 FP64 ops (B200
+// runs FP32 at twice the FP64 rate); undecided pairs are ~1e-5 of all.
 __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict__ X, int64_t n, int d,
                                                         int64_t nt, double thr, int all,
                                                         unsigned long long* __restrict__ masks,
                                                         uint32_t* __restrict__ rowtile_cnt, int64_t ti_lo,
                                                         int64_t ti_hi, int64_t mask_base) {
     int64_t ti, tj;
-    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
-    __shared__ double sA[kDC][kT];
-    __shared__ double sB[kDC][kT];
+    tile_of_cta(nt, ti_lo, ti_hi, mask_base, ti, tj);
+    __shared__ float fA[kDC][kT];
+    __shared__ float fB[kDC][kT];
     __shared__ unsigned long long mrow[kT];
+    __shared__ unsigned s_m;   // max |coordinate| of the tile's points (float bits)
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int64_t i0 = ti * kT, j0 = tj * kT;
-    if (threadIdx.x < kT) mrow[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) s_m = 0u;
 
-    double acc[4][4];
+    float acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+    float mloc = 0.0f;
+    bool huge = false;
     if (!all) {
         for (int c0 = 0; c0 < d; c0 += kDC) {
             const int dc = min(kDC, d - c0);
@@ -87,25 +112,34 @@ __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict
                     if (i0 + r < n) va = X[(i0 + r) * d + c0 + c];
                     if (j0 + r < n) vb = X[(j0 + r) * d + c0 + c];
                 }
-                sA[c][r] = va;
-                sB[c][r] = vb;
+                huge |= !(fabs(va) < 1e15) || !(fabs(vb) < 1e15);
+                fA[c][r] = __double2float_rn(va);
+                fB[c][r] = __double2float_rn(vb);
+                mloc = fmaxf(mloc, fmaxf(fabsf(fA[c][r]), fabsf(fB[c][r])));
             }
             __syncthreads();
             for (int c = 0; c < dc; ++c) {
-                double a[4], b[4];
+                float a[4], b[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) { a[q] = sA[c][ty + 16 * q]; b[q] = sB[c][tx + 16 * q]; }
+                for (int q = 0; q < 4; ++q) { a[q] = fA[c][ty + 16 * q]; b[q] = fB[c][tx + 16 * q]; }
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const double t = __dsub_rn(a[p], b[q]);
-                        acc[p][q] = __dadd_rn(acc[p][q], __dmul_rn(t, t));
+                        const float t = __fsub_rn(a[p], b[q]);
+                        acc[p][q] = __fmaf_rn(t, t, acc[p][q]);
                     }
             }
         }
     }
+    // huge coordinates (float overflow / the bound's squares): every pair exact
+    atomicMax(&s_m, huge ? 0x7F800000u : __float_as_uint(mloc));
     __syncthreads();
+    const double M = (double)__uint_as_float(s_m) * (1.0 + 1e-6);   // |x'| <= M: |x| <= M (1 + u)
+    const bool exact_all = s_m >= 0x7F800000u;
+    const double u = 5.9604644775390625e-08;   // 2^-24
+    const double Bc = 2.0 * (double)d * (17.0 * u * M * M + 4.2 * u * M) + 1e-30;
+    const double Bs = 2.0 * 1.05 * (double)d * u + 1e-15 * (double)d;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int64_t i = i0 + ty + 16 * p;
@@ -113,10 +147,30 @@ __global__ void __launch_bounds__(kThreads) k_dist_mask(const double* __restrict
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t j = j0 + tx + 16 * q;
-            const bool keep = i < n && j < n && j > i && (all || acc[p][q] <= thr);
+            if (!(i < n && j < n && j > i)) continue;
+            bool keep = all != 0;
+            if (!all) {
+                const double s32 = (double)acc[p][q];
+                const double B = Bc + Bs * s32;
+                if (!exact_all && s32 + B <= thr) {
+                    keep = true;
+                } else if (!exact_all && s32 - B > thr) {
+                    keep = false;
+                } else {   // undecided: the exact FP64 fold (A5)
+                    double e = 0.0;
+                    for (int c = 0; c < d; ++c) {
+                        const double t = __dsub_rn(X[i * d + c], X[j * d + c]);
+                        e = __dadd_rn(e, __dmul_rn(t, t));
+                    }
+                    keep = e <= thr;
+                }
+            }
             if (keep) bits |= 1ull << (tx + 16 * q);
         }
-        if (bits) atomicOr(&mrow[ty + 16 * p], bits);
+        // the row's 16 threads are one half-warp (lanes tx): OR their bits
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        if (tx == 0) mrow[ty + 16 * p] = bits;
     }
     __syncthreads();
     if (threadIdx.x < kT) {
@@ -147,7 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_dist_fill(const double* __restrict
                                                         uint32_t* __restrict__ pij, int64_t ti_lo,
                                                         int64_t ti_hi, int64_t mask_base) {
     int64_t ti, tj;
-    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    tile_of_cta(nt, ti_lo, ti_hi, mask_base, ti, tj);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t i0 = ti * kT, j0 = tj * kT;
     const int64_t row_lo = ti_lo * kT;
@@ -317,7 +371,7 @@ __global__ void __launch_bounds__(kThreads) k_dist_full(const double* __restrict
                                                         int64_t ti_lo, int64_t ti_hi, int64_t mask_base,
                                                         unsigned long long* __restrict__ range) {
     int64_t ti, tj;
-    tile_of_block(blockIdx.x, nt, ti_lo, ti_hi, mask_base, ti, tj);
+    tile_of_cta(nt, ti_lo, ti_hi, mask_base, ti, tj);
     __shared__ double sA[kDC][kT];
     __shared__ double sB[kDC][kT];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;

@@ -166,3 +166,20 @@ def test_tiny(vrb):
     for n in (0, 1, 2, 3):
         X = workloads.random_cloud(7700 + n, n, 2, "uniform")
         edges_equal(vrb, X, math.inf)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-3, 1e-30, 1e12, 1e17])
+def test_cap_at_pair_lengths(vrb, scale, monkeypatch):
+    # the cap decision (S2, reading A1) is taken on an FP32 fold with an
+    # error bound and re-done in FP64 near the threshold: caps exactly at
+    # pair lengths (inclusive keeps the pair, strict drops it) and one ulp
+    # around them, at scales where FP32 rounding, subnormals or overflow bite
+    monkeypatch.delenv("VRB_EDGE_PATH")
+    X = workloads.random_cloud(7900, 300, 5, "gauss") * scale
+    rng = np.random.default_rng(7901)
+    for _ in range(3):
+        i, j = sorted(rng.choice(300, 2, replace=False))
+        L = oracle.length(X, int(i), int(j))
+        for r in (L, np.nextafter(L, 0.0), np.nextafter(L, np.inf)):
+            for strict in (False, True):
+                edges_equal(vrb, X, float(r), strict=strict)
