@@ -258,195 +258,162 @@ __global__ void k_rowmap(const uint32_t* __restrict__ keep, const uint64_t* __re
 }
 
 // Columns in tiles: a thread takes kCPT consecutive columns (3 kCPT rows,
-// read as 16-byte vectors), a CTA of kCTh threads one tile of kCT columns.
-// Pass 1 sums each tile's kept rows, a scan of the tile sums gives tile
-// offsets, pass 2 scans the threads' counts in the block and writes colptr
-// and the kept (renumbered) rows -- the D_2 rows are read twice, colptr and
-// the output written once.  Whether a row survives and its new number come
-// from the (sorted) forest itself, held in shared memory with a coarse
-// index: blk[b] = #forest positions below b << shift, so a row r searches
-// forest[blk[r >> shift], blk[(r >> shift) + 1]) -- with the shift chosen so
-// a block holds about one forest position on average (the forest has n - c
-// of E edges, most of them among the shortest) -- instead of two random
-// global lookups per row.  Persistent CTAs load the
-// index once and stride over the tiles.
-constexpr int kCTh = 1024;           // threads per CTA
-constexpr int kCPT = 8;              // columns per thread (24 rows = 6 uint4)
+// read as 16-byte vectors), a CTA of kCTh threads one tile of kCT columns;
+// tiles are taken in order (a counter) and chained by a decoupled look-back
+// over their kept-row counts, so D_2's rows are read once.  Whether a row
+// survives and its new number come from a table of 16-byte entries per 64
+// edge positions (the forest's bits there, and the number of forest
+// positions below): one L2-resident load per row, all of a thread's issued
+// together (C5B: 2.4 MB for 9.7e6 edges).  Each warp stages its output (kept
+// rows and colptr) in shared memory and writes both as contiguous runs.
+#ifndef VRB_CC_THREADS
+#define VRB_CC_THREADS 512
+#endif
+#ifndef VRB_CC_CPT
+#define VRB_CC_CPT 4
+#endif
+constexpr int kCTh = VRB_CC_THREADS;   // threads per CTA
+constexpr int kCPT = VRB_CC_CPT;       // columns per thread (3 kCPT rows, 16-byte loads)
 constexpr int kCT = kCTh * kCPT;     // columns per tile
+constexpr int kCWarps = kCTh / 32;
+constexpr unsigned long long kCAgg = 1ull << 62, kCPre = 2ull << 62, kCVal = (1ull << 62) - 1;
 
-struct ForestIndex {
-    const uint32_t* f;     // sorted forest positions
-    const uint32_t* blk;   // coarse index
-    int shift;
-    __device__ __forceinline__ bool kept(uint32_t r, uint32_t& newr) const {
-        const uint32_t b = r >> shift;
-        uint32_t lo = blk[b], hi = blk[b + 1];
-        const uint32_t end = hi;
-        // lower bound of r in the block's forest positions: the forest's
-        // (short) edges crowd the first blocks, so search, not scan
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (f[mid] < r) lo = mid + 1; else hi = mid;
-        }
-        newr = r - lo;
-        return !(lo < end && f[lo] == r);
-    }
-};
-
-__device__ __forceinline__ ForestIndex load_forest(unsigned char* smem, const uint32_t* __restrict__ forest,
-                                                   int64_t nf, const uint32_t* __restrict__ blk, int64_t nblk,
-                                                   int shift, bool in_smem) {
-    if (!in_smem) return ForestIndex{forest, blk, shift};   // too large for shared memory: read it through L2
-    uint32_t* f = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* b = f + nf;
-    for (int64_t q = threadIdx.x; q < nf; q += blockDim.x) f[q] = forest[q];
-    for (int64_t q = threadIdx.x; q <= nblk; q += blockDim.x) b[q] = blk[q];
-    __syncthreads();
-    return ForestIndex{f, b, shift};
+__device__ __forceinline__ bool ftab_kept(const ulonglong2& e, uint32_t r, uint32_t& newr) {
+    const int o = (int)(r & 63u);
+    newr = r - (uint32_t)(e.y + (uint64_t)__popcll(e.x & ((1ull << o) - 1ull)));
+    return !((e.x >> o) & 1ull);
 }
 
-// the kCPT columns of thread slot j0 .. j0 + kCPT: kept flags, new rows, and
-// the number kept per column (columns >= ncols keep nothing)
-struct ColGroup {
-    uint32_t r[3 * kCPT];
-    uint32_t keepmask;   // bit 3 c + q: row q of column c kept
-};
-
-__device__ __forceinline__ uint32_t load_group(const uint32_t* __restrict__ rows, int64_t ncols, int64_t j0,
-                                               const ForestIndex& FI, ColGroup& G) {
-    if (j0 + kCPT <= ncols) {
-        const uint4* v = reinterpret_cast<const uint4*>(rows + 3 * j0);
-#pragma unroll
-        for (int q = 0; q < 3 * kCPT / 4; ++q) {
-            const uint4 w = __ldcs(v + q);
-            G.r[4 * q] = w.x; G.r[4 * q + 1] = w.y; G.r[4 * q + 2] = w.z; G.r[4 * q + 3] = w.w;
-        }
-    } else {
-#pragma unroll
-        for (int q = 0; q < 3 * kCPT; ++q) G.r[q] = j0 + q / 3 < ncols ? __ldcs(rows + 3 * j0 + q) : 0u;
-    }
-    uint32_t mask = 0, cnt = 0;
-    uint32_t last = 0xFFFFFFFFu, lastnew = 0;
-    bool lastkept = false;
-#pragma unroll
-    for (int q = 0; q < 3 * kCPT; ++q) {
-        if (j0 + q / 3 >= ncols) continue;
-        uint32_t nr;
-        bool k;
-        if (G.r[q] == last) {   // the owner edge's row repeats along its triangles
-            nr = lastnew;
-            k = lastkept;
-        } else {
-            k = FI.kept(G.r[q], nr);
-            last = G.r[q];
-            lastnew = nr;
-            lastkept = k;
-        }
-        G.r[q] = nr;
-        if (k) { mask |= 1u << q; ++cnt; }
-    }
-    G.keepmask = mask;
-    return cnt;
-}
-
-__global__ void __launch_bounds__(kCTh) k_col_tile_sums(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                        const uint32_t* __restrict__ forest, int64_t nf,
-                                                        const uint32_t* __restrict__ blk, int64_t nblk, int shift,
-                                                        int in_smem, unsigned long long* __restrict__ sums) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long red[kCTh / 32];
-    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk, shift, in_smem != 0);
-    const int64_t tiles = (ncols + kCT - 1) / kCT;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        ColGroup G;
-        unsigned long long a = load_group(rows, ncols, t * kCT + (int64_t)threadIdx.x * kCPT, FI, G);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            unsigned long long v = red[threadIdx.x];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            if (threadIdx.x == 0) sums[t] = v;
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kCTh) k_col_tile_fill(const uint32_t* __restrict__ rows, int64_t ncols,
-                                                        const uint32_t* __restrict__ forest, int64_t nf,
-                                                        const uint32_t* __restrict__ blk, int64_t nblk, int shift,
-                                                        int in_smem, const uint64_t* __restrict__ tile_off,
-                                                        uint64_t* __restrict__ colptr, uint32_t* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long wt[kCTh / 32];
-    const ForestIndex FI = load_forest(smem, forest, nf, blk, nblk, shift, in_smem != 0);
+__global__ void __launch_bounds__(kCTh) k_col_compress(const uint32_t* __restrict__ rows, int64_t ncols,
+                                                       const ulonglong2* __restrict__ ftab,
+                                                       unsigned long long* __restrict__ status,
+                                                       unsigned* __restrict__ counter, uint64_t* __restrict__ colptr,
+                                                       uint32_t* __restrict__ out) {
+    __shared__ uint32_t srow_all[kCWarps][32 * 3 * kCPT];
+    __shared__ uint64_t scp_all[kCWarps][32 * kCPT];
+    __shared__ uint32_t wt[kCWarps];
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_prefix;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* srow = srow_all[wid];
+    uint64_t* scp = scp_all[wid];
     const int64_t tiles = (ncols + kCT - 1) / kCT;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+        __syncthreads();
+        const int64_t t = s_tile;
+        if (t >= tiles) break;
         const int64_t j0 = t * kCT + (int64_t)threadIdx.x * kCPT;
-        ColGroup G;
-        const uint32_t c = load_group(rows, ncols, j0, FI, G);
-        unsigned long long x = c;
+        // rows and their table entries, all loads issued before any use
+        uint32_t r[3 * kCPT];
+        if (j0 + kCPT <= ncols) {
+            const uint4* v = reinterpret_cast<const uint4*>(rows + 3 * j0);
+#pragma unroll
+            for (int q = 0; q < 3 * kCPT / 4; ++q) {
+                const uint4 w = __ldcs(v + q);
+                r[4 * q] = w.x; r[4 * q + 1] = w.y; r[4 * q + 2] = w.z; r[4 * q + 3] = w.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3 * kCPT; ++q) r[q] = j0 + q / 3 < ncols ? __ldcs(rows + 3 * j0 + q) : 0u;
+        }
+        ulonglong2 e[3 * kCPT];
+#pragma unroll
+        for (int q = 0; q < 3 * kCPT; ++q) e[q] = __ldg(ftab + (r[q] >> 6));
+        uint32_t mask = 0, c = 0;
+#pragma unroll
+        for (int q = 0; q < 3 * kCPT; ++q) {
+            uint32_t nr;
+            const bool k = j0 + q / 3 < ncols && ftab_kept(e[q], r[q], nr);
+            r[q] = nr;
+            if (k) { mask |= 1u << q; ++c; }
+        }
+        uint32_t x = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        if (lane == 31) wt[wid] = x;
+        const uint32_t wsum = __shfl_sync(0xffffffffu, x, 31);
+        if (lane == 31) wt[wid] = wsum;
         __syncthreads();
         if (wid == 0) {
-            unsigned long long v = wt[lane], s = v;
+            const uint32_t v = lane < kCWarps ? wt[lane] : 0u;
+            uint32_t incl = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
-            wt[lane] = s - v;   // exclusive prefix of the warp totals
+            const unsigned long long total = __shfl_sync(0xffffffffu, incl, 31);
+            volatile unsigned long long* st = status;
+            unsigned long long excl = 0;
+            if (t == 0) {
+                if (lane == 0) st[0] = kCPre | total;
+            } else {
+                if (lane == 0) st[t] = kCAgg | total;
+                int64_t j = t - 1;
+                for (;;) {
+                    const int64_t jj = j - lane;
+                    unsigned long long sv = kCPre;
+                    if (jj >= 0) {
+                        sv = st[jj];
+                        while ((sv & (kCAgg | kCPre)) == 0) sv = st[jj];
+                    }
+                    const unsigned pre = __ballot_sync(0xffffffffu, (sv & kCPre) != 0);
+                    const int first = pre ? __ffs(pre) - 1 : 32;
+                    unsigned long long part = lane <= first ? (sv & kCVal) : 0ull;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                    excl += part;
+                    if (pre) break;
+                    j -= 32;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    st[t] = kCPre | (excl + total);
+                }
+            }
+            if (lane < kCWarps) wt[lane] = incl - v;   // exclusive per warp
+            if (lane == 0) s_prefix = excl;
         }
         __syncthreads();
-        uint64_t o = tile_off[t] + wt[wid] + x - c;
-        if (j0 + kCPT <= ncols) {
-            uint64_t cp[kCPT];
+        const uint64_t wbase = s_prefix + wt[wid];   // the warp's first output row
+        uint32_t lo = x - c;
 #pragma unroll
-            for (int q = 0; q < kCPT; ++q) {
-                cp[q] = o;
+        for (int q = 0; q < kCPT; ++q) {
+            scp[lane * kCPT + q] = wbase + lo;
 #pragma unroll
-                for (int e = 0; e < 3; ++e)
-                    if ((G.keepmask >> (3 * q + e)) & 1u) out[o++] = G.r[3 * q + e];
-            }
-            ulonglong2* d = reinterpret_cast<ulonglong2*>(colptr + j0);
-#pragma unroll
-            for (int q = 0; q < kCPT / 2; ++q) __stcs(d + q, make_ulonglong2(cp[2 * q], cp[2 * q + 1]));
-            if (j0 + kCPT == ncols) colptr[ncols] = o;
-        } else {
-#pragma unroll
-            for (int q = 0; q < kCPT; ++q) {
-                if (j0 + q >= ncols) break;
-                colptr[j0 + q] = o;
-#pragma unroll
-                for (int e = 0; e < 3; ++e)
-                    if ((G.keepmask >> (3 * q + e)) & 1u) out[o++] = G.r[3 * q + e];
-                if (j0 + q == ncols - 1) colptr[ncols] = o;
-            }
+            for (int e2 = 0; e2 < 3; ++e2)
+                if ((mask >> (3 * q + e2)) & 1u) srow[lo++] = r[3 * q + e2];
         }
-        __syncthreads();
+        __syncwarp();
+        for (uint32_t i = lane; i < wsum; i += 32) __stcs(out + wbase + i, srow[i]);
+        const int64_t c0 = t * kCT + (int64_t)wid * 32 * kCPT;
+        for (int i = lane; i < 32 * kCPT; i += 32)
+            if (c0 + i < ncols) __stcs(reinterpret_cast<unsigned long long*>(colptr) + c0 + i, scp[i]);
+        if (lane == 0 && c0 <= ncols - 1 && ncols - 1 < c0 + 32 * kCPT) colptr[ncols] = wbase + wsum;
+        __syncthreads();   // s_tile, wt and the staging are reused
     }
 }
 
-__global__ void k_forest_blocks(const uint32_t* __restrict__ forest, int64_t nf, int64_t nblk, int shift,
-                                uint32_t* __restrict__ blk) {
-    GRID_STRIDE(b, nblk + 1) {
-        const uint64_t v = (uint64_t)b << shift;
-        int64_t lo = 0, hi = nf;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if ((uint64_t)forest[mid] < v) lo = mid + 1; else hi = mid;
-        }
-        blk[b] = (uint32_t)lo;
+// forest table: bits of the forest positions per 64-position block, then
+// the count below each block (an exclusive scan of the blocks' popcounts)
+__global__ void k_ftab_bits(const uint32_t* __restrict__ forest, int64_t nf, ulonglong2* __restrict__ tab) {
+    GRID_STRIDE(q, nf) {
+        const uint32_t f = forest[q];
+        atomicOr(reinterpret_cast<unsigned long long*>(&tab[f >> 6].x), 1ull << (f & 63u));
     }
 }
+
+__global__ void k_ftab_pop(const ulonglong2* __restrict__ tab, int64_t nb, uint32_t* __restrict__ pop) {
+    GRID_STRIDE(b, nb) pop[b] = (uint32_t)__popcll(tab[b].x);
+}
+
+__global__ void k_ftab_below(ulonglong2* __restrict__ tab, int64_t nb, const uint64_t* __restrict__ below) {
+    GRID_STRIDE(b, nb) tab[b].y = below[b];
+}
+
 
 }  // namespace
 
@@ -477,39 +444,40 @@ int64_t compress_d2(const uint32_t* forest, int64_t nf, int64_t E, const uint32_
         VRB_CUDA(cudaMemsetAsync(colptr, 0, sizeof(uint64_t), s));
         return 0;
     }
-    // coarse index granularity: about one forest position per block, as long
-    // as forest + index fit shared memory (else the index goes to L2)
-    const int64_t budget = (int64_t)device_max_smem_optin() - 4096;
-    int shift = 6;
-    while (shift < 31 && (((E >> shift) > 2 * nf + 1024) || 4 * (nf + (E >> shift) + 2) > budget)) ++shift;
-    const int64_t nblk = (E >> shift) + 1;
-    DBuf<uint32_t> blk(nblk + 1, s);
-    k_forest_blocks<<<grid_for(nblk + 1), 256, 0, s>>>(forest, nf, nblk, shift, blk.get());
-    VRB_LAUNCH_CHECK();
-    size_t smem = (size_t)4 * (nf + nblk + 1);
-    int in_smem = 1;
-    if ((int64_t)smem > budget) {   // large forests: index in global memory
-        smem = 0;
-        in_smem = 0;
+    // the forest table (16 bytes per 64 edge positions)
+    const int64_t ntab = (E >> 6) + 1;
+    DBuf<ulonglong2> ftab(ntab, s);
+    VRB_CUDA(cudaMemsetAsync(ftab.get(), 0, ntab * sizeof(ulonglong2), s));
+    if (nf) {
+        k_ftab_bits<<<grid_for(nf), 256, 0, s>>>(forest, nf, ftab.get());
+        VRB_LAUNCH_CHECK();
     }
-    VRB_CUDA(cudaFuncSetAttribute(k_col_tile_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    VRB_CUDA(cudaFuncSetAttribute(k_col_tile_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 1;
-    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_tile_fill, kCTh, smem));
+    {
+        DBuf<uint32_t> pop(ntab, s);
+        DBuf<uint64_t> below(ntab + 1, s);
+        k_ftab_pop<<<grid_for(ntab), 256, 0, s>>>(ftab.get(), ntab, pop.get());
+        VRB_LAUNCH_CHECK();
+        exclusive_scan(pop.get(), below.get(), ntab, s);
+        k_ftab_below<<<grid_for(ntab), 256, 0, s>>>(ftab.get(), ntab, below.get());
+        VRB_LAUNCH_CHECK();
+    }
+    // one pass over D_2: tiles chained by a look-back over their kept counts
     const int64_t tiles = ceil_div(ncols, kCT);
+    DBuf<unsigned long long> status(tiles, s);
+    DBuf<unsigned> counter(1, s);
+    VRB_CUDA(cudaMemsetAsync(status.get(), 0, tiles * sizeof(unsigned long long), s));
+    VRB_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned), s));
+    // nnz: 3 ncols less the forest rows -- known only after the pass, so the
+    // output is allocated for 3 ncols and the count read back afterwards
+    uint32_t* rv = alloc_out(3 * ncols, ctx);
+    *rowval_out = rv;
+    int per_sm = 1;
+    VRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_compress, kCTh, 0));
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)device_sm_count() * std::max(1, per_sm));
-    DBuf<unsigned long long> sums(tiles, s);
-    DBuf<uint64_t> toff(tiles + 1, s);
-    k_col_tile_sums<<<grid, kCTh, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, shift, in_smem, sums.get());
+    k_col_compress<<<grid, kCTh, 0, s>>>(rows, ncols, ftab.get(), status.get(), counter.get(), colptr, rv);
     VRB_LAUNCH_CHECK();
-    exclusive_scan(reinterpret_cast<const uint64_t*>(sums.get()), toff.get(), tiles, s);
     uint64_t nnz = 0;
-    VRB_CUDA(cudaMemcpyAsync(&nnz, toff.get() + tiles, sizeof(nnz), cudaMemcpyDeviceToHost, s));
-    VRB_CUDA(cudaStreamSynchronize(s));
-    *rowval_out = alloc_out((int64_t)nnz, ctx);
-    k_col_tile_fill<<<grid, kCTh, smem, s>>>(rows, ncols, forest, nf, blk.get(), nblk, shift, in_smem, toff.get(),
-                                             colptr, *rowval_out);
-    VRB_LAUNCH_CHECK();
+    VRB_CUDA(cudaMemcpyAsync(&nnz, colptr + ncols, sizeof(nnz), cudaMemcpyDeviceToHost, s));
     VRB_CUDA(cudaStreamSynchronize(s));
     return (int64_t)nnz;
 }
