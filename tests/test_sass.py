@@ -44,3 +44,13 @@ def test_distance_fold_has_no_contraction():
         # DMULs outnumber the fold's)
         assert ops["DFMA"] <= 8 * ops["MUFU"]
         assert ops["DADD"] > 0 and ops["DMUL"] > 0
+
+
+def test_bucket_rank_loads_by_tma():
+    # the S3 chunk kernel takes its records by one cp.async.bulk (TMA) copy
+    # completing on an mbarrier: UBLKCP plus the SYNCS barrier operations
+    c = _census()
+    rank = [v for k, v in c.items() if "k_bk_rank" in k]
+    assert rank
+    for ops in rank:
+        assert ops["UBLKCP"] >= 1 and ops["SYNCS"] >= 2
