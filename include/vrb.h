@@ -49,12 +49,16 @@ typedef enum {
     VRB_EOVERFLOW = 3,  /* a count needs more than 32 bits where the layout
                            stores u32 positions (E, T, Q >= 2^32), or n >= 2^21 */
     VRB_ECUDA = 4,      /* CUDA runtime error; text in vrb_last_error() */
-    VRB_ECOMM = 5,      /* the collective callback of vrb_build_dist failed */
+    VRB_ECOMM = 5,      /* the collective callback of vrb_build_dist failed
+                           (SURVEY 8(b)'s VRB_ENCCL: the callbacks run NCCL or gloo) */
     VRB_ENOTSUP = 6     /* configuration outside what this build implements:
                            maxdim 2 with n above the tetrahedron kernels'
                            shared-memory map (38 784 on a B200; checked before
                            any work) -- DESIGN.md section 10 "Limits" */
 } vrb_status;
+/* SURVEY 8(b)'s name for the collective error (the collectives are NCCL when
+ * the callbacks use torch.distributed's NCCL backend). */
+#define VRB_ENCCL VRB_ECOMM
 
 /* vrb_opts.flags */
 #define VRB_STRICT_RADIUS    0x1u  /* keep len < radius instead of len <= radius (reading A1) */
