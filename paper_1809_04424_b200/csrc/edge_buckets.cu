@@ -68,6 +68,9 @@ constexpr int kBkOffStage = 1024;       // a chunk's bucket offsets staged in sh
 constexpr int kBkMaxLogNB = 23;
 constexpr unsigned long long kBkAgg = 1ull << 62, kBkPre = 2ull << 62, kBkVal = (1ull << 62) - 1;
 
+#ifndef VRB_BK_FILLBL
+#define VRB_BK_FILLBL 1   // staged chunks: the bucket of each position by a warp fill, not a search
+#endif
 #ifndef VRB_BK_TMA
 #define VRB_BK_TMA 1   // the chunk's records come in by one cp.async.bulk (TMA) copy on an mbarrier
 #endif
@@ -291,8 +294,25 @@ __global__ void __launch_bounds__(kBkThreads, kBkMinBlocks) k_bk_rank(BkArgs A) 
     // ---- sub-bucket of every item: bucket bl (chunk-relative) of m_b items
     // owns sub-buckets [4 off(bl), 4 off(bl) + 2^L), 2 m_b <= 2^L < 4 m_b, by
     // the residual's L high bits (about 1 item per 2 to 4 sub-buckets)
+    // staged chunks: each warp writes the bucket index over its buckets'
+    // positions (lane-strided); others: a binary search in off[] per item
+#if VRB_BK_FILLBL
+    if (staged) {
+        __syncthreads();   // the TMA copy's barrier wait and s_off are complete for all
+        for (int bl = wid; bl < (int)nbk; bl += kBkWarps) {
+            const int st = s_off[bl], en = s_off[bl + 1];
+            for (int t = st + lane; t < en; t += 32) s_bl[t] = (uint32_t)bl;
+        }
+        __syncthreads();
+    }
+#endif
     for (int t = tid; t < m; t += kBkThreads) {
         uint32_t lo = 0, hi = nbk;   // off(lo) <= t < off(hi)
+#if VRB_BK_FILLBL
+        if (staged) {
+            lo = s_bl[t];
+        } else
+#endif
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
             if (off_of(mid) <= t) lo = mid; else hi = mid;
