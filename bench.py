@@ -160,6 +160,12 @@ def run_reference(args, rank, world):
         return
     w = workloads.WORKLOADS[args.workload]
     m = min(ORACLE_SAMPLE.get(args.workload, 2000), w.points().shape[0])
+    # ORACLE_SAMPLE is sized for ~10-30 s per step; many steps shrink the
+    # sample so the whole run stays within a few minutes (the oracle's work
+    # grows as m^3 with triangles, m^2 for edges only)
+    nrun = max(1, args.steps + args.warmup)
+    if nrun > 8:
+        m = max(50, int(m * (8.0 / nrun) ** (1.0 / (3.0 if w.maxdim >= 1 else 2.0))))
     for _ in range(args.warmup):
         oracle_sample(w, m)
     tot_units, tot_s = 0, 0.0
