@@ -253,7 +253,8 @@ vrb_status vrb_h0(vrb_handle h, void* stream, const uint32_t** forest_pos, const
  *   nnz    : entries of the compressed matrix
  *   colptr : this handle's D_2 columns + 1 u64 offsets (column j of the
  *            slice = rows rowval[colptr[j] .. colptr[j+1]), ascending)
- *   rowval : u32 compressed row indices
+ *   rowval : u32 compressed row indices (nnz of them are meaningful; the
+ *            allocation holds 3 x columns, the bound known before the pass)
  *   rowmap : nrows u32, compressed row -> edge position (ascending)
  * A column keeps 1 to 3 rows (a forest holds no triangle's three edges).
  * VRB_EINVAL without dimension 2 or with VRB_SKIP_BOUNDARY. */
