@@ -64,7 +64,10 @@ constexpr int kBkMax = 2 * kBkC;        // items of a chunk: < C + largest bucke
 constexpr int kBkThreads = VRB_BK_THREADS;
 constexpr int kBkMinBlocks = (2048 / kBkThreads) < 2 ? 1 : (2048 / kBkThreads) / 2;
 constexpr int kBkWarps = kBkThreads / 32;
-constexpr int kBkOffStage = 1024;       // a chunk's bucket offsets staged in shared memory up to this many buckets
+#ifndef VRB_BK_OFFSTAGE
+#define VRB_BK_OFFSTAGE 1024
+#endif
+constexpr int kBkOffStage = VRB_BK_OFFSTAGE;       // a chunk's bucket offsets staged in shared memory up to this many buckets
 constexpr int kBkMaxLogNB = 23;
 constexpr unsigned long long kBkAgg = 1ull << 62, kBkPre = 2ull << 62, kBkVal = (1ull << 62) - 1;
 
