@@ -316,11 +316,15 @@ __device__ __forceinline__ void face_pos2(const TetArgs& A, const FaceQuery& q1,
     const bool d2 = face_block(b0, b1, q2.a, small_ids, lo2, hi2);
     if (d1) apex_narrow(A.apex, lo1, hi1, q1.a);
     if (d2) apex_narrow(A.apex, lo2, hi2, q2.a);
+    // a block of one entry is the face itself (the apex is in the list): no
+    // second round trip (every owner edge of <= 13 triangles: the record's
+    // separators are its apexes)
+    const bool x1 = d1 && hi1 - lo1 > 1, x2 = d2 && hi2 - lo2 > 1;
     uint4 c10, c11, c20, c21;
-    if (d1) apex_chunks(A.apex, lo1, hi1, c10, c11);
-    if (d2) apex_chunks(A.apex, lo2, hi2, c20, c21);
-    r1 = d1 ? apex_count(c10, c11, lo1, hi1, q1.a, small_ids) : tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2);
-    r2 = d2 ? apex_count(c20, c21, lo2, hi2, q2.a, small_ids) : tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2);
+    if (x1) apex_chunks(A.apex, lo1, hi1, c10, c11);
+    if (x2) apex_chunks(A.apex, lo2, hi2, c20, c21);
+    r1 = d1 ? (x1 ? apex_count(c10, c11, lo1, hi1, q1.a, small_ids) : lo1) : tri_pos(A, q1.f, q1.a0, q1.a1, q1.a2);
+    r2 = d2 ? (x2 ? apex_count(c20, c21, lo2, hi2, q2.a, small_ids) : lo2) : tri_pos(A, q2.f, q2.a0, q2.a1, q2.a2);
 }
 
 __global__ void k_tri_hash(const uint32_t* __restrict__ tv, int64_t T, ulonglong2* __restrict__ slots,
