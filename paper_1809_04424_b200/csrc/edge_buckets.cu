@@ -7,27 +7,34 @@
 // doubles, so the order of their bit patterns is the order of the lengths.
 // With kmin = the smallest key, d = key - kmin:
 //   bucket   b = d >> shift                   (monotone in the key)
-//   record   r = ((d mod 2^shift) >> tz) << vb | q
-// where q is the edge's lex index (its slot in the lex-ordered kept-edge
-// arrays: (i, j) order) and tz the trailing zero bits common to every d.
-// Inside a bucket, r orders exactly as (len, i, j): one u64 per edge.
+//   record   r = ((d mod 2^shift) >> tz) << vb | id
+// where id is (i << bn | j) when the packed ids fit beside the residual (or E
+// is too large to gather ids later), else the edge's lex index q (its slot
+// in the lex-ordered kept-edge arrays) -- both order as (i, j) -- and tz the
+// trailing zero bits common to every d.  Inside a bucket, r orders exactly as
+// (len, i, j): one u64 per edge.
 //   k_bk_hist    : bucket counts (global atomics on an L2-resident array)
 //   scan         : bucket offsets
 //   k_bk_scatter : r to slot atomicAdd(cur[b]) (the order inside a bucket is
-//                  arbitrary: the record restores it)
-//   k_bk_rank    : per chunk of whole buckets (<= 2 kBkC items), in shared
-//                  memory: each bucket split into 2^ceil(log2 m_b) sub-buckets
-//                  by its residual's high bits (a counting sort), each item
-//                  ranked inside its sub-bucket by comparing records; heads of
-//                  equal lengths counted by warp ballots and turned into dense
-//                  ranks by a chained scan over chunks (decoupled look-back,
-//                  chunks taken in order); (i, j), filt and value_of_rank
-//                  written in lane-consecutive rounds.
-// HBM: 8 B read (hist) + 8 B read + 8 B written (scatter) + 8 B read + 12 B
-// written + <= 8 B value_of_rank (rank) per edge, against 4 radix passes of
-// 24 B and a 32 B epilogue.  A bucket larger than kBkC items after two
-// refinements of the bucket width (ties, or a very spiky distribution), or a
-// record that would not fit 64 bits: the caller runs the radix path.
+//                  arbitrary: the record restores it), in slices of the bucket
+//                  range so the partially written sector of each bucket stays
+//                  in L2 until it fills
+//   k_bk_rank    : per chunk of whole buckets (< 2 kBkC items; records by one
+//                  TMA bulk copy on an mbarrier), in shared memory: the bucket
+//                  of each position by a warp fill over the staged offsets,
+//                  each bucket of m_b items split into 2^(ceil(log2 m_b) + 1)
+//                  sub-buckets by its residual's high bits (a counting sort
+//                  with packed u16 counters), each item ranked inside its
+//                  sub-bucket by comparing records (equal lengths found there
+//                  too: the chunk's level count is published before the
+//                  outputs); dense ranks by a chained scan over chunks
+//                  (decoupled look-back, chunks taken in order); (i, j), filt
+//                  and value_of_rank written in lane-consecutive rounds.
+// HBM: 8 B read (hist) + (12 B read per slice) + 8 B written (scatter) + 8 B
+// read + 12 B written + <= 8 B value_of_rank (rank) per edge, against 4 radix
+// passes of 24 B and a 32 B epilogue.  A bucket larger than kBkC items after
+// two refinements of the bucket width (ties, or a very spiky distribution),
+// or a record that would not fit 64 bits: the caller runs the radix path.
 #include <algorithm>
 #include <cstdlib>
 #include <functional>
