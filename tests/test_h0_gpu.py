@@ -206,11 +206,11 @@ def test_compress_d2_vs_oracle(vrb, case):
 
 
 def test_compress_d2_large_forest_index_in_global_memory(vrb):
-    # 80 000 points: the forest (~70 000 edges, 280 KB) is too large for the
-    # shared-memory index, so the column passes read it through L2; the
-    # result must still be D_2 without the forest rows, renumbered (checked
-    # against that definition on the GPU's own D_2 and forest, whose parity
-    # the tests above establish)
+    # 80 000 points: a forest of ~70 000 edges and hundreds of column tiles
+    # chained by the look-back of the one-pass compress; the result must
+    # still be D_2 without the forest rows, renumbered (checked against that
+    # definition on the GPU's own D_2 and forest, whose parity the tests
+    # above establish)
     X = workloads.random_cloud(60, 80000, 3, "uniform")
     res = vrb.build(X, maxdim=1, radius=0.03)
     pos, _, _ = res.h0()
